@@ -1,0 +1,479 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (no GPU).
+
+Each test names the passage or closed form it pins.
+None of them retypes the oracle's own loop: they use closed forms, finite
+differences, dense textbook products (numpy), brute force, bisection and
+independent re-evaluation.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import mlgen
+import oracle
+
+LAM_TOL = 1e-6
+
+
+def _tight(**kw):
+    return oracle.default_opts(tol_kkt=1e-12, max_cycles=2000, **kw)
+
+
+# ----------------------------------------------------------------------------- scalar pieces
+def test_soft_shrink_examples():
+    """Eq. 6; SPEC examples S:53-55."""
+    L = oracle.lib()
+    assert L.mlo_soft_shrink(3.0, 1.0) == 2.0
+    assert L.mlo_soft_shrink(0.5, 1.0) == 0.0
+    assert L.mlo_soft_shrink(-5.0, 2.0) == -3.0
+
+
+def test_scalar_prox_sign_fixed():
+    """Eq. 11 minimiser; the printed closed form P:182-190 has a sign typo (DESIGN Q1).
+    (2,3,1) -> -1 is the grid-search minimum; stationarity 0 in a z + b + lam d|z| by cases."""
+    L = oracle.lib()
+    assert L.mlo_scalar_prox(1.0, 0.0, 1.0) == 0.0
+    assert L.mlo_scalar_prox(2.0, 3.0, 1.0) == -1.0
+    assert L.mlo_scalar_prox(1.0, -0.5, 1.0) == 0.0
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        a, b, lam = rng.uniform(0.1, 5), rng.normal(0, 3), rng.uniform(0, 2)
+        z = L.mlo_scalar_prox(a, b, lam)
+        if z != 0.0:
+            assert abs(a * z + b + lam * math.copysign(1.0, z)) <= 1e-12 * (abs(b) + lam + 1)
+        else:
+            assert abs(b) <= lam + 1e-15
+        # grid check of the minimiser
+        grid = np.linspace(z - 1, z + 1, 2001)
+        obj = 0.5 * a * grid ** 2 + b * grid + lam * np.abs(grid)
+        assert obj.min() >= 0.5 * a * z * z + b * z + lam * abs(z) - 1e-12
+
+
+def test_logistic_pieces_closed_forms():
+    """tau, ell, D of P:796: tau(t)+tau(-t)=1, ell(t)-ell(-t)=-t, D = 1/(2+2cosh t), asymptotics."""
+    L = oracle.lib()
+    for t in np.r_[np.linspace(-40, 40, 161), [-700.0, 700.0, 1e-12, -1e-12]]:
+        t = float(t)
+        assert abs(L.mlo_tau(t) + L.mlo_tau(-t) - 1.0) <= 2.3e-16
+        if abs(t) < 30:
+            assert abs((L.mlo_logloss(t) - L.mlo_logloss(-t)) - (-t)) <= 4e-16 * max(1.0, abs(t))
+        ref_D = 1.0 / (2.0 + 2.0 * math.cosh(t))
+        assert abs(L.mlo_weight(t) - ref_D) <= 1e-15 * ref_D
+    assert L.mlo_logloss(0.0) == math.log(2.0)
+    for t in (40.0, 100.0, 600.0):
+        assert abs(L.mlo_logloss(t) - math.exp(-t)) <= 1e-15 * math.exp(-t) + 1e-300
+        assert abs(L.mlo_logloss(-t) - t) <= 1e-15 * t
+
+
+# ----------------------------------------------------------------------------- F, g, H
+def _dense_problem(m=30, n=8, seed=3):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((m, n)).astype(np.float32)
+    y = np.where(rng.random(m) < 0.5, 1, -1).astype(np.int8)
+    return mlgen.from_dense(X, y, lam=0.3), X.astype(np.float64), y.astype(np.float64)
+
+
+def test_values_at_zero():
+    """At w = 0: F = m log 2, g = -1/2 X^T y, D = 1/4 (App. A.1)."""
+    ds = mlgen.make(1)
+    o = oracle.Oracle(ds)
+    F, g, h = o.eval_f_grad()
+    assert abs(F - ds.m * math.log(2.0)) <= 1e-13 * F
+    X = ds.dense()
+    gref = -0.5 * (X.T @ ds.y.astype(np.float64))
+    assert np.max(np.abs(g - gref)) <= 1e-12 * np.max(np.abs(gref))
+    z, r, D, ell = o.rows()
+    assert np.all(D == 0.25) and np.all(z == 0.0)
+    assert np.allclose(h, 0.25 * (X * X).sum(0), rtol=1e-13)
+    # generator's lambda_max (the config's definition) == the oracle's ||g(0)||_inf
+    assert abs(np.max(np.abs(g)) - ds.lambda_max) <= 1e-13 * ds.lambda_max
+
+
+def test_gradient_finite_differences():
+    """g = X^T r against central differences of F away from kinks."""
+    ds, X, y = _dense_problem()
+    rng = np.random.default_rng(7)
+    w = rng.uniform(0.2, 0.6, ds.n) * np.where(rng.random(ds.n) < 0.5, 1, -1)
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    F0, g, h = o.eval_f_grad()
+    for j in range(ds.n):
+        e = 1e-5 * max(1.0, abs(w[j]))
+        wp, wm = w.copy(), w.copy()
+        wp[j] += e
+        wm[j] -= e
+        o.set_w(wp)
+        Fp = o.eval_f_grad(np.array([0], np.int32))[0]
+        o.set_w(wm)
+        Fm = o.eval_f_grad(np.array([0], np.int32))[0]
+        fd = (Fp - Fm) / (2 * e) - ds.lam * np.sign(w[j])
+        assert abs(fd - g[j]) <= 1e-6 * max(1.0, abs(g[j])), (j, fd, g[j])
+
+
+def test_hessian_dense_and_fd():
+    """H = X^T D X: hessvec and diag vs the dense textbook product with D = 1/(2+2cosh t);
+    directional finite differences of g; symmetry <Hu,v> = <u,Hv>."""
+    ds, X, y = _dense_problem(m=40, n=9, seed=5)
+    rng = np.random.default_rng(11)
+    w = rng.normal(0, 0.5, ds.n)
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    F0, g0, h = o.eval_f_grad()
+    t = y * (X @ w)
+    Dref = 1.0 / (2.0 + 2.0 * np.cosh(t))
+    H = X.T @ (Dref[:, None] * X)
+    assert np.allclose(h, np.diag(H), rtol=1e-12, atol=0)
+    C = np.arange(ds.n, dtype=np.int32)
+    for _ in range(3):
+        v = rng.standard_normal(ds.n)
+        Hv = o.hessvec(C, v)
+        assert np.linalg.norm(Hv - H @ v) <= 1e-12 * np.linalg.norm(H @ v)
+        u = rng.standard_normal(ds.n)
+        assert abs(u @ o.hessvec(C, v) - v @ o.hessvec(C, u)) <= 1e-12 * np.linalg.norm(H) * np.linalg.norm(u) * np.linalg.norm(v)
+        e = 1e-5
+        o.set_w(w + e * v)
+        gp = o.eval_f_grad()[1]
+        o.set_w(w - e * v)
+        gm = o.eval_f_grad()[1]
+        o.set_w(w)
+        fd = (gp - gm) / (2 * e)
+        assert np.linalg.norm(fd - Hv) <= 1e-6 * np.linalg.norm(Hv)
+    # restricted C: only the C block of H
+    Cs = np.array([1, 4, 7], np.int32)
+    v = rng.standard_normal(3)
+    assert np.allclose(o.hessvec(Cs, v), H[np.ix_(Cs, Cs)] @ v, rtol=1e-12)
+
+
+# ----------------------------------------------------------------------------- lambda_max / zero solution
+def test_lambda_max_zero_solution():
+    """w = 0 is optimal iff lam >= lam_max = 1/2 ||X^T y||_inf (App. A.1; sub-differential P:248-256)."""
+    ds = mlgen.make(1)
+    o = oracle.Oracle(ds.with_lambda(ds.lambda_max * (1 + 1e-9)))
+    rep = o.solve()
+    assert rep["status"] == 0 and rep["cycles"] == 0 and rep["nnz_w"] == 0
+    assert np.all(o.get_w() == 0.0)
+    X = ds.dense()
+    c = np.abs(X.T @ ds.y.astype(np.float64))
+    jmax = int(np.argmax(c))
+    assert np.sum(c >= c[jmax] * (1 - 1e-3)) == 1  # unique max in this data
+    o = oracle.Oracle(ds.with_lambda(ds.lambda_max * (1 - 1e-3)))
+    rep = o.solve(_tight())
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert list(np.nonzero(w)[0]) == [jmax]
+
+
+# ----------------------------------------------------------------------------- n = 1
+def test_n1_identical_margins_closed_form():
+    """App. A.2: m copies of y x = a  ->  w* = sign(a) log(m|a|/lam - 1)/|a| when lam < m|a|/2."""
+    for a, m, lam in ((0.75, 10, 1.0), (-1.25, 7, 0.5), (2.0, 3, 2.9)):
+        X = np.full((m, 1), abs(a), np.float32)
+        y = np.full(m, 1 if a > 0 else -1, np.int8)
+        ds = mlgen.from_dense(X, y, lam)
+        o = oracle.Oracle(ds)
+        rep = o.solve(_tight())
+        w = o.get_w()[0]
+        wref = math.copysign(math.log(m * abs(a) / lam - 1.0) / abs(a), a)
+        assert rep["status"] == 0
+        assert abs(w - wref) <= 1e-10 * abs(wref)
+        Fref = m * math.log1p(math.exp(-abs(a) * abs(wref))) + lam * abs(wref)
+        assert abs(rep["F"] - Fref) <= 1e-12 * Fref
+    # lam >= m|a|/2: w* = 0
+    X = np.full((4, 1), 0.5, np.float32)
+    ds = mlgen.from_dense(X, np.ones(4, np.int8), 1.0)
+    o = oracle.Oracle(ds)
+    assert o.solve()["nnz_w"] == 0
+
+
+def test_n1_mixed_bisection():
+    """n = 1, mixed data: L'(w) + lam sign(w) = 0 by bisection on the monotone derivative (App. A.2)."""
+    rng = np.random.default_rng(2)
+    m = 25
+    x = rng.uniform(0.2, 2.0, m).astype(np.float32)
+    y = np.where(rng.random(m) < 0.7, 1, -1).astype(np.int8)
+    lam = 1.0
+    xs, ys = x.astype(np.float64), y.astype(np.float64)
+
+    def dL(w):  # derivative of sum log(1+exp(-y x w)), written from P:792 (tau(s)-1) y x
+        s = ys * xs * w
+        return np.sum((1.0 / (1.0 + np.exp(-s)) - 1.0) * ys * xs)
+
+    assert abs(dL(0.0)) > lam
+    sgn = -np.sign(dL(0.0))
+    lo, hi = 0.0, 50.0 * sgn
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if (dL(mid) + lam * sgn) * sgn < 0:
+            lo = mid
+        else:
+            hi = mid
+    wref = 0.5 * (lo + hi)
+    ds = mlgen.from_dense(x[:, None], y, lam)
+    o = oracle.Oracle(ds)
+    rep = o.solve(_tight())
+    assert abs(o.get_w()[0] - wref) <= 1e-10 * abs(wref)
+
+
+# ----------------------------------------------------------------------------- one-hot closed form
+def _onehot_reference(a, p, q, lam):
+    d = np.abs(p - q).astype(np.float64)
+    act = lam < a * d / 2
+    w = np.zeros(len(a))
+    big, small = np.maximum(p, q).astype(np.float64), np.minimum(p, q).astype(np.float64)
+    w[act] = np.sign(p - q)[act] / a[act] * np.log((a[act] * big[act] - lam) / (a[act] * small[act] + lam))
+
+    def ell(t):
+        return np.logaddexp(0.0, -t)
+
+    F = np.sum(p * ell(a * w) + q * ell(-a * w) + lam * np.abs(w))
+    return w, F
+
+
+@pytest.mark.parametrize("n,seed", [(40, 1), (600, 2)])
+def test_onehot_separable_closed_form(n, seed):
+    """App. A.3: one-hot design, w*_j in closed form; exercises top-k, support growth and all levels."""
+    ds, a, p, q = mlgen.onehot(n, seed)
+    wref, Fref = _onehot_reference(a, p, q, ds.lam)
+    o = oracle.Oracle(ds)
+    rep = o.solve(_tight())
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    nz = wref != 0
+    assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-8
+    assert abs(rep["F"] - Fref) <= 1e-12 * Fref
+    assert max(rep["relax_per_level"][1:]) > 0  # coarse levels were used
+
+
+# ----------------------------------------------------------------------------- brute force
+def _brute_force(X, y, lam):
+    """Enumerate supports S and signs s (3^n); damped Newton on the smooth phi(w_S) = L(X_S w_S) + lam s^T w_S;
+    accept iff signs agree and |g_j| <= lam off S.  Returns (w*, F*)."""
+    m, n = X.shape
+    best = None
+
+    def Lgrad(wS, XS):
+        t = y * (XS @ wS)
+        r = -y / (1.0 + np.exp(t))
+        D = 1.0 / (2.0 + 2.0 * np.cosh(t))
+        return np.sum(np.logaddexp(0, -t)), XS.T @ r, XS.T @ (D[:, None] * XS)
+
+    for k in range(n + 1):
+        for S in itertools.combinations(range(n), k):
+            S = list(S)
+            for sg in itertools.product((-1.0, 1.0), repeat=k):
+                sg = np.array(sg)
+                XS = X[:, S]
+                wS = np.zeros(k)
+                ok = True
+                for _ in range(100):
+                    if k == 0:
+                        break
+                    Lv, g, H = Lgrad(wS, XS)
+                    gr = g + lam * sg
+                    step = np.linalg.solve(H + 1e-14 * np.eye(k), -gr)
+                    phi0 = Lv + lam * sg @ wS
+                    tstep = 1.0
+                    while tstep > 1e-12:
+                        wn = wS + tstep * step
+                        if np.sum(np.logaddexp(0, -y * (XS @ wn))) + lam * sg @ wn <= phi0 + 1e-4 * tstep * gr @ step:
+                            break
+                        tstep *= 0.5
+                    wS = wS + tstep * step
+                    if np.max(np.abs(wS)) > 1e6:
+                        ok = False
+                        break
+                    if np.linalg.norm(gr) < 1e-13:
+                        break
+                if not ok or (k and np.any(np.sign(wS) != sg)):
+                    continue
+                w = np.zeros(n)
+                w[S] = wS
+                t = y * (X @ w)
+                g = X.T @ (-y / (1.0 + np.exp(t)))
+                off = [j for j in range(n) if j not in S]
+                if k and np.max(np.abs(g[S] + lam * sg)) > 1e-8:
+                    continue
+                if off and np.max(np.abs(g[off])) > lam * (1 + 1e-9):
+                    continue
+                F = np.sum(np.logaddexp(0, -t)) + lam * np.abs(w).sum()
+                if best is None or F < best[1]:
+                    best = (w, F)
+    return best
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.filterwarnings("ignore::RuntimeWarning")
+def test_brute_force_small(seed):
+    """Solver on general tiny data vs brute-force support/sign enumeration."""
+    rng = np.random.default_rng(100 + seed)
+    m, n = 24, 6
+    X = rng.standard_normal((m, n)).astype(np.float32)
+    y = np.where(X[:, 0] + 0.5 * rng.standard_normal(m) > 0, 1, -1).astype(np.int8)
+    lmax = 0.5 * np.max(np.abs(X.astype(np.float64).T @ y))
+    lam = 0.15 * lmax
+    wref, Fref = _brute_force(X.astype(np.float64), y.astype(np.float64), lam)
+    o = oracle.Oracle(mlgen.from_dense(X, y, lam))
+    rep = o.solve(_tight())
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    assert abs(rep["F"] - Fref) <= 1e-12 * Fref
+
+
+# ----------------------------------------------------------------------------- small-lambda limit
+def test_small_lambda_irls_limit():
+    """App. A.4: w*(lam) = w_MLE - lam H(w_MLE)^{-1} sign(w_MLE) + O(lam^2), w_MLE by textbook IRLS."""
+    rng = np.random.default_rng(9)
+    m, n = 600, 4
+    X = rng.standard_normal((m, n)).astype(np.float32)
+    wt = np.array([1.0, -0.7, 0.5, 0.3])
+    Xd = X.astype(np.float64)
+    y = np.where(rng.random(m) < 1 / (1 + np.exp(-Xd @ wt)), 1, -1).astype(np.int8)
+    yd = y.astype(np.float64)
+    w = np.zeros(n)
+    for _ in range(50):  # IRLS / Newton on the unregularised loss
+        s = yd * (Xd @ w)
+        p = 1 / (1 + np.exp(-s))
+        g = Xd.T @ ((p - 1) * yd)
+        H = Xd.T @ ((p * (1 - p))[:, None] * Xd)
+        w = w - np.linalg.solve(H, g)
+    s = yd * (Xd @ w)
+    p = 1 / (1 + np.exp(-s))
+    H = Xd.T @ ((p * (1 - p))[:, None] * Xd)
+    res = []
+    for lam in (0.4, 0.2):
+        o = oracle.Oracle(mlgen.from_dense(X, y, lam))
+        o.solve(_tight())
+        pred = w - lam * np.linalg.solve(H, np.sign(w))
+        res.append(np.linalg.norm(o.get_w() - pred))
+    assert res[1] <= 0.3 * res[0]  # second-order residual: halving lam cuts it ~4x
+    assert res[1] <= 0.05 * 0.2 * np.linalg.norm(np.linalg.solve(H, np.sign(w)))
+
+
+# ----------------------------------------------------------------------------- KKT at convergence
+def test_kkt_reverification_cfg1():
+    """Independent KKT re-check at the returned w, with a long-double gradient."""
+    ds = mlgen.make(1)
+    o = oracle.Oracle(ds)
+    rep = o.solve()
+    assert rep["status"] == 0 and rep["kappa"] <= 1e-6
+    w = o.get_w()
+    X = ds.dense().astype(np.longdouble)
+    y = ds.y.astype(np.longdouble)
+    t = y * (X @ w.astype(np.longdouble))
+    g = X.T @ (-y / (1 + np.exp(t)))
+    g = g.astype(np.float64)
+    lam = ds.lam
+    S = w != 0
+    assert np.max(np.abs(g[~S])) <= lam * (1 + 1e-6)
+    assert np.max(np.abs(g[S] + lam * np.sign(w[S]))) <= 1e-6 * lam
+
+
+# ----------------------------------------------------------------------------- ML machinery
+def test_level_sizes():
+    """P:194 size rule and termination; S:152-154 examples."""
+    assert oracle.level_sizes(100, 5, 100) == [100, 50, 25, 13, 7, 5]
+    assert oracle.level_sizes(8, 2, 8) == [8, 4, 2]
+    assert oracle.level_sizes(1, 1, 1) == [1]          # |C_1| = n: L = 0
+    assert oracle.level_sizes(3, 3, 10) == [10, 3]      # ceil(|A|/2) < |S|: straight to supp
+
+
+def test_select_coarse_vs_lexsort():
+    """supp(w) U top-(k-|supp|) of |g| off-support, ties by ascending index, vs numpy lexsort."""
+    rng = np.random.default_rng(4)
+    ds = mlgen.random_sparse(20, 300, 0.3, seed=4)
+    o = oracle.Oracle(ds)
+    w = np.zeros(ds.n)
+    S = rng.choice(ds.n, 17, replace=False)
+    w[S] = rng.normal(size=17)
+    o.set_w(w)
+    g = np.round(rng.normal(size=ds.n), 1)  # many exact ties
+    for k in (0, 17, 18, 60, 299, 300, 400):
+        C = o.select_coarse(g, k)
+        off = np.setdiff1d(np.arange(ds.n), S)
+        order = off[np.lexsort((off, -np.abs(g[off])))]
+        take = max(0, min(k - 17, len(off)))
+        ref = np.sort(np.r_[S, order[:take]])
+        assert np.array_equal(C, ref), k
+
+
+def test_corollary_exact_coarse_solution():
+    """Corollary P:324-326 via Lemma P:313-318: if C_L contains supp(w*) and the coarsest problem is
+    solved exactly, the global problem is solved (one-hot w* known in closed form)."""
+    ds, a, p, q = mlgen.onehot(200, 7)
+    wref, Fref = _onehot_reference(a, p, q, ds.lam)
+    C = np.sort(np.r_[np.nonzero(wref)[0], np.arange(0, 200, 37)])
+    C = np.unique(C).astype(np.int32)
+    o = oracle.Oracle(ds)
+    opts = _tight()
+    for _ in range(200):
+        st, oc = o.relax(C, 10, opts)
+        if oc == oracle.R_CONVERGED:
+            break
+    assert oc == oracle.R_CONVERGED
+    F, g, h = o.eval_f_grad()
+    w = o.get_w()
+    v = np.where(w != 0, g + ds.lam * np.sign(w), np.sign(g) * np.maximum(np.abs(g) - ds.lam, 0))
+    assert np.max(np.abs(v)) / ds.lam <= 1e-10
+    assert abs(F - Fref) <= 1e-12 * Fref
+
+
+def test_no_stagnation_theorem():
+    """Theorem P:330-349: with C_L missing part of supp(w*), solving C_L exactly leaves some j outside
+    C_L with |g_j| > lam, so a finer relaxation must change the support."""
+    ds, a, p, q = mlgen.onehot(100, 8)
+    wref, _ = _onehot_reference(a, p, q, ds.lam)
+    sup = np.nonzero(wref)[0]
+    C = np.sort(sup[: len(sup) // 2]).astype(np.int32)
+    o = oracle.Oracle(ds)
+    for _ in range(200):
+        st, oc = o.relax(C, 10, _tight())
+        if oc == oracle.R_CONVERGED:
+            break
+    F, g, h = o.eval_f_grad()
+    outside = np.setdiff1d(np.arange(ds.n), C)
+    assert np.max(np.abs(g[outside])) > ds.lam
+    supp0 = set(np.nonzero(o.get_w())[0])
+    o.relax(None, 1, oracle.default_opts())
+    assert set(np.nonzero(o.get_w())[0]) != supp0
+
+
+def test_monotone_relaxations_and_invariants():
+    """Lemma P:207-243: F never increases across a relaxation; supp(w) stays inside C_l."""
+    for ds in (mlgen.make(1), mlgen.make(3, m=3000, n=6000)):
+        o = oracle.Oracle(ds)
+        rep = o.solve()
+        assert rep["status"] == 0
+        tr = o.trace()
+        assert len(tr) > 5
+        for row in tr:
+            assert row["F_after"] <= row["F_before"] * (1 + 1e-12) + 1e-12
+        assert any(row["level"] >= 1 for row in tr)
+
+
+def test_linesearch_armijo_decision():
+    """Eq. 4 with Armijo (DESIGN Q7): the accepted alpha passes, 2*alpha fails; F re-evaluated from the
+    definition P:786 in numpy."""
+    ds, X, y = _dense_problem(m=50, n=10, seed=21)
+    o = oracle.Oracle(ds)
+    rng = np.random.default_rng(3)
+    w = rng.normal(0, 0.3, ds.n) * (rng.random(ds.n) < 0.6)
+    o.set_w(w)
+    F0, g, h = o.eval_f_grad()
+    C = np.arange(ds.n, dtype=np.int32)
+    d = rng.normal(0, 3.0, ds.n)   # a long step so that backtracking is needed
+    d = -np.sign(g) * np.abs(d)
+
+    def F(wv):
+        return np.sum(np.logaddexp(0, -y * (X @ wv))) + ds.lam * np.abs(wv).sum()
+
+    Delta = g @ d + ds.lam * (np.abs(w + d).sum() - np.abs(w).sum())
+    alpha, Fn, st = o.shrink_linesearch(C, g, d=d)
+    assert st == 0 and 0 < alpha < 1
+    assert F(w + alpha * d) - F(w) <= 1e-2 * alpha * Delta + 1e-12
+    assert F(w + 2 * alpha * d) - F(w) > 1e-2 * 2 * alpha * Delta
+    assert np.allclose(o.get_w(), w + alpha * d, rtol=0, atol=1e-15)
+    assert abs(Fn - F(w + alpha * d)) <= 1e-12 * Fn
