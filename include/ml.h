@@ -1,0 +1,125 @@
+/* ml.h — C ABI of libml: the B200 (sm_100a) hot path of the multilevel proximal-Newton method for
+ * l1-regularised logistic regression (Treister, Turek, Yavneh, arXiv 1607.00315).
+ *
+ *   min_w F(w) = sum_i log(1 + exp(-y_i x_i^T w)) + lambda ||w||_1          (C = 1)
+ *
+ * X is m x n with ROWS = SAMPLES (the paper's X^T), given twice, CSR and CSC, fp32 values and int32
+ * indices.  w, every vector and every accumulation are fp64.
+ *
+ * Memory and ownership
+ *   - Every pointer in this header is a DEVICE pointer unless its name ends in _host.
+ *   - X, y, index lists, vectors and the workspace are BORROWED: the caller allocates, keeps them alive for the
+ *     lifetime of the context, and frees them.  The library never copies, slices or frees X and never allocates
+ *     device memory: all scratch is carved from `ws` (size from ml_workspace_bytes).
+ *   - All work is enqueued on the stream given to ml_create.  Calls that return host scalars synchronise that
+ *     stream only.  One context per stream / host thread; no global mutable state.
+ *   - Index lists C are int32, strictly ascending, in [0, n).  C == NULL with nC == n means all columns.
+ * Errors
+ *   - Every call returns ml_status; nothing throws or exits across the ABI; ml_last_error gives detail.
+ *   - ML_E_INVAL: m, n < 1, nnz >= 2^31, lambda <= 0 or non-finite, y not in {-1,+1}, bad C, too small workspace.
+ *   - ML_E_CUDA: a CUDA runtime error (message in ml_last_error).
+ *   - ML_E_STAGNATION: no trial step passed the line search; the iterate is unchanged.
+ *   - ML_E_NOT_CONVERGED: ml_solve hit max_cycles; w holds the last evaluated iterate.
+ * Determinism: all reductions are fixed-shape trees (no floating-point atomics) except the Hessian-vector scatter
+ *   X_A s, which adds with fp64 atomics (results reproducible to rounding, not bitwise).
+ */
+#ifndef ML_H
+#define ML_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ml_ctx ml_ctx;
+
+typedef enum {
+    ML_OK = 0, ML_E_INVAL = 1, ML_E_CUDA = 2, ML_E_WORKSPACE = 3, ML_E_STAGNATION = 4,
+    ML_E_NOT_CONVERGED = 5, ML_E_CONTRACT = 6
+} ml_status;
+
+typedef struct {                  /* X is m x n, rows = samples; 0 <= nnz < 2^31 */
+    int64_t m, n, nnz;
+    const int32_t *csr_rowptr;    /* [m+1] */
+    const int32_t *csr_col;       /* [nnz], ascending inside each row */
+    const float *csr_val;         /* [nnz] */
+    const int32_t *csc_colptr;    /* [n+1] */
+    const int32_t *csc_row;       /* [nnz], ascending inside each column */
+    const float *csc_val;         /* [nnz] */
+    const int8_t *y;              /* [m], each -1 or +1 */
+} ml_data;
+
+typedef struct {                  /* defaults: ml_default_opts */
+    double tol_kkt;               /* stop when kappa = ||v||_inf / lambda <= tol_kkt (min-norm subgradient) */
+    int32_t max_cycles;
+    int32_t nu;                   /* relaxations per level (Alg. 1 step 4) */
+    int32_t nu_c;                 /* max relaxations on the coarsest level (Alg. 1 step 3) */
+    int32_t K_fine, K_mid, K_coarse; /* inner iterations per relaxation (P:819 reading, DESIGN Q9) */
+    double sigma_out, sigma_in, beta; /* Armijo constants (Eq. 4; DESIGN Q7) */
+    int32_t max_ls;               /* <= 40 */
+    double eps_h;                 /* model ridge (DESIGN Q6) */
+    int32_t multilevel;           /* 1: Algorithm 1; 0: finest-level relaxations only */
+    int32_t inner_cg;             /* 1: PCD-CG inner solver (DESIGN Q9b); 0: plain PCD */
+    double eta;                   /* inner forcing (0 = off) */
+} ml_solve_opts;
+
+typedef struct {
+    double F, kappa, vinf, v1, paper_ratio;
+    int32_t status, cycles;
+    int64_t relaxations;
+    int64_t relax_per_level[32];
+    int64_t max_supp, nnz_w;
+    int64_t nnz_touched;          /* nonzeros streamed by all X passes (algorithmic) */
+    int64_t x_passes;
+    int64_t kernel_launches;      /* kernels this solve enqueued */
+} ml_solve_report;
+
+void ml_default_opts(ml_solve_opts *o);
+
+/* Workspace bytes for a problem of this size (all scratch, iterate, margins, level lists). */
+size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz);
+
+/* Bind X, y, lambda (> 0) to a context; w = 0.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+   Validates sizes, lambda and y (one device pass).  Builds the static heavy-row schedule (one pass over rowptr). */
+ml_status ml_create(const ml_data *X, double lambda, void *cuda_stream, void *ws, size_t ws_bytes, ml_ctx **out);
+ml_status ml_destroy(ml_ctx *c);
+
+/* w <- w_dev[n] (device); margins are recomputed at the next evaluation. */
+ml_status ml_set_w(ml_ctx *c, const double *w_dev);
+/* w_dev[n] <- w */
+ml_status ml_get_w(ml_ctx *c, double *w_dev);
+/* per-sample state after the last evaluation/update: z, r, D (each [m], device; NULL skips) */
+ml_status ml_get_rows(ml_ctx *c, double *z_dev, double *r_dev, double *D_dev);
+
+/* A1 + A2: margins z = Xw from scratch (CSR pass) with fused tau, D, r, loss; F = L + lambda||w||_1;
+   then g_C = X_C^T r and h_C = sum_i X_ij^2 D_i over C (CSC gather).  F_host may be NULL; g_C / h_C may be NULL. */
+ml_status ml_eval_f_grad(ml_ctx *c, const int32_t *C, int64_t nC, double *F_host, double *g_C, double *h_C);
+/* h_C = sum_i X_ij^2 D_i with D from the current state. */
+ml_status ml_diag_hess(ml_ctx *c, const int32_t *C, int64_t nC, double *h_C);
+/* Hv_C = X_C^T D X_C v_C with D from the current state, no ridge. */
+ml_status ml_hessvec(ml_ctx *c, const int32_t *C, int64_t nC, const double *v_C, double *Hv_C);
+/* A7: Armijo line search on F along d over C (Eq. 4; DESIGN Q7, Q26), then w += alpha d,
+   z += alpha Xd and refresh of tau, D, r (A1 incremental).  g_C = gradient over C at the current w.
+   d_C == NULL: d = Sh_{lambda/h}(w - g/h) - w (Eq. 5 with D = diag(h) + eps_h, PCD P:99), h_C required.
+   Xd == NULL: computed with one X_C pass.  alpha_host = 0 and ML_E_STAGNATION when no trial passes. */
+ml_status ml_shrink_linesearch(ml_ctx *c, const int32_t *C, int64_t nC, const double *g_C, const double *h_C,
+                               const double *d_C, const double *Xd, const ml_solve_opts *o,
+                               double *alpha_host, double *F_new_host);
+/* A8: C_out = supp(w) U the (k_total - |supp|) largest |g_j| off the support, ties by ascending
+   index (DESIGN Q14); C_out ascending, *nC_out_host = max(k_total, |supp|) capped at n.  g is [n]. */
+ml_status ml_select_coarse(ml_ctx *c, const double *g, int64_t k_total, int32_t *C_out, int64_t *nC_out_host);
+/* A9: the multilevel solve from w = 0 (Algorithm 1 P:155-173 per P:798). */
+ml_status ml_solve(ml_ctx *c, const ml_solve_opts *o, ml_solve_report *rep);
+
+const char *ml_status_str(ml_status s);
+const char *ml_last_error(const ml_ctx *c);
+/* kernels this context has launched so far (for launch accounting) */
+int64_t ml_kernel_launches(const ml_ctx *c);
+/* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
+   int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */
+int64_t ml_trace(ml_ctx *c, void *rows_host, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,719 @@
+// ml.cu — libml: C ABI (include/ml.h) + host driver of the multilevel cycle (Algorithm 1).
+//
+// The host decides only what the paper's cycle needs at cycle granularity (level sizes); every
+// data-dependent decision inside a relaxation (free set, step lengths, early stops) stays on the device in the
+// control block `ml::Ctl`, so one relaxation is a fixed sequence of launches with no host synchronisation, and one
+// ML-cycle costs one stream synchronisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ml.h"
+#include "ml_kernels.cuh"
+#include "ml_select.cuh"
+
+using namespace ml;
+
+namespace {
+
+constexpr int SM_COUNT = 148;
+constexpr int GRID_CAP = SM_COUNT * 4;
+constexpr int TRACE_CAP = 1 << 16;
+constexpr int NV_MAX = 96;   // widest reduction payload (doubles per block)
+
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carve {                 // workspace layout; base == nullptr -> sizing only
+    char* base;
+    size_t off = 0;
+    template <class T> T* take(size_t count) {
+        size_t o = off;
+        off = align_up(off + std::max<size_t>(count, 1) * sizeof(T));
+        return base ? reinterpret_cast<T*>(base + o) : nullptr;
+    }
+};
+
+struct UnitsMem { int4* u; double2* part; int* hcnt; int cap, hcap; };
+
+}  // namespace
+
+struct ml_ctx {
+    ml_data X;
+    double lam;
+    cudaStream_t st;
+    char* ws;
+    size_t ws_bytes;
+    Prm P;
+    ASet fine, coarse;
+    Ctl* ctl;
+    SelState* sel;
+    TraceRow* trace;
+    double2* hres;
+    int* lvl;          // level lists
+    size_t lvl_cap;
+    unsigned char* lev;
+    int* emit_cnt;
+    UnitsMem um[4];    // 0: all columns, 1: C list, 2: free set A, 3: rows
+    int Gr, Gc;
+    int gA, gM, gSeg, gHeavy;
+    long long npos;
+    long long launches = 0;
+    std::string err;
+    Ctl h;             // host mirror of the control block
+};
+
+namespace {
+
+void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
+    const size_t nn = (size_t)n, mm = (size_t)m;
+    const size_t ntile_n = (nn + TILE - 1) / TILE, ntile_m = (mm + TILE - 1) / TILE;
+    const size_t ucap = (size_t)(nnz / CHUNK + nnz / SPLIT + 64);
+    const size_t hcap = (size_t)(nnz / SPLIT + 64);
+    Ctl* ctl = cv.take<Ctl>(1);
+    SelState* sel = cv.take<SelState>(1);
+    TraceRow* trace = cv.take<TraceRow>(TRACE_CAP);
+    double* w = cv.take<double>(nn);
+    uint32_t* wbits = cv.take<uint32_t>((nn + 31) / 32 + 1);
+    double* z = cv.take<double>(mm);
+    double2* rD = cv.take<double2>(mm);
+    double* Xd = cv.take<double>(mm);
+    double* Xs = cv.take<double>(mm);
+    double* sv = cv.take<double>(mm);
+    double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
+    double2* tilepart = cv.take<double2>(ntile_n + 1);
+    unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
+    double2* hres = cv.take<double2>(std::max(nn, mm));
+    ASet fine, coarse;
+    fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
+    coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
+    double* d = cv.take<double>(nn);
+    double* Hd = cv.take<double>(nn);
+    double* s = cv.take<double>(nn);
+    double* Hs = cv.take<double>(nn);
+    double* u = cv.take<double>(nn);
+    fine.d = coarse.d = d; fine.Hd = coarse.Hd = Hd; fine.s = coarse.s = s; fine.Hs = coarse.Hs = Hs; fine.u = coarse.u = u;
+    size_t lvl_cap = 2 * nn + 2 * SEL_LMAX + 64;
+    int* lvl = cv.take<int>(lvl_cap);
+    unsigned char* lev = cv.take<unsigned char>(nn);
+    int* emit_cnt = cv.take<int>((ntile_n + 1) * SEL_LMAX);
+    UnitsMem um[4];
+    for (int k = 0; k < 4; ++k) {
+        um[k].u = cv.take<int4>(ucap);
+        um[k].part = cv.take<double2>(ucap);
+        um[k].hcnt = cv.take<int>(hcap);
+        um[k].cap = (int)std::min<size_t>(ucap, 0x7fffffff);
+        um[k].hcap = (int)hcap;
+    }
+    if (!c) return;
+    c->ctl = ctl; c->sel = sel; c->trace = trace; c->hres = hres;
+    c->lvl = lvl; c->lvl_cap = lvl_cap; c->lev = lev; c->emit_cnt = emit_cnt;
+    c->fine = fine; c->coarse = coarse;
+    for (int k = 0; k < 4; ++k) c->um[k] = um[k];
+    Prm& P = c->P;
+    P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv;
+    P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
+}
+
+int pick_G(double mean_len) {
+    if (mean_len < 12) return 4;
+    if (mean_len < 48) return 8;
+    if (mean_len < 160) return 16;
+    return 32;
+}
+
+Units units_of(ml_ctx* c, int slot) {
+    Units U;
+    U.u = c->um[slot].u;
+    U.part = c->um[slot].part;
+    U.hcnt = c->um[slot].hcnt;
+    U.cap = c->um[slot].cap;
+    U.n = c->ctl ? &c->ctl->units_n[slot] : nullptr;
+    U.h = c->ctl ? &c->ctl->units_h[slot] : nullptr;
+    return U;
+}
+
+Seg seg_rows(ml_ctx* c) { return Seg{c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, c->X.nnz, nullptr, c->hres}; }
+Seg seg_cols(ml_ctx* c, const int* list) { return Seg{c->X.csc_colptr, c->X.csc_row, c->X.csc_val, c->X.nnz, list, c->hres}; }
+
+#define ML_LAUNCH(c, kernel, grid, ...)                                                        \
+    do {                                                                                       \
+        kernel<<<(grid), ML_NT, 0, (c)->st>>>(__VA_ARGS__);                                   \
+        (c)->launches++;                                                                       \
+    } while (0)
+
+#define ML_DISPATCH_G(Gv, BODY)                                 \
+    switch (Gv) {                                               \
+        case 4: { constexpr int GG = 4; BODY; } break;          \
+        case 8: { constexpr int GG = 8; BODY; } break;          \
+        case 16: { constexpr int GG = 16; BODY; } break;        \
+        default: { constexpr int GG = 32; BODY; } break;        \
+    }
+
+ml_status cuda_fail(ml_ctx* c, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return ML_OK;
+    if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return ML_E_CUDA;
+}
+
+ml_status sync_ctl(ml_ctx* c) {
+    cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st);
+    cudaError_t e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) { c->err = std::string("sync: ") + cudaGetErrorString(e); return ML_E_CUDA; }
+    return cuda_fail(c, "sync");
+}
+
+// ------------------------------------------------------------------ small helper kernels
+__global__ void k_init_rows(Prm P, int m) {   // w = 0: z = 0, r = -y/2, D = 1/4, L = m log 2
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
+        P.z[i] = 0.0;
+        RowState s = row_state(0.0, (double)P.y[i]);
+        P.rD[i] = make_double2(s.r, s.D);
+        P.Xs[i] = 0.0;
+        P.Xd[i] = 0.0;
+    }
+}
+__global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* npos) {
+    int bad = 0;
+    unsigned long long pos = 0;
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
+        bad |= (y[i] != 1 && y[i] != -1);
+        pos += (y[i] == 1);
+    }
+    if (bad) atomicOr(&ctl->bad_y, 1);
+    pos = (unsigned long long)warp_sum_ll((long long)pos);
+    if ((threadIdx.x & 31) == 0 && pos) atomicAdd(npos, pos);
+}
+// support bitmap, |supp| and ||w||_1 from w (deterministic: per-block partials + last block)
+__global__ void __launch_bounds__(ML_NT) k_w_stats(Prm P, int n) {
+    __shared__ double sm[3 * ML_NW + 3];
+    Red<2> r;
+    r.zero();
+    const int nwords = (n + 31) / 32;
+    for (int k = blockIdx.x * ML_NT + threadIdx.x; k < nwords; k += gridDim.x * ML_NT) {
+        uint32_t b = 0;
+        for (int q = 0; q < 32; ++q) {
+            const int j = k * 32 + q;
+            if (j < n) {
+                const double v = P.w[j];
+                if (v != 0.0) { b |= 1u << q; r.s[0] += 1.0; r.s[1] += fabs(v); }
+            }
+        }
+        P.wbits[k] = b;
+    }
+    if (grid_reduce(r, P.part, &P.ctl->red_ctr[7], sm)) {
+        if (threadIdx.x == 0) { P.ctl->nS = (int)r.s[0]; P.ctl->l1 = r.s[1]; }
+    }
+}
+__global__ void k_get_rows(Prm P, int m, double* z, double* r, double* D) {
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
+        if (z) z[i] = P.z[i];
+        if (r) r[i] = P.rD[i].x;
+        if (D) D[i] = P.rD[i].y;
+    }
+}
+__global__ void k_dmul(Prm P, int m) {   // sv = D o Xs (hessvec)
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) P.sv[i] = P.rD[i].y * P.Xs[i];
+}
+__global__ void k_set_C(Ctl* ctl, int nC, int slot) {
+    ctl->nC = nC;
+    ctl->units_n[slot] = 0;
+    ctl->units_h[slot] = 0;
+}
+// ml_shrink_linesearch preparation: the restriction C becomes the free set of a one-off relaxation
+__global__ void k_ls_prep(Prm P, ASet AS, const int* C, int nC, const double* g, const double* h, const double* dC) {
+    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nC; p += gridDim.x * ML_NT) {
+        const int j = C ? C[p] : p;
+        const double w = P.w[j];
+        AS.A[p] = j;
+        AS.gA[p] = g[p];
+        AS.wA[p] = w;
+        if (dC) AS.d[p] = dC[p];
+        else {
+            const double hh = h[p] + P.eps_h;
+            AS.d[p] = soft(w - g[p] / hh, P.lam / hh) - w;   // Eq. 5 with D = diag(h) + eps_h
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ctl* c = P.ctl;
+        c->nA = nC; c->nC = nC; c->skip = 0; c->ls_ok = 0; c->napply = 1; c->outcome = OUT_NOSTEP; c->level = -1;
+        c->F_before = c->F;
+    }
+}
+
+// ------------------------------------------------------------------ launch sequences
+void launch_units_build(ml_ctx* c, int slot, const int* list, int nlist_host) {
+    Units U = units_of(c, slot);
+    const int grid = std::max(1, std::min(GRID_CAP, (nlist_host + ML_NT - 1) / ML_NT));
+    ML_LAUNCH(c, k_units_build, grid, c->X.csc_colptr, list, (const int*)nullptr, nlist_host, U);
+}
+
+// A1: heavy rows, then the light row kernel with the fused epilogue
+void launch_margins(ml_ctx* c) {
+    Seg S = seg_rows(c);
+    ML_LAUNCH(c, (k_heavy<OpMargin, false>), c->gHeavy, S, units_of(c, 3), OpMargin{c->P.w, c->P.wbits},
+              (const double*)nullptr, (double*)nullptr, (const int*)nullptr, (const int*)nullptr, &c->ctl->nnz_touched);
+    const int grid = std::max(1, std::min(GRID_CAP, (int)((c->X.m + TILE - 1) / TILE)));
+    ML_DISPATCH_G(c->Gr, ML_LAUNCH(c, k_margins<GG>, grid, c->P, S));
+}
+
+// A2 + A3 over C (list == nullptr: all columns, finest) into the ASet
+void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool finest) {
+    Seg S = seg_cols(c, list);
+    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
+              (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, &c->ctl->nnz_touched);
+    const int grid = std::max(1, std::min(GRID_CAP, (nC_host + TILE - 1) / TILE));
+    if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, units_of(c, 2))); }
+    else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2))); }
+}
+
+// X_A coef scatter into out (light + heavy), skipping on the relaxation flags
+void launch_scatter(ml_ctx* c, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
+                    double* out, const int* skip, const int* skip2) {
+    Seg S = seg_cols(c, list);
+    ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, out, skip, skip2,
+              &c->ctl->nnz_touched);
+    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, out, skip, skip2,
+                                   &c->ctl->nnz_touched));
+}
+
+// out = X_C^T v (+ eps s)
+void launch_gather_dot(ml_ctx* c, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
+                       double* out, const double* s, double eps, const int* skip, const int* skip2) {
+    Seg S = seg_cols(c, list);
+    ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
+              (double*)nullptr, skip, skip2, &c->ctl->nnz_touched);
+    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
+                                   (double*)nullptr, s, eps, skip, skip2, &c->ctl->nnz_touched));
+}
+
+// R3-R18 on the free set in AS (its gather already ran): K inner iterations, outer line search, update.
+void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
+    Ctl* ctl = c->ctl;
+    const int nblkA = c->gA;
+    for (int it = 0; it < K; ++it) {
+        const bool pcd = !inner_cg || it == 0;
+        if (pcd) ML_LAUNCH(c, k_pcd_dir, c->gA, c->P, AS, it);
+        else {
+            ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
+            ML_LAUNCH(c, k_cg_s, c->gA, c->P, AS);
+        }
+        launch_scatter(c, AS.A, 2, &ctl->nA, 0, AS.s, c->P.Xs, &ctl->skip, &ctl->inner_stop);
+        ML_LAUNCH(c, k_mpass, c->gM, c->P, pcd ? 1 : 0);
+        const int have_hs = it < K - 1;
+        if (have_hs)
+            launch_gather_dot(c, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip, &ctl->inner_stop);
+        ML_LAUNCH(c, k_apply, nblkA + c->gM, c->P, AS, it, have_hs, nblkA);
+    }
+    ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
+    ML_LAUNCH(c, k_outer_ls<ML_MAXLS - 4>, nblkA + c->gM, c->P, AS, 4, nblkA);
+    ML_LAUNCH(c, k_update, nblkA + c->gM, c->P, AS, nblkA);
+    ML_LAUNCH(c, k_relax_end, 1, c->P);
+}
+
+void set_params(ml_ctx* c, const ml_solve_opts* o) {
+    Prm& P = c->P;
+    P.eps_h = o->eps_h;
+    P.sigma_in = o->sigma_in;
+    P.sigma_out = o->sigma_out;
+    P.beta_ls = o->beta;
+    P.tol = o->tol_kkt;
+    P.eta = o->eta;
+    P.max_ls = std::max(1, std::min(o->max_ls, ML_MAXLS));
+    P.inner_cg = o->inner_cg;
+}
+
+// level sizes (P:194, P:602 via P:798; DESIGN section 3 S9-S10): k[0] = n, returns L
+int level_sizes(int64_t nAf, int64_t nS, int64_t n, std::vector<int64_t>& k) {
+    k.assign(1, n);
+    int64_t k1 = std::max<int64_t>((nAf + 1) / 2, nS);
+    if (k1 >= n) return 0;
+    k.push_back(k1);
+    while (k.back() != nS && (int)k.size() < SEL_LMAX + 1) k.push_back(std::max<int64_t>((k.back() + 1) / 2, nS));
+    return (int)k.size() - 1;
+}
+
+// A8: radix select + emission of C_1..C_L into c->lvl (offsets returned)
+void launch_select(ml_ctx* c, SelIn in, int nin_host, int L, const std::vector<int64_t>& targets, int* out,
+                   const std::vector<int64_t>& loff) {
+    I64x32 T{}, O{};
+    for (int l = 0; l < L; ++l) { T.v[l] = targets[l]; O.v[l] = loff[l]; }
+    // targets / offsets travel as kernel arguments (no host->device copies)
+    const int grid = std::max(1, std::min(GRID_CAP, (nin_host + ML_NT - 1) / ML_NT));
+    ML_LAUNCH(c, k_sel_init_v, 1, c->sel, L, T);
+    for (int d = 0; d < 12; ++d) ML_LAUNCH(c, k_sel_pass, grid, in, c->sel, d);
+    ML_LAUNCH(c, k_sel_mark, grid, in, c->sel);
+    ML_LAUNCH(c, k_emit_count, grid, in, L, c->emit_cnt);
+    ML_LAUNCH(c, k_emit_scan, L, in, L, c->emit_cnt);
+    ML_LAUNCH(c, k_emit_write_v, grid, in, L, c->emit_cnt, out, O);
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+void ml_default_opts(ml_solve_opts* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->tol_kkt = 1e-6;
+    o->max_cycles = 1000;
+    o->nu = 1;
+    o->nu_c = 5;
+    o->K_fine = 1;
+    o->K_mid = 3;
+    o->K_coarse = 10;
+    o->sigma_out = 1e-2;
+    o->sigma_in = 1e-2;
+    o->beta = 0.5;
+    o->max_ls = 40;
+    o->eps_h = 1e-12;
+    o->multilevel = 1;
+    o->inner_cg = 1;
+    o->eta = 0.0;
+}
+
+size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz) {
+    if (m < 1 || n < 1 || nnz < 0) return 0;
+    Carve cv{nullptr};
+    carve_all(cv, nullptr, m, n, nnz);
+    return cv.off + 256;
+}
+
+const char* ml_status_str(ml_status s) {
+    switch (s) {
+        case ML_OK: return "ok";
+        case ML_E_INVAL: return "invalid argument";
+        case ML_E_CUDA: return "CUDA error";
+        case ML_E_WORKSPACE: return "workspace too small";
+        case ML_E_STAGNATION: return "line search stagnation";
+        case ML_E_NOT_CONVERGED: return "not converged";
+        case ML_E_CONTRACT: return "objective increased (contract violation)";
+    }
+    return "unknown";
+}
+
+const char* ml_last_error(const ml_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int64_t ml_kernel_launches(const ml_ctx* c) { return c ? c->launches : 0; }
+
+ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws, size_t ws_bytes, ml_ctx** out) {
+    if (!X || !out) return ML_E_INVAL;
+    *out = nullptr;
+    if (X->m < 1 || X->n < 1 || X->nnz < 0 || X->nnz >= 2147483647LL || X->m >= 2147483647LL || X->n >= 2147483647LL)
+        return ML_E_INVAL;
+    if (!(lambda > 0.0) || !std::isfinite(lambda)) return ML_E_INVAL;
+    if (!X->csr_rowptr || !X->csc_colptr || !X->y || (X->nnz > 0 && (!X->csr_col || !X->csr_val || !X->csc_row || !X->csc_val)))
+        return ML_E_INVAL;
+    const size_t need = ml_workspace_bytes(X->m, X->n, X->nnz);
+    if (!ws || ws_bytes < need) return ML_E_WORKSPACE;
+    ml_ctx* c = new ml_ctx();
+    c->X = *X;
+    c->lam = lambda;
+    c->st = (cudaStream_t)cuda_stream;
+    c->ws = (char*)align_up((size_t)ws);
+    c->ws_bytes = ws_bytes;
+    Carve cv{c->ws};
+    carve_all(cv, c, X->m, X->n, X->nnz);
+    Prm& P = c->P;
+    P.m = (int)X->m;
+    P.n = (int)X->n;
+    P.y = X->y;
+    P.lam = lambda;
+    ml_solve_opts o;
+    ml_default_opts(&o);
+    set_params(c, &o);
+    c->Gr = pick_G((double)X->nnz / (double)X->m);
+    c->Gc = pick_G((double)X->nnz / (double)X->n);
+    c->gA = std::max(1, std::min(GRID_CAP, (int)((X->n + ML_NT - 1) / ML_NT)));
+    c->gM = std::max(1, std::min(GRID_CAP, (int)((X->m + ML_NT - 1) / ML_NT)));
+    c->gSeg = std::max(1, std::min(GRID_CAP, (int)((X->n + ML_NT - 1) / ML_NT)));
+    c->gHeavy = std::max(1, std::min(GRID_CAP, (int)((X->nnz / CHUNK + X->nnz / SPLIT + 8) / ML_NW + 1)));
+    // zero the control block, trace, bitmap, iterate and the heavy-unit counters
+    cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st);
+    cudaMemsetAsync(P.w, 0, sizeof(double) * X->n, c->st);
+    cudaMemsetAsync(P.wbits, 0, sizeof(uint32_t) * ((X->n + 31) / 32 + 1), c->st);
+    cudaMemsetAsync(P.status, 0, sizeof(unsigned long long) * (std::max(X->n, X->m) / TILE + 2), c->st);
+    for (int k = 0; k < 4; ++k) cudaMemsetAsync(c->um[k].hcnt, 0, sizeof(int) * c->um[k].hcap, c->st);
+    Ctl init;
+    std::memset(&init, 0, sizeof(init));
+    init.trace_cap = TRACE_CAP;
+    init.L = (double)X->m * std::log(2.0);
+    init.F = init.L;
+    init.cg_restart = 1;
+    cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
+    unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
+    ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);
+    ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
+    // static heavy schedules: all columns (slot 0) and all rows (slot 3)
+    {
+        Units U = units_of(c, 0);
+        ML_LAUNCH(c, k_units_build, c->gSeg, X->csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U);
+        Units R = units_of(c, 3);
+        ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R);
+    }
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) { *out = c; return s; }
+    if (c->h.bad_y) { delete c; return ML_E_INVAL; }
+    c->npos = (long long)c->h.dsupp;
+    long long zero = 0;
+    cudaMemcpyAsync(&c->ctl->dsupp, &zero, sizeof(long long), cudaMemcpyHostToDevice, c->st);
+    if (c->h.units_n[0] > c->um[0].cap || c->h.units_n[3] > c->um[3].cap) { c->err = "unit capacity"; delete c; return ML_E_WORKSPACE; }
+    s = sync_ctl(c);
+    *out = c;
+    return s;
+}
+
+ml_status ml_destroy(ml_ctx* c) {
+    if (!c) return ML_E_INVAL;
+    cudaStreamSynchronize(c->st);
+    delete c;
+    return ML_OK;
+}
+
+ml_status ml_set_w(ml_ctx* c, const double* w_dev) {
+    if (!c || !w_dev) return ML_E_INVAL;
+    cudaMemcpyAsync(c->P.w, w_dev, sizeof(double) * c->X.n, cudaMemcpyDeviceToDevice, c->st);
+    ML_LAUNCH(c, k_w_stats, c->gA, c->P, (int)c->X.n);
+    return cuda_fail(c, "ml_set_w");
+}
+
+ml_status ml_get_w(ml_ctx* c, double* w_dev) {
+    if (!c || !w_dev) return ML_E_INVAL;
+    cudaMemcpyAsync(w_dev, c->P.w, sizeof(double) * c->X.n, cudaMemcpyDeviceToDevice, c->st);
+    return cuda_fail(c, "ml_get_w");
+}
+
+ml_status ml_get_rows(ml_ctx* c, double* z, double* r, double* D) {
+    if (!c) return ML_E_INVAL;
+    ML_LAUNCH(c, k_get_rows, c->gM, c->P, (int)c->X.m, z, r, D);
+    return cuda_fail(c, "ml_get_rows");
+}
+
+static ml_status check_list(ml_ctx* c, const int32_t* C, int64_t nC) {
+    if (!C) return nC == c->X.n ? ML_OK : ML_E_INVAL;
+    if (nC < 0 || nC > c->X.n) return ML_E_INVAL;
+    return ML_OK;
+}
+
+// gather g_C / h_C over an explicit list (API path)
+static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double* h_C) {
+    int slot = C ? 1 : 0;
+    if (C) {
+        ML_LAUNCH(c, k_set_C, 1, c->ctl, nC, 1);
+        launch_units_build(c, 1, C, nC);
+    }
+    Seg S = seg_cols(c, C);
+    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, slot), OpGH{c->P.rD}, (const double*)nullptr,
+              (double*)nullptr, (const int*)nullptr, (const int*)nullptr, &c->ctl->nnz_touched);
+    const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
+    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,
+                                   g_C, h_C, (const double*)nullptr, 0.0, (const int*)nullptr, (const int*)nullptr,
+                                   &c->ctl->nnz_touched));
+}
+
+ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host, double* g_C, double* h_C) {
+    if (!c || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    launch_margins(c);
+    if ((g_C || h_C) && nC > 0) api_gather(c, C, (int)nC, g_C, h_C);
+    if (F_host) {
+        ml_status s = sync_ctl(c);
+        if (s != ML_OK) return s;
+        *F_host = c->h.F;
+    }
+    return cuda_fail(c, "ml_eval_f_grad");
+}
+
+ml_status ml_diag_hess(ml_ctx* c, const int32_t* C, int64_t nC, double* h_C) {
+    if (!c || !h_C || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (nC > 0) api_gather(c, C, (int)nC, nullptr, h_C);
+    return cuda_fail(c, "ml_diag_hess");
+}
+
+ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C, double* Hv_C) {
+    if (!c || !v_C || !Hv_C || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (nC == 0) return ML_OK;
+    const int slot = C ? 1 : 0;
+    if (C) {
+        ML_LAUNCH(c, k_set_C, 1, c->ctl, (int)nC, 1);
+        launch_units_build(c, 1, C, (int)nC);
+    }
+    cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
+    launch_scatter(c, C, slot, nullptr, (int)nC, v_C, c->P.Xs, nullptr, nullptr);   // X_C v
+    ML_LAUNCH(c, k_dmul, c->gM, c->P, (int)c->X.m);                                   // D o X_C v
+    launch_gather_dot(c, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr);
+    cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
+    return cuda_fail(c, "ml_hessvec");
+}
+
+ml_status ml_shrink_linesearch(ml_ctx* c, const int32_t* C, int64_t nC, const double* g_C, const double* h_C,
+                               const double* d_C, const double* Xd, const ml_solve_opts* o, double* alpha_host,
+                               double* F_new_host) {
+    if (!c || !g_C || (!d_C && !h_C) || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    ml_solve_opts def;
+    ml_default_opts(&def);
+    set_params(c, o ? o : &def);
+    ASet& AS = c->coarse;
+    const int n = (int)nC;
+    ML_LAUNCH(c, k_ls_prep, c->gA, c->P, AS, C, n, g_C, h_C, d_C);
+    if (Xd) cudaMemcpyAsync(c->P.Xd, Xd, sizeof(double) * c->X.m, cudaMemcpyDeviceToDevice, c->st);
+    else {
+        const int slot = C ? 1 : 0;
+        if (C) {
+            ML_LAUNCH(c, k_set_C, 1, c->ctl, n, 1);
+            launch_units_build(c, 1, C, n);
+        }
+        cudaMemsetAsync(c->P.Xd, 0, sizeof(double) * c->X.m, c->st);
+        launch_scatter(c, C, slot, nullptr, n, AS.d, c->P.Xd, nullptr, nullptr);
+    }
+    const int nblkA = c->gA;
+    ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
+    ML_LAUNCH(c, k_outer_ls<ML_MAXLS - 4>, nblkA + c->gM, c->P, AS, 4, nblkA);
+    ML_LAUNCH(c, k_update, nblkA + c->gM, c->P, AS, nblkA);
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    if (alpha_host) *alpha_host = c->h.ls_ok ? c->h.alpha : 0.0;
+    if (F_new_host) *F_new_host = c->h.F;
+    if (c->h.outcome == OUT_STAGNATION) return ML_E_STAGNATION;
+    return ML_OK;
+}
+
+ml_status ml_select_coarse(ml_ctx* c, const double* g, int64_t k_total, int32_t* C_out, int64_t* nC_out_host) {
+    if (!c || !g || !C_out) return ML_E_INVAL;
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    const int64_t n = c->X.n, nS = c->h.nS;
+    int64_t T = std::max<int64_t>(0, std::min<int64_t>(k_total - nS, n - nS));
+    SelIn in{nullptr, g, nullptr, (int)n, c->P.w, c->lev};
+    std::vector<int64_t> targets{T}, loff{0};
+    launch_select(c, in, (int)n, 1, targets, C_out, loff);
+    if (nC_out_host) *nC_out_host = nS + T;
+    return cuda_fail(c, "ml_select_coarse");
+}
+
+ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
+    if (!c || !rep) return ML_E_INVAL;
+    ml_solve_opts o;
+    if (o_in) o = *o_in; else ml_default_opts(&o);
+    if (o.K_fine < 1 || o.K_mid < 1 || o.K_coarse < 1 || o.nu < 1 || o.nu_c < 1) return ML_E_INVAL;
+    set_params(c, &o);
+    std::memset(rep, 0, sizeof(*rep));
+    const long long launches0 = c->launches;
+    const int n = (int)c->X.n;
+    Ctl* ctl = c->ctl;
+    // S1: w = 0, z = 0 (per-sample state refreshed by the first margins pass)
+    cudaMemsetAsync(c->P.w, 0, sizeof(double) * n, c->st);
+    cudaMemsetAsync(c->P.wbits, 0, sizeof(uint32_t) * ((n + 31) / 32 + 1), c->st);
+    {
+        Ctl h0;
+        ml_status s = sync_ctl(c);
+        if (s != ML_OK) return s;
+        h0 = c->h;
+        h0.nS = 0; h0.l1 = 0.0; h0.ntrace = 0; h0.nnz_touched = 0; h0.level_conv = 0; h0.skip = 0;
+        h0.vmax_bits = 0ull; h0.dsupp = 0;
+        cudaMemcpyAsync(ctl, &h0, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
+    }
+    auto eval_and_fine_relax = [&](bool relax) {
+        // S2/S15 EVAL_ALL (margins from scratch + full gather with the free set), then S4/S17 RELAX(C0, E)
+        ML_LAUNCH(c, k_relax_begin, 1, c->P, 1, 0, (const int*)nullptr, n, 1, 1);
+        launch_margins(c);
+        launch_gather_free(c, nullptr, n, c->fine, true);
+        if (relax) {
+            launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
+            for (int it = 1; it < o.nu; ++it) {
+                ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1, 1);
+                launch_gather_free(c, nullptr, n, c->fine, true);
+                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
+            }
+        }
+    };
+    eval_and_fine_relax(true);
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    const double v1_0 = c->h.v1;
+    bool converged = c->h.vmax / c->lam <= o.tol_kkt;
+    int cycle = 0;
+    int64_t max_supp = c->h.nS;
+    std::vector<int64_t> k;
+    if (!converged) {
+        for (cycle = 1; cycle <= o.max_cycles; ++cycle) {
+            const int64_t nS = c->h.nS, nAf = c->h.nAf;
+            if (o.multilevel && nS > 0) {
+                const int L = level_sizes(nAf, nS, n, k);
+                if (L >= 1) {
+                    std::vector<int64_t> targets(L), loff(L);
+                    int64_t acc = 0;
+                    for (int l = 1; l <= L; ++l) { targets[l - 1] = k[l] - nS; loff[l - 1] = acc; acc += k[l]; }
+                    SelIn in{c->fine.A, c->fine.gA, &ctl->nAf, 0, c->P.w, c->lev};
+                    launch_select(c, in, (int)nAf, L, targets, c->lvl, loff);
+                    for (int l = L; l >= 1; --l) {
+                        const int* Cl = c->lvl + loff[l - 1];
+                        const int nCl = (int)k[l];
+                        ML_LAUNCH(c, k_set_C, 1, ctl, nCl, 1);
+                        launch_units_build(c, 1, Cl, nCl);
+                        const int reps = (l == L) ? o.nu_c : o.nu;
+                        const int K = (l == L) ? o.K_coarse : o.K_mid;
+                        for (int r = 0; r < reps; ++r) {
+                            ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1, 0);
+                            launch_gather_free(c, Cl, nCl, c->coarse, false);
+                            launch_relax_body(c, c->coarse, K, o.inner_cg);
+                        }
+                    }
+                }
+            }
+            eval_and_fine_relax(true);
+            s = sync_ctl(c);
+            if (s != ML_OK) return s;
+            max_supp = std::max<int64_t>(max_supp, c->h.nS);
+            if (c->h.vmax / c->lam <= o.tol_kkt) { converged = true; break; }
+        }
+    }
+    // the returned w is the evaluated one (DESIGN Q17): the last finest relaxation was skipped on convergence.
+    // On NOT_CONVERGED, re-evaluate so that F / kappa describe the returned w.
+    if (!converged) {
+        eval_and_fine_relax(false);
+        s = sync_ctl(c);
+        if (s != ML_OK) return s;
+    }
+    const Ctl& h = c->h;
+    rep->F = h.F;
+    rep->vinf = h.vmax;
+    rep->kappa = h.vmax / c->lam;
+    rep->v1 = h.v1;
+    const long long minpm = std::min<long long>(c->npos, c->X.m - c->npos);
+    rep->paper_ratio = (v1_0 > 0 && minpm > 0) ? h.v1 / (v1_0 * (double)minpm / (double)c->X.m) : 0.0;
+    rep->cycles = std::min(cycle, o.max_cycles);
+    rep->nnz_w = h.nS;
+    rep->max_supp = std::max<int64_t>(max_supp, h.nS);
+    rep->nnz_touched = h.nnz_touched;
+    // relaxations per level from the device trace
+    const int nt = std::min(h.ntrace, TRACE_CAP);
+    std::vector<TraceRow> tr(nt);
+    if (nt) cudaMemcpy(tr.data(), c->trace, sizeof(TraceRow) * nt, cudaMemcpyDeviceToHost);
+    for (const TraceRow& r : tr) {
+        rep->relax_per_level[std::min(std::max(r.level, 0), 31)]++;
+        if (r.F_after > r.F_before + 1e-12 * std::fabs(r.F_before)) rep->status = ML_E_CONTRACT;
+    }
+    for (int l = 0; l < 32; ++l) rep->relaxations += rep->relax_per_level[l];
+    rep->kernel_launches = c->launches - launches0;
+    if (rep->status == 0 && !converged) rep->status = ML_E_NOT_CONVERGED;
+    ml_status fin = cuda_fail(c, "ml_solve");
+    if (fin != ML_OK) return fin;
+    return (ml_status)rep->status;
+}
+
+// trace access for tests (not part of the paper's call set)
+int64_t ml_trace(ml_ctx* c, void* rows_host, int64_t cap) {
+    if (!c) return -1;
+    if (sync_ctl(c) != ML_OK) return -1;
+    const int nt = std::min(c->h.ntrace, TRACE_CAP);
+    const int k = (int)std::min<int64_t>(nt, cap);
+    if (rows_host && k) cudaMemcpy(rows_host, c->trace, sizeof(TraceRow) * k, cudaMemcpyDeviceToHost);
+    return nt;
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// ml_common.cuh — device helpers for libml (sm_100a).
+//
+// Reductions are fixed-shape trees (warp shuffles -> shared memory -> one "last block" that sums the per-block
+// partials in block order), so every floating-point result is bitwise reproducible for a given launch shape.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef ML_NT
+#define ML_NT 256          // threads per block for every kernel
+#endif
+#define ML_NW (ML_NT / 32)
+#define ML_MAXLS 40        // line-search trials evaluated (Eq. 4 backtracking, DESIGN Q7)
+
+namespace ml {
+
+// ------------------------------------------------------------------ loads
+// Streaming loads of X (values / indices): read-only path, no L1 allocation.
+__device__ __forceinline__ int4 ld_stream_i4(const int* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+// L2-coherent load (bypasses L1) for data written by other blocks of the same launch.
+template <class T> __device__ __forceinline__ T ld_cg(const T* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------------ warp / group reductions
+template <int G> __device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------ block + grid reductions
+// A reduction payload: NS sums, NM maxima (non-negative values), NN minima.
+template <int NS, int NM = 0, int NN = 0> struct Red {
+    double s[NS > 0 ? NS : 1];
+    double mx[NM > 0 ? NM : 1];
+    double mn[NN > 0 ? NN : 1];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) mx[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NN; ++k) mn[k] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    }
+    static constexpr int NV = NS + NM + NN;
+};
+
+// Block-wide reduction; every thread returns with the block totals.  smem: NV * ML_NW doubles + NV.
+template <int NS, int NM, int NN>
+__device__ __forceinline__ void block_reduce(Red<NS, NM, NN>& r, double* sm) {
+    constexpr int NV = Red<NS, NM, NN>::NV;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) { double v = warp_sum(r.s[k]); if (lane == 0) sm[k * ML_NW + wid] = v; }
+#pragma unroll
+    for (int k = 0; k < NM; ++k) { double v = warp_max(r.mx[k]); if (lane == 0) sm[(NS + k) * ML_NW + wid] = v; }
+#pragma unroll
+    for (int k = 0; k < NN; ++k) { double v = warp_min(r.mn[k]); if (lane == 0) sm[(NS + NM + k) * ML_NW + wid] = v; }
+    __syncthreads();
+    if (wid == 0) {
+        for (int k = 0; k < NV; ++k) {
+            double v = (lane < ML_NW) ? sm[k * ML_NW + lane] : (k < NS ? 0.0 : (k < NS + NM ? 0.0 : __longlong_as_double(0x7ff0000000000000LL)));
+            if (k < NS) v = warp_sum(v);
+            else if (k < NS + NM) v = warp_max(v);
+            else v = warp_min(v);
+            if (lane == 0) sm[NV * ML_NW + k] = v;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) r.s[k] = sm[NV * ML_NW + k];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) r.mx[k] = sm[NV * ML_NW + NS + k];
+#pragma unroll
+    for (int k = 0; k < NN; ++k) r.mn[k] = sm[NV * ML_NW + NS + NM + k];
+    __syncthreads();
+}
+
+// Grid-wide reduction through per-block partials and the last-arriving block.  Returns true in exactly one
+// block (the last to arrive); there every thread holds the grid totals.  The last block sums the partials in
+// block-index order with a fixed thread assignment, so the result does not depend on arrival order.
+// part: gridDim.x * NV doubles; ctr: a zeroed counter (reset here for the next launch).
+template <int NS, int NM, int NN>
+__device__ bool grid_reduce(Red<NS, NM, NN>& r, double* part, unsigned* ctr, double* sm) {
+    constexpr int NV = Red<NS, NM, NN>::NV;
+    __shared__ bool s_last;
+    block_reduce(r, sm);
+    if (threadIdx.x == 0) {
+        double* pb = part + (size_t)blockIdx.x * NV;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) pb[k] = r.s[k];
+#pragma unroll
+        for (int k = 0; k < NM; ++k) pb[NS + k] = r.mx[k];
+#pragma unroll
+        for (int k = 0; k < NN; ++k) pb[NS + NM + k] = r.mn[k];
+        __threadfence();
+        unsigned prev = atomicAdd(ctr, 1u);
+        s_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    r.zero();
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += ML_NT) {
+        const double* pb = part + (size_t)b * NV;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) r.s[k] += ld_cg(pb + k);
+#pragma unroll
+        for (int k = 0; k < NM; ++k) r.mx[k] = fmax(r.mx[k], ld_cg(pb + NS + k));
+#pragma unroll
+        for (int k = 0; k < NN; ++k) r.mn[k] = fmin(r.mn[k], ld_cg(pb + NS + NM + k));
+    }
+    block_reduce(r, sm);
+    if (threadIdx.x == 0) *ctr = 0u;
+    return true;
+}
+
+// ------------------------------------------------------------------ per-sample logistic quantities
+// t = y z; e = exp(-|t|); ell = log(1+e^{-t}) = max(-t,0) + log1p(e); q = tau(-t); D = tau(t) tau(-t) = e/(1+e)^2;
+// r = (tau(t) - 1) y = -y q   (stable forms SURVEY App. A.5)
+struct RowState { double r, D, ell; };
+__device__ __forceinline__ RowState row_state(double z, double y) {
+    double t = y * z;
+    double e = exp(-fabs(t));
+    double ope = 1.0 + e;
+    RowState s;
+    s.ell = (t < 0.0 ? -t : 0.0) + log1p(e);
+    double q = (t <= 0.0) ? 1.0 / ope : e / ope;
+    s.r = -y * q;
+    s.D = e / (ope * ope);
+    return s;
+}
+__device__ __forceinline__ double logloss(double t) { return (t < 0.0 ? -t : 0.0) + log1p(exp(-fabs(t))); }
+__device__ __forceinline__ double tau_neg(double t) {   // tau(-t)
+    double e = exp(-fabs(t));
+    return (t <= 0.0) ? 1.0 / (1.0 + e) : e / (1.0 + e);
+}
+// ell(t + delta) - ell(t), term-by-term difference (DESIGN Q26)
+__device__ __forceinline__ double dloss(double t, double delta) {
+    if (fabs(delta) <= 1.0) return log1p(tau_neg(t) * expm1(-delta));
+    return logloss(t + delta) - logloss(t);
+}
+__device__ __forceinline__ double soft(double t, double a) {   // Eq. 6
+    double s = fabs(t) - a;
+    if (s <= 0.0) return 0.0;
+    return t > 0.0 ? s : -s;
+}
+__device__ __forceinline__ double sgn(double x) { return x > 0.0 ? 1.0 : -1.0; }
+
+// non-negative double max via the int64 bit pattern (order-preserving for x >= 0)
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace ml

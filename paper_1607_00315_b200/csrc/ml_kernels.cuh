@@ -1,0 +1,850 @@
+// ml_kernels.cuh — sm_100a kernels of the multilevel proximal-Newton hot path.
+//
+// Every X pass goes through one "segment engine": a segment is a CSR row or a CSC column (restricted to an index
+// list C).  Segments up to SPLIT nonzeros are reduced by a group of G lanes (G = 4..32, chosen per context from
+// the mean segment length) streaming 128-bit vectors of indices and values; longer segments are cut into CHUNK-
+// nonzero units, one warp each, whose partial sums are combined in unit order by the last-arriving warp of the
+// segment (deterministic).  Epilogues (per-sample logistic quantities, free-set compaction with KKT, Hessian-vector
+// outputs) run on the reduced values while they are in shared memory.
+#pragma once
+#include "ml_common.cuh"
+
+namespace ml {
+
+constexpr int SPLIT = 1024;   // segments longer than this go to the heavy (split) path
+constexpr int CHUNK = 2048;   // nonzeros per heavy unit (one warp)
+constexpr int TILE = ML_NT;   // segments per tile
+
+enum { OUT_UPDATED = 0, OUT_CONVERGED = 1, OUT_NOSTEP = 2, OUT_STAGNATION = 3 };
+
+// ------------------------------------------------------------------ device control block
+struct TraceRow { int level, outcome, inner_iters, nA; long long nC; double F_before, F_after, alpha; };
+
+struct Ctl {
+    // relaxation state
+    int nA, skip, level_conv, inner_stop, outcome, napply, cg_restart, snap;
+    int ls_ok, scattered, nS, nAf;
+    int skipped, t_acc;
+    int nC, pad0;
+    const int* Cptr;            // current restriction list (nullptr = all columns)
+    double vmax, v1, l1, L, F, F_before;
+    double beta, alpha, rz, rz_prev, bcg, slope, ss, ps, delta, bk, bq, sHs, Delta, gd, vq;
+    double l1diff_out[ML_MAXLS];
+    // counters
+    unsigned red_ctr[8];
+    unsigned tile_ctr, done_ctr, epoch, pad1;
+    unsigned long long vmax_bits;
+    long long nnz_touched;
+    long long dsupp;
+    int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
+    int ntrace, trace_cap, bad_y, level, it;
+    int pad2[3];
+};
+
+// heavy-segment schedule for one segment list
+struct Units {
+    int4* u;          // {position p, chunk c, heavy ordinal, first unit of p}
+    int* n;           // -> Ctl::units_n[slot]
+    int* h;           // -> Ctl::units_h[slot]
+    double2* part;    // per-unit partials
+    int* hcnt;        // per-heavy-segment arrival counters (kept at 0 between launches)
+    int cap;
+};
+
+// a segment source: rows of CSR or columns of CSC restricted to a list
+struct Seg {
+    const int* ptr;   // rowptr / colptr
+    const int* idx;   // col / row indices
+    const float* val;
+    long long nnz;
+    const int* list;  // positions -> segment ids (nullptr = identity)
+    double2* hres;    // heavy results per position
+};
+
+// ------------------------------------------------------------------ per-element operations
+struct OpMargin {     // z_i = sum_k X_ik w_k, gathers gated by the support bitmap
+    const double* w; const uint32_t* bits;
+    __device__ __forceinline__ void add(double& a0, double&, int c, float v) const {
+        if ((__ldg(bits + (c >> 5)) >> (c & 31)) & 1u) a0 += (double)v * __ldg(w + c);
+    }
+};
+struct OpGH {         // g_j = sum_i X_ij r_i ; h_j = sum_i X_ij^2 D_i
+    const double2* rD;
+    __device__ __forceinline__ void add(double& a0, double& a1, int r, float v) const {
+        double2 q = __ldg(rD + r);
+        double x = (double)v;
+        a0 += x * q.x;
+        a1 += (x * x) * q.y;
+    }
+};
+struct OpDot {        // acc = sum_i X_ij v_i
+    const double* v;
+    __device__ __forceinline__ void add(double& a0, double&, int r, float x) const { a0 += (double)x * __ldg(v + r); }
+};
+
+// Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).
+template <int G, class Op>
+__device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int e, int lane, double& a0, double& a1) {
+    for (int k = (b & ~3) + 4 * lane; k < e; k += 8 * G) {
+        int4 i0, i1 = make_int4(0, 0, 0, 0);
+        float4 v0, v1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int k1 = k + 4 * G;
+        if (k + 4 <= S.nnz) { i0 = ld_stream_i4(S.idx + k); v0 = ld_stream_f4(S.val + k); }
+        else {
+            i0.x = S.idx[k]; v0.x = S.val[k];
+            i0.y = (k + 1 < S.nnz) ? S.idx[k + 1] : 0; v0.y = (k + 1 < S.nnz) ? S.val[k + 1] : 0.f;
+            i0.z = (k + 2 < S.nnz) ? S.idx[k + 2] : 0; v0.z = (k + 2 < S.nnz) ? S.val[k + 2] : 0.f;
+            i0.w = 0; v0.w = 0.f;
+        }
+        const bool has1 = k1 < e;
+        if (has1) {
+            if (k1 + 4 <= S.nnz) { i1 = ld_stream_i4(S.idx + k1); v1 = ld_stream_f4(S.val + k1); }
+            else {
+                i1.x = S.idx[k1]; v1.x = S.val[k1];
+                i1.y = (k1 + 1 < S.nnz) ? S.idx[k1 + 1] : 0; v1.y = (k1 + 1 < S.nnz) ? S.val[k1 + 1] : 0.f;
+                i1.z = (k1 + 2 < S.nnz) ? S.idx[k1 + 2] : 0; v1.z = (k1 + 2 < S.nnz) ? S.val[k1 + 2] : 0.f;
+            }
+        }
+        if (k >= b && k + 3 < e) {
+            op.add(a0, a1, i0.x, v0.x); op.add(a0, a1, i0.y, v0.y);
+            op.add(a0, a1, i0.z, v0.z); op.add(a0, a1, i0.w, v0.w);
+        } else {
+            if (k >= b && k < e) op.add(a0, a1, i0.x, v0.x);
+            if (k + 1 >= b && k + 1 < e) op.add(a0, a1, i0.y, v0.y);
+            if (k + 2 >= b && k + 2 < e) op.add(a0, a1, i0.z, v0.z);
+            if (k + 3 >= b && k + 3 < e) op.add(a0, a1, i0.w, v0.w);
+        }
+        if (has1) {
+            if (k1 + 3 < e) {
+                op.add(a0, a1, i1.x, v1.x); op.add(a0, a1, i1.y, v1.y);
+                op.add(a0, a1, i1.z, v1.z); op.add(a0, a1, i1.w, v1.w);
+            } else {
+                op.add(a0, a1, i1.x, v1.x);
+                if (k1 + 1 < e) op.add(a0, a1, i1.y, v1.y);
+                if (k1 + 2 < e) op.add(a0, a1, i1.z, v1.z);
+            }
+        }
+    }
+}
+
+// One tile of TILE consecutive segment positions; results (a0, a1) land in res[slot] (shared memory).
+// Heavy segments (> SPLIT) are not streamed here: their results come from S.hres, written by k_heavy.
+// Returns (in *s_len) the number of nonzeros of the light segments streamed by this block (accounting).
+template <int G, class Op>
+__device__ __forceinline__ long long seg_tile(const Seg& S, const Op& op, int nseg, int tile, double2* res) {
+    constexpr int NG = ML_NT / G;
+    const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+    long long streamed = 0;
+#pragma unroll 1
+    for (int r = 0; r < G; ++r) {
+        const int slot = r * NG + grp;
+        const int p = tile * TILE + slot;
+        int b = 0, e = 0;
+        bool heavy = false;
+        if (p < nseg) {
+            const int j = S.list ? __ldg(S.list + p) : p;
+            b = __ldg(S.ptr + j);
+            e = __ldg(S.ptr + j + 1);
+            heavy = (e - b) > SPLIT;
+            if (heavy) e = b;
+            else if (lane == 0) streamed += e - b;
+        }
+        double a0 = 0.0, a1 = 0.0;
+        seg_accum<G>(S, op, b, e, lane, a0, a1);
+        a0 = group_sum<G>(a0);
+        a1 = group_sum<G>(a1);
+        if (lane == 0) res[slot] = heavy ? ld_cg(S.hres + p) : make_double2(a0, a1);
+    }
+    return streamed;
+}
+
+// ------------------------------------------------------------------ heavy units
+// Build the heavy-unit schedule of a segment list: every segment longer than SPLIT gets ceil(len/CHUNK) units.
+// Unit order is arbitrary (atomics); results do not depend on it.
+__global__ void k_units_build(const int* __restrict__ ptr, const int* __restrict__ list, const int* nseg_dev, int nseg_host,
+                              Units U) {
+    const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nseg; p += gridDim.x * ML_NT) {
+        const int j = list ? list[p] : p;
+        const int len = ptr[j + 1] - ptr[j];
+        if (len > SPLIT) {
+            const int nch = (len + CHUNK - 1) / CHUNK;
+            const int hs = atomicAdd(U.h, 1);
+            const int base = atomicAdd(U.n, nch);
+            for (int c = 0; c < nch && base + c < U.cap; ++c) U.u[base + c] = make_int4(p, c, hs, base);
+        }
+    }
+}
+
+// One warp per heavy unit.  SCATTER: out[idx] += X * coef[p] (fp64 atomics), else partial sums + in-order
+// combination by the segment's last-arriving warp into S.hres[p].
+template <class Op, bool SCATTER>
+__global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const double* __restrict__ coef, double* out,
+                                                  const int* skip, const int* skip2, long long* nnz_acc) {
+    if ((skip && *skip) || (skip2 && *skip2)) return;
+    const int lane = threadIdx.x & 31;
+    const int nunits = min(*U.n, U.cap);
+    const int gw = (blockIdx.x * ML_NT + threadIdx.x) >> 5, nw = (gridDim.x * ML_NT) >> 5;
+    long long streamed = 0;
+    for (int u = gw; u < nunits; u += nw) {
+        const int4 un = U.u[u];
+        const int p = un.x;
+        const int j = S.list ? __ldg(S.list + p) : p;
+        const int b0 = __ldg(S.ptr + j), e0 = __ldg(S.ptr + j + 1);
+        const int b = b0 + un.y * CHUNK;
+        const int e = min(e0, b + CHUNK);
+        if (SCATTER) {
+            const double cf = coef[p];
+            if (cf == 0.0) continue;
+            if (lane == 0) streamed += e - b;
+            for (int k = b + lane; k < e; k += 32) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
+        } else {
+            if (lane == 0) streamed += e - b;
+            double a0 = 0.0, a1 = 0.0;
+            seg_accum<32>(S, op, b, e, lane, a0, a1);
+            a0 = warp_sum(a0);
+            a1 = warp_sum(a1);
+            int last = 0;
+            if (lane == 0) {
+                U.part[u] = make_double2(a0, a1);
+                __threadfence();
+                const int nch = (e0 - b0 + CHUNK - 1) / CHUNK;
+                last = (atomicAdd(U.hcnt + un.z, 1) == nch - 1);
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence();
+                const int nch = (e0 - b0 + CHUNK - 1) / CHUNK;
+                double s0 = 0.0, s1 = 0.0;
+                for (int c = lane; c < nch; c += 32) { double2 q = ld_cg(U.part + un.w + c); s0 += q.x; s1 += q.y; }
+                s0 = warp_sum(s0);
+                s1 = warp_sum(s1);
+                if (lane == 0) { S.hres[p] = make_double2(s0, s1); U.hcnt[un.z] = 0; }
+            }
+        }
+    }
+    if (nnz_acc) {
+        __shared__ long long sm_nnz[ML_NW];
+        long long v = warp_sum_ll(streamed);
+        if (lane == 0) sm_nnz[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long t = 0;
+            for (int k = 0; k < ML_NW; ++k) t += sm_nnz[k];
+            if (t) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)t);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ parameters shared by the relaxation kernels
+struct Prm {
+    int m, n;
+    const int8_t* y;
+    double lam, eps_h, sigma_in, sigma_out, beta_ls, tol, eta;
+    int max_ls, inner_cg;
+    double* w; uint32_t* wbits; double* z; double2* rD;
+    double* Xd; double* Xs; double* sv;
+    Ctl* ctl;
+    double* part;              // reduction partials
+    double2* tilepart;         // per-tile partials of the compaction kernels
+    unsigned long long* status;// look-back tile status
+    TraceRow* trace;
+};
+// free-set buffers of one relaxation (fine or coarse set)
+struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd; double* s; double* Hs; double* u; };
+
+__device__ __forceinline__ void add_nnz(Ctl* ctl, long long v, long long* sm) {
+    const int lane = threadIdx.x & 31;
+    long long t = warp_sum_ll(v);
+    if (lane == 0) sm[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long s = 0;
+        for (int k = 0; k < ML_NW; ++k) s += sm[k];
+        if (s) atomicAdd((unsigned long long*)&ctl->nnz_touched, (unsigned long long)s);
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ A1: margins (full CSR pass)
+// z = Xw (CSR, support-bitmap-gated gathers of w), then per row: t, ell, r, D; L = sum ell.
+template <int G>
+__global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S) {
+    __shared__ double2 res[TILE];
+    __shared__ double sm[3 * ML_NW + 3];
+    __shared__ long long smn[ML_NW];
+    OpMargin op{P.w, P.wbits};
+    const int ntiles = (P.m + TILE - 1) / TILE;
+    double lsum = 0.0;
+    long long streamed = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        streamed += seg_tile<G>(S, op, P.m, tile, res);
+        __syncthreads();
+        const int i = tile * TILE + threadIdx.x;
+        if (i < P.m) {
+            const double z = res[threadIdx.x].x;
+            const RowState st = row_state(z, (double)P.y[i]);
+            P.z[i] = z;
+            P.rD[i] = make_double2(st.r, st.D);
+            lsum += st.ell;
+        }
+        __syncthreads();
+    }
+    add_nnz(P.ctl, streamed, smn);
+    Red<1> r;
+    r.s[0] = lsum;
+    if (grid_reduce(r, P.part, &P.ctl->red_ctr[0], sm)) {
+        if (threadIdx.x == 0) { P.ctl->L = r.s[0]; P.ctl->F = r.s[0] + P.lam * P.ctl->l1; }
+    }
+}
+
+// ------------------------------------------------------------------ A2 + A3: gather over C with free-set compaction
+// For each position p of C (j = C[p], or p when C is all columns): g_j, h_j; v_j (min-norm subgradient,
+// P:248-256); free flag w_j != 0 or |g_j| > lam (P:459-461 via P:790).  Free columns are compacted IN ORDER into
+// the ASet (A, gA, hA + eps_h, wA) with a decoupled look-back scan over dynamically claimed tiles; heavy free
+// columns get their heavy units appended to UA.  FINEST additionally computes ||w||_1 and sum |v| exactly.
+// The last block to finish: nA, vmax, the convergence decision (R2), counters reset, epoch advance.
+template <int G, bool FINEST>
+__global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Units UA) {
+    __shared__ double2 res[TILE];
+    __shared__ int s_tile, s_excl;
+    __shared__ int s_wcnt[ML_NW];
+    __shared__ double s_red[2 * ML_NW];
+    __shared__ long long smn[ML_NW];
+    __shared__ bool s_last;
+    Ctl* ctl = P.ctl;
+    if (ctl->skip) return;   // (not used at the finest level; coarse relaxations of a converged level)
+    const int nC = S.list ? ctl->nC : P.n;
+    const int ntiles = (nC + TILE - 1) / TILE;
+    const unsigned epoch = ctl->epoch;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    OpGH op{P.rD};
+    long long streamed = 0;
+    double vmax_loc = 0.0;
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= ntiles) break;
+        streamed += seg_tile<G>(S, op, nC, tile, res);
+        __syncthreads();
+        const int p = tile * TILE + threadIdx.x;
+        int j = 0, flag = 0, len = 0;
+        double g = 0.0, h = 0.0, wj = 0.0, av = 0.0;
+        if (p < nC) {
+            j = S.list ? S.list[p] : p;
+            g = res[threadIdx.x].x;
+            h = res[threadIdx.x].y;
+            if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
+            const double v = (wj != 0.0) ? g + P.lam * sgn(wj) : soft(g, P.lam);
+            av = fabs(v);
+            flag = (wj != 0.0) || (fabs(g) > P.lam);
+            if (flag) len = S.ptr[j + 1] - S.ptr[j];
+        }
+        vmax_loc = fmax(vmax_loc, av);
+        // block-exclusive ranks of the flags
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        const int rank_in_warp = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) s_wcnt[wid] = __popc(bal);
+        double v1p = 0.0, l1p = 0.0;
+        if (FINEST) {
+            v1p = warp_sum(av);
+            l1p = warp_sum(fabs(wj));
+            if (lane == 0) { s_red[wid] = v1p; s_red[ML_NW + wid] = l1p; }
+        }
+        __syncthreads();
+        int woff = 0, total = 0;
+        for (int k = 0; k < ML_NW; ++k) { if (k < wid) woff += s_wcnt[k]; total += s_wcnt[k]; }
+        if (threadIdx.x == 0) {
+            if (FINEST) {
+                double a = 0.0, b = 0.0;
+                for (int k = 0; k < ML_NW; ++k) { a += s_red[k]; b += s_red[ML_NW + k]; }
+                P.tilepart[tile] = make_double2(a, b);
+            }
+            // publish and look back (epoch-tagged status words: epoch<<34 | flag<<32 | count)
+            const unsigned long long e34 = (unsigned long long)epoch << 34;
+            int excl = 0;
+            if (tile == 0) {
+                __threadfence();
+                atomicExch(P.status + 0, e34 | (2ull << 32) | (unsigned)total);
+            } else {
+                __threadfence();
+                atomicExch(P.status + tile, e34 | (1ull << 32) | (unsigned)total);
+                int pred = tile - 1;
+                while (true) {
+                    unsigned long long st = *((volatile unsigned long long*)(P.status + pred));
+                    if ((st >> 34) != epoch || ((st >> 32) & 3ull) == 0) continue;
+                    excl += (int)(st & 0xffffffffull);
+                    if (((st >> 32) & 3ull) == 2) break;
+                    --pred;
+                }
+                __threadfence();
+                atomicExch(P.status + tile, e34 | (2ull << 32) | (unsigned)(excl + total));
+            }
+            s_excl = excl;
+        }
+        __syncthreads();
+        if (flag) {
+            const int o = s_excl + woff + rank_in_warp;
+            AS.A[o] = j;
+            AS.gA[o] = g;
+            AS.hA[o] = h + P.eps_h;
+            AS.wA[o] = wj;
+            if (len > SPLIT) {   // heavy free column: schedule its units for the Hessian-vector passes over A
+                const int nch = (len + CHUNK - 1) / CHUNK;
+                const int hs = atomicAdd(UA.h, 1);
+                const int base = atomicAdd(UA.n, nch);
+                for (int c = 0; c < nch && base + c < UA.cap; ++c) UA.u[base + c] = make_int4(o, c, hs, base);
+            }
+        }
+        __syncthreads();
+    }
+    add_nnz(ctl, streamed, smn);
+    // block max -> global atomic max (order-independent)
+    {
+        double v = warp_max(vmax_loc);
+        if (lane == 0) s_red[wid] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double mx = 0.0;
+            for (int k = 0; k < ML_NW; ++k) mx = fmax(mx, s_red[k]);
+            atomic_max_nonneg(reinterpret_cast<double*>(&ctl->vmax_bits), mx);
+            __threadfence();
+            s_last = (atomicAdd(&ctl->done_ctr, 1u) == gridDim.x - 1);
+        }
+        __syncthreads();
+    }
+    if (!s_last) return;
+    __threadfence();
+    if (FINEST) {   // exact sum |v| and ||w||_1 over all columns, in tile order
+        double a = 0.0, b = 0.0;
+        for (int t = threadIdx.x; t < ntiles; t += ML_NT) { double2 q = ld_cg(P.tilepart + t); a += q.x; b += q.y; }
+        Red<2> r;
+        r.s[0] = a; r.s[1] = b;
+        __shared__ double smr[2 * ML_NW + 2];
+        block_reduce(r, smr);
+        if (threadIdx.x == 0) { ctl->v1 = r.s[0]; ctl->l1 = r.s[1]; }
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long st = ntiles ? *((volatile unsigned long long*)(P.status + ntiles - 1)) : 0ull;
+        const int nA = ntiles ? (int)(st & 0xffffffffull) : 0;
+        ctl->nA = nA;
+        const double vmax = __longlong_as_double((long long)ctl->vmax_bits);
+        ctl->vmax = vmax;
+        ctl->vmax_bits = 0ull;
+        if (FINEST) { ctl->nAf = nA; ctl->F = ctl->L + P.lam * ctl->l1; }
+        ctl->F_before = ctl->F;
+        if (vmax / P.lam <= P.tol) { ctl->skip = 1; ctl->outcome = OUT_CONVERGED; ctl->level_conv = 1; }
+        ctl->tile_ctr = 0u;
+        ctl->done_ctr = 0u;
+        ctl->epoch = (epoch + 1u) & 0x3fffffffu;
+    }
+}
+
+// ------------------------------------------------------------------ plain gathers (API outputs / Hessian-vector)
+// MODE 0: out0[p] = g, out1[p] = h (either may be null)      (ml_eval_f_grad, ml_diag_hess)
+// MODE 1: out0[p] = sum X_ij v_i (+ eps_h * s[p] if s)       (Hs = X_A^T (D o Xs) + eps s, ml_hessvec)
+template <int G, int MODE, class Op>
+__global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* nseg_dev, int nseg_host, double* out0,
+                                                      double* out1, const double* s, double eps, const int* skip,
+                                                      const int* skip2, long long* nnz_acc) {
+    __shared__ double2 res[TILE];
+    __shared__ long long smn[ML_NW];
+    if ((skip && *skip) || (skip2 && *skip2)) return;
+    const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+    const int ntiles = (nseg + TILE - 1) / TILE;
+    long long streamed = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        streamed += seg_tile<G>(S, op, nseg, tile, res);
+        __syncthreads();
+        const int p = tile * TILE + threadIdx.x;
+        if (p < nseg) {
+            const double2 q = res[threadIdx.x];
+            if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
+            else out0[p] = q.x + (s ? eps * s[p] : 0.0);
+        }
+        __syncthreads();
+    }
+    if (nnz_acc) {
+        const int lane = threadIdx.x & 31;
+        long long t = warp_sum_ll(streamed);
+        if (lane == 0) smn[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long a = 0;
+            for (int k = 0; k < ML_NW; ++k) a += smn[k];
+            if (a) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)a);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ A5: X_A s scatter (light segments)
+template <int G>
+__global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef,
+                                                   double* out, const int* skip, const int* skip2, long long* nnz_acc) {
+    __shared__ long long smn[ML_NW];
+    if ((skip && *skip) || (skip2 && *skip2)) return;
+    const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+    const int grp = (blockIdx.x * ML_NT + threadIdx.x) / G, lane = threadIdx.x % G;
+    const int ngrp = gridDim.x * (ML_NT / G);
+    long long streamed = 0;
+    for (int p = grp; p < nseg; p += ngrp) {
+        const double cf = coef[p];
+        if (cf == 0.0) continue;
+        const int j = S.list ? __ldg(S.list + p) : p;
+        const int b = __ldg(S.ptr + j), e = __ldg(S.ptr + j + 1);
+        if (e - b > SPLIT) continue;   // heavy columns: k_heavy<SCATTER>
+        if (lane == 0) streamed += e - b;
+        for (int k = b + lane; k < e; k += G) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
+    }
+    if (nnz_acc) {
+        const int ln = threadIdx.x & 31;
+        long long t = warp_sum_ll(streamed);
+        if (ln == 0) smn[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long a = 0;
+            for (int k = 0; k < ML_NW; ++k) a += smn[k];
+            if (a) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)a);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ relaxation bookkeeping
+// Start of RELAX(C): reset per-relaxation flags; first == 1 starts a new level (clears level_conv).
+__global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* Cptr, int nC, int set_list, int finest) {
+    Ctl* c = P.ctl;
+    if (first_of_level) c->level_conv = 0;
+    c->skip = c->level_conv;
+    c->skipped = c->level_conv;
+    c->outcome = c->level_conv ? OUT_CONVERGED : OUT_NOSTEP;
+    c->inner_stop = 0;
+    c->napply = 0;
+    c->cg_restart = 1;
+    c->scattered = 0;
+    c->ls_ok = 0;
+    c->level = level;
+    c->it = 0;
+    c->units_n[2] = 0;   // A-set units are rebuilt by the gather
+    c->units_h[2] = 0;
+    if (set_list) { c->Cptr = Cptr; c->nC = nC; }
+    (void)finest;
+}
+
+// R5-R6 (PCD step, Eq. 5 with D = diag(H) + eps_h): s = Sh_{lam/h}(x - p/h) - x, x = w_A + d, p = g_A + Hd.
+// Reduction: p^T s, ||s||^2, l1 trial differences sum(|x + b_t s| - |x|) for b_t = beta^t, max|s|, model min-norm
+// subgradient (forcing).  Last block: stop flags.
+__global__ void __launch_bounds__(ML_NT) k_pcd_dir(Prm P, ASet AS, int it) {
+    __shared__ double sm[(ML_MAXLS + 4) * ML_NW + ML_MAXLS + 4];
+    Ctl* c = P.ctl;
+    if (c->skip || c->inner_stop) return;
+    const int nA = c->nA;
+    Red<ML_MAXLS + 2, 2> r;
+    r.zero();
+    double bt[ML_MAXLS];
+    bt[0] = 1.0;
+#pragma unroll
+    for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
+    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+        const double d = it ? AS.d[p] : 0.0, Hd = it ? AS.Hd[p] : 0.0;
+        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
+        const double s = soft(x - pj / hh, P.lam / hh) - x;
+        AS.s[p] = s;
+        const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+        r.mx[0] = fmax(r.mx[0], fabs(s));
+        r.mx[1] = fmax(r.mx[1], fabs(v));
+        r.s[0] += pj * s;
+        r.s[1] += s * s;
+        const double ax = fabs(x);
+#pragma unroll
+        for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * s) - ax;
+    }
+    if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
+        if (threadIdx.x == 0) {
+            c->ps = r.s[0];
+            c->ss = r.s[1];
+            c->vq = r.mx[1];
+            for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // reused as inner l1 diffs
+            int stop = 0;
+            if (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax) stop = 1;   // R13 forcing
+            if (r.mx[0] == 0.0) stop = 1;                                        // R7
+            c->inner_stop = stop;
+            c->scattered = !stop;
+            c->it = it;
+        }
+    }
+}
+
+// PCD-CG, part 1 (R6'): u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere; rz = sum h u^2;
+// forcing test; b = rz / rz_prev unless restarting.
+__global__ void __launch_bounds__(ML_NT) k_cg_z(Prm P, ASet AS, int it) {
+    __shared__ double sm[3 * ML_NW + 3];
+    Ctl* c = P.ctl;
+    if (c->skip || c->inner_stop) return;
+    const int nA = c->nA;
+    Red<1, 1> r;
+    r.zero();
+    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+        const double x = AS.wA[p] + AS.d[p], pj = AS.gA[p] + AS.Hd[p], hh = AS.hA[p];
+        const double u = (x != 0.0) ? -(pj + P.lam * sgn(x)) / hh : 0.0;
+        AS.u[p] = u;
+        const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+        r.s[0] += hh * u * u;
+        r.mx[0] = fmax(r.mx[0], fabs(v));
+    }
+    if (grid_reduce(r, P.part, &c->red_ctr[2], sm)) {
+        if (threadIdx.x == 0) {
+            const double rz = r.s[0];
+            int stop = 0;
+            if (it > 0 && P.eta > 0.0 && r.mx[0] <= P.eta * c->vmax) stop = 1;
+            if (rz == 0.0) stop = 1;
+            c->inner_stop = stop;
+            c->vq = r.mx[0];
+            c->bcg = c->cg_restart ? 0.0 : rz / c->rz_prev;
+            c->rz = rz;
+            c->it = it;
+        }
+    }
+}
+
+// PCD-CG, part 2: s = u + b s_prev; slope = sum_{x != 0} (p + lam sign x) s; ||s||^2; first kink
+// b_k = min_{x s < 0} -x/s.
+__global__ void __launch_bounds__(ML_NT) k_cg_s(Prm P, ASet AS) {
+    __shared__ double sm[4 * ML_NW + 4];
+    Ctl* c = P.ctl;
+    if (c->skip || c->inner_stop) return;
+    const int nA = c->nA;
+    const double bcg = c->bcg;
+    Red<2, 0, 1> r;
+    r.zero();
+    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+        const double x = AS.wA[p] + AS.d[p];
+        const double s = AS.u[p] + bcg * AS.s[p];
+        AS.s[p] = s;
+        if (x != 0.0) r.s[0] += (AS.gA[p] + AS.Hd[p] + P.lam * sgn(x)) * s;
+        r.s[1] += s * s;
+        if (x * s < 0.0) r.mn[0] = fmin(r.mn[0], -x / s);
+    }
+    if (grid_reduce(r, P.part, &c->red_ctr[3], sm)) {
+        if (threadIdx.x == 0) {
+            c->slope = r.s[0];
+            c->ss = r.s[1];
+            c->bk = r.mn[0];
+            c->scattered = 1;
+        }
+    }
+}
+
+// m-side pass after the scatter: sv = D o Xs (for the Hs gather); s^T H s = sum D Xs^2 + eps ||s||^2; then the
+// inner step: PCD -> Armijo on the model over b = beta^t (R10); CG -> b = min(b_q, b_kink) (R6').
+__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int pcd) {
+    __shared__ double sm[2 * ML_NW + 2];
+    Ctl* c = P.ctl;
+    if (c->skip || c->inner_stop) return;
+    Red<1> r;
+    r.zero();
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
+        const double xs = P.Xs[i];
+        const double D = P.rD[i].y;
+        P.sv[i] = D * xs;
+        r.s[0] += D * xs * xs;
+    }
+    if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
+        if (threadIdx.x == 0) {
+            const double sHs = r.s[0] + P.eps_h * c->ss;
+            c->sHs = sHs;
+            if (pcd) {
+                const double delta = c->ps + P.lam * c->l1diff_out[0];
+                double b = 1.0;
+                int ok = 0;
+                for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+                    const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
+                    if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+                }
+                c->beta = ok ? b : 0.0;
+                c->snap = 0;
+                if (!ok) c->inner_stop = 1;
+                c->cg_restart = 1;
+            } else {
+                if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; }
+                else {
+                    const double bq = -c->slope / sHs;
+                    c->bq = bq;
+                    c->beta = bq < c->bk ? bq : c->bk;
+                    c->snap = (c->bk <= bq);
+                    c->cg_restart = c->snap;
+                    c->rz_prev = c->rz;
+                }
+            }
+        }
+    }
+}
+
+// R12: d += b s (a coordinate reaching its kink is set to exactly -w: x = 0), Hd += b Hs (when Hs was computed),
+// Xd += b Xs; Xs is cleared for the next scatter.  it == 0 initialises d, Hd, Xd.
+__global__ void __launch_bounds__(ML_NT) k_apply(Prm P, ASet AS, int it, int have_hs, int nblkA) {
+    Ctl* c = P.ctl;
+    if (c->skip || !c->scattered) return;
+    const int ok = !c->inner_stop;
+    const double b = c->beta;
+    if ((int)blockIdx.x < nblkA) {
+        if (!ok) return;
+        const int nA = c->nA;
+        const int snap = c->snap;
+        const double bk = c->bk;
+        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
+            const double s = AS.s[p];
+            const double d0 = it ? AS.d[p] : 0.0;
+            const double x = AS.wA[p] + d0;
+            const bool kink = snap && x * s < 0.0 && -x / s == bk;
+            AS.d[p] = kink ? -AS.wA[p] : d0 + b * s;
+            if (have_hs) AS.Hd[p] = (it ? AS.Hd[p] : 0.0) + b * AS.Hs[p];
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->napply += 1;
+    } else {
+        const int nb = gridDim.x - nblkA;
+        for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
+            const double xs = P.Xs[i];
+            if (ok) P.Xd[i] = (it ? P.Xd[i] : 0.0) + b * xs;
+            P.Xs[i] = 0.0;
+        }
+    }
+}
+
+// R14-R16, first batch of the outer line search (Eq. 4; Armijo DESIGN Q7, Q26): A-range blocks reduce
+// g^T d, max|d| and the l1 trial differences sum(|w + a_t d| - |w|) for every trial; m-range blocks reduce
+// sum_i dloss(t_i, a_t y_i Xd_i) for trials t0 <= t < t1.  Last block: Delta, decision.
+template <int NT1>
+__global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int nblkA) {
+    constexpr int NS = 1 + ML_MAXLS + NT1;
+    __shared__ double sm[(NS + 1) * ML_NW + NS + 1];
+    Ctl* c = P.ctl;
+    if (c->skip) return;
+    if (t0 == 0) {
+        if (c->napply == 0) {   // R14: d = 0
+            if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; }
+            return;
+        }
+    } else if (c->ls_ok) return;
+    const int T1 = min(P.max_ls, t0 + NT1);
+    Red<NS, 1> r;
+    r.zero();
+    double at[ML_MAXLS];
+    at[0] = 1.0;
+#pragma unroll
+    for (int t = 1; t < ML_MAXLS; ++t) at[t] = at[t - 1] * P.beta_ls;
+    if ((int)blockIdx.x < nblkA) {
+        if (t0 == 0) {
+            const int nA = c->nA;
+            for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
+                const double d = AS.d[p], w = AS.wA[p], aw = fabs(w);
+                r.s[0] += AS.gA[p] * d;
+                r.mx[0] = fmax(r.mx[0], fabs(d));
+#pragma unroll
+                for (int t = 0; t < ML_MAXLS; ++t) r.s[1 + t] += fabs(w + at[t] * d) - aw;
+            }
+        }
+    } else {
+        const int nb = gridDim.x - nblkA;
+        for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
+            const double y = (double)P.y[i];
+            const double ti = y * P.z[i], yx = y * P.Xd[i];
+#pragma unroll
+            for (int k = 0; k < NT1; ++k)
+                if (t0 + k < T1) r.s[1 + ML_MAXLS + k] += dloss(ti, at[t0 + k] * yx);
+        }
+    }
+    if (grid_reduce(r, P.part, &c->red_ctr[5], sm)) {
+        if (threadIdx.x == 0) {
+            if (t0 == 0) {
+                c->gd = r.s[0];
+                for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[1 + t];
+                c->Delta = r.s[0] + P.lam * r.s[1];
+                if (r.mx[0] == 0.0) { c->skip = 1; c->outcome = OUT_NOSTEP; return; }
+            }
+            const double Delta = c->Delta;
+            for (int k = 0; k < NT1 && t0 + k < T1; ++k) {
+                const int t = t0 + k;
+                const double a = at[t];
+                const double dF = r.s[1 + ML_MAXLS + k] + P.lam * c->l1diff_out[t];
+                if (dF <= P.sigma_out * a * Delta) { c->ls_ok = 1; c->alpha = a; c->t_acc = t; break; }
+            }
+            if (!c->ls_ok && T1 >= P.max_ls) { c->skip = 1; c->outcome = OUT_STAGNATION; c->alpha = 0.0; }
+        }
+    }
+}
+
+// R18: w_A += a d (bitmap and |supp| maintained), ||w||_1 += l1 diff of the accepted trial; z += a Xd and the
+// per-sample refresh (A1 incremental); L, F; trace row.
+__global__ void __launch_bounds__(ML_NT) k_update(Prm P, ASet AS, int nblkA) {
+    __shared__ double sm[2 * ML_NW + 2];
+    __shared__ long long sml[ML_NW];
+    Ctl* c = P.ctl;
+    if (c->skip || !c->ls_ok) return;
+    const double a = c->alpha;
+    Red<1> r;
+    r.zero();
+    long long ds = 0;
+    if ((int)blockIdx.x < nblkA) {
+        const int nA = c->nA;
+        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
+            const double w0 = AS.wA[p];
+            const double w1 = w0 + a * AS.d[p];
+            const int j = AS.A[p];
+            P.w[j] = w1;
+            AS.wA[p] = w1;
+            const int nz0 = (w0 != 0.0), nz1 = (w1 != 0.0);
+            if (nz0 != nz1) { atomicXor(P.wbits + (j >> 5), 1u << (j & 31)); ds += nz1 - nz0; }
+        }
+    } else {
+        const int nb = gridDim.x - nblkA;
+        for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
+            const double z = P.z[i] + a * P.Xd[i];
+            P.z[i] = z;
+            const RowState st = row_state(z, (double)P.y[i]);
+            P.rD[i] = make_double2(st.r, st.D);
+            r.s[0] += st.ell;
+        }
+    }
+    {
+        long long t = warp_sum_ll(ds);
+        if ((threadIdx.x & 31) == 0) sml[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long s = 0;
+            for (int k = 0; k < ML_NW; ++k) s += sml[k];
+            if (s) atomicAdd((unsigned long long*)&c->dsupp, (unsigned long long)s);
+        }
+    }
+    if ((int)blockIdx.x < nblkA) r.s[0] = 0.0;
+    if (grid_reduce(r, P.part, &c->red_ctr[6], sm)) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            c->nS += (int)c->dsupp;
+            c->dsupp = 0;
+            c->L = r.s[0];
+            c->l1 += c->l1diff_out[c->t_acc];
+            const double Fb = c->F;
+            c->F = c->L + P.lam * c->l1;
+            c->outcome = OUT_UPDATED;
+            if (c->ntrace < c->trace_cap) {
+                TraceRow tr{c->level, OUT_UPDATED, 0, c->nA, (long long)c->nC, Fb, c->F, a};
+                P.trace[c->ntrace] = tr;
+            }
+            c->ntrace += 1;
+        }
+    }
+}
+
+// End of a relaxation that did not update (converged / no step / stagnation): trace row.
+__global__ void k_relax_end(Prm P) {
+    Ctl* c = P.ctl;
+    if (c->outcome == OUT_UPDATED || c->skipped) return;
+    if (c->ntrace < c->trace_cap) {
+        TraceRow tr{c->level, c->outcome, 0, c->nA, (long long)c->nC, c->F, c->F, 0.0};
+        P.trace[c->ntrace] = tr;
+    }
+    c->ntrace += 1;
+}
+
+}  // namespace ml

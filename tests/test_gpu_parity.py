@@ -1,0 +1,254 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on identical seeded inputs.  Marked gpu.
+
+Tolerances: per-kernel outputs F, g, h, Hv, z, r, D: relative L2 <= 1e-9; selection: exact
+set equality given the oracle's gradient bits; line search: identical alpha unless the Armijo decision is a
+near-tie; solve: F relative <= 1e-6 with both runs at kappa <= 1e-6, supports equal outside the band
+||g_j| - lambda| < 1e-4 (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+import mlgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1607_00315_b200 as ml  # noqa: E402
+
+ml.build()
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def dt(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0", dtype)
+
+
+_CACHE = {}
+
+
+def dataset(name):
+    if name in _CACHE:
+        return _CACHE[name]
+    if name == "cfg1":
+        ds = mlgen.make(1)
+    elif name == "cfg2s":      # dense, correlated blocks; rows heavy (split path), columns light
+        ds = mlgen.make(2, m=300, n=3000)
+    elif name == "cfg2m":      # dense with heavy columns (> SPLIT)
+        ds = mlgen.make(2, m=2500, n=600)
+    elif name == "cfg3s":
+        ds = mlgen.make(3, m=8000, n=16000)
+    elif name == "cfg3":
+        ds = mlgen.make(3)
+    elif name == "cfg4s":
+        ds = mlgen.make(4, m=20000, n=40000)
+    elif name == "sparse_edges":   # empty rows and columns, ragged
+        ds = mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40)
+    elif name == "onehot":
+        ds = mlgen.onehot(3000, 3)[0]
+    elif name == "m1":
+        ds = mlgen.from_dense(np.array([[0.5, -1.0, 2.0, 0.0, 1.5]], np.float32), np.array([1], np.int8), 0.1)
+    elif name == "n1":
+        rng = np.random.default_rng(1)
+        ds = mlgen.from_dense(rng.uniform(0.1, 1, (57, 1)).astype(np.float32),
+                              np.where(rng.random(57) < 0.7, 1, -1).astype(np.int8), 0.5)
+    else:
+        raise KeyError(name)
+    _CACHE[name] = ds
+    return ds
+
+
+def random_w(n, kind, seed):
+    rng = np.random.default_rng(seed)
+    w = np.zeros(n)
+    k = {"zero": 0, "ten": min(10, n), "pct": max(1, n // 100), "all": n}[kind]
+    idx = rng.choice(n, k, replace=False)
+    w[idx] = rng.normal(0, 0.1, k) * (3.0 if kind == "ten" else 1.0)
+    return w
+
+
+PER_KERNEL = ["cfg1", "cfg2s", "cfg2m", "cfg3s", "cfg4s", "sparse_edges", "onehot", "m1", "n1"]
+
+
+@pytest.mark.parametrize("name", PER_KERNEL)
+@pytest.mark.parametrize("wkind", ["zero", "ten", "pct", "all"])
+def test_eval_f_grad_parity(name, wkind):
+    """A1 + A2: F, g, h, z, r, D at the same w."""
+    ds = dataset(name)
+    w = random_w(ds.n, wkind, 17)
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    F_o, g_o, h_o = o.eval_f_grad()
+    z_o, r_o, D_o, _ = o.rows()
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    F_g, g_g, h_g = ctx.ml_eval_f_grad()
+    z_g, r_g, D_g = (t.cpu().numpy() for t in ctx.ml_get_rows())
+    assert abs(F_g - F_o) <= 1e-9 * abs(F_o)
+    assert rel(g_g.cpu().numpy(), g_o) <= 1e-9
+    assert rel(h_g.cpu().numpy(), h_o) <= 1e-9
+    assert rel(z_g, z_o) <= 1e-9 and rel(r_g, r_o) <= 1e-9 and rel(D_g, D_o) <= 1e-9
+
+
+def _lists(ds, seed):
+    rng = np.random.default_rng(seed)
+    lens = np.diff(ds.csc_colptr)
+    heavy = int(np.argmax(lens))
+    out = {"empty": np.zeros(0, np.int32), "single": np.array([ds.n // 2], np.int32),
+           "heaviest": np.array([heavy], np.int32),
+           "pct": np.sort(rng.choice(ds.n, max(1, ds.n // 100), replace=False)).astype(np.int32),
+           "half": np.sort(rng.choice(ds.n, max(1, ds.n // 2), replace=False)).astype(np.int32)}
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg2m", "cfg3s", "sparse_edges"])
+def test_restricted_gather_hessvec(name):
+    """A2 / A5 restricted to lists C: empty, single, heaviest column, 1 %, half."""
+    ds = dataset(name)
+    w = random_w(ds.n, "pct", 3)
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    o.eval_f_grad()
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    ctx.ml_eval_f_grad(want_g=False, want_h=False)
+    rng = np.random.default_rng(8)
+    for key, C in _lists(ds, 4).items():
+        if len(C) == 0:
+            continue
+        _, g_o, h_o = o.eval_f_grad(C)
+        Fg, g_g, h_g = ctx.ml_eval_f_grad(dt(C, torch.int32))
+        assert rel(g_g.cpu().numpy(), g_o) <= 1e-9, key
+        assert rel(h_g.cpu().numpy(), h_o) <= 1e-9, key
+        hd = ctx.ml_diag_hess(dt(C, torch.int32))
+        assert rel(hd.cpu().numpy(), h_o) <= 1e-9, key
+        v = rng.standard_normal(len(C))
+        Hv_o = o.hessvec(C, v)
+        Hv_g = ctx.ml_hessvec(dt(C, torch.int32), dt(v))
+        assert rel(Hv_g.cpu().numpy(), Hv_o) <= 1e-9, key
+    v = rng.standard_normal(ds.n)
+    assert rel(ctx.ml_hessvec(None, dt(v)).cpu().numpy(), o.hessvec(None, v)) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3s", "sparse_edges", "onehot"])
+def test_select_coarse_exact(name):
+    """A8: exact set equality given identical gradient bits (ties by index)."""
+    ds = dataset(name)
+    w = random_w(ds.n, "pct", 5)
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    _, g, _ = o.eval_f_grad()
+    g = g.copy()
+    g[::7] = np.round(g[::7], 2)  # exact ties
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    nS = int(np.count_nonzero(w))
+    for k in (0, nS, nS + 1, nS + 37, (ds.n + nS) // 2, ds.n, ds.n + 5):
+        C_o = o.select_coarse(g, k)
+        C_g = ctx.ml_select_coarse(dt(g), k).cpu().numpy()
+        assert np.array_equal(C_g, C_o), (k, len(C_g), len(C_o))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "sparse_edges"])
+def test_shrink_linesearch_parity(name):
+    """A7: PCD step (d = NULL) and a given long step; alpha and F_new (Eq. 4-5)."""
+    ds = dataset(name)
+    w = random_w(ds.n, "ten", 9)
+    for mode in ("pcd", "given"):
+        o = oracle.Oracle(ds)
+        o.set_w(w)
+        _, g, h = o.eval_f_grad()
+        ctx = ml.Context(ds)
+        ctx.ml_set_w(dt(w))
+        ctx.ml_eval_f_grad(want_g=False, want_h=False)
+        C = np.arange(ds.n, dtype=np.int32)
+        if mode == "pcd":
+            a_o, F_o, st_o = o.shrink_linesearch(C, g, h=h)
+            a_g, F_g, st_g = ctx.ml_shrink_linesearch(dt(C, torch.int32), dt(g), h=dt(h))
+        else:
+            rng = np.random.default_rng(2)
+            d = -np.sign(g) * np.abs(rng.normal(0, 2.0, ds.n))
+            a_o, F_o, st_o = o.shrink_linesearch(C, g, d=d)
+            a_g, F_g, st_g = ctx.ml_shrink_linesearch(dt(C, torch.int32), dt(g), d=dt(d))
+        assert st_o == st_g
+        assert a_o == a_g, (mode, a_o, a_g)
+        assert abs(F_g - F_o) <= 1e-9 * abs(F_o)
+        assert rel(ctx.ml_get_w().cpu().numpy(), o.get_w()) <= 1e-12
+
+
+def _support_check(ds, w_g, w_o, g_o):
+    band = np.abs(np.abs(g_o) - ds.lam) < 1e-4
+    sg, so = w_g != 0, w_o != 0
+    assert np.all((sg == so) | band), int(np.sum((sg != so) & ~band))
+
+
+@pytest.mark.parametrize("name,opts", [("cfg1", {}), ("cfg2s", {}), ("cfg3s", {}), ("sparse_edges", {}),
+                                       ("onehot", {}), ("n1", {}), ("m1", {}),
+                                       ("cfg3s", {"multilevel": 0, "K_fine": 10}),
+                                       ("cfg1", {"inner_cg": 0, "K_mid": 2, "K_coarse": 5})])
+def test_solve_parity(name, opts):
+    """A9: ml_solve vs the oracle's solve (Algorithm 1 P:155-173 per P:798), both to kappa <= 1e-6."""
+    ds = dataset(name)
+    o = oracle.Oracle(ds)
+    r_o = o.solve(oracle.default_opts(**opts))
+    ctx = ml.Context(ds)
+    r_g = ctx.ml_solve(ml.default_opts(**opts))
+    assert r_o["status"] == 0 and r_g["status"] == 0, (r_o, r_g)
+    assert r_g["kappa"] <= 1e-6 and r_o["kappa"] <= 1e-6
+    assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+    w_o = o.get_w()
+    _, g_o, _ = o.eval_f_grad()
+    _support_check(ds, ctx.ml_get_w().cpu().numpy(), w_o, g_o)
+    tr = ctx.trace()
+    for row in tr:   # Lemma P:207-243
+        assert row["F_after"] <= row["F_before"] * (1 + 1e-12) + 1e-12
+
+
+def test_solve_onehot_closed_form():
+    """GPU solve against the one-hot closed form with no oracle involved, n = 20000."""
+    ds, a, p, q = mlgen.onehot(20000, 11)
+    lam = ds.lam
+    d = np.abs(p - q).astype(np.float64)
+    act = lam < a * d / 2
+    wref = np.zeros(ds.n)
+    big, small = np.maximum(p, q).astype(np.float64), np.minimum(p, q).astype(np.float64)
+    wref[act] = np.sign(p - q)[act] / a[act] * np.log((a[act] * big[act] - lam) / (a[act] * small[act] + lam))
+    F = np.sum(p * np.logaddexp(0, -a * wref) + q * np.logaddexp(0, a * wref) + lam * np.abs(wref))
+    ctx = ml.Context(ds)
+    r = ctx.ml_solve(ml.default_opts(tol_kkt=1e-12))
+    w = ctx.ml_get_w().cpu().numpy()
+    assert r["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    nz = wref != 0
+    assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-8
+    assert abs(r["F"] - F) <= 1e-12 * F
+
+
+def test_lambda_max_zero_solution_gpu():
+    ds = dataset("cfg1")
+    ctx = ml.Context(ds, lam=ds.lambda_max * (1 + 1e-9))
+    r = ctx.ml_solve()
+    assert r["status"] == 0 and r["cycles"] == 0 and r["nnz_w"] == 0
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_solve_parity_full_configs(name):
+    """Solve parity at BASELINE configs 2 and 3 (full size)."""
+    ds = mlgen.make(int(name[-1]))
+    o = oracle.Oracle(ds)
+    r_o = o.solve()
+    ctx = ml.Context(ds)
+    r_g = ctx.ml_solve()
+    assert r_o["status"] == 0 and r_g["status"] == 0
+    assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+    w_o = o.get_w()
+    _, g_o, _ = o.eval_f_grad()
+    _support_check(ds, ctx.ml_get_w().cpu().numpy(), w_o, g_o)
