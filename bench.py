@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — multilevel proximal-Newton l1-logistic regression on B200 (BASELINE.json metric).
+
+One STEP = one full `ml_solve` from w = 0 to KKT <= 1e-6 (Algorithm 1; every SURVEY §8a row runs
+inside it) on one BASELINE.json configuration (default: configs[1], the 2000 x 20000 dense correlated design).
+
+  value     data-pass GB/s over the whole timed region: 8 bytes (fp32 value + int32 index) for every nonzero of X
+            streamed by the solve's X passes (device counters), summed over ranks, / max-over-ranks time
+  e2e       the same metric through the public API with host buffers: pinned H2D of X and y, ml_create, ml_solve,
+            D2H of w inside the timed region
+  roofline  the pass class with the largest device-time share (CUDA events around each of its passes, on the
+            library's stream, inside the timed region); algorithmic bytes per DESIGN.md section 9
+  cpu_baseline  the CPU oracle (single thread) solving the same workload on this host (rank 0, N = 1)
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+For N > 1 launch under torch.distributed.run; the path does not shard (BASELINE: one GPU), so ranks run
+independent replicas (weak scaling) synchronised only by barriers.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "data-pass HBM GB/s (% of B200 peak); multilevel solve time-to-KKT 1e-6 vs CPU oracle"
+CFG_NAMES = {1: "cfg1 dense 200x1000 iid", 2: "cfg2 dense 2000x20000 corr-blocks", 3: "cfg3 zipf 50000x100000",
+             4: "cfg4 zipf 500000x1000000", 5: "cfg5 zipf 2000000x20000000"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx, self.rows, self.proc = gpu_index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, ws, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce(vals, op, ws, device):
+    if ws == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def class_bytes(name, prof, ds):
+    """Algorithmic bytes of a pass class: X stream 8 B/nnz, pointer pairs 8 B/segment,
+    list 4 B/segment, each m-vector once per pass, outputs once."""
+    p = prof[name]
+    nnz, segs, passes = p["nnz"], p["segs"], max(p["passes"], 1)
+    m = ds.m
+    if name == "margins":      # X (CSR) + rowptr + y + z, r, D written + w gathers of the support (upper: 8/seg)
+        return 8 * nnz + 4 * segs + passes * (m * 1 + 24 * m)
+    if name in ("gather_fine", "gather_coarse"):   # X (CSC) + colptr pairs + (r, D) once + outputs 28 B/col
+        return 8 * nnz + 8 * segs + passes * 16 * m + 12 * segs
+    if name == "scatter_XAs":  # X_A (nonzero-coefficient columns) + colptr + coef + Xs read-modify-write once
+        return 8 * nnz + 12 * segs + passes * 16 * m
+    if name == "gather_Hs":    # X_A + colptr + sv once + Hs out
+        return 8 * nnz + 16 * segs + passes * 8 * m
+    return 8 * nnz
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import mlgen
+    import paper_1607_00315_b200 as ml
+
+    rank, ws, local = dist_setup(args.gpus)
+    device = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(device)
+    ml.build()
+    ds = mlgen.make(args.config)
+    ctx = ml.Context(ds, device=str(device))
+    opts = ml.default_opts()
+
+    # warm-up; the last warm-up step times every pass class to find the dominant one
+    for k in range(args.warmup):
+        ctx.ml_profile((1 << 13) - 1 if k == args.warmup - 1 else 0)
+        rep = ctx.ml_solve(opts)
+    prof_w = ctx.ml_profile_read()
+    dom = max((n for n in prof_w if n not in ("book", "api")), key=lambda n: prof_w[n]["ms"])
+    dom_idx = ml.Context.CLASSES.index(dom)
+    share_warm = {n: prof_w[n]["ms"] for n in prof_w}
+    tot_warm = sum(share_warm.values()) or 1.0
+
+    # timed region: events only around the dominant class's passes
+    ctx.ml_profile(1 << dom_idx)
+    torch.cuda.synchronize(device)
+    barrier(ws)
+    torch.cuda.synchronize(device)
+    launches0 = ctx.ml_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    with ClockSampler(local) as clk:
+        e0.record(ctx.stream)
+        for _ in range(args.steps):
+            reps.append(ctx.ml_solve(opts))
+        e1.record(ctx.stream)
+        torch.cuda.synchronize(device)
+    barrier(ws)
+    t_ms = e0.elapsed_time(e1)
+    launches = ctx.ml_kernel_launches() - launches0
+    prof = ctx.ml_profile_read()
+    ok = all(r["status"] == 0 and r["kappa"] <= 1e-6 for r in reps)
+    nnz_total = sum(r["nnz_touched"] for r in reps)
+    bytes_total = 8.0 * nnz_total
+    t_max, = allreduce([t_ms], "max", ws, device)
+    bytes_all, = allreduce([bytes_total], "sum", ws, device)
+    value = bytes_all / (t_max * 1e-3) / 1e9
+
+    # roofline of the dominant pass class, measured in the timed region
+    peak, peak_kind = peaks()
+    dom_ms = prof[dom]["ms"]
+    dom_bytes = class_bytes(dom, prof, ds)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
+            "traffic": traffic, "passes_timed": prof[dom]["passes"],
+            "bytes_per_pass": int(dom_bytes / max(prof[dom]["passes"], 1)),
+            "ms_per_pass": dom_ms / max(prof[dom]["passes"], 1),
+            "share_of_step": round(share_warm[dom] / tot_warm, 3),
+            "shares": {n: round(v / tot_warm, 3) for n, v in share_warm.items() if v > 0}}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        keep = [np.ascontiguousarray(a) for a in (ds.csr_rowptr, ds.csr_col, ds.csr_val, ds.csc_colptr, ds.csc_row,
+                                                  ds.csc_val, ds.y)]
+        pinned = [torch.from_numpy(a).pin_memory() for a in keep]
+        h2d = sum(t.numel() * t.element_size() for t in pinned)
+        d2h = 8 * ds.n
+        e2e_steps = max(1, min(args.steps, 3))
+        barrier(ws)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        nnz_e = 0
+        for _ in range(e2e_steps):
+            c2 = ml.Context.from_host(ds, pinned, device=str(device))
+            r2 = c2.ml_solve(opts)
+            w = c2.ml_get_w().cpu()
+            nnz_e += r2["nnz_touched"]
+            c2.close()
+            del c2, w
+        torch.cuda.synchronize(device)
+        te = (time.perf_counter() - t0) * 1e3
+        te_max, = allreduce([te], "max", ws, device)
+        be, = allreduce([8.0 * nnz_e], "sum", ws, device)
+        e2e = {"value": round(be / (te_max * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": te_max / e2e_steps, "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(ds, args.config)
+
+    if rank == 0:
+        r0 = reps[-1]
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CFG_NAMES[args.config], "m": ds.m, "n": ds.n, "nnz": ds.nnz,
+                       "lambda": ds.lam, "tol_kkt": 1e-6, "parallelism": f"replicas{ws}",
+                       "l2": "inputs larger than L2 (X CSR+CSC %.0f MB > 126 MB); no flush" % (16 * ds.nnz / 1e6)
+                       if 16 * ds.nnz > 126e6 else "small config: L2-resident",
+                       "step": "one ml_solve from w=0 to kappa<=1e-6"},
+            "time_to_kkt_ms": t_max / args.steps,
+            "solve": {"ok": ok, "F": r0["F"], "kappa": r0["kappa"], "cycles": r0["cycles"],
+                      "relaxations": r0["relaxations"], "nnz_w": r0["nnz_w"], "x_nnz_streamed": r0["nnz_touched"],
+                      "x_passes": r0["x_passes"]},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(ds, cfg):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same workload."""
+    import oracle
+    o = oracle.Oracle(ds)
+    if cfg <= 3:
+        t0 = time.perf_counter()
+        r = o.solve()
+        t = time.perf_counter() - t0
+        return {"value": round(8.0 * r["nnz_touched"] / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                "sample": f"one full oracle solve to kappa<=1e-6 ({r['cycles']} cycles)", "seconds": round(t, 2),
+                "time_to_kkt_ms": t * 1e3, "F": r["F"]}
+    t0 = time.perf_counter()
+    n0 = 0
+    o.eval_f_grad()   # margins + gradient/diag over all columns: one CSR and one CSC pass
+    t = time.perf_counter() - t0
+    return {"value": round(8.0 * 2 * ds.nnz / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": "one oracle eval_f_grad (full CSR margins pass + full CSC gather)", "seconds": round(t, 2)}
+
+
+def run_reference(args):
+    """The oracle (this tier's reference arm), timed as it stands on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import mlgen
+    import oracle
+    ds = mlgen.make(args.config)
+    o = oracle.Oracle(ds)
+
+    def step():
+        if args.config <= 3:
+            r = o.solve()
+            return 8.0 * r["nnz_touched"]
+        o.eval_f_grad()
+        return 8.0 * 2 * ds.nnz
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    b = 0.0
+    for _ in range(args.steps):
+        b += step()
+    t = time.perf_counter() - t0
+    v = b / t / 1e9
+    sample = ("one full oracle solve to kappa<=1e-6 per step" if args.config <= 3
+              else "one oracle eval_f_grad (CSR + CSC pass) per step")
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CFG_NAMES[args.config], "m": ds.m, "n": ds.n, "nnz": ds.nnz},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--single", action="store_true", help="one untimed solve (for ncu launch lists / captures)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+    if args.single:
+        import mlgen
+        import paper_1607_00315_b200 as ml
+        ml.build()
+        ds = mlgen.make(args.config)
+        ctx = ml.Context(ds)
+        r = ctx.ml_solve(ml.default_opts())
+        print(json.dumps({"single": True, "config": args.config, "status": r["status"], "kappa": r["kappa"],
+                          "cycles": r["cycles"], "kernel_launches": r["kernel_launches"]}))
+        return
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,14 @@ const char *ml_status_str(ml_status s);
 const char *ml_last_error(const ml_ctx *c);
 /* kernels this context has launched so far (for launch accounting) */
 int64_t ml_kernel_launches(const ml_ctx *c);
+/* Measurement.  Pass classes: 0 margins (A1), 1 finest gather (A2/A3), 2 coarse gather, 3 X_A s scatter (A5),
+   4 X_A^T (D o Xs) gather (A5), 5 inner direction (A4), 6 m-side model pass (A6), 7 step apply (A6), 8 outer line
+   search (A7), 9 update (A7), 10 selection (A8), 11 bookkeeping, 12 API-call passes.
+   ml_profile: reset the per-class counters and record a CUDA event pair around every logical pass of the classes
+   in class_mask (0 = no event timing).  ml_profile_read (synchronises): per class [16] the summed event time (ms),
+   the passes launched, and the nonzeros streamed and segments (rows / columns) visited on the device. */
+ml_status ml_profile(ml_ctx *c, uint32_t class_mask);
+ml_status ml_profile_read(ml_ctx *c, double *ms_host, int64_t *passes_host, int64_t *nnz_host, int64_t *segs_host);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */
 int64_t ml_trace(ml_ctx *c, void *rows_host, int64_t cap);

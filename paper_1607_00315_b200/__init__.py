@@ -70,7 +70,8 @@ class TraceRow(ctypes.Structure):
 
 EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
-           "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace"]
+           "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
+           "ml_profile_read"]
 
 _lib = None
 
@@ -117,6 +118,10 @@ def load(path: str | None = None):
     L.ml_last_error.argtypes = [P]
     L.ml_kernel_launches.restype = i64
     L.ml_kernel_launches.argtypes = [P]
+    L.ml_profile.restype = i32
+    L.ml_profile.argtypes = [P, ctypes.c_uint32]
+    L.ml_profile_read.restype = i32
+    L.ml_profile_read.argtypes = [P, P, P, P, P]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
     _lib = L
@@ -148,7 +153,7 @@ class Context:
     region).  All methods take / return torch CUDA tensors.
     """
 
-    def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None):
+    def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None, host_tensors=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libml needs a CUDA device (no CPU fallback)")
@@ -159,16 +164,20 @@ class Context:
         self.lam = float(ds.lam if lam is None else lam)
         dev = self.device
 
-        def up(a, dt):
-            return torch.from_numpy(a).to(dev, dt)
+        if host_tensors is not None:   # pinned host tensors (rowptr, col, val, colptr, row, val, y): H2D copies
+            (self.csr_rowptr, self.csr_col, self.csr_val, self.csc_colptr, self.csc_row, self.csc_val,
+             self.y) = (t.to(dev, non_blocking=True) for t in host_tensors)
+        else:
+            def up(a, dt):
+                return torch.from_numpy(a).to(dev, dt)
 
-        self.csr_rowptr = up(ds.csr_rowptr, torch.int32)
-        self.csr_col = up(ds.csr_col, torch.int32)
-        self.csr_val = up(ds.csr_val, torch.float32)
-        self.csc_colptr = up(ds.csc_colptr, torch.int32)
-        self.csc_row = up(ds.csc_row, torch.int32)
-        self.csc_val = up(ds.csc_val, torch.float32)
-        self.y = up(ds.y, torch.int8)
+            self.csr_rowptr = up(ds.csr_rowptr, torch.int32)
+            self.csr_col = up(ds.csr_col, torch.int32)
+            self.csr_val = up(ds.csr_val, torch.float32)
+            self.csc_colptr = up(ds.csc_colptr, torch.int32)
+            self.csc_row = up(ds.csc_row, torch.int32)
+            self.csc_val = up(ds.csc_val, torch.float32)
+            self.y = up(ds.y, torch.int8)
         self.stream = stream or torch.cuda.current_stream(dev)
         wsb = int(L.ml_workspace_bytes(self.m, self.n, self.nnz))
         self.ws = torch.empty(wsb + 512, dtype=torch.uint8, device=dev)
@@ -180,6 +189,11 @@ class Context:
         if st != ML_OK:
             raise MLError(st, L.ml_status_str(st).decode())
         self.h = h
+
+    @classmethod
+    def from_host(cls, ds, pinned, device="cuda:0"):
+        """Public entry with host buffers: H2D of X (CSR + CSC) and y from pinned memory, then ml_create."""
+        return cls(ds, device=device, host_tensors=pinned)
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st, allow=()):
@@ -265,6 +279,19 @@ class Context:
         d = {f: getattr(rep, f) for f, _ in SolveReport._fields_ if f != "relax_per_level"}
         d["relax_per_level"] = list(rep.relax_per_level)
         return d
+
+    CLASSES = ["margins", "gather_fine", "gather_coarse", "scatter_XAs", "gather_Hs", "inner_dir", "mpass", "apply",
+               "outer_ls", "update", "select", "book", "api"]
+
+    def ml_profile(self, mask=0):
+        return self._check(load().ml_profile(self.h, int(mask)))
+
+    def ml_profile_read(self):
+        ms = (ctypes.c_double * 16)()
+        ps, nz, sg = ((ctypes.c_int64 * 16)() for _ in range(3))
+        self._check(load().ml_profile_read(self.h, ms, ps, nz, sg))
+        return {name: {"ms": ms[k], "passes": ps[k], "nnz": nz[k], "segs": sg[k]}
+                for k, name in enumerate(self.CLASSES)}
 
     def ml_kernel_launches(self):
         return int(load().ml_kernel_launches(self.h))

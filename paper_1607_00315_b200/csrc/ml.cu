@@ -25,6 +25,7 @@ constexpr int SM_COUNT = 148;
 constexpr int GRID_CAP = SM_COUNT * 4;
 constexpr int TRACE_CAP = 1 << 16;
 constexpr int NV_MAX = 96;   // widest reduction payload (doubles per block)
+constexpr int SMALL_M = 8192;   // m-vectors up to this size are accumulated in shared memory (k_scatter_smem)
 
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -40,6 +41,10 @@ struct Carve {                 // workspace layout; base == nullptr -> sizing on
 };
 
 struct UnitsMem { int4* u; double2* part; int* hcnt; int cap, hcap; };
+
+// pass classes for accounting (device nonzero/segment counters) and optional CUDA-event timing
+enum { CLS_MARGINS = 0, CLS_GATHER_FINE, CLS_GATHER_COARSE, CLS_SCATTER, CLS_HS, CLS_DIR, CLS_MPASS, CLS_APPLY,
+       CLS_OUTER, CLS_UPDATE, CLS_SELECT, CLS_BOOK, CLS_API, CLS_N };
 
 }  // namespace
 
@@ -62,8 +67,22 @@ struct ml_ctx {
     UnitsMem um[4];    // 0: all columns, 1: C list, 2: free set A, 3: rows
     int Gr, Gc;
     int gA, gM, gSeg, gHeavy;
+    // small-m shared-memory scatter
+    bool sm_scatter = false;
+    int scat_W = 0, scat_P = 0, gMP = 1;
+    size_t scat_bytes = 0;
+    bool sm_gather = false;
+    int gath_W = 0, gath_P = 0;
+    size_t gath_bytes = 0;
+    double* parts = nullptr;
     long long npos;
     long long launches = 0;
+    // profiling: event pairs per pass class (enabled classes only)
+    uint32_t prof_mask = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<int> ev_cls;      // class of each recorded pair (pair k = events 2k, 2k+1)
+    long long prof_passes[16] = {0};
     std::string err;
     Ctl h;             // host mirror of the control block
 };
@@ -73,8 +92,8 @@ namespace {
 void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     const size_t nn = (size_t)n, mm = (size_t)m;
     const size_t ntile_n = (nn + TILE - 1) / TILE, ntile_m = (mm + TILE - 1) / TILE;
-    const size_t ucap = (size_t)(nnz / CHUNK + nnz / SPLIT + 64);
-    const size_t hcap = (size_t)(nnz / SPLIT + 64);
+    const size_t hcap = (size_t)std::min<int64_t>(std::max(m, n), nnz / SPLIT_MIN) + 64;
+    const size_t ucap = (size_t)(nnz / CHUNK) + hcap;
     Ctl* ctl = cv.take<Ctl>(1);
     SelState* sel = cv.take<SelState>(1);
     TraceRow* trace = cv.take<TraceRow>(TRACE_CAP);
@@ -89,6 +108,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double2* tilepart = cv.take<double2>(ntile_n + 1);
     unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
     double2* hres = cv.take<double2>(std::max(nn, mm));
+    double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)SM_COUNT * 4 * mm : 1);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -112,7 +132,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     }
     if (!c) return;
     c->ctl = ctl; c->sel = sel; c->trace = trace; c->hres = hres;
-    c->lvl = lvl; c->lvl_cap = lvl_cap; c->lev = lev; c->emit_cnt = emit_cnt;
+    c->lvl = lvl; c->lvl_cap = lvl_cap; c->lev = lev; c->emit_cnt = emit_cnt; c->parts = parts;
     c->fine = fine; c->coarse = coarse;
     for (int k = 0; k < 4; ++k) c->um[k] = um[k];
     Prm& P = c->P;
@@ -138,8 +158,10 @@ Units units_of(ml_ctx* c, int slot) {
     return U;
 }
 
-Seg seg_rows(ml_ctx* c) { return Seg{c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, c->X.nnz, nullptr, c->hres}; }
-Seg seg_cols(ml_ctx* c, const int* list) { return Seg{c->X.csc_colptr, c->X.csc_row, c->X.csc_val, c->X.nnz, list, c->hres}; }
+Seg seg_rows(ml_ctx* c) { return Seg{c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, c->X.nnz, nullptr, c->hres, 8 * c->Gr}; }
+Seg seg_cols(ml_ctx* c, const int* list) {
+    return Seg{c->X.csc_colptr, c->X.csc_row, c->X.csc_val, c->X.nnz, list, c->hres, 8 * c->Gc};
+}
 
 #define ML_LAUNCH(c, kernel, grid, ...)                                                        \
     do {                                                                                       \
@@ -161,6 +183,28 @@ ml_status cuda_fail(ml_ctx* c, const char* where) {
     if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
     return ML_E_CUDA;
 }
+
+// RAII pass timer: records an event pair around one logical pass of class `cls` when that class is profiled
+struct PassScope {
+    ml_ctx* c;
+    int cls;
+    long long pair = -1;
+    PassScope(ml_ctx* c_, int cls_) : c(c_), cls(cls_) {
+        c->prof_passes[cls]++;
+        if (!(c->prof_mask & (1u << cls))) return;
+        if (c->ev_used + 2 > c->ev_pool.size()) {
+            for (int k = 0; k < 256; ++k) { cudaEvent_t e; cudaEventCreate(&e); c->ev_pool.push_back(e); }
+        }
+        pair = (long long)(c->ev_used / 2);
+        cudaEventRecord(c->ev_pool[c->ev_used], c->st);
+        c->ev_used += 2;
+        c->ev_cls.push_back(cls);
+    }
+    ~PassScope() {
+        if (pair >= 0) cudaEventRecord(c->ev_pool[2 * pair + 1], c->st);
+    }
+};
+inline long long* acc_of(ml_ctx* c, int cls) { return &c->ctl->cls[0][cls]; }
 
 ml_status sync_ctl(ml_ctx* c) {
     cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st);
@@ -251,46 +295,65 @@ __global__ void k_ls_prep(Prm P, ASet AS, const int* C, int nC, const double* g,
 void launch_units_build(ml_ctx* c, int slot, const int* list, int nlist_host) {
     Units U = units_of(c, slot);
     const int grid = std::max(1, std::min(GRID_CAP, (nlist_host + ML_NT - 1) / ML_NT));
-    ML_LAUNCH(c, k_units_build, grid, c->X.csc_colptr, list, (const int*)nullptr, nlist_host, U);
+    ML_LAUNCH(c, k_units_build, grid, c->X.csc_colptr, list, (const int*)nullptr, nlist_host, U, 8 * c->Gc);
 }
 
 // A1: heavy rows, then the light row kernel with the fused epilogue
 void launch_margins(ml_ctx* c) {
+    PassScope ps(c, CLS_MARGINS);
     Seg S = seg_rows(c);
     ML_LAUNCH(c, (k_heavy<OpMargin, false>), c->gHeavy, S, units_of(c, 3), OpMargin{c->P.w, c->P.wbits},
-              (const double*)nullptr, (double*)nullptr, (const int*)nullptr, (const int*)nullptr, &c->ctl->nnz_touched);
+              (const double*)nullptr, (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_MARGINS));
     const int grid = std::max(1, std::min(GRID_CAP, (int)((c->X.m + TILE - 1) / TILE)));
-    ML_DISPATCH_G(c->Gr, ML_LAUNCH(c, k_margins<GG>, grid, c->P, S));
+    ML_DISPATCH_G(c->Gr, ML_LAUNCH(c, k_margins<GG>, grid, c->P, S, acc_of(c, CLS_MARGINS)));
 }
 
 // A2 + A3 over C (list == nullptr: all columns, finest) into the ASet
 void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool finest) {
+    const int cls = finest ? CLS_GATHER_FINE : CLS_GATHER_COARSE;
+    PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
-              (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, &c->ctl->nnz_touched);
+              (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
     const int grid = std::max(1, std::min(GRID_CAP, (nC_host + TILE - 1) / TILE));
-    if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, units_of(c, 2))); }
-    else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2))); }
+    if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
+    else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
 }
 
-// X_A coef scatter into out (light + heavy), skipping on the relaxation flags
-void launch_scatter(ml_ctx* c, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
-                    double* out, const int* skip, const int* skip2) {
+// X_A coef scatter (A5).  Small m: shared-memory accumulation into per-block partials (summed into `out` here, or
+// by k_mpass when to_parts); otherwise light + heavy fp64-atomic scatter into `out` (zeroed by the caller).
+void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
+                    double* out, const int* skip, const int* skip2, bool to_parts = false) {
+    PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
+    if (c->sm_scatter) {
+        k_scatter_smem<<<c->scat_P, 32 * c->scat_W, c->scat_bytes, c->st>>>(S, nseg_dev, nseg_host, coef, c->parts,
+                                                                           (int)c->X.m, skip, skip2, acc_of(c, cls));
+        c->launches++;
+        if (!to_parts) ML_LAUNCH(c, k_parts_sum, c->gM, c->parts, c->scat_P, (int)c->X.m, out);
+        return;
+    }
     ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, out, skip, skip2,
-              &c->ctl->nnz_touched);
+              acc_of(c, cls));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, out, skip, skip2,
-                                   &c->ctl->nnz_touched));
+                                   acc_of(c, cls)));
 }
 
 // out = X_C^T v (+ eps s)
-void launch_gather_dot(ml_ctx* c, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
+void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
                        double* out, const double* s, double eps, const int* skip, const int* skip2) {
+    PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
+    if (c->sm_gather) {
+        k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out, s,
+                                                                         eps, skip, skip2, acc_of(c, cls));
+        c->launches++;
+        return;
+    }
     ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
-              (double*)nullptr, skip, skip2, &c->ctl->nnz_touched);
+              (double*)nullptr, skip, skip2, acc_of(c, cls));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
-                                   (double*)nullptr, s, eps, skip, skip2, &c->ctl->nnz_touched));
+                                   (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls)));
 }
 
 // R3-R18 on the free set in AS (its gather already ran): K inner iterations, outer line search, update.
@@ -299,22 +362,33 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
     const int nblkA = c->gA;
     for (int it = 0; it < K; ++it) {
         const bool pcd = !inner_cg || it == 0;
-        if (pcd) ML_LAUNCH(c, k_pcd_dir, c->gA, c->P, AS, it);
-        else {
-            ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
-            ML_LAUNCH(c, k_cg_s, c->gA, c->P, AS);
+        {
+            PassScope ps(c, CLS_DIR);
+            if (pcd) ML_LAUNCH(c, k_pcd_dir, c->gA, c->P, AS, it);
+            else {
+                ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
+                ML_LAUNCH(c, k_cg_s, c->gA, c->P, AS);
+            }
         }
-        launch_scatter(c, AS.A, 2, &ctl->nA, 0, AS.s, c->P.Xs, &ctl->skip, &ctl->inner_stop);
-        ML_LAUNCH(c, k_mpass, c->gM, c->P, pcd ? 1 : 0);
+        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, AS.s, c->P.Xs, &ctl->skip, &ctl->inner_stop, true);
+        {
+            PassScope ps(c, CLS_MPASS);
+            ML_LAUNCH(c, k_mpass, c->sm_scatter ? c->gMP : c->gM, c->P, pcd ? 1 : 0,
+                      c->sm_scatter ? (const double*)c->parts : nullptr, c->sm_scatter ? c->scat_P : 0);
+        }
         const int have_hs = it < K - 1;
         if (have_hs)
-            launch_gather_dot(c, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip, &ctl->inner_stop);
-        ML_LAUNCH(c, k_apply, nblkA + c->gM, c->P, AS, it, have_hs, nblkA);
+            launch_gather_dot(c, CLS_HS, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip,
+                              &ctl->inner_stop);
+        { PassScope ps(c, CLS_APPLY); ML_LAUNCH(c, k_apply, nblkA + c->gM, c->P, AS, it, have_hs, nblkA); }
     }
-    ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
-    ML_LAUNCH(c, k_outer_ls<ML_MAXLS - 4>, nblkA + c->gM, c->P, AS, 4, nblkA);
-    ML_LAUNCH(c, k_update, nblkA + c->gM, c->P, AS, nblkA);
-    ML_LAUNCH(c, k_relax_end, 1, c->P);
+    {
+        PassScope ps(c, CLS_OUTER);
+        ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
+        ML_LAUNCH(c, k_outer_ls<ML_MAXLS - 4>, nblkA + c->gM, c->P, AS, 4, nblkA);
+    }
+    { PassScope ps(c, CLS_UPDATE); ML_LAUNCH(c, k_update, nblkA + c->gM, c->P, AS, nblkA); }
+    { PassScope ps(c, CLS_BOOK); ML_LAUNCH(c, k_relax_end, 1, c->P); }
 }
 
 void set_params(ml_ctx* c, const ml_solve_opts* o) {
@@ -346,6 +420,7 @@ void launch_select(ml_ctx* c, SelIn in, int nin_host, int L, const std::vector<i
     for (int l = 0; l < L; ++l) { T.v[l] = targets[l]; O.v[l] = loff[l]; }
     // targets / offsets travel as kernel arguments (no host->device copies)
     const int grid = std::max(1, std::min(GRID_CAP, (nin_host + ML_NT - 1) / ML_NT));
+    PassScope ps(c, CLS_SELECT);
     ML_LAUNCH(c, k_sel_init_v, 1, c->sel, L, T);
     for (int d = 0; d < 12; ++d) ML_LAUNCH(c, k_sel_pass, grid, in, c->sel, d);
     ML_LAUNCH(c, k_sel_mark, grid, in, c->sel);
@@ -432,7 +507,34 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     c->gA = std::max(1, std::min(GRID_CAP, (int)((X->n + ML_NT - 1) / ML_NT)));
     c->gM = std::max(1, std::min(GRID_CAP, (int)((X->m + ML_NT - 1) / ML_NT)));
     c->gSeg = std::max(1, std::min(GRID_CAP, (int)((X->n + ML_NT - 1) / ML_NT)));
-    c->gHeavy = std::max(1, std::min(GRID_CAP, (int)((X->nnz / CHUNK + X->nnz / SPLIT + 8) / ML_NW + 1)));
+    c->gHeavy = std::max(1, std::min(GRID_CAP, (int)((X->nnz / CHUNK + std::min<int64_t>(std::max(X->m, X->n), X->nnz / SPLIT_MIN) + 8) / ML_NW + 1)));
+    if (X->m <= SMALL_M) {   // shared-memory passes: W warps per block, private m-vectors / shared sv + TMA rings
+        int W = 16;
+        while (W > 1 && scatter_smem_bytes(W, (int)X->m) > 200 * 1024) --W;
+        size_t bytes = scatter_smem_bytes(W, (int)X->m);
+        if (W >= 2 && bytes <= 220 * 1024 &&
+            cudaFuncSetAttribute(k_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
+            const int bps = std::max(1, std::min(4, (int)((228 * 1024) / (bytes + 1024))));
+            c->sm_scatter = true;
+            c->scat_W = W;
+            c->scat_bytes = bytes;
+            c->scat_P = SM_COUNT * bps;
+            c->gMP = std::max(1, std::min(GRID_CAP, (int)((X->m + 15) / 16)));
+            c->gMP = std::max(c->gMP, (int)((X->m + ML_NT - 1) / ML_NT));
+        }
+        W = 16;
+        while (W > 1 && gather_smem_bytes(W, (int)X->m) > 200 * 1024) --W;
+        bytes = gather_smem_bytes(W, (int)X->m);
+        if (W >= 2 && bytes <= 220 * 1024 &&
+            cudaFuncSetAttribute(k_gather_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
+            const int bps = std::max(1, std::min(4, (int)((228 * 1024) / (bytes + 1024))));
+            c->sm_gather = true;
+            c->gath_W = W;
+            c->gath_bytes = bytes;
+            c->gath_P = SM_COUNT * bps;
+        }
+        cudaGetLastError();
+    }
     // zero the control block, trace, bitmap, iterate and the heavy-unit counters
     cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st);
     cudaMemsetAsync(P.w, 0, sizeof(double) * X->n, c->st);
@@ -452,9 +554,9 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
         Units U = units_of(c, 0);
-        ML_LAUNCH(c, k_units_build, c->gSeg, X->csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U);
+        ML_LAUNCH(c, k_units_build, c->gSeg, X->csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U, 8 * c->Gc);
         Units R = units_of(c, 3);
-        ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R);
+        ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R, 8 * c->Gr);
     }
     ml_status s = sync_ctl(c);
     if (s != ML_OK) { *out = c; return s; }
@@ -471,6 +573,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
 ml_status ml_destroy(ml_ctx* c) {
     if (!c) return ML_E_INVAL;
     cudaStreamSynchronize(c->st);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return ML_OK;
 }
@@ -507,13 +610,14 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
         ML_LAUNCH(c, k_set_C, 1, c->ctl, nC, 1);
         launch_units_build(c, 1, C, nC);
     }
+    PassScope ps(c, CLS_API);
     Seg S = seg_cols(c, C);
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, slot), OpGH{c->P.rD}, (const double*)nullptr,
-              (double*)nullptr, (const int*)nullptr, (const int*)nullptr, &c->ctl->nnz_touched);
+              (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_API));
     const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,
                                    g_C, h_C, (const double*)nullptr, 0.0, (const int*)nullptr, (const int*)nullptr,
-                                   &c->ctl->nnz_touched));
+                                   acc_of(c, CLS_API)));
 }
 
 ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host, double* g_C, double* h_C) {
@@ -543,9 +647,9 @@ ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C,
         launch_units_build(c, 1, C, (int)nC);
     }
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
-    launch_scatter(c, C, slot, nullptr, (int)nC, v_C, c->P.Xs, nullptr, nullptr);   // X_C v
+    launch_scatter(c, CLS_API, C, slot, nullptr, (int)nC, v_C, c->P.Xs, nullptr, nullptr);   // X_C v
     ML_LAUNCH(c, k_dmul, c->gM, c->P, (int)c->X.m);                                   // D o X_C v
-    launch_gather_dot(c, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr);
+    launch_gather_dot(c, CLS_API, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr);
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
     return cuda_fail(c, "ml_hessvec");
 }
@@ -568,7 +672,7 @@ ml_status ml_shrink_linesearch(ml_ctx* c, const int32_t* C, int64_t nC, const do
             launch_units_build(c, 1, C, n);
         }
         cudaMemsetAsync(c->P.Xd, 0, sizeof(double) * c->X.m, c->st);
-        launch_scatter(c, C, slot, nullptr, n, AS.d, c->P.Xd, nullptr, nullptr);
+        launch_scatter(c, CLS_API, C, slot, nullptr, n, AS.d, c->P.Xd, nullptr, nullptr);
     }
     const int nblkA = c->gA;
     ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
@@ -603,6 +707,9 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     set_params(c, &o);
     std::memset(rep, 0, sizeof(*rep));
     const long long launches0 = c->launches;
+    long long nnz0 = 0;
+    const long long passes0 = c->prof_passes[CLS_MARGINS] + c->prof_passes[CLS_GATHER_FINE] +
+                              c->prof_passes[CLS_GATHER_COARSE] + c->prof_passes[CLS_SCATTER] + c->prof_passes[CLS_HS];
     const int n = (int)c->X.n;
     Ctl* ctl = c->ctl;
     // S1: w = 0, z = 0 (per-sample state refreshed by the first margins pass)
@@ -613,7 +720,8 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
         ml_status s = sync_ctl(c);
         if (s != ML_OK) return s;
         h0 = c->h;
-        h0.nS = 0; h0.l1 = 0.0; h0.ntrace = 0; h0.nnz_touched = 0; h0.level_conv = 0; h0.skip = 0;
+        for (int k = 0; k < 16; ++k) nnz0 += h0.cls[0][k];
+        h0.nS = 0; h0.l1 = 0.0; h0.ntrace = 0; h0.level_conv = 0; h0.skip = 0;
         h0.vmax_bits = 0ull; h0.dsupp = 0;
         cudaMemcpyAsync(ctl, &h0, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     }
@@ -689,7 +797,10 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     rep->cycles = std::min(cycle, o.max_cycles);
     rep->nnz_w = h.nS;
     rep->max_supp = std::max<int64_t>(max_supp, h.nS);
-    rep->nnz_touched = h.nnz_touched;
+    rep->nnz_touched = -nnz0;
+    for (int k = 0; k < 16; ++k) rep->nnz_touched += h.cls[0][k];
+    rep->x_passes = c->prof_passes[CLS_MARGINS] + c->prof_passes[CLS_GATHER_FINE] + c->prof_passes[CLS_GATHER_COARSE] +
+                    c->prof_passes[CLS_SCATTER] + c->prof_passes[CLS_HS] - passes0;
     // relaxations per level from the device trace
     const int nt = std::min(h.ntrace, TRACE_CAP);
     std::vector<TraceRow> tr(nt);
@@ -704,6 +815,36 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     ml_status fin = cuda_fail(c, "ml_solve");
     if (fin != ML_OK) return fin;
     return (ml_status)rep->status;
+}
+
+ml_status ml_profile(ml_ctx* c, uint32_t class_mask) {
+    if (!c) return ML_E_INVAL;
+    cudaStreamSynchronize(c->st);
+    c->prof_mask = class_mask;
+    c->ev_used = 0;
+    c->ev_cls.clear();
+    for (int k = 0; k < 16; ++k) c->prof_passes[k] = 0;
+    long long z[2][16] = {{0}};
+    cudaMemcpyAsync(&c->ctl->cls[0][0], z, sizeof(z), cudaMemcpyHostToDevice, c->st);
+    return cuda_fail(c, "ml_profile");
+}
+
+ml_status ml_profile_read(ml_ctx* c, double* ms, int64_t* passes, int64_t* nnz, int64_t* segs) {
+    if (!c) return ML_E_INVAL;
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    for (int k = 0; k < 16; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (passes) passes[k] = c->prof_passes[k];
+        if (nnz) nnz[k] = c->h.cls[0][k];
+        if (segs) segs[k] = c->h.cls[1][k];
+    }
+    if (ms)
+        for (size_t p = 0; p < c->ev_cls.size(); ++p) {
+            float t = 0.f;
+            if (cudaEventElapsedTime(&t, c->ev_pool[2 * p], c->ev_pool[2 * p + 1]) == cudaSuccess) ms[c->ev_cls[p]] += t;
+        }
+    return cuda_fail(c, "ml_profile_read");
 }
 
 // trace access for tests (not part of the paper's call set)

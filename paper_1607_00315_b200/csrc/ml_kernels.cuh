@@ -11,8 +11,8 @@
 
 namespace ml {
 
-constexpr int SPLIT = 1024;   // segments longer than this go to the heavy (split) path
-constexpr int CHUNK = 2048;   // nonzeros per heavy unit (one warp)
+constexpr int CHUNK = 1024;      // nonzeros per heavy unit (one warp)
+constexpr int SPLIT_MIN = 32;    // smallest heavy threshold (capacity bound); per-family threshold Seg::split = 8 G
 constexpr int TILE = ML_NT;   // segments per tile
 
 enum { OUT_UPDATED = 0, OUT_CONVERGED = 1, OUT_NOSTEP = 2, OUT_STAGNATION = 3 };
@@ -34,7 +34,7 @@ struct Ctl {
     unsigned red_ctr[8];
     unsigned tile_ctr, done_ctr, epoch, pad1;
     unsigned long long vmax_bits;
-    long long nnz_touched;
+    long long cls[2][16];         // per pass class: [0] nonzeros streamed, [1] segments (rows/columns) visited
     long long dsupp;
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
     int ntrace, trace_cap, bad_y, level, it;
@@ -59,6 +59,7 @@ struct Seg {
     long long nnz;
     const int* list;  // positions -> segment ids (nullptr = identity)
     double2* hres;    // heavy results per position
+    int split;        // segments longer than this take the heavy (split) path
 };
 
 // ------------------------------------------------------------------ per-element operations
@@ -82,92 +83,102 @@ struct OpDot {        // acc = sum_i X_ij v_i
     __device__ __forceinline__ void add(double& a0, double&, int r, float x) const { a0 += (double)x * __ldg(v + r); }
 };
 
-// Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).
-template <int G, class Op>
+// Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).  Each lane streams U 16-byte vectors of
+// indices and U of values per iteration (all loads issued before use), peeling the unaligned ends.
+template <int G, int U = 2, class Op>
 __device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int e, int lane, double& a0, double& a1) {
-    for (int k = (b & ~3) + 4 * lane; k < e; k += 8 * G) {
-        int4 i0, i1 = make_int4(0, 0, 0, 0);
-        float4 v0, v1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int k1 = k + 4 * G;
-        if (k + 4 <= S.nnz) { i0 = ld_stream_i4(S.idx + k); v0 = ld_stream_f4(S.val + k); }
-        else {
-            i0.x = S.idx[k]; v0.x = S.val[k];
-            i0.y = (k + 1 < S.nnz) ? S.idx[k + 1] : 0; v0.y = (k + 1 < S.nnz) ? S.val[k + 1] : 0.f;
-            i0.z = (k + 2 < S.nnz) ? S.idx[k + 2] : 0; v0.z = (k + 2 < S.nnz) ? S.val[k + 2] : 0.f;
-            i0.w = 0; v0.w = 0.f;
+    for (int k = (b & ~3) + 4 * lane; k < e; k += 4 * U * G) {
+        int4 iv[U];
+        float4 vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int ku = k + 4 * G * u;
+            if (ku < e && ku + 4 <= S.nnz) { iv[u] = ld_stream_i4(S.idx + ku); vv[u] = ld_stream_f4(S.val + ku); }
+            else if (ku < e) {
+                iv[u].x = S.idx[ku]; vv[u].x = S.val[ku];
+                iv[u].y = (ku + 1 < S.nnz) ? S.idx[ku + 1] : 0; vv[u].y = (ku + 1 < S.nnz) ? S.val[ku + 1] : 0.f;
+                iv[u].z = (ku + 2 < S.nnz) ? S.idx[ku + 2] : 0; vv[u].z = (ku + 2 < S.nnz) ? S.val[ku + 2] : 0.f;
+                iv[u].w = 0; vv[u].w = 0.f;
+            } else { iv[u] = make_int4(0, 0, 0, 0); vv[u] = make_float4(0.f, 0.f, 0.f, 0.f); }
         }
-        const bool has1 = k1 < e;
-        if (has1) {
-            if (k1 + 4 <= S.nnz) { i1 = ld_stream_i4(S.idx + k1); v1 = ld_stream_f4(S.val + k1); }
-            else {
-                i1.x = S.idx[k1]; v1.x = S.val[k1];
-                i1.y = (k1 + 1 < S.nnz) ? S.idx[k1 + 1] : 0; v1.y = (k1 + 1 < S.nnz) ? S.val[k1 + 1] : 0.f;
-                i1.z = (k1 + 2 < S.nnz) ? S.idx[k1 + 2] : 0; v1.z = (k1 + 2 < S.nnz) ? S.val[k1 + 2] : 0.f;
-            }
-        }
-        if (k >= b && k + 3 < e) {
-            op.add(a0, a1, i0.x, v0.x); op.add(a0, a1, i0.y, v0.y);
-            op.add(a0, a1, i0.z, v0.z); op.add(a0, a1, i0.w, v0.w);
-        } else {
-            if (k >= b && k < e) op.add(a0, a1, i0.x, v0.x);
-            if (k + 1 >= b && k + 1 < e) op.add(a0, a1, i0.y, v0.y);
-            if (k + 2 >= b && k + 2 < e) op.add(a0, a1, i0.z, v0.z);
-            if (k + 3 >= b && k + 3 < e) op.add(a0, a1, i0.w, v0.w);
-        }
-        if (has1) {
-            if (k1 + 3 < e) {
-                op.add(a0, a1, i1.x, v1.x); op.add(a0, a1, i1.y, v1.y);
-                op.add(a0, a1, i1.z, v1.z); op.add(a0, a1, i1.w, v1.w);
-            } else {
-                op.add(a0, a1, i1.x, v1.x);
-                if (k1 + 1 < e) op.add(a0, a1, i1.y, v1.y);
-                if (k1 + 2 < e) op.add(a0, a1, i1.z, v1.z);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int ku = k + 4 * G * u;
+            if (ku >= b && ku + 3 < e) {
+                op.add(a0, a1, iv[u].x, vv[u].x); op.add(a0, a1, iv[u].y, vv[u].y);
+                op.add(a0, a1, iv[u].z, vv[u].z); op.add(a0, a1, iv[u].w, vv[u].w);
+            } else if (ku < e) {
+                if (ku >= b) op.add(a0, a1, iv[u].x, vv[u].x);
+                if (ku + 1 >= b && ku + 1 < e) op.add(a0, a1, iv[u].y, vv[u].y);
+                if (ku + 2 >= b && ku + 2 < e) op.add(a0, a1, iv[u].z, vv[u].z);
+                if (ku + 3 >= b && ku + 3 < e) op.add(a0, a1, iv[u].w, vv[u].w);
             }
         }
     }
 }
 
 // One tile of TILE consecutive segment positions; results (a0, a1) land in res[slot] (shared memory).
-// Heavy segments (> SPLIT) are not streamed here: their results come from S.hres, written by k_heavy.
-// Returns (in *s_len) the number of nonzeros of the light segments streamed by this block (accounting).
+// The tile's segment bounds are loaded once, in parallel (one thread per segment), so the G rounds only stream.
+// Heavy segments (> S.split) are not streamed here: their results come from S.hres, written by k_heavy.
 template <int G, class Op>
-__device__ __forceinline__ long long seg_tile(const Seg& S, const Op& op, int nseg, int tile, double2* res) {
+__device__ __forceinline__ void seg_tile(const Seg& S, const Op& op, int nseg, int tile, double2* res, long long& streamed,
+                                         long long& segs) {
     constexpr int NG = ML_NT / G;
-    const int grp = threadIdx.x / G, lane = threadIdx.x % G;
-    long long streamed = 0;
-#pragma unroll 1
-    for (int r = 0; r < G; ++r) {
-        const int slot = r * NG + grp;
-        const int p = tile * TILE + slot;
+    __shared__ int sb[TILE], se[TILE];
+    {
+        const int p = tile * TILE + threadIdx.x;
         int b = 0, e = 0;
-        bool heavy = false;
         if (p < nseg) {
             const int j = S.list ? __ldg(S.list + p) : p;
             b = __ldg(S.ptr + j);
             e = __ldg(S.ptr + j + 1);
-            heavy = (e - b) > SPLIT;
-            if (heavy) e = b;
-            else if (lane == 0) streamed += e - b;
+            segs += 1;
+            if (e - b > S.split) { res[threadIdx.x] = ld_cg(S.hres + p); b = 0; e = -1; }
+            else streamed += e - b;
         }
+        sb[threadIdx.x] = b;
+        se[threadIdx.x] = e;
+    }
+    __syncthreads();
+    const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+#pragma unroll 1
+    for (int r = 0; r < G; ++r) {
+        const int slot = r * NG + grp;
+        const int b = sb[slot], e = se[slot];
         double a0 = 0.0, a1 = 0.0;
         seg_accum<G>(S, op, b, e, lane, a0, a1);
         a0 = group_sum<G>(a0);
         a1 = group_sum<G>(a1);
-        if (lane == 0) res[slot] = heavy ? ld_cg(S.hres + p) : make_double2(a0, a1);
+        if (lane == 0 && e >= 0) res[slot] = make_double2(a0, a1);
     }
-    return streamed;
+}
+
+// pass accounting: acc[0] += nonzeros streamed, acc[16] += segments visited (block-reduced, integer atomics)
+__device__ __forceinline__ void acc_add(long long* acc, long long nnz, long long segs) {
+    __shared__ long long s_acc[2][32];
+    const int lane = threadIdx.x & 31;
+    long long a = warp_sum_ll(nnz), b = warp_sum_ll(segs);
+    if (lane == 0) { s_acc[0][threadIdx.x >> 5] = a; s_acc[1][threadIdx.x >> 5] = b; }
+    __syncthreads();
+    if (threadIdx.x == 0 && acc) {
+        long long x = 0, y = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { x += s_acc[0][k]; y += s_acc[1][k]; }
+        if (x) atomicAdd((unsigned long long*)acc, (unsigned long long)x);
+        if (y) atomicAdd((unsigned long long*)(acc + 16), (unsigned long long)y);
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------ heavy units
 // Build the heavy-unit schedule of a segment list: every segment longer than SPLIT gets ceil(len/CHUNK) units.
 // Unit order is arbitrary (atomics); results do not depend on it.
 __global__ void k_units_build(const int* __restrict__ ptr, const int* __restrict__ list, const int* nseg_dev, int nseg_host,
-                              Units U) {
+                              Units U, int split) {
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nseg; p += gridDim.x * ML_NT) {
         const int j = list ? list[p] : p;
         const int len = ptr[j + 1] - ptr[j];
-        if (len > SPLIT) {
+        if (len > split) {
             const int nch = (len + CHUNK - 1) / CHUNK;
             const int hs = atomicAdd(U.h, 1);
             const int base = atomicAdd(U.n, nch);
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
         } else {
             if (lane == 0) streamed += e - b;
             double a0 = 0.0, a1 = 0.0;
-            seg_accum<32>(S, op, b, e, lane, a0, a1);
+            seg_accum<32, 4>(S, op, b, e, lane, a0, a1);
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
             int last = 0;
@@ -223,19 +234,8 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
             }
         }
     }
-    if (nnz_acc) {
-        __shared__ long long sm_nnz[ML_NW];
-        long long v = warp_sum_ll(streamed);
-        if (lane == 0) sm_nnz[threadIdx.x >> 5] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            long long t = 0;
-            for (int k = 0; k < ML_NW; ++k) t += sm_nnz[k];
-            if (t) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)t);
-        }
-    }
+    acc_add(nnz_acc, streamed, 0);
 }
-
 // ------------------------------------------------------------------ parameters shared by the relaxation kernels
 struct Prm {
     int m, n;
@@ -253,32 +253,19 @@ struct Prm {
 // free-set buffers of one relaxation (fine or coarse set)
 struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd; double* s; double* Hs; double* u; };
 
-__device__ __forceinline__ void add_nnz(Ctl* ctl, long long v, long long* sm) {
-    const int lane = threadIdx.x & 31;
-    long long t = warp_sum_ll(v);
-    if (lane == 0) sm[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long s = 0;
-        for (int k = 0; k < ML_NW; ++k) s += sm[k];
-        if (s) atomicAdd((unsigned long long*)&ctl->nnz_touched, (unsigned long long)s);
-    }
-    __syncthreads();
-}
 
 // ------------------------------------------------------------------ A1: margins (full CSR pass)
 // z = Xw (CSR, support-bitmap-gated gathers of w), then per row: t, ell, r, D; L = sum ell.
 template <int G>
-__global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S) {
+__global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc) {
     __shared__ double2 res[TILE];
     __shared__ double sm[3 * ML_NW + 3];
-    __shared__ long long smn[ML_NW];
     OpMargin op{P.w, P.wbits};
     const int ntiles = (P.m + TILE - 1) / TILE;
     double lsum = 0.0;
-    long long streamed = 0;
+    long long streamed = 0, segs = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        streamed += seg_tile<G>(S, op, P.m, tile, res);
+        seg_tile<G>(S, op, P.m, tile, res, streamed, segs);
         __syncthreads();
         const int i = tile * TILE + threadIdx.x;
         if (i < P.m) {
@@ -290,7 +277,7 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S) {
         }
         __syncthreads();
     }
-    add_nnz(P.ctl, streamed, smn);
+    acc_add(acc, streamed, segs);
     Red<1> r;
     r.s[0] = lsum;
     if (grid_reduce(r, P.part, &P.ctl->red_ctr[0], sm)) {
@@ -305,12 +292,11 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S) {
 // columns get their heavy units appended to UA.  FINEST additionally computes ||w||_1 and sum |v| exactly.
 // The last block to finish: nA, vmax, the convergence decision (R2), counters reset, epoch advance.
 template <int G, bool FINEST>
-__global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Units UA) {
+__global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Units UA, long long* acc) {
     __shared__ double2 res[TILE];
     __shared__ int s_tile, s_excl;
     __shared__ int s_wcnt[ML_NW];
     __shared__ double s_red[2 * ML_NW];
-    __shared__ long long smn[ML_NW];
     __shared__ bool s_last;
     Ctl* ctl = P.ctl;
     if (ctl->skip) return;   // (not used at the finest level; coarse relaxations of a converged level)
@@ -319,14 +305,14 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
     const unsigned epoch = ctl->epoch;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     OpGH op{P.rD};
-    long long streamed = 0;
+    long long streamed = 0, segs = 0;
     double vmax_loc = 0.0;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
-        streamed += seg_tile<G>(S, op, nC, tile, res);
+        seg_tile<G>(S, op, nC, tile, res, streamed, segs);
         __syncthreads();
         const int p = tile * TILE + threadIdx.x;
         int j = 0, flag = 0, len = 0;
@@ -390,7 +376,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
             AS.gA[o] = g;
             AS.hA[o] = h + P.eps_h;
             AS.wA[o] = wj;
-            if (len > SPLIT) {   // heavy free column: schedule its units for the Hessian-vector passes over A
+            if (len > S.split) {   // heavy free column: schedule its units for the Hessian-vector passes over A
                 const int nch = (len + CHUNK - 1) / CHUNK;
                 const int hs = atomicAdd(UA.h, 1);
                 const int base = atomicAdd(UA.n, nch);
@@ -399,7 +385,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
         }
         __syncthreads();
     }
-    add_nnz(ctl, streamed, smn);
+    acc_add(acc, streamed, segs);
     // block max -> global atomic max (order-independent)
     {
         double v = warp_max(vmax_loc);
@@ -449,13 +435,12 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
                                                       double* out1, const double* s, double eps, const int* skip,
                                                       const int* skip2, long long* nnz_acc) {
     __shared__ double2 res[TILE];
-    __shared__ long long smn[ML_NW];
     if ((skip && *skip) || (skip2 && *skip2)) return;
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int ntiles = (nseg + TILE - 1) / TILE;
-    long long streamed = 0;
+    long long streamed = 0, segs = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        streamed += seg_tile<G>(S, op, nseg, tile, res);
+        seg_tile<G>(S, op, nseg, tile, res, streamed, segs);
         __syncthreads();
         const int p = tile * TILE + threadIdx.x;
         if (p < nseg) {
@@ -465,48 +450,283 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
         }
         __syncthreads();
     }
-    if (nnz_acc) {
-        const int lane = threadIdx.x & 31;
-        long long t = warp_sum_ll(streamed);
-        if (lane == 0) smn[threadIdx.x >> 5] = t;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            long long a = 0;
-            for (int k = 0; k < ML_NW; ++k) a += smn[k];
-            if (a) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)a);
-        }
-    }
+    acc_add(nnz_acc, streamed, segs);
 }
-
 // ------------------------------------------------------------------ A5: X_A s scatter (light segments)
 template <int G>
 __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef,
                                                    double* out, const int* skip, const int* skip2, long long* nnz_acc) {
-    __shared__ long long smn[ML_NW];
     if ((skip && *skip) || (skip2 && *skip2)) return;
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int grp = (blockIdx.x * ML_NT + threadIdx.x) / G, lane = threadIdx.x % G;
     const int ngrp = gridDim.x * (ML_NT / G);
-    long long streamed = 0;
+    long long streamed = 0, segs = 0;
     for (int p = grp; p < nseg; p += ngrp) {
         const double cf = coef[p];
         if (cf == 0.0) continue;
         const int j = S.list ? __ldg(S.list + p) : p;
         const int b = __ldg(S.ptr + j), e = __ldg(S.ptr + j + 1);
-        if (e - b > SPLIT) continue;   // heavy columns: k_heavy<SCATTER>
+        if (lane == 0) segs += 1;
+        if (e - b > S.split) continue;   // heavy columns: k_heavy<SCATTER>
         if (lane == 0) streamed += e - b;
         for (int k = b + lane; k < e; k += G) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
     }
-    if (nnz_acc) {
-        const int ln = threadIdx.x & 31;
-        long long t = warp_sum_ll(streamed);
-        if (ln == 0) smn[threadIdx.x >> 5] = t;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            long long a = 0;
-            for (int k = 0; k < ML_NW; ++k) a += smn[k];
-            if (a) atomicAdd((unsigned long long*)nnz_acc, (unsigned long long)a);
+    acc_add(nnz_acc, streamed, segs);
+}
+// ------------------------------------------------------------------ A5 for small m: shared-memory passes
+// When an m-vector fits in shared memory, the Hessian-vector passes over X_A stream whole columns per warp through
+// a TMA-staged ring: one elected lane issues cp.async.bulk copies of SCH-element chunks of indices and values
+// (mbarrier completion), NSTG chunks in flight per warp independently of occupancy; column metadata (coefficient,
+// column pointers) is fetched 32 columns at a time, one per lane, and shuffled out, so no lane walks a dependent
+// load chain per chunk.  Block b owns positions [b*q, (b+1)*q); warp w takes every W-th position of that range.
+// SCH: elements per staged chunk (4*SCH bytes of indices + 4*SCH of values); NSTG: chunks in flight per warp.
+
+struct ChunkDesc { int a, vb, ve, ce; int p, last; double cf; };   // copy start, valid [vb, ve), copied to ce
+
+template <int SCH, int NSTG>
+struct ColStream {
+    // warp-uniform producer state
+    int p0, p1, W, wid, lane, nnz4;
+    int batch, kk, noff;
+    int mb, me;        // this lane's metadata for position p0 + wid + W * (batch * 32 + lane)
+    double mcf;
+    long long streamed, segs;
+    const Seg* S;
+    const double* coef;
+    int* sidx; float* sval; uint64_t* bar; ChunkDesc* desc;
+
+    __device__ void load_batch() {
+        const int p = p0 + wid + W * (batch * 32 + lane);
+        mb = 0; me = 0; mcf = 0.0;
+        if (p < p1) {
+            mcf = coef ? coef[p] : 1.0;
+            if (mcf != 0.0) {
+                const int j = S->list ? __ldg(S->list + p) : p;
+                mb = __ldg(S->ptr + j);
+                me = __ldg(S->ptr + j + 1);
+            }
         }
+        kk = 0;
+    }
+    // next chunk descriptor (all lanes, uniform); false when the warp's range is exhausted
+    __device__ bool next(ChunkDesc& d) {
+        while (true) {
+            if (kk == 32) { ++batch; load_batch(); }
+            const int p = p0 + wid + W * (batch * 32 + kk);
+            if (p >= p1) return false;
+            const int b = __shfl_sync(0xffffffffu, mb, kk), e = __shfl_sync(0xffffffffu, me, kk);
+            const double cf = __shfl_sync(0xffffffffu, mcf, kk);
+            const int start = b + noff;
+            if (cf == 0.0 || start >= e) {
+                if (!coef && noff == 0 && cf != 0.0) {   // gather mode: an empty column still gets its (zero) output
+                    d.a = b & ~3; d.vb = b; d.ve = b; d.ce = d.a; d.cf = 1.0; d.p = p; d.last = 1;
+                    ++kk;
+                    return true;
+                }
+                ++kk; noff = 0; continue;
+            }
+            if (noff == 0 && lane == 0) { streamed += e - b; segs += 1; }
+            d.a = start & ~3;
+            d.vb = start;
+            d.ve = min(e, d.a + SCH);
+            d.ce = min((d.ve + 3) & ~3, nnz4);
+            if (d.ce < d.a) d.ce = d.a;
+            d.cf = cf;
+            d.p = p;
+            d.last = (d.ve == e);
+            if (d.last) { ++kk; noff = 0; } else noff = d.ve - b;
+            return true;
+        }
+    }
+    __device__ void issue(int st, const ChunkDesc& d) {   // lane 0 only
+        const uint32_t bytes = 4u * (uint32_t)(d.ce - d.a);
+        if (bytes) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(bar + st, 2 * bytes);
+            bulk_g2s(sidx + st * SCH, S->idx + d.a, bytes, bar + st);
+            bulk_g2s(sval + st * SCH, S->val + d.a, bytes, bar + st);
+        } else {
+            mbar_arrive(bar + st);
+        }
+    }
+};
+
+// per-warp shared-memory layout: [idx NSTG*SCH int][val NSTG*SCH float][bars NSTG][desc NSTG][acc m double (scatter)]
+template <int SCH, int NSTG>
+__host__ __device__ inline size_t stream_warp_bytes(int m_acc) {
+    const size_t b = (size_t)8 * NSTG * SCH + 8 * NSTG + NSTG * sizeof(ChunkDesc) + (size_t)8 * m_acc;
+    return (b + 15) / 16 * 16;
+}
+constexpr int SC_SCH = 512, SC_NSTG = 2;   // scatter ring (the private m-vector shares the warp's shared memory)
+constexpr int GA_SCH = 512, GA_NSTG = 3;   // gather ring
+__host__ __device__ inline size_t scatter_smem_bytes(int W, int m) { return (size_t)W * stream_warp_bytes<SC_SCH, SC_NSTG>(m); }
+__host__ __device__ inline size_t gather_smem_bytes(int W, int m) {
+    return (size_t)W * stream_warp_bytes<GA_SCH, GA_NSTG>(0) + (size_t)8 * m;
+}
+
+template <int SCH, int NSTG>
+__device__ __forceinline__ void stream_setup(ColStream<SCH, NSTG>& cs, unsigned char* base, const Seg& S, const double* coef, int nseg,
+                                             int m_acc) {
+    cs.W = blockDim.x >> 5;
+    cs.wid = threadIdx.x >> 5;
+    cs.lane = threadIdx.x & 31;
+    const int q = (nseg + gridDim.x - 1) / gridDim.x;
+    cs.p0 = blockIdx.x * q;
+    cs.p1 = min(nseg, cs.p0 + q);
+    cs.nnz4 = (int)(S.nnz & ~3LL);
+    cs.batch = 0;
+    cs.noff = 0;
+    cs.streamed = 0;
+    cs.segs = 0;
+    cs.S = &S;
+    cs.coef = coef;
+    cs.sidx = reinterpret_cast<int*>(base);
+    cs.sval = reinterpret_cast<float*>(base + 4 * NSTG * SCH);
+    cs.bar = reinterpret_cast<uint64_t*>(base + 8 * NSTG * SCH);
+    cs.desc = reinterpret_cast<ChunkDesc*>(cs.bar + NSTG);
+    (void)m_acc;
+    if (cs.lane == 0) {
+        for (int k = 0; k < NSTG; ++k) mbar_init(cs.bar + k, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    cs.load_batch();
+    // prologue: fill the ring
+    for (int st = 0; st < NSTG; ++st) {
+        ChunkDesc d;
+        const bool ok = cs.next(d);
+        if (cs.lane == 0) {
+            if (ok) { cs.desc[st] = d; cs.issue(st, d); }
+            else cs.desc[st].cf = 0.0;   // cf == 0 marks "no chunk"
+        }
+        if (!ok) {
+            for (int s2 = st + 1; s2 < NSTG; ++s2) if (cs.lane == 0) cs.desc[s2].cf = 0.0;
+            break;
+        }
+    }
+    __syncwarp();
+}
+
+// X_A s into per-block partials (see above); every warp accumulates into its private shared m-vector: rows inside one
+// column are distinct, so lanes never collide (plain LDS/STS, no atomics); warps and blocks are combined in fixed order.
+__global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef, double* parts,
+                               int m, const int* skip, const int* skip2, long long* acc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    if ((skip && *skip) || (skip2 && *skip2)) return;
+    constexpr int SCH = SC_SCH, NSTG = SC_NSTG;
+    const size_t pw = stream_warp_bytes<SCH, NSTG>(m);
+    unsigned char* base = smraw + (size_t)(threadIdx.x >> 5) * pw;
+    double* mine = reinterpret_cast<double*>(base + stream_warp_bytes<SCH, NSTG>(0));
+    for (int i = (threadIdx.x & 31); i < m; i += 32) mine[i] = 0.0;
+    const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+    ColStream<SCH, NSTG> cs;
+    stream_setup(cs, base, S, coef, nseg, m);
+    uint32_t phase = 0u;
+    int st = 0;
+    while (true) {
+        const ChunkDesc d = cs.desc[st];
+        if (d.cf == 0.0) break;
+        mbar_wait(cs.bar + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const int* ci = cs.sidx + st * SCH - d.a;
+        const float* cv = cs.sval + st * SCH - d.a;
+        const int kend = min(d.ve, d.ce);
+        int k = d.vb + cs.lane;
+        for (; k + 96 < kend; k += 128) {   // four independent read-modify-writes (distinct rows)
+            const int r0 = ci[k], r1 = ci[k + 32], r2 = ci[k + 64], r3 = ci[k + 96];
+            const double x0 = mine[r0], x1 = mine[r1], x2 = mine[r2], x3 = mine[r3];
+            mine[r0] = fma((double)cv[k], d.cf, x0);
+            mine[r1] = fma((double)cv[k + 32], d.cf, x1);
+            mine[r2] = fma((double)cv[k + 64], d.cf, x2);
+            mine[r3] = fma((double)cv[k + 96], d.cf, x3);
+        }
+        for (; k < kend; k += 32) { const int r = ci[k]; mine[r] = fma((double)cv[k], d.cf, mine[r]); }
+        for (; k < d.ve; k += 32) {   // array tail not covered by 16-byte copies
+            const int r = __ldg(S.idx + k);
+            mine[r] = fma((double)__ldg(S.val + k), d.cf, mine[r]);
+        }
+        __syncwarp();
+        ChunkDesc nd;
+        const bool ok = cs.next(nd);
+        if (cs.lane == 0) {
+            if (ok) { cs.desc[st] = nd; cs.issue(st, nd); }
+            else cs.desc[st].cf = 0.0;
+        }
+        __syncwarp();
+        st = (st + 1) % NSTG;
+    }
+    __syncthreads();
+    const int W = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < W; ++w)
+            t += reinterpret_cast<const double*>(smraw + (size_t)w * pw + stream_warp_bytes<SCH, NSTG>(0))[i];
+        parts[(size_t)blockIdx.x * m + i] = t;
+    }
+    acc_add(acc, cs.streamed, cs.segs);
+}
+
+// Hs_p = sum_i X_ij sv_i + eps s_p over the positions of A, with sv staged once per block in shared memory and the
+// columns streamed through the TMA ring; one warp per column, lane partials reduced at the column's last chunk.
+__global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ v, int m, double* out,
+                              const double* s, double eps, const int* skip, const int* skip2, long long* acc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    if ((skip && *skip) || (skip2 && *skip2)) return;
+    constexpr int SCH = GA_SCH, NSTG = GA_NSTG;
+    const int W = blockDim.x >> 5;
+    double* sv = reinterpret_cast<double*>(smraw + (size_t)W * stream_warp_bytes<SCH, NSTG>(0));
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sv[i] = v[i];
+    __syncthreads();
+    unsigned char* base = smraw + (size_t)(threadIdx.x >> 5) * stream_warp_bytes<SCH, NSTG>(0);
+    const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+    ColStream<SCH, NSTG> cs;
+    stream_setup(cs, base, S, nullptr, nseg, 0);
+    uint32_t phase = 0u;
+    int st = 0;
+    double a = 0.0;
+    while (true) {
+        const ChunkDesc d = cs.desc[st];
+        if (d.cf == 0.0) break;
+        mbar_wait(cs.bar + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const int* ci = cs.sidx + st * SCH - d.a;
+        const float* cv = cs.sval + st * SCH - d.a;
+        const int kend = min(d.ve, d.ce);
+        int k = d.vb + cs.lane;
+        double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (; k + 96 < kend; k += 128) {
+            a = fma((double)cv[k], sv[ci[k]], a);
+            a1 = fma((double)cv[k + 32], sv[ci[k + 32]], a1);
+            a2 = fma((double)cv[k + 64], sv[ci[k + 64]], a2);
+            a3 = fma((double)cv[k + 96], sv[ci[k + 96]], a3);
+        }
+        a += (a1 + a2) + a3;
+        for (; k < kend; k += 32) a = fma((double)cv[k], sv[ci[k]], a);
+        for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv[__ldg(S.idx + k)], a);
+        if (d.last) {
+            const double t = warp_sum(a);
+            if (cs.lane == 0) out[d.p] = t + (s ? eps * s[d.p] : 0.0);
+            a = 0.0;
+        }
+        __syncwarp();
+        ChunkDesc nd;
+        const bool ok = cs.next(nd);
+        if (cs.lane == 0) {
+            if (ok) { cs.desc[st] = nd; cs.issue(st, nd); }
+            else cs.desc[st].cf = 0.0;
+        }
+        __syncwarp();
+        st = (st + 1) % NSTG;
+    }
+    acc_add(acc, cs.streamed, cs.segs);
+}
+
+// out[i] = sum_b parts[b][i] (block order)
+__global__ void k_parts_sum(const double* __restrict__ parts, int nparts, int m, double* out) {
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
+        double t = 0.0;
+        for (int b = 0; b < nparts; ++b) t += parts[(size_t)b * m + i];
+        out[i] = t;
     }
 }
 
@@ -637,46 +857,72 @@ __global__ void __launch_bounds__(ML_NT) k_cg_s(Prm P, ASet AS) {
 
 // m-side pass after the scatter: sv = D o Xs (for the Hs gather); s^T H s = sum D Xs^2 + eps ||s||^2; then the
 // inner step: PCD -> Armijo on the model over b = beta^t (R10); CG -> b = min(b_q, b_kink) (R6').
-__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int pcd) {
+// With the shared-memory scatter, Xs_i is first summed from the per-block partials: block b takes a slice of R
+// rows and its 256 threads split the partials of each row into 256/R interleaved groups, combined in group order.
+__device__ __forceinline__ void mpass_decide(Prm& P, Ctl* c, double dxs2, int pcd) {
+    const double sHs = dxs2 + P.eps_h * c->ss;
+    c->sHs = sHs;
+    if (pcd) {
+        const double delta = c->ps + P.lam * c->l1diff_out[0];
+        double b = 1.0;
+        int ok = 0;
+        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+            const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
+            if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+        }
+        c->beta = ok ? b : 0.0;
+        c->snap = 0;
+        if (!ok) c->inner_stop = 1;
+        c->cg_restart = 1;
+    } else {
+        if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; }
+        else {
+            const double bq = -c->slope / sHs;
+            c->bq = bq;
+            c->beta = bq < c->bk ? bq : c->bk;
+            c->snap = (c->bk <= bq);
+            c->cg_restart = c->snap;
+            c->rz_prev = c->rz;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int pcd, const double* __restrict__ parts, int nparts) {
     __shared__ double sm[2 * ML_NW + 2];
+    __shared__ double sred[ML_NT];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     Red<1> r;
     r.zero();
-    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
-        const double xs = P.Xs[i];
-        const double D = P.rD[i].y;
-        P.sv[i] = D * xs;
-        r.s[0] += D * xs * xs;
+    if (parts) {
+        const int R = (P.m + gridDim.x - 1) / gridDim.x;           // rows per block (<= ML_NT by construction)
+        const int ng = max(1, ML_NT / max(R, 1));                  // partial groups per row
+        const int row0 = blockIdx.x * R;
+        const int rr = threadIdx.x % R, grp = threadIdx.x / R;
+        double t = 0.0;
+        if (grp < ng && row0 + rr < P.m)
+            for (int b = grp; b < nparts; b += ng) t += parts[(size_t)b * P.m + row0 + rr];
+        sred[threadIdx.x] = t;
+        __syncthreads();
+        if (threadIdx.x < R && row0 + threadIdx.x < P.m) {
+            double xs = 0.0;
+            for (int g = 0; g < ng; ++g) xs += sred[g * R + threadIdx.x];
+            const int i = row0 + threadIdx.x;
+            const double D = P.rD[i].y;
+            P.Xs[i] = xs;
+            P.sv[i] = D * xs;
+            r.s[0] += D * xs * xs;
+        }
+    } else {
+        for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
+            const double xs = P.Xs[i];
+            const double D = P.rD[i].y;
+            P.sv[i] = D * xs;
+            r.s[0] += D * xs * xs;
+        }
     }
     if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
-        if (threadIdx.x == 0) {
-            const double sHs = r.s[0] + P.eps_h * c->ss;
-            c->sHs = sHs;
-            if (pcd) {
-                const double delta = c->ps + P.lam * c->l1diff_out[0];
-                double b = 1.0;
-                int ok = 0;
-                for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
-                    const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
-                    if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
-                }
-                c->beta = ok ? b : 0.0;
-                c->snap = 0;
-                if (!ok) c->inner_stop = 1;
-                c->cg_restart = 1;
-            } else {
-                if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; }
-                else {
-                    const double bq = -c->slope / sHs;
-                    c->bq = bq;
-                    c->beta = bq < c->bk ? bq : c->bk;
-                    c->snap = (c->bk <= bq);
-                    c->cg_restart = c->snap;
-                    c->rz_prev = c->rz;
-                }
-            }
-        }
+        if (threadIdx.x == 0) mpass_decide(P, c, r.s[0], pcd);
     }
 }
 
@@ -711,12 +957,13 @@ __global__ void __launch_bounds__(ML_NT) k_apply(Prm P, ASet AS, int it, int hav
     }
 }
 
-// R14-R16, first batch of the outer line search (Eq. 4; Armijo DESIGN Q7, Q26): A-range blocks reduce
-// g^T d, max|d| and the l1 trial differences sum(|w + a_t d| - |w|) for every trial; m-range blocks reduce
-// sum_i dloss(t_i, a_t y_i Xd_i) for trials t0 <= t < t1.  Last block: Delta, decision.
+// R14-R16: one batch of trials [t0, t0 + NT1) of the outer line search (Eq. 4; Armijo DESIGN Q7, Q26).
+// A-range blocks reduce the l1 trial differences sum(|w + a_t d| - |w|) of the batch (and, in the first batch,
+// g^T d and max|d|); m-range blocks reduce sum_i dloss(t_i, a_t y_i Xd_i).  Last block: Delta, decision.
+// The first batch is {1, 1/2, 1/4, 1/8}; the second (rare) covers the remaining trials up to max_ls.
 template <int NT1>
 __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int nblkA) {
-    constexpr int NS = 1 + ML_MAXLS + NT1;
+    constexpr int NS = 1 + 2 * NT1;
     __shared__ double sm[(NS + 1) * ML_NW + NS + 1];
     Ctl* c = P.ctl;
     if (c->skip) return;
@@ -729,20 +976,23 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     const int T1 = min(P.max_ls, t0 + NT1);
     Red<NS, 1> r;
     r.zero();
-    double at[ML_MAXLS];
-    at[0] = 1.0;
+    double at[NT1];
+    {
+        double a = 1.0;
+        for (int t = 0; t < t0; ++t) a *= P.beta_ls;
 #pragma unroll
-    for (int t = 1; t < ML_MAXLS; ++t) at[t] = at[t - 1] * P.beta_ls;
+        for (int k = 0; k < NT1; ++k) { at[k] = a; a *= P.beta_ls; }
+    }
     if ((int)blockIdx.x < nblkA) {
-        if (t0 == 0) {
-            const int nA = c->nA;
-            for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
-                const double d = AS.d[p], w = AS.wA[p], aw = fabs(w);
+        const int nA = c->nA;
+        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
+            const double d = AS.d[p], w = AS.wA[p], aw = fabs(w);
+            if (t0 == 0) {
                 r.s[0] += AS.gA[p] * d;
                 r.mx[0] = fmax(r.mx[0], fabs(d));
-#pragma unroll
-                for (int t = 0; t < ML_MAXLS; ++t) r.s[1 + t] += fabs(w + at[t] * d) - aw;
             }
+#pragma unroll
+            for (int k = 0; k < NT1; ++k) r.s[1 + k] += fabs(w + at[k] * d) - aw;
         }
     } else {
         const int nb = gridDim.x - nblkA;
@@ -751,23 +1001,21 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
             const double ti = y * P.z[i], yx = y * P.Xd[i];
 #pragma unroll
             for (int k = 0; k < NT1; ++k)
-                if (t0 + k < T1) r.s[1 + ML_MAXLS + k] += dloss(ti, at[t0 + k] * yx);
+                if (t0 + k < T1) r.s[1 + NT1 + k] += dloss(ti, at[k] * yx);
         }
     }
     if (grid_reduce(r, P.part, &c->red_ctr[5], sm)) {
         if (threadIdx.x == 0) {
             if (t0 == 0) {
                 c->gd = r.s[0];
-                for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[1 + t];
                 c->Delta = r.s[0] + P.lam * r.s[1];
                 if (r.mx[0] == 0.0) { c->skip = 1; c->outcome = OUT_NOSTEP; return; }
             }
+            for (int k = 0; k < NT1 && t0 + k < T1; ++k) c->l1diff_out[t0 + k] = r.s[1 + k];
             const double Delta = c->Delta;
             for (int k = 0; k < NT1 && t0 + k < T1; ++k) {
-                const int t = t0 + k;
-                const double a = at[t];
-                const double dF = r.s[1 + ML_MAXLS + k] + P.lam * c->l1diff_out[t];
-                if (dF <= P.sigma_out * a * Delta) { c->ls_ok = 1; c->alpha = a; c->t_acc = t; break; }
+                const double dF = r.s[1 + NT1 + k] + P.lam * r.s[1 + k];
+                if (dF <= P.sigma_out * at[k] * Delta) { c->ls_ok = 1; c->alpha = at[k]; c->t_acc = t0 + k; break; }
             }
             if (!c->ls_ok && T1 >= P.max_ls) { c->skip = 1; c->outcome = OUT_STAGNATION; c->alpha = 0.0; }
         }
