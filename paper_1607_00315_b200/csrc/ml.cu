@@ -104,11 +104,12 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* Xd = cv.take<double>(mm);
     double* Xs = cv.take<double>(mm);
     double* sv = cv.take<double>(mm);
+    double* Xu = cv.take<double>(mm);
     double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
     double2* tilepart = cv.take<double2>(ntile_n + 1);
     unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
     double2* hres = cv.take<double2>(std::max(nn, mm));
-    double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)SM_COUNT * 4 * mm : 1);
+    double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -136,7 +137,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     c->fine = fine; c->coarse = coarse;
     for (int k = 0; k < 4; ++k) c->um[k] = um[k];
     Prm& P = c->P;
-    P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv;
+    P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
 
@@ -221,6 +222,7 @@ __global__ void k_init_rows(Prm P, int m) {   // w = 0: z = 0, r = -y/2, D = 1/4
         P.rD[i] = make_double2(s.r, s.D);
         P.Xs[i] = 0.0;
         P.Xd[i] = 0.0;
+        P.Xu[i] = 0.0;
     }
 }
 __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* npos) {
@@ -287,6 +289,7 @@ __global__ void k_ls_prep(Prm P, ASet AS, const int* C, int nC, const double* g,
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Ctl* c = P.ctl;
         c->nA = nC; c->nC = nC; c->skip = 0; c->ls_ok = 0; c->napply = 1; c->outcome = OUT_NOSTEP; c->level = -1;
+        c->acc_steps = 1; c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1;
         c->F_before = c->F;
     }
 }
@@ -320,43 +323,66 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
     else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
 }
 
-// X_A coef scatter (A5).  Small m: shared-memory accumulation into per-block partials (summed into `out` here, or
-// by k_mpass when to_parts); otherwise light + heavy fp64-atomic scatter into `out` (zeroed by the caller).
+// X_A coef scatter (A5).  mode 0 (API): the result lands in `out` (atomic path: out zeroed by the caller; small-m
+// path: partials summed by k_parts_sum).  mode 1/2 (relaxation, PCD / PCD-CG): small m -> k_scatter_smem with its
+// fused m-side pass; otherwise atomics into P.Xu followed by k_mpass.
 void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
-                    double* out, const int* skip, const int* skip2, bool to_parts = false) {
-    PassScope ps(c, cls);
+                    double* out, const int* skip, const int* skip2, int mode = 0) {
     Seg S = seg_cols(c, list);
     if (c->sm_scatter) {
-        k_scatter_smem<<<c->scat_P, 32 * c->scat_W, c->scat_bytes, c->st>>>(S, nseg_dev, nseg_host, coef, c->parts,
-                                                                           (int)c->X.m, skip, skip2, acc_of(c, cls));
-        c->launches++;
-        if (!to_parts) ML_LAUNCH(c, k_parts_sum, c->gM, c->parts, c->scat_P, (int)c->X.m, out);
+        {
+            PassScope ps(c, cls);
+            Prm Pc = c->P;
+            int m = (int)c->X.m;
+            long long* ac = acc_of(c, cls);
+            double* parts = c->parts;
+            void* args[] = {(void*)&S, (void*)&nseg_dev, (void*)&nseg_host, (void*)&coef, (void*)&parts, (void*)&m,
+                            (void*)&skip, (void*)&skip2, (void*)&ac, (void*)&Pc, (void*)&mode, (void*)&out};
+            cudaLaunchCooperativeKernel((const void*)k_scatter_smem, dim3(c->scat_P), dim3(32 * c->scat_W), args,
+                                        c->scat_bytes, c->st);
+            c->launches++;
+        }
         return;
     }
-    ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, out, skip, skip2,
-              acc_of(c, cls));
-    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, out, skip, skip2,
-                                   acc_of(c, cls)));
+    double* dst = mode ? c->P.Xu : out;
+    {
+        PassScope ps(c, cls);
+        ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, dst, skip, skip2,
+                  acc_of(c, cls));
+        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, dst, skip, skip2,
+                                       acc_of(c, cls)));
+    }
+    if (mode) { PassScope ps(c, CLS_MPASS); ML_LAUNCH(c, k_mpass, c->gM, c->P, mode); }
 }
 
-// out = X_C^T v (+ eps s)
+// out = X_C^T v (+ eps s); mode 2: the PCD-CG epilogue and step decision (see k_gather_out / k_gather_smem)
 void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
-                       double* out, const double* s, double eps, const int* skip, const int* skip2) {
+                       double* out, const double* s, double eps, const int* skip, const int* skip2, int mode = 1,
+                       const ASet* AS = nullptr) {
     PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
+    const ASet A0 = AS ? *AS : c->coarse;
     if (c->sm_gather) {
         k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out, s,
-                                                                         eps, skip, skip2, acc_of(c, cls));
+                                                                         eps, skip, skip2, acc_of(c, cls), c->P, A0,
+                                                                         mode);
         c->launches++;
         return;
     }
     ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
               (double*)nullptr, skip, skip2, acc_of(c, cls));
-    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
-                                   (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls)));
+    if (mode == 2) {
+        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 2, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
+                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
+    } else {
+        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
+                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
+    }
 }
 
 // R3-R18 on the free set in AS (its gather already ran): K inner iterations, outer line search, update.
+// Per inner iteration: direction kernel (applies the previous step), scatter X_A s (+ m-side pass and, for PCD, the
+// step decision), Hs gather (+ for PCD-CG the step decision).  Steps are applied lazily (see decide_pcd).
 void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
     Ctl* ctl = c->ctl;
     const int nblkA = c->gA;
@@ -365,22 +391,14 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
         {
             PassScope ps(c, CLS_DIR);
             if (pcd) ML_LAUNCH(c, k_pcd_dir, c->gA, c->P, AS, it);
-            else {
-                ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
-                ML_LAUNCH(c, k_cg_s, c->gA, c->P, AS);
-            }
+            else ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
         }
-        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, AS.s, c->P.Xs, &ctl->skip, &ctl->inner_stop, true);
-        {
-            PassScope ps(c, CLS_MPASS);
-            ML_LAUNCH(c, k_mpass, c->sm_scatter ? c->gMP : c->gM, c->P, pcd ? 1 : 0,
-                      c->sm_scatter ? (const double*)c->parts : nullptr, c->sm_scatter ? c->scat_P : 0);
-        }
-        const int have_hs = it < K - 1;
-        if (have_hs)
+        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, pcd ? AS.s : AS.u, nullptr, &ctl->skip, &ctl->inner_stop,
+                       pcd ? 1 : 2);
+        if (it < K - 1)
             launch_gather_dot(c, CLS_HS, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip,
-                              &ctl->inner_stop);
-        { PassScope ps(c, CLS_APPLY); ML_LAUNCH(c, k_apply, nblkA + c->gM, c->P, AS, it, have_hs, nblkA); }
+                              &ctl->inner_stop, pcd ? 1 : 2, &AS);
+        else if (!pcd) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, c->gA, c->P, AS); }
     }
     {
         PassScope ps(c, CLS_OUTER);
@@ -514,8 +532,10 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
         size_t bytes = scatter_smem_bytes(W, (int)X->m);
         if (W >= 2 && bytes <= 220 * 1024 &&
             cudaFuncSetAttribute(k_scatter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
-            const int bps = std::max(1, std::min(4, (int)((228 * 1024) / (bytes + 1024))));
-            c->sm_scatter = true;
+            int bps = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_scatter_smem, 32 * W, bytes);
+            bps = std::min(bps, 4);
+            c->sm_scatter = bps >= 1;
             c->scat_W = W;
             c->scat_bytes = bytes;
             c->scat_P = SM_COUNT * bps;
@@ -617,7 +637,7 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
     const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,
                                    g_C, h_C, (const double*)nullptr, 0.0, (const int*)nullptr, (const int*)nullptr,
-                                   acc_of(c, CLS_API)));
+                                   acc_of(c, CLS_API), c->P, c->coarse));
 }
 
 ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host, double* g_C, double* h_C) {
@@ -649,7 +669,7 @@ ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C,
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
     launch_scatter(c, CLS_API, C, slot, nullptr, (int)nC, v_C, c->P.Xs, nullptr, nullptr);   // X_C v
     ML_LAUNCH(c, k_dmul, c->gM, c->P, (int)c->X.m);                                   // D o X_C v
-    launch_gather_dot(c, CLS_API, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr);
+    launch_gather_dot(c, CLS_API, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr, 0);
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
     return cuda_fail(c, "ml_hessvec");
 }

@@ -7,7 +7,11 @@
 // segment (deterministic).  Epilogues (per-sample logistic quantities, free-set compaction with KKT, Hessian-vector
 // outputs) run on the reduced values while they are in shared memory.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "ml_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ml {
 
@@ -26,6 +30,9 @@ struct Ctl {
     int ls_ok, scattered, nS, nAf;
     int skipped, t_acc;
     int nC, pad0;
+    int pend, pend_m, d_init, xd_init, acc_steps, combine, pcd_mode, pad3;
+    unsigned grp_ctr[128];
+    unsigned grp_done, pad4;
     const int* Cptr;            // current restriction list (nullptr = all columns)
     double vmax, v1, l1, L, F, F_before;
     double beta, alpha, rz, rz_prev, bcg, slope, ss, ps, delta, bk, bq, sHs, Delta, gd, vq;
@@ -169,6 +176,46 @@ __device__ __forceinline__ void acc_add(long long* acc, long long nnz, long long
     __syncthreads();
 }
 
+// Block-wide sum / min for any blockDim (multiple of 32); every thread returns the block value.
+__device__ __forceinline__ double block_sum_any(double v) {
+    __shared__ double sh[32];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    __syncthreads();
+    return t;
+}
+__device__ __forceinline__ double block_min_any(double v) {
+    __shared__ double sh[32];
+    v = warp_min(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = sh[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) t = fmin(t, sh[k]);
+    __syncthreads();
+    return t;
+}
+// Grid-wide min through per-block partials and the last-arriving block (any blockDim); true in the last block.
+__device__ bool grid_min_any(double& v, double* part, unsigned* ctr) {
+    __shared__ bool s_last;
+    const double b = block_min_any(v);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = b;
+        __threadfence();
+        s_last = (atomicAdd(ctr, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    double t = __longlong_as_double(0x7ff0000000000000LL);
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) t = fmin(t, ld_cg(part + k));
+    v = block_min_any(t);
+    if (threadIdx.x == 0) *ctr = 0u;
+    return true;
+}
+
 // ------------------------------------------------------------------ heavy units
 // Build the heavy-unit schedule of a segment list: every segment longer than SPLIT gets ceil(len/CHUNK) units.
 // Unit order is arbitrary (atomics); results do not depend on it.
@@ -243,7 +290,8 @@ struct Prm {
     double lam, eps_h, sigma_in, sigma_out, beta_ls, tol, eta;
     int max_ls, inner_cg;
     double* w; uint32_t* wbits; double* z; double2* rD;
-    double* Xd; double* Xs; double* sv;
+    double* Xd; double* Xs; double* sv; double* Xu;   // Xu: scatter target of the atomic path (kept zero between uses)
+    double* parts; int nparts;                        // small-m scatter: per-block partials (+ group partials)
     Ctl* ctl;
     double* part;              // reduction partials
     double2* tilepart;         // per-tile partials of the compaction kernels
@@ -253,6 +301,66 @@ struct Prm {
 // free-set buffers of one relaxation (fine or coarse set)
 struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd; double* s; double* Hs; double* u; };
 
+
+// ------------------------------------------------------------------ inner-step decisions and deferred application
+// The inner step s accepted in iteration `it` (length beta, optional kink snap) is applied lazily: to d and Hd by the
+// next direction kernel (or the outer line search), to Xd by the next m-side pass (or the outer line search).
+// R6-R10, PCD: Armijo on the model over beta = 1, 1/2, ... with delta the model's linear part at beta = 1.
+__device__ __forceinline__ void decide_pcd(const Prm& P, Ctl* c, double sHs) {
+    c->sHs = sHs;
+    const double delta = c->ps + P.lam * c->l1diff_out[0];
+    double b = 1.0;
+    int ok = 0;
+    for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+        const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
+        if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+    }
+    c->cg_restart = 1;
+    if (!ok) { c->inner_stop = 1; c->beta = 0.0; return; }
+    c->beta = b;
+    c->snap = 0;
+    c->pend = 1;
+    c->pend_m = 1;
+    c->acc_steps += 1;
+}
+// R6', PCD-CG: exact step on the quadratic piece, truncated at the first kink (b_k), kink coordinates snapped to 0.
+__device__ __forceinline__ void decide_cg(const Prm& P, Ctl* c, double bk) {
+    c->bk = bk;
+    const double sHs = c->sHs;
+    if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; return; }
+    const double bq = -c->slope / sHs;
+    c->bq = bq;
+    c->beta = bq < bk ? bq : bk;
+    c->snap = (bk <= bq);
+    c->cg_restart = c->snap;
+    c->rz_prev = c->rz;
+    c->pend = 1;
+    c->pend_m = 1;
+    c->acc_steps += 1;
+}
+struct Pending {   // a snapshot of the pending step, read once per kernel
+    int on, init, snap;
+    double beta, bk;
+};
+__device__ __forceinline__ Pending pending_A(const Ctl* c) { return Pending{c->pend, c->d_init, c->snap, c->beta, c->bk}; }
+__device__ __forceinline__ Pending pending_m(const Ctl* c) { return Pending{c->pend_m, c->xd_init, 0, c->beta, 0.0}; }
+// d (and Hd when Hs is valid) after the pending step at position p; writes them back
+__device__ __forceinline__ double apply_A(const Pending& q, const ASet& AS, int p, bool with_hd, double* Hd_out) {
+    double d = q.init ? AS.d[p] : 0.0;
+    double hd = (with_hd && q.init) ? AS.Hd[p] : 0.0;
+    if (q.on) {
+        const double sp = AS.s[p];
+        const double x = AS.wA[p] + d;
+        const bool kink = q.snap && x * sp < 0.0 && -x / sp == q.bk;
+        d = kink ? -AS.wA[p] : d + q.beta * sp;   // a coordinate reaching its kink becomes exactly 0
+        AS.d[p] = d;
+        if (with_hd) { hd += q.beta * AS.Hs[p]; AS.Hd[p] = hd; }
+    }
+    if (Hd_out) *Hd_out = hd;
+    return d;
+}
+__device__ __forceinline__ void consume_A(Ctl* c) { if (c->pend) { c->pend = 0; c->d_init = 1; } }
+__device__ __forceinline__ void consume_m(Ctl* c) { if (c->pend_m) { c->pend_m = 0; c->xd_init = 1; } }
 
 // ------------------------------------------------------------------ A1: margins (full CSR pass)
 // z = Xw (CSR, support-bitmap-gated gathers of w), then per row: t, ell, r, D; L = sum ell.
@@ -430,15 +538,22 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
 // ------------------------------------------------------------------ plain gathers (API outputs / Hessian-vector)
 // MODE 0: out0[p] = g, out1[p] = h (either may be null)      (ml_eval_f_grad, ml_diag_hess)
 // MODE 1: out0[p] = sum X_ij v_i (+ eps_h * s[p] if s)       (Hs = X_A^T (D o Xs) + eps s, ml_hessvec)
+// MODE 2: PCD-CG epilogue: s_p = u_p + b s_prev_p, Hs_p = acc + eps s_p, first kink b_k = min_{x s < 0} -x/s,
+//         last block: the CG step decision (R6')
 template <int G, int MODE, class Op>
 __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* nseg_dev, int nseg_host, double* out0,
                                                       double* out1, const double* s, double eps, const int* skip,
-                                                      const int* skip2, long long* nnz_acc) {
+                                                      const int* skip2, long long* nnz_acc, Prm P, ASet AS) {
     __shared__ double2 res[TILE];
+    __shared__ double smr[2 * ML_NW + 2];
     if ((skip && *skip) || (skip2 && *skip2)) return;
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int ntiles = (nseg + TILE - 1) / TILE;
     long long streamed = 0, segs = 0;
+    double bcg = 0.0;
+    if (MODE == 2) bcg = P.ctl->bcg;
+    Red<0, 0, 1> r;
+    r.zero();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         seg_tile<G>(S, op, nseg, tile, res, streamed, segs);
         __syncthreads();
@@ -446,12 +561,24 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
         if (p < nseg) {
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
-            else out0[p] = q.x + (s ? eps * s[p] : 0.0);
+            else if (MODE == 1) out0[p] = q.x + (s ? eps * s[p] : 0.0);
+            else {
+                const double sp = AS.u[p] + bcg * AS.s[p];
+                AS.s[p] = sp;
+                out0[p] = q.x + eps * sp;
+                const double x = AS.wA[p] + AS.d[p];
+                if (x * sp < 0.0) r.mn[0] = fmin(r.mn[0], -x / sp);
+            }
         }
         __syncthreads();
     }
     acc_add(nnz_acc, streamed, segs);
+    if (MODE == 2) {
+        if (grid_reduce(r, P.part, &P.ctl->red_ctr[3], smr))
+            if (threadIdx.x == 0) decide_cg(P, P.ctl, r.mn[0]);
+    }
 }
+
 // ------------------------------------------------------------------ A5: X_A s scatter (light segments)
 template <int G>
 __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef,
@@ -609,8 +736,12 @@ __device__ __forceinline__ void stream_setup(ColStream<SCH, NSTG>& cs, unsigned 
 
 // X_A s into per-block partials (see above); every warp accumulates into its private shared m-vector: rows inside one
 // column are distinct, so lanes never collide (plain LDS/STS, no atomics); warps and blocks are combined in fixed order.
+// Cooperative launch.  After the per-block partials, one grid barrier; then every block combines its slice of rows
+// over all partials (fixed order) and runs the m-side pass on it: mode 0 (API) out = X_A coef; mode 1 / 2 (PCD /
+// PCD-CG relaxation step): pending Xd += beta Xs, Xs = Xu (+ b Xs_prev for CG), sv = D o Xs, and s^T H s summed in
+// block order by the last block, which also takes the PCD decision.
 __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef, double* parts,
-                               int m, const int* skip, const int* skip2, long long* acc) {
+                               int m, const int* skip, const int* skip2, long long* acc, Prm P, int mode, double* out_api) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if ((skip && *skip) || (skip2 && *skip2)) return;
     constexpr int SCH = SC_SCH, NSTG = SC_NSTG;
@@ -664,12 +795,70 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         parts[(size_t)blockIdx.x * m + i] = t;
     }
     acc_add(acc, cs.streamed, cs.segs);
+    // all partials written -> grid barrier (cooperative launch: every block is resident)
+    __threadfence();
+    cg::this_grid().sync();
+    // block b combines rows [b*R, b*R + R) over all partials: thread t sums the partials k = g, g + ng, ... of row
+    // t % R (g = t / R); groups are combined in order -> deterministic
+    Ctl* c = P.ctl;
+    const int R = (m + gridDim.x - 1) / gridDim.x;
+    const int ng = max(1, (int)blockDim.x / max(R, 1));
+    const int row0 = blockIdx.x * R, rr = threadIdx.x % max(R, 1), grp = threadIdx.x / max(R, 1);
+    double* red = reinterpret_cast<double*>(smraw);   // the staging rings are no longer needed
+    double t = 0.0;
+    if (grp < ng && row0 + rr < m && rr < R)
+        for (int k = grp; k < (int)gridDim.x; k += ng) t += ld_cg(parts + (size_t)k * m + row0 + rr);
+    red[threadIdx.x] = t;
+    __syncthreads();
+    double a2 = 0.0;
+    const Pending q = pending_m(c);
+    const double bcg = (mode == 2) ? c->bcg : 0.0;
+    if ((int)threadIdx.x < R && row0 + (int)threadIdx.x < m) {
+        double xu = 0.0;
+        for (int g = 0; g < ng; ++g) xu += red[g * R + threadIdx.x];
+        const int i = row0 + threadIdx.x;
+        if (mode == 0) out_api[i] = xu;
+        else {
+            const double xs_old = P.Xs[i];
+            if (q.on) P.Xd[i] = (q.init ? P.Xd[i] : 0.0) + q.beta * xs_old;
+            const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
+            P.Xs[i] = xs;
+            const double D = P.rD[i].y;
+            P.sv[i] = D * xs;
+            a2 = D * xs * xs;
+        }
+    }
+    if (mode == 0) return;
+    // grid sum of D Xs^2 through per-block partials and the last block (block order)
+    __shared__ bool s_last;
+    const double bs = block_sum_any(a2);
+    if (threadIdx.x == 0) {
+        parts[(size_t)gridDim.x * m + blockIdx.x] = bs;
+        __threadfence();
+        s_last = (atomicAdd(&c->grp_done, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double tt = 0.0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) tt += ld_cg(parts + (size_t)gridDim.x * m + k);
+    const double tot = block_sum_any(tt);
+    if (threadIdx.x == 0) {
+        consume_m(c);
+        const double sHs = tot + P.eps_h * c->ss;
+        if (mode == 1) decide_pcd(P, c, sHs);
+        else c->sHs = sHs;
+        c->grp_done = 0u;
+    }
 }
 
 // Hs_p = sum_i X_ij sv_i + eps s_p over the positions of A, with sv staged once per block in shared memory and the
 // columns streamed through the TMA ring; one warp per column, lane partials reduced at the column's last chunk.
+// mode 0/1: out_p = acc (+ eps s_p); mode 2: PCD-CG epilogue (s_p = u_p + b s_prev_p, Hs_p = acc + eps s_p, first kink)
+// and the CG decision in the last block.
 __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ v, int m, double* out,
-                              const double* s, double eps, const int* skip, const int* skip2, long long* acc) {
+                              const double* s, double eps, const int* skip, const int* skip2, long long* acc, Prm P,
+                              ASet AS, int mode) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if ((skip && *skip) || (skip2 && *skip2)) return;
     constexpr int SCH = GA_SCH, NSTG = GA_NSTG;
@@ -684,6 +873,8 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
     uint32_t phase = 0u;
     int st = 0;
     double a = 0.0;
+    const double bcg = (mode == 2) ? P.ctl->bcg : 0.0;
+    double bkmin = __longlong_as_double(0x7ff0000000000000LL);
     while (true) {
         const ChunkDesc d = cs.desc[st];
         if (d.cf == 0.0) break;
@@ -705,7 +896,15 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv[__ldg(S.idx + k)], a);
         if (d.last) {
             const double t = warp_sum(a);
-            if (cs.lane == 0) out[d.p] = t + (s ? eps * s[d.p] : 0.0);
+            if (cs.lane == 0) {
+                if (mode == 2) {
+                    const double sp = AS.u[d.p] + bcg * AS.s[d.p];
+                    AS.s[d.p] = sp;
+                    out[d.p] = t + eps * sp;
+                    const double x = AS.wA[d.p] + AS.d[d.p];
+                    if (x * sp < 0.0) bkmin = fmin(bkmin, -x / sp);
+                } else out[d.p] = t + (s ? eps * s[d.p] : 0.0);
+            }
             a = 0.0;
         }
         __syncwarp();
@@ -719,6 +918,10 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         st = (st + 1) % NSTG;
     }
     acc_add(acc, cs.streamed, cs.segs);
+    if (mode == 2) {
+        if (grid_min_any(bkmin, P.part, &P.ctl->red_ctr[3]))
+            if (threadIdx.x == 0) decide_cg(P, P.ctl, bkmin);
+    }
 }
 
 // out[i] = sum_b parts[b][i] (block order)
@@ -745,20 +948,28 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
     c->ls_ok = 0;
     c->level = level;
     c->it = 0;
+    c->pend = 0;
+    c->pend_m = 0;
+    c->d_init = 0;
+    c->xd_init = 0;
+    c->acc_steps = 0;
+    c->combine = 0;
     c->units_n[2] = 0;   // A-set units are rebuilt by the gather
     c->units_h[2] = 0;
     if (set_list) { c->Cptr = Cptr; c->nC = nC; }
     (void)finest;
 }
 
-// R5-R6 (PCD step, Eq. 5 with D = diag(H) + eps_h): s = Sh_{lam/h}(x - p/h) - x, x = w_A + d, p = g_A + Hd.
-// Reduction: p^T s, ||s||^2, l1 trial differences sum(|x + b_t s| - |x|) for b_t = beta^t, max|s|, model min-norm
-// subgradient (forcing).  Last block: stop flags.
+// R5-R7 (PCD step, Eq. 5 with D = diag(H) + eps_h): first the pending step of the previous iteration is applied
+// to d and Hd; then s = Sh_{lam/h}(x - p/h) - x with x = w_A + d, p = g_A + Hd.  Reduction: p^T s, ||s||^2, the l1
+// trial differences sum(|x + b_t s| - |x|) for b_t = beta^t (all max_ls trials of R10), max|s|, and the model's
+// min-norm subgradient (forcing, R13).
 __global__ void __launch_bounds__(ML_NT) k_pcd_dir(Prm P, ASet AS, int it) {
     __shared__ double sm[(ML_MAXLS + 4) * ML_NW + ML_MAXLS + 4];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     const int nA = c->nA;
+    const Pending q = pending_A(c);
     Red<ML_MAXLS + 2, 2> r;
     r.zero();
     double bt[ML_MAXLS];
@@ -766,201 +977,143 @@ __global__ void __launch_bounds__(ML_NT) k_pcd_dir(Prm P, ASet AS, int it) {
 #pragma unroll
     for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
     for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        const double d = it ? AS.d[p] : 0.0, Hd = it ? AS.Hd[p] : 0.0;
+        double Hd;
+        const double d = apply_A(q, AS, p, true, &Hd);
         const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-        const double s = soft(x - pj / hh, P.lam / hh) - x;
-        AS.s[p] = s;
+        const double sp = soft(x - pj / hh, P.lam / hh) - x;
+        AS.s[p] = sp;
         const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
-        r.mx[0] = fmax(r.mx[0], fabs(s));
+        r.mx[0] = fmax(r.mx[0], fabs(sp));
         r.mx[1] = fmax(r.mx[1], fabs(v));
-        r.s[0] += pj * s;
-        r.s[1] += s * s;
+        r.s[0] += pj * sp;
+        r.s[1] += sp * sp;
         const double ax = fabs(x);
 #pragma unroll
-        for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * s) - ax;
+        for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * sp) - ax;
     }
     if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
         if (threadIdx.x == 0) {
+            consume_A(c);
             c->ps = r.s[0];
             c->ss = r.s[1];
             c->vq = r.mx[1];
-            for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // reused as inner l1 diffs
+            for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // inner l1 trial differences
             int stop = 0;
             if (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax) stop = 1;   // R13 forcing
             if (r.mx[0] == 0.0) stop = 1;                                        // R7
             c->inner_stop = stop;
-            c->scattered = !stop;
+            c->pcd_mode = 1;
+            c->combine = 0;
+            c->bcg = 0.0;
             c->it = it;
         }
     }
 }
 
-// PCD-CG, part 1 (R6'): u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere; rz = sum h u^2;
-// forcing test; b = rz / rz_prev unless restarting.
+// PCD-CG direction (R6'): after applying the pending step, u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere;
+// rz = sum h u^2; b = rz / rz_prev unless restarting.  The search direction s = u + b s_prev is formed later (in the
+// Hs gather); its slope and squared norm come from the decomposition over (u, s_prev) reduced here.
 __global__ void __launch_bounds__(ML_NT) k_cg_z(Prm P, ASet AS, int it) {
-    __shared__ double sm[3 * ML_NW + 3];
+    __shared__ double sm[7 * ML_NW + 7];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     const int nA = c->nA;
-    Red<1, 1> r;
+    const Pending q = pending_A(c);
+    Red<6, 1> r;
     r.zero();
     for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        const double x = AS.wA[p] + AS.d[p], pj = AS.gA[p] + AS.Hd[p], hh = AS.hA[p];
-        const double u = (x != 0.0) ? -(pj + P.lam * sgn(x)) / hh : 0.0;
+        double Hd;
+        const double d = apply_A(q, AS, p, true, &Hd);
+        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
+        const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;     // gradient of the model on the orthant
+        const double u = (x != 0.0) ? -gx / hh : 0.0;
         AS.u[p] = u;
-        const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
-        r.s[0] += hh * u * u;
+        const double sp = AS.s[p];
+        const double v = (x != 0.0) ? gx : soft(pj, P.lam);
+        r.s[0] += hh * u * u;     // rz
+        r.s[1] += gx * u;         // slope part of u
+        r.s[2] += gx * sp;        // slope part of s_prev
+        r.s[3] += u * u;
+        r.s[4] += u * sp;
+        r.s[5] += sp * sp;
         r.mx[0] = fmax(r.mx[0], fabs(v));
     }
     if (grid_reduce(r, P.part, &c->red_ctr[2], sm)) {
         if (threadIdx.x == 0) {
+            consume_A(c);
             const double rz = r.s[0];
             int stop = 0;
             if (it > 0 && P.eta > 0.0 && r.mx[0] <= P.eta * c->vmax) stop = 1;
             if (rz == 0.0) stop = 1;
             c->inner_stop = stop;
             c->vq = r.mx[0];
-            c->bcg = c->cg_restart ? 0.0 : rz / c->rz_prev;
+            const double b = c->cg_restart ? 0.0 : rz / c->rz_prev;
+            c->bcg = b;
             c->rz = rz;
+            c->slope = r.s[1] + b * r.s[2];
+            c->ss = r.s[3] + 2.0 * b * r.s[4] + b * b * r.s[5];
+            c->pcd_mode = 0;
+            c->combine = 1;
             c->it = it;
         }
     }
 }
 
-// PCD-CG, part 2: s = u + b s_prev; slope = sum_{x != 0} (p + lam sign x) s; ||s||^2; first kink
-// b_k = min_{x s < 0} -x/s.
-__global__ void __launch_bounds__(ML_NT) k_cg_s(Prm P, ASet AS) {
-    __shared__ double sm[4 * ML_NW + 4];
+// Last inner iteration of PCD-CG (no Hs needed): s = u + b s_prev, first kink, decision.
+__global__ void __launch_bounds__(ML_NT) k_cg_finish(Prm P, ASet AS) {
+    __shared__ double sm[2 * ML_NW + 2];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     const int nA = c->nA;
     const double bcg = c->bcg;
-    Red<2, 0, 1> r;
+    Red<0, 0, 1> r;
     r.zero();
     for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+        const double sp = AS.u[p] + bcg * AS.s[p];
+        AS.s[p] = sp;
         const double x = AS.wA[p] + AS.d[p];
-        const double s = AS.u[p] + bcg * AS.s[p];
-        AS.s[p] = s;
-        if (x != 0.0) r.s[0] += (AS.gA[p] + AS.Hd[p] + P.lam * sgn(x)) * s;
-        r.s[1] += s * s;
-        if (x * s < 0.0) r.mn[0] = fmin(r.mn[0], -x / s);
+        if (x * sp < 0.0) r.mn[0] = fmin(r.mn[0], -x / sp);
     }
-    if (grid_reduce(r, P.part, &c->red_ctr[3], sm)) {
-        if (threadIdx.x == 0) {
-            c->slope = r.s[0];
-            c->ss = r.s[1];
-            c->bk = r.mn[0];
-            c->scattered = 1;
-        }
-    }
+    if (grid_reduce(r, P.part, &c->red_ctr[3], sm))
+        if (threadIdx.x == 0) decide_cg(P, c, r.mn[0]);
 }
 
-// m-side pass after the scatter: sv = D o Xs (for the Hs gather); s^T H s = sum D Xs^2 + eps ||s||^2; then the
-// inner step: PCD -> Armijo on the model over b = beta^t (R10); CG -> b = min(b_q, b_kink) (R6').
-// With the shared-memory scatter, Xs_i is first summed from the per-block partials: block b takes a slice of R
-// rows and its 256 threads split the partials of each row into 256/R interleaved groups, combined in group order.
-__device__ __forceinline__ void mpass_decide(Prm& P, Ctl* c, double dxs2, int pcd) {
-    const double sHs = dxs2 + P.eps_h * c->ss;
-    c->sHs = sHs;
-    if (pcd) {
-        const double delta = c->ps + P.lam * c->l1diff_out[0];
-        double b = 1.0;
-        int ok = 0;
-        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
-            const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
-            if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
-        }
-        c->beta = ok ? b : 0.0;
-        c->snap = 0;
-        if (!ok) c->inner_stop = 1;
-        c->cg_restart = 1;
-    } else {
-        if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; }
-        else {
-            const double bq = -c->slope / sHs;
-            c->bq = bq;
-            c->beta = bq < c->bk ? bq : c->bk;
-            c->snap = (c->bk <= bq);
-            c->cg_restart = c->snap;
-            c->rz_prev = c->rz;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int pcd, const double* __restrict__ parts, int nparts) {
+// m-side pass of the atomic-scatter path: Xu -> (pending Xd += beta Xs) -> Xs = Xu (+ b Xs_prev) -> sv = D o Xs,
+// s^T H s; Xu is cleared for the next scatter; PCD decision (R10).
+__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int mode) {
     __shared__ double sm[2 * ML_NW + 2];
-    __shared__ double sred[ML_NT];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
+    const Pending q = pending_m(c);
+    const double bcg = (mode == 2) ? c->bcg : 0.0;
     Red<1> r;
     r.zero();
-    if (parts) {
-        const int R = (P.m + gridDim.x - 1) / gridDim.x;           // rows per block (<= ML_NT by construction)
-        const int ng = max(1, ML_NT / max(R, 1));                  // partial groups per row
-        const int row0 = blockIdx.x * R;
-        const int rr = threadIdx.x % R, grp = threadIdx.x / R;
-        double t = 0.0;
-        if (grp < ng && row0 + rr < P.m)
-            for (int b = grp; b < nparts; b += ng) t += parts[(size_t)b * P.m + row0 + rr];
-        sred[threadIdx.x] = t;
-        __syncthreads();
-        if (threadIdx.x < R && row0 + threadIdx.x < P.m) {
-            double xs = 0.0;
-            for (int g = 0; g < ng; ++g) xs += sred[g * R + threadIdx.x];
-            const int i = row0 + threadIdx.x;
-            const double D = P.rD[i].y;
-            P.Xs[i] = xs;
-            P.sv[i] = D * xs;
-            r.s[0] += D * xs * xs;
-        }
-    } else {
-        for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
-            const double xs = P.Xs[i];
-            const double D = P.rD[i].y;
-            P.sv[i] = D * xs;
-            r.s[0] += D * xs * xs;
-        }
+    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
+        const double xu = P.Xu[i];
+        P.Xu[i] = 0.0;
+        const double xs_old = P.Xs[i];
+        if (q.on) P.Xd[i] = (q.init ? P.Xd[i] : 0.0) + q.beta * xs_old;
+        const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
+        P.Xs[i] = xs;
+        const double D = P.rD[i].y;
+        P.sv[i] = D * xs;
+        r.s[0] += D * xs * xs;
     }
     if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
-        if (threadIdx.x == 0) mpass_decide(P, c, r.s[0], pcd);
-    }
-}
-
-// R12: d += b s (a coordinate reaching its kink is set to exactly -w: x = 0), Hd += b Hs (when Hs was computed),
-// Xd += b Xs; Xs is cleared for the next scatter.  it == 0 initialises d, Hd, Xd.
-__global__ void __launch_bounds__(ML_NT) k_apply(Prm P, ASet AS, int it, int have_hs, int nblkA) {
-    Ctl* c = P.ctl;
-    if (c->skip || !c->scattered) return;
-    const int ok = !c->inner_stop;
-    const double b = c->beta;
-    if ((int)blockIdx.x < nblkA) {
-        if (!ok) return;
-        const int nA = c->nA;
-        const int snap = c->snap;
-        const double bk = c->bk;
-        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
-            const double s = AS.s[p];
-            const double d0 = it ? AS.d[p] : 0.0;
-            const double x = AS.wA[p] + d0;
-            const bool kink = snap && x * s < 0.0 && -x / s == bk;
-            AS.d[p] = kink ? -AS.wA[p] : d0 + b * s;
-            if (have_hs) AS.Hd[p] = (it ? AS.Hd[p] : 0.0) + b * AS.Hs[p];
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) c->napply += 1;
-    } else {
-        const int nb = gridDim.x - nblkA;
-        for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
-            const double xs = P.Xs[i];
-            if (ok) P.Xd[i] = (it ? P.Xd[i] : 0.0) + b * xs;
-            P.Xs[i] = 0.0;
+        if (threadIdx.x == 0) {
+            consume_m(c);
+            const double sHs = r.s[0] + P.eps_h * c->ss;
+            if (mode == 1) decide_pcd(P, c, sHs);
+            else c->sHs = sHs;
         }
     }
 }
 
 // R14-R16: one batch of trials [t0, t0 + NT1) of the outer line search (Eq. 4; Armijo DESIGN Q7, Q26).
-// A-range blocks reduce the l1 trial differences sum(|w + a_t d| - |w|) of the batch (and, in the first batch,
-// g^T d and max|d|); m-range blocks reduce sum_i dloss(t_i, a_t y_i Xd_i).  Last block: Delta, decision.
-// The first batch is {1, 1/2, 1/4, 1/8}; the second (rare) covers the remaining trials up to max_ls.
+// The first batch first applies the pending inner step (d, Xd).  A-range blocks reduce the l1 trial differences
+// sum(|w + a_t d| - |w|) of the batch (and, in the first batch, g^T d and max|d|); m-range blocks reduce
+// sum_i dloss(t_i, a_t y_i Xd_i).  Last block: Delta, decision.  First batch {1, 1/2, 1/4, 1/8}; the second (rare)
+// covers the remaining trials up to max_ls.
 template <int NT1>
 __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int nblkA) {
     constexpr int NS = 1 + 2 * NT1;
@@ -968,7 +1121,7 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     Ctl* c = P.ctl;
     if (c->skip) return;
     if (t0 == 0) {
-        if (c->napply == 0) {   // R14: d = 0
+        if (c->acc_steps == 0) {   // R14: d = 0
             if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; }
             return;
         }
@@ -985,8 +1138,10 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     }
     if ((int)blockIdx.x < nblkA) {
         const int nA = c->nA;
+        const Pending q = pending_A(c);
         for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
-            const double d = AS.d[p], w = AS.wA[p], aw = fabs(w);
+            const double d = (t0 == 0) ? apply_A(q, AS, p, false, nullptr) : AS.d[p];
+            const double w = AS.wA[p], aw = fabs(w);
             if (t0 == 0) {
                 r.s[0] += AS.gA[p] * d;
                 r.mx[0] = fmax(r.mx[0], fabs(d));
@@ -996,9 +1151,13 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
         }
     } else {
         const int nb = gridDim.x - nblkA;
+        const Pending q = pending_m(c);
         for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
+            double xd;
+            if (t0 == 0 && q.on) { xd = (q.init ? P.Xd[i] : 0.0) + q.beta * P.Xs[i]; P.Xd[i] = xd; }
+            else xd = P.Xd[i];
             const double y = (double)P.y[i];
-            const double ti = y * P.z[i], yx = y * P.Xd[i];
+            const double ti = y * P.z[i], yx = y * xd;
 #pragma unroll
             for (int k = 0; k < NT1; ++k)
                 if (t0 + k < T1) r.s[1 + NT1 + k] += dloss(ti, at[k] * yx);
@@ -1007,6 +1166,8 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     if (grid_reduce(r, P.part, &c->red_ctr[5], sm)) {
         if (threadIdx.x == 0) {
             if (t0 == 0) {
+                consume_A(c);
+                consume_m(c);
                 c->gd = r.s[0];
                 c->Delta = r.s[0] + P.lam * r.s[1];
                 if (r.mx[0] == 0.0) { c->skip = 1; c->outcome = OUT_NOSTEP; return; }
