@@ -59,7 +59,7 @@ typedef struct {                  /* defaults: ml_default_opts (DESIGN.md sectio
     int32_t max_ls;               /* <= 40 */
     double eps_h;                 /* model ridge (DESIGN Q6) */
     int32_t multilevel;           /* 1: Algorithm 1; 0: finest-level relaxations only */
-    int32_t inner_cg;             /* 1: PCD-CG inner solver (DESIGN Q9b); 0: plain PCD */
+    int32_t inner_cg;             /* 1: PCD-CG (default); 2: PCD-CG + a PCD step after every kink; 0: plain PCD (DESIGN Q9b) */
     double eta;                   /* inner forcing (0 = off) */
 } ml_solve_opts;
 

@@ -369,7 +369,7 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
         double *wA = (double *)malloc(sizeof(double) * (size_t)(nA ? nA : 1));
         for (int64_t p = 0; p < nA; ++p) { hh[p] = hA[p] + o->eps_h; wA[p] = c->w[A[p]]; }
         int32_t it;
-        int cg_restart = 1;
+        int cg_restart = 1, kinked = 0;
         double rz_prev = 0.0;
         for (it = 0; it < K; ++it) {                                 /* R4 */
             /* R5: model gradient p = g + H d at x = w_A + d; model min-norm subgradient (P:248-256 on Eq. 3) */
@@ -380,7 +380,9 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
                 if (fabs(v) > vq) vq = fabs(v);
             }
             if (it > 0 && o->eta > 0.0 && vq <= o->eta * vmax) break; /* R13: inexact-Newton forcing */
-            int pcd = (!o->inner_cg) || it == 0;
+            /* inner_cg = 1: PCD at it = 0, PCD-CG after; inner_cg = 2: also a PCD step after every kink-truncated CG
+               step (the shrinkage step can zero many coordinates at once, a truncated CG step only one) */
+            int pcd = (!o->inner_cg) || it == 0 || (o->inner_cg == 2 && kinked);
             if (pcd) {
                 /* R6: PCD direction, Eq. 5 with D = diag(H) + eps_h */
                 double umax = 0.0;
@@ -415,6 +417,7 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
                 for (int64_t p = 0; p < nA; ++p) { d[p] += beta * s[p]; Hd[p] += beta * Hs[p]; } /* R12 */
                 for (int64_t i = 0; i < m; ++i) Xd[i] += beta * Xs[i];
                 cg_restart = 1;
+                kinked = 0;
             } else {
                 /* R6': PCD-CG (DESIGN Q9b): preconditioned CG on the model restricted to the current orthant,
                    F = {j : x_j != 0}, signs xi = sign(x) fixed, zeros frozen.  Preconditioner diag(H) + eps_h
@@ -449,6 +452,7 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
                 }
                 for (int64_t i = 0; i < m; ++i) Xd[i] += beta * Xs[i];
                 cg_restart = (bk <= bq);
+                kinked = (bk <= bq);
                 rz_prev = rz;
             }
         }

@@ -36,7 +36,7 @@ typedef struct {
     int32_t max_ls;
     double eps_h;        /* ridge added to the quadratic model only (DESIGN Q6) */
     int32_t multilevel;  /* 1: Algorithm 1; 0: finest-level relaxations only (newGLMNET-like baseline) */
-    int32_t inner_cg;    /* 1: PCD-CG inner solver (DESIGN Q9b); 0: plain PCD */
+    int32_t inner_cg;    /* 1: PCD-CG (default); 2: PCD-CG + a PCD step after every kink; 0: plain PCD (DESIGN Q9b) */
     double eta;          /* inner forcing: stop when the model's min-norm subgradient <= eta * its value at d = 0 (0 = off) */
 } mlo_opts;
 

@@ -327,8 +327,9 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
 // path: partials summed by k_parts_sum).  mode 1/2 (relaxation, PCD / PCD-CG): small m -> k_scatter_smem with its
 // fused m-side pass; otherwise atomics into P.Xu followed by k_mpass.
 void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
-                    double* out, const int* skip, const int* skip2, int mode = 0) {
+                    double* out, const int* skip, const int* skip2, int mode = 0, const double* coef2 = nullptr) {
     Seg S = seg_cols(c, list);
+    const int* use1 = &c->ctl->pcd_mode;   // relaxation (mode < 0): coef (s) on PCD steps, coef2 (u) on PCD-CG steps
     if (c->sm_scatter) {
         {
             PassScope ps(c, cls);
@@ -337,7 +338,8 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
             long long* ac = acc_of(c, cls);
             double* parts = c->parts;
             void* args[] = {(void*)&S, (void*)&nseg_dev, (void*)&nseg_host, (void*)&coef, (void*)&parts, (void*)&m,
-                            (void*)&skip, (void*)&skip2, (void*)&ac, (void*)&Pc, (void*)&mode, (void*)&out};
+                            (void*)&skip, (void*)&skip2, (void*)&ac, (void*)&Pc, (void*)&mode, (void*)&out,
+                            (void*)&coef2};
             cudaLaunchCooperativeKernel((const void*)k_scatter_smem, dim3(c->scat_P), dim3(32 * c->scat_W), args,
                                         c->scat_bytes, c->st);
             c->launches++;
@@ -345,12 +347,13 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
         return;
     }
     double* dst = mode ? c->P.Xu : out;
+    const int* u1 = mode ? use1 : nullptr;
     {
         PassScope ps(c, cls);
         ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, dst, skip, skip2,
-                  acc_of(c, cls));
+                  acc_of(c, cls), coef2, u1);
         ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, dst, skip, skip2,
-                                       acc_of(c, cls)));
+                                       acc_of(c, cls), coef2, u1));
     }
     if (mode) { PassScope ps(c, CLS_MPASS); ML_LAUNCH(c, k_mpass, c->gM, c->P, mode); }
 }
@@ -365,7 +368,7 @@ void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int*
     if (c->sm_gather) {
         k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out, s,
                                                                          eps, skip, skip2, acc_of(c, cls), c->P, A0,
-                                                                         mode);
+                                                                         mode == 2 ? -1 : mode);
         c->launches++;
         return;
     }
@@ -387,18 +390,12 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
     Ctl* ctl = c->ctl;
     const int nblkA = c->gA;
     for (int it = 0; it < K; ++it) {
-        const bool pcd = !inner_cg || it == 0;
-        {
-            PassScope ps(c, CLS_DIR);
-            if (pcd) ML_LAUNCH(c, k_pcd_dir, c->gA, c->P, AS, it);
-            else ML_LAUNCH(c, k_cg_z, c->gA, c->P, AS, it);
-        }
-        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, pcd ? AS.s : AS.u, nullptr, &ctl->skip, &ctl->inner_stop,
-                       pcd ? 1 : 2);
+        { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_dir, c->gA, c->P, AS, it); }
+        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, AS.s, nullptr, &ctl->skip, &ctl->inner_stop, -1, AS.u);
         if (it < K - 1)
             launch_gather_dot(c, CLS_HS, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip,
-                              &ctl->inner_stop, pcd ? 1 : 2, &AS);
-        else if (!pcd) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, c->gA, c->P, AS); }
+                              &ctl->inner_stop, 2, &AS);
+        else if (inner_cg) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, c->gA, c->P, AS); }
     }
     {
         PassScope ps(c, CLS_OUTER);

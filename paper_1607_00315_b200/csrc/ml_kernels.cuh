@@ -30,7 +30,7 @@ struct Ctl {
     int ls_ok, scattered, nS, nAf;
     int skipped, t_acc;
     int nC, pad0;
-    int pend, pend_m, d_init, xd_init, acc_steps, combine, pcd_mode, pad3;
+    int pend, pend_m, d_init, xd_init, acc_steps, combine, pcd_mode, next_pcd;
     unsigned grp_ctr[128];
     unsigned grp_done, pad4;
     const int* Cptr;            // current restriction list (nullptr = all columns)
@@ -237,9 +237,11 @@ __global__ void k_units_build(const int* __restrict__ ptr, const int* __restrict
 // One warp per heavy unit.  SCATTER: out[idx] += X * coef[p] (fp64 atomics), else partial sums + in-order
 // combination by the segment's last-arriving warp into S.hres[p].
 template <class Op, bool SCATTER>
-__global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const double* __restrict__ coef, double* out,
-                                                  const int* skip, const int* skip2, long long* nnz_acc) {
+__global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const double* coef, double* out,
+                                                  const int* skip, const int* skip2, long long* nnz_acc,
+                                                  const double* coef2 = nullptr, const int* use_coef1 = nullptr) {
     if ((skip && *skip) || (skip2 && *skip2)) return;
+    if (coef2 && use_coef1 && !*use_coef1) coef = coef2;
     const int lane = threadIdx.x & 31;
     const int nunits = min(*U.n, U.cap);
     const int gw = (blockIdx.x * ML_NT + threadIdx.x) >> 5, nw = (gridDim.x * ML_NT) >> 5;
@@ -316,6 +318,7 @@ __device__ __forceinline__ void decide_pcd(const Prm& P, Ctl* c, double sHs) {
         if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
     }
     c->cg_restart = 1;
+    c->next_pcd = (P.inner_cg == 0);
     if (!ok) { c->inner_stop = 1; c->beta = 0.0; return; }
     c->beta = b;
     c->snap = 0;
@@ -333,6 +336,7 @@ __device__ __forceinline__ void decide_cg(const Prm& P, Ctl* c, double bk) {
     c->beta = bq < bk ? bq : bk;
     c->snap = (bk <= bq);
     c->cg_restart = c->snap;
+    c->next_pcd = (P.inner_cg == 2) && c->snap;   // inner_cg = 2: a shrinkage step after every kink (DESIGN Q9b)
     c->rz_prev = c->rz;
     c->pend = 1;
     c->pend_m = 1;
@@ -551,7 +555,8 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
     const int ntiles = (nseg + TILE - 1) / TILE;
     long long streamed = 0, segs = 0;
     double bcg = 0.0;
-    if (MODE == 2) bcg = P.ctl->bcg;
+    int pcdm = 0;
+    if (MODE == 2) { bcg = P.ctl->bcg; pcdm = P.ctl->pcd_mode; }
     Red<0, 0, 1> r;
     r.zero();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -562,6 +567,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
             else if (MODE == 1) out0[p] = q.x + (s ? eps * s[p] : 0.0);
+            else if (pcdm) out0[p] = q.x + eps * s[p];
             else {
                 const double sp = AS.u[p] + bcg * AS.s[p];
                 AS.s[p] = sp;
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
         __syncthreads();
     }
     acc_add(nnz_acc, streamed, segs);
-    if (MODE == 2) {
+    if (MODE == 2 && !pcdm) {
         if (grid_reduce(r, P.part, &P.ctl->red_ctr[3], smr))
             if (threadIdx.x == 0) decide_cg(P, P.ctl, r.mn[0]);
     }
@@ -581,9 +587,11 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
 
 // ------------------------------------------------------------------ A5: X_A s scatter (light segments)
 template <int G>
-__global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef,
-                                                   double* out, const int* skip, const int* skip2, long long* nnz_acc) {
+__global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* coef,
+                                                   double* out, const int* skip, const int* skip2, long long* nnz_acc,
+                                                   const double* coef2, const int* use_coef1) {
     if ((skip && *skip) || (skip2 && *skip2)) return;
+    if (coef2 && use_coef1 && !*use_coef1) coef = coef2;
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int grp = (blockIdx.x * ML_NT + threadIdx.x) / G, lane = threadIdx.x % G;
     const int ngrp = gridDim.x * (ML_NT / G);
@@ -740,10 +748,13 @@ __device__ __forceinline__ void stream_setup(ColStream<SCH, NSTG>& cs, unsigned 
 // over all partials (fixed order) and runs the m-side pass on it: mode 0 (API) out = X_A coef; mode 1 / 2 (PCD /
 // PCD-CG relaxation step): pending Xd += beta Xs, Xs = Xu (+ b Xs_prev for CG), sv = D o Xs, and s^T H s summed in
 // block order by the last block, which also takes the PCD decision.
-__global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ coef, double* parts,
-                               int m, const int* skip, const int* skip2, long long* acc, Prm P, int mode, double* out_api) {
+__global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const double* coef, double* parts,
+                               int m, const int* skip, const int* skip2, long long* acc, Prm P, int mode, double* out_api,
+                               const double* coef2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if ((skip && *skip) || (skip2 && *skip2)) return;
+    if (mode < 0) mode = P.ctl->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
+    if (mode == 2 && coef2) coef = coef2;   // PCD-CG scatters u (Xs = Xu + b Xs_prev)
     constexpr int SCH = SC_SCH, NSTG = SC_NSTG;
     const size_t pw = stream_warp_bytes<SCH, NSTG>(m);
     unsigned char* base = smraw + (size_t)(threadIdx.x >> 5) * pw;
@@ -861,6 +872,7 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
                               ASet AS, int mode) {
     extern __shared__ __align__(16) unsigned char smraw[];
     if ((skip && *skip) || (skip2 && *skip2)) return;
+    if (mode < 0) mode = P.ctl->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
     constexpr int SCH = GA_SCH, NSTG = GA_NSTG;
     const int W = blockDim.x >> 5;
     double* sv = reinterpret_cast<double*>(smraw + (size_t)W * stream_warp_bytes<SCH, NSTG>(0));
@@ -954,107 +966,103 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
     c->xd_init = 0;
     c->acc_steps = 0;
     c->combine = 0;
+    c->next_pcd = 1;
     c->units_n[2] = 0;   // A-set units are rebuilt by the gather
     c->units_h[2] = 0;
     if (set_list) { c->Cptr = Cptr; c->nC = nC; }
     (void)finest;
 }
 
-// R5-R7 (PCD step, Eq. 5 with D = diag(H) + eps_h): first the pending step of the previous iteration is applied
-// to d and Hd; then s = Sh_{lam/h}(x - p/h) - x with x = w_A + d, p = g_A + Hd.  Reduction: p^T s, ||s||^2, the l1
-// trial differences sum(|x + b_t s| - |x|) for b_t = beta^t (all max_ls trials of R10), max|s|, and the model's
-// min-norm subgradient (forcing, R13).
-__global__ void __launch_bounds__(ML_NT) k_pcd_dir(Prm P, ASet AS, int it) {
+// Inner direction (R5-R7 / R6'), one kernel for both iteration types; the type is chosen on the device (ctl->next_pcd:
+// a PCD step at it = 0, after every kink with inner_cg = 2, and always with inner_cg = 0).  First the pending step of the
+// previous iteration is applied to d and Hd; x = w_A + d, p = g_A + Hd.
+//  PCD (Eq. 5 with D = diag(H) + eps_h): s = Sh_{lam/h}(x - p/h) - x; reduce p^T s, ||s||^2, the l1 trial
+//      differences sum(|x + b_t s| - |x|) for all max_ls trials b_t = beta^t (R10), max|s|.
+//  PCD-CG: u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere; reduce rz = sum h u^2 and the pieces of the
+//      slope and squared norm of s = u + b s_prev (formed later, in the Hs gather).
+//  Both: the model's min-norm subgradient (forcing, R13).
+__global__ void __launch_bounds__(ML_NT) k_dir(Prm P, ASet AS, int it) {
     __shared__ double sm[(ML_MAXLS + 4) * ML_NW + ML_MAXLS + 4];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     const int nA = c->nA;
+    const int pcd = c->next_pcd;   // grid-uniform: both branches end in their own grid reduction
     const Pending q = pending_A(c);
-    Red<ML_MAXLS + 2, 2> r;
-    r.zero();
-    double bt[ML_MAXLS];
-    bt[0] = 1.0;
+    if (pcd) {
+        Red<ML_MAXLS + 2, 2> r;
+        r.zero();
+        double bt[ML_MAXLS];
+        bt[0] = 1.0;
 #pragma unroll
-    for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        double Hd;
-        const double d = apply_A(q, AS, p, true, &Hd);
-        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-        const double sp = soft(x - pj / hh, P.lam / hh) - x;
-        AS.s[p] = sp;
-        const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
-        r.mx[0] = fmax(r.mx[0], fabs(sp));
-        r.mx[1] = fmax(r.mx[1], fabs(v));
-        r.s[0] += pj * sp;
-        r.s[1] += sp * sp;
-        const double ax = fabs(x);
+        for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
+        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+            double Hd;
+            const double d = apply_A(q, AS, p, true, &Hd);
+            const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
+            const double sp = soft(x - pj / hh, P.lam / hh) - x;
+            AS.s[p] = sp;
+            const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+            r.mx[0] = fmax(r.mx[0], fabs(sp));
+            r.mx[1] = fmax(r.mx[1], fabs(v));
+            r.s[0] += pj * sp;
+            r.s[1] += sp * sp;
+            const double ax = fabs(x);
 #pragma unroll
-        for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * sp) - ax;
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
-        if (threadIdx.x == 0) {
-            consume_A(c);
-            c->ps = r.s[0];
-            c->ss = r.s[1];
-            c->vq = r.mx[1];
-            for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // inner l1 trial differences
-            int stop = 0;
-            if (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax) stop = 1;   // R13 forcing
-            if (r.mx[0] == 0.0) stop = 1;                                        // R7
-            c->inner_stop = stop;
-            c->pcd_mode = 1;
-            c->combine = 0;
-            c->bcg = 0.0;
-            c->it = it;
+            for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * sp) - ax;
         }
-    }
-}
-
-// PCD-CG direction (R6'): after applying the pending step, u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere;
-// rz = sum h u^2; b = rz / rz_prev unless restarting.  The search direction s = u + b s_prev is formed later (in the
-// Hs gather); its slope and squared norm come from the decomposition over (u, s_prev) reduced here.
-__global__ void __launch_bounds__(ML_NT) k_cg_z(Prm P, ASet AS, int it) {
-    __shared__ double sm[7 * ML_NW + 7];
-    Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop) return;
-    const int nA = c->nA;
-    const Pending q = pending_A(c);
-    Red<6, 1> r;
-    r.zero();
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        double Hd;
-        const double d = apply_A(q, AS, p, true, &Hd);
-        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-        const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;     // gradient of the model on the orthant
-        const double u = (x != 0.0) ? -gx / hh : 0.0;
-        AS.u[p] = u;
-        const double sp = AS.s[p];
-        const double v = (x != 0.0) ? gx : soft(pj, P.lam);
-        r.s[0] += hh * u * u;     // rz
-        r.s[1] += gx * u;         // slope part of u
-        r.s[2] += gx * sp;        // slope part of s_prev
-        r.s[3] += u * u;
-        r.s[4] += u * sp;
-        r.s[5] += sp * sp;
-        r.mx[0] = fmax(r.mx[0], fabs(v));
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[2], sm)) {
-        if (threadIdx.x == 0) {
-            consume_A(c);
-            const double rz = r.s[0];
-            int stop = 0;
-            if (it > 0 && P.eta > 0.0 && r.mx[0] <= P.eta * c->vmax) stop = 1;
-            if (rz == 0.0) stop = 1;
-            c->inner_stop = stop;
-            c->vq = r.mx[0];
-            const double b = c->cg_restart ? 0.0 : rz / c->rz_prev;
-            c->bcg = b;
-            c->rz = rz;
-            c->slope = r.s[1] + b * r.s[2];
-            c->ss = r.s[3] + 2.0 * b * r.s[4] + b * b * r.s[5];
-            c->pcd_mode = 0;
-            c->combine = 1;
-            c->it = it;
+        if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
+            if (threadIdx.x == 0) {
+                consume_A(c);
+                c->vq = r.mx[1];
+                int stop = (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax);   // R13 forcing
+                c->ps = r.s[0];
+                c->ss = r.s[1];
+                for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // inner l1 trial differences
+                if (r.mx[0] == 0.0) stop = 1;                                        // R7
+                c->combine = 0;
+                c->bcg = 0.0;
+                c->inner_stop = stop;
+                c->pcd_mode = 1;
+                c->it = it;
+            }
+        }
+    } else {
+        Red<6, 1> r;
+        r.zero();
+        for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
+            double Hd;
+            const double d = apply_A(q, AS, p, true, &Hd);
+            const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
+            const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;   // gradient of the model on the orthant
+            const double u = (x != 0.0) ? -gx / hh : 0.0;
+            AS.u[p] = u;
+            const double sp = AS.s[p];
+            const double v = (x != 0.0) ? gx : soft(pj, P.lam);
+            r.s[0] += hh * u * u;   // rz
+            r.s[1] += gx * u;       // slope part of u
+            r.s[2] += gx * sp;      // slope part of s_prev
+            r.s[3] += u * u;
+            r.s[4] += u * sp;
+            r.s[5] += sp * sp;
+            r.mx[0] = fmax(r.mx[0], fabs(v));
+        }
+        if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
+            if (threadIdx.x == 0) {
+                consume_A(c);
+                c->vq = r.mx[0];
+                int stop = (it > 0 && P.eta > 0.0 && r.mx[0] <= P.eta * c->vmax);
+                const double rz = r.s[0];
+                if (rz == 0.0) stop = 1;
+                const double b = c->cg_restart ? 0.0 : rz / c->rz_prev;
+                c->bcg = b;
+                c->rz = rz;
+                c->slope = r.s[1] + b * r.s[2];
+                c->ss = r.s[3] + 2.0 * b * r.s[4] + b * b * r.s[5];
+                c->combine = 1;
+                c->inner_stop = stop;
+                c->pcd_mode = 0;
+                c->it = it;
+            }
         }
     }
 }
@@ -1063,7 +1071,7 @@ __global__ void __launch_bounds__(ML_NT) k_cg_z(Prm P, ASet AS, int it) {
 __global__ void __launch_bounds__(ML_NT) k_cg_finish(Prm P, ASet AS) {
     __shared__ double sm[2 * ML_NW + 2];
     Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop) return;
+    if (c->skip || c->inner_stop || c->pcd_mode) return;
     const int nA = c->nA;
     const double bcg = c->bcg;
     Red<0, 0, 1> r;
@@ -1084,6 +1092,7 @@ __global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int mode) {
     __shared__ double sm[2 * ML_NW + 2];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
+    if (mode < 0) mode = c->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
     const Pending q = pending_m(c);
     const double bcg = (mode == 2) ? c->bcg : 0.0;
     Red<1> r;

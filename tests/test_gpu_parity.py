@@ -252,3 +252,55 @@ def test_solve_parity_full_configs(name):
     w_o = o.get_w()
     _, g_o, _ = o.eval_f_grad()
     _support_check(ds, ctx.ml_get_w().cpu().numpy(), w_o, g_o)
+
+
+@pytest.mark.parametrize("name,opts", [("cfg2s", {"inner_cg": 2}), ("cfg1", {"inner_cg": 2}), ("onehot", {"inner_cg": 2})])
+def test_solve_parity_inner_variants(name, opts):
+    """The other inner solver (DESIGN Q9b): PCD-CG with a shrinkage step after every kink.  (Plain PCD is covered on
+    cfg 1 by test_solve_parity; it does not reach kappa <= 1e-6 on the Zipf designs in either implementation.)"""
+    test_solve_parity(name, opts)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_sampled_eval_parity(cfg):
+    """BASELINE configs 4 and 5 at full size: F, g_C, h_C on a sampled column list (random + the 20 heaviest
+    columns), in the launch configuration the bench uses, against the oracle's one-by-one evaluation."""
+    ds = mlgen.make(cfg)
+    rng = np.random.default_rng(cfg)
+    lens = np.diff(ds.csc_colptr)
+    C = np.unique(np.r_[rng.choice(ds.n, 2000, replace=False), np.argsort(lens)[-20:]]).astype(np.int32)
+    w = np.zeros(ds.n)
+    idx = rng.choice(ds.n, 5000, replace=False)
+    w[idx] = rng.normal(0, 0.2, len(idx))
+    w[np.argsort(lens)[-5:]] = 0.1   # heavy columns in the support
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    F_o, g_o, h_o = o.eval_f_grad(C)
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    F_g, g_g, h_g = ctx.ml_eval_f_grad(dt(C, torch.int32))
+    assert abs(F_g - F_o) <= 1e-9 * abs(F_o)
+    assert rel(g_g.cpu().numpy(), g_o) <= 1e-9
+    assert rel(h_g.cpu().numpy(), h_o) <= 1e-9
+    v = rng.standard_normal(len(C))
+    assert rel(ctx.ml_hessvec(dt(C, torch.int32), dt(v)).cpu().numpy(), o.hessvec(C, v)) <= 1e-9
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_solve_kkt_by_oracle(cfg):
+    """Full-size GPU solve; the oracle re-evaluates the gradient at the GPU's w and checks the KKT conditions
+    (|g_j| <= lam(1+1e-6) off the support, |g_j + lam sign w_j| <= 1e-6 lam on it) and F."""
+    ds = mlgen.make(cfg)
+    ctx = ml.Context(ds)
+    r = ctx.ml_solve()
+    assert r["status"] == 0 and r["kappa"] <= 1e-6, r
+    w = ctx.ml_get_w().cpu().numpy()
+    del ctx
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    F_o, g_o, _ = o.eval_f_grad()
+    S = w != 0
+    lam = ds.lam
+    assert np.max(np.abs(g_o[~S])) <= lam * (1 + 1e-6)
+    assert np.max(np.abs(g_o[S] + lam * np.sign(w[S]))) <= 1e-6 * lam
+    assert abs(F_o - r["F"]) <= 1e-9 * abs(F_o)
