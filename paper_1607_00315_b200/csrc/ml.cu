@@ -455,7 +455,7 @@ void ml_default_opts(ml_solve_opts* o) {
     o->max_cycles = 1000;
     o->nu = 1;
     o->nu_c = 5;
-    o->K_fine = 1;
+    o->K_fine = 2;
     o->K_mid = 3;
     o->K_coarse = 10;
     o->sigma_out = 1e-2;
