@@ -123,6 +123,9 @@ int64_t ml_kernel_launches(const ml_ctx *c);
    the passes launched, and the nonzeros streamed and segments (rows / columns) visited on the device. */
 ml_status ml_profile(ml_ctx *c, uint32_t class_mask);
 ml_status ml_profile_read(ml_ctx *c, double *ms_host, int64_t *passes_host, int64_t *nnz_host, int64_t *segs_host);
+/* Diagnostics: nanoseconds spent per phase of the persistent small-m inner solver (block 0; 0 direction, 1 its
+   barrier + totals, 2 scatter stream, 3 scatter barrier, 4 m-side + barrier, 5 Hs stream, 6 Hs barrier + decision). */
+ml_status ml_inner_phases(ml_ctx *c, uint64_t *ns_host, int reset);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */
 int64_t ml_trace(ml_ctx *c, void *rows_host, int64_t cap);

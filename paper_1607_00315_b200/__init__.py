@@ -71,7 +71,7 @@ class TraceRow(ctypes.Structure):
 EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
            "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
-           "ml_profile_read"]
+           "ml_profile_read", "ml_inner_phases"]
 
 _lib = None
 
@@ -122,6 +122,8 @@ def load(path: str | None = None):
     L.ml_profile.argtypes = [P, ctypes.c_uint32]
     L.ml_profile_read.restype = i32
     L.ml_profile_read.argtypes = [P, P, P, P, P]
+    L.ml_inner_phases.restype = i32
+    L.ml_inner_phases.argtypes = [P, P, i32]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
     _lib = L
@@ -281,7 +283,7 @@ class Context:
         return d
 
     CLASSES = ["margins", "gather_fine", "gather_coarse", "scatter_XAs", "gather_Hs", "inner_dir", "mpass", "apply",
-               "outer_ls", "update", "select", "book", "api"]
+               "outer_ls", "update", "select", "book", "api", "inner_fused"]
 
     def ml_profile(self, mask=0):
         return self._check(load().ml_profile(self.h, int(mask)))
@@ -292,6 +294,11 @@ class Context:
         self._check(load().ml_profile_read(self.h, ms, ps, nz, sg))
         return {name: {"ms": ms[k], "passes": ps[k], "nnz": nz[k], "segs": sg[k]}
                 for k, name in enumerate(self.CLASSES)}
+
+    def ml_inner_phases(self, reset=True):
+        ns = (ctypes.c_uint64 * 8)()
+        self._check(load().ml_inner_phases(self.h, ns, int(reset)))
+        return [int(x) for x in ns]
 
     def ml_kernel_launches(self):
         return int(load().ml_kernel_launches(self.h))

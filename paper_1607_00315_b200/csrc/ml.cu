@@ -44,7 +44,7 @@ struct UnitsMem { int4* u; double2* part; int* hcnt; int cap, hcap; };
 
 // pass classes for accounting (device nonzero/segment counters) and optional CUDA-event timing
 enum { CLS_MARGINS = 0, CLS_GATHER_FINE, CLS_GATHER_COARSE, CLS_SCATTER, CLS_HS, CLS_DIR, CLS_MPASS, CLS_APPLY,
-       CLS_OUTER, CLS_UPDATE, CLS_SELECT, CLS_BOOK, CLS_API, CLS_N };
+       CLS_OUTER, CLS_UPDATE, CLS_SELECT, CLS_BOOK, CLS_API, CLS_INNER, CLS_N };
 
 }  // namespace
 
@@ -72,13 +72,16 @@ struct ml_ctx {
     int scat_W = 0, scat_P = 0, gMP = 1;
     size_t scat_bytes = 0;
     bool sm_gather = false;
+    bool sm_inner = false;   // persistent cooperative inner solver (k_inner_small)
+    int inner_W = 0, inner_P = 0;
+    size_t inner_bytes = 0;
     int gath_W = 0, gath_P = 0;
     size_t gath_bytes = 0;
     double* parts = nullptr;
     long long npos;
     long long launches = 0;
     // profiling: event pairs per pass class (enabled classes only)
-    uint32_t prof_mask = 0;
+    uint32_t prof_mask = 0;   // bit k: time pass class k (CLS_*)
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<int> ev_cls;      // class of each recorded pair (pair k = events 2k, 2k+1)
@@ -386,16 +389,39 @@ void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int*
 // R3-R18 on the free set in AS (its gather already ran): K inner iterations, outer line search, update.
 // Per inner iteration: direction kernel (applies the previous step), scatter X_A s (+ m-side pass and, for PCD, the
 // step decision), Hs gather (+ for PCD-CG the step decision).  Steps are applied lazily (see decide_pcd).
-void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
+void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
     Ctl* ctl = c->ctl;
-    const int nblkA = c->gA;
+    // A-side grids sized by this level's |C| (>= |A|): fewer idle blocks in the grid reductions at coarse levels
+    const int gAl = std::max(1, std::min(c->gA, (nC_host + ML_NT - 1) / ML_NT));
+    const int nblkA = gAl;
+    if (c->sm_inner) {   // one persistent cooperative launch for all K inner iterations
+        PassScope ps(c, CLS_INNER);
+        Prm Pc = c->P;
+        ASet A2 = AS;
+        Seg S = seg_cols(c, AS.A);
+        int Kk = K, icg = inner_cg;
+        long long* a1 = acc_of(c, CLS_SCATTER);
+        long long* a2 = acc_of(c, CLS_HS);
+        void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
+        cudaLaunchCooperativeKernel((const void*)k_inner_small, dim3(c->inner_P), dim3(32 * c->inner_W), args,
+                                    c->inner_bytes, c->st);
+        c->launches++;
+    } else
     for (int it = 0; it < K; ++it) {
-        { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_dir, c->gA, c->P, AS, it); }
+        {
+            // inner_cg 0 / 1: the iteration type is known here (PCD at it = 0 / always); inner_cg = 2 decides on
+            // the device after a kink, so both kernels are launched and one returns immediately
+            PassScope ps(c, CLS_DIR);
+            const bool may_pcd = !inner_cg || it == 0 || inner_cg == 2;
+            const bool may_cg = inner_cg && it > 0;
+            if (may_pcd) ML_LAUNCH(c, k_dir_pcd, gAl, c->P, AS, it);
+            if (may_cg) ML_LAUNCH(c, k_dir_cg, gAl, c->P, AS, it);
+        }
         launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, AS.s, nullptr, &ctl->skip, &ctl->inner_stop, -1, AS.u);
         if (it < K - 1)
             launch_gather_dot(c, CLS_HS, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip,
                               &ctl->inner_stop, 2, &AS);
-        else if (inner_cg) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, c->gA, c->P, AS); }
+        else if (inner_cg) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, gAl, c->P, AS); }
     }
     {
         PassScope ps(c, CLS_OUTER);
@@ -549,6 +575,19 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->gath_W = W;
             c->gath_bytes = bytes;
             c->gath_P = SM_COUNT * bps;
+        }
+        W = 8;
+        while (W > 1 && inner_smem_bytes(W, (int)X->m) > 196 * 1024) --W;
+        bytes = inner_smem_bytes(W, (int)X->m);
+        if (W >= 2 && cudaFuncSetAttribute(k_inner_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
+            int bps = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inner_small, 32 * W, bytes);
+            if (bps >= 1) {
+                c->sm_inner = c->sm_scatter && c->sm_gather;
+                c->inner_W = W;
+                c->inner_bytes = bytes;
+                c->inner_P = SM_COUNT;
+            }
         }
         cudaGetLastError();
     }
@@ -748,11 +787,11 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
         launch_margins(c);
         launch_gather_free(c, nullptr, n, c->fine, true);
         if (relax) {
-            launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
+            launch_relax_body(c, c->fine, o.K_fine, o.inner_cg, n);
             for (int it = 1; it < o.nu; ++it) {
                 ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1, 1);
                 launch_gather_free(c, nullptr, n, c->fine, true);
-                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
+                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg, n);
             }
         }
     };
@@ -785,7 +824,7 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
                         for (int r = 0; r < reps; ++r) {
                             ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1, 0);
                             launch_gather_free(c, Cl, nCl, c->coarse, false);
-                            launch_relax_body(c, c->coarse, K, o.inner_cg);
+                            launch_relax_body(c, c->coarse, K, o.inner_cg, nCl);
                         }
                     }
                 }
@@ -862,6 +901,16 @@ ml_status ml_profile_read(ml_ctx* c, double* ms, int64_t* passes, int64_t* nnz, 
             if (cudaEventElapsedTime(&t, c->ev_pool[2 * p], c->ev_pool[2 * p + 1]) == cudaSuccess) ms[c->ev_cls[p]] += t;
         }
     return cuda_fail(c, "ml_profile_read");
+}
+
+// diagnostics: ns per phase of the persistent inner solver (block 0), accumulated since the last reset
+ml_status ml_inner_phases(ml_ctx* c, uint64_t* ns_host, int reset) {
+    if (!c) return ML_E_INVAL;
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    for (int k = 0; k < 8; ++k) if (ns_host) ns_host[k] = c->h.tph[k];
+    if (reset) { unsigned long long z[8] = {0}; cudaMemcpyAsync(c->ctl->tph, z, sizeof(z), cudaMemcpyHostToDevice, c->st); }
+    return cuda_fail(c, "ml_inner_phases");
 }
 
 // trace access for tests (not part of the paper's call set)
