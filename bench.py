@@ -115,6 +115,15 @@ def allreduce(vals, op, ws, device):
     return t.tolist()
 
 
+def parse_opts(text):
+    """--opts "multilevel=0,K_fine=10" -> dict of ml_solve_opts overrides"""
+    out = {}
+    for kv in filter(None, (text or "").split(",")):
+        k, v = kv.split("=")
+        out[k.strip()] = float(v) if "." in v or "e" in v else int(v)
+    return out
+
+
 def class_bytes(name, prof, ds):
     """Algorithmic bytes of a pass class: X stream 8 B/nnz, pointer pairs 8 B/segment,
     list 4 B/segment, each m-vector once per pass, outputs once."""
@@ -148,7 +157,7 @@ def run_ours(args):
     ml.build()
     ds = mlgen.make(args.config)
     ctx = ml.Context(ds, device=str(device))
-    opts = ml.default_opts()
+    opts = ml.default_opts(**parse_opts(args.opts))
 
     # warm-up; the last warm-up step times every pass class to find the dominant one
     for k in range(args.warmup):
@@ -248,7 +257,8 @@ def run_ours(args):
                        "lambda": ds.lam, "tol_kkt": 1e-6, "parallelism": f"replicas{ws}",
                        "l2": "inputs larger than L2 (X CSR+CSC %.0f MB > 126 MB); no flush" % (16 * ds.nnz / 1e6)
                        if 16 * ds.nnz > 126e6 else "small config: L2-resident",
-                       "step": "one ml_solve from w=0 to kappa<=1e-6"},
+                       "step": "one ml_solve from w=0 to kappa<=1e-6",
+                       **({"opts": parse_opts(args.opts)} if args.opts else {})},
             "time_to_kkt_ms": t_max / args.steps,
             "solve": {"ok": ok, "F": r0["F"], "kappa": r0["kappa"], "cycles": r0["cycles"],
                       "relaxations": r0["relaxations"], "nnz_w": r0["nnz_w"], "x_nnz_streamed": r0["nnz_touched"],
@@ -327,6 +337,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--opts", default="", help="ml_solve_opts overrides, e.g. multilevel=0,K_fine=10")
     ap.add_argument("--single", action="store_true", help="one untimed solve (for ncu launch lists / captures)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
@@ -336,7 +347,7 @@ def main():
         ml.build()
         ds = mlgen.make(args.config)
         ctx = ml.Context(ds)
-        r = ctx.ml_solve(ml.default_opts())
+        r = ctx.ml_solve(ml.default_opts(**parse_opts(args.opts)))
         print(json.dumps({"single": True, "config": args.config, "status": r["status"], "kappa": r["kappa"],
                           "cycles": r["cycles"], "kernel_launches": r["kernel_launches"]}))
         return

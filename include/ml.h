@@ -59,8 +59,11 @@ typedef struct {                  /* defaults: ml_default_opts (DESIGN.md sectio
     int32_t max_ls;               /* <= 40 */
     double eps_h;                 /* model ridge (DESIGN Q6) */
     int32_t multilevel;           /* 1: Algorithm 1; 0: finest-level relaxations only */
-    int32_t inner_cg;             /* 1: PCD-CG (default); 2: PCD-CG + a PCD step after every kink; 0: plain PCD (DESIGN Q9b) */
+    int32_t inner_cg;             /* 2: PCD-CG + a PCD step after every kink (default); 1: PCD-CG; 0: plain PCD (DESIGN Q9b) */
     double eta;                   /* inner forcing (0 = off) */
+    int32_t pcd_snap;             /* 1 (default): a PCD step first tries the path that sets the coordinates its shrinkage
+                                     sends to 0 exactly to 0 for every step length (DESIGN Q27); 0: plain PCD steps */
+    int32_t pad;
 } ml_solve_opts;
 
 typedef struct {

@@ -58,7 +58,7 @@ void mlo_default_opts(mlo_opts *o) {
     o->tol_kkt = 1e-6; o->max_cycles = 1000; o->nu = 1; o->nu_c = 5;
     o->K_fine = 2; o->K_mid = 3; o->K_coarse = 10;   /* tuned with this oracle, DESIGN "Defaults" */
     o->sigma_out = 1e-2; o->sigma_in = 1e-2; o->beta = 0.5; o->max_ls = 40;
-    o->eps_h = 1e-12; o->multilevel = 1; o->inner_cg = 1; o->eta = 0.0;
+    o->eps_h = 1e-12; o->multilevel = 1; o->inner_cg = 2; o->eta = 0.0; o->pcd_snap = 1;
 }
 
 /* --------------------------------------------------------------- context */
@@ -365,6 +365,8 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
         double *s = (double *)calloc((size_t)(nA ? nA : 1), sizeof(double));
         double *Hs = (double *)calloc((size_t)(nA ? nA : 1), sizeof(double));
         double *Xs = (double *)calloc((size_t)m, sizeof(double));
+        double *Xz = (double *)calloc((size_t)m, sizeof(double));
+        double *Hz = (double *)calloc((size_t)(nA ? nA : 1), sizeof(double));
         double *hh = (double *)malloc(sizeof(double) * (size_t)(nA ? nA : 1));
         double *wA = (double *)malloc(sizeof(double) * (size_t)(nA ? nA : 1));
         for (int64_t p = 0; p < nA; ++p) { hh[p] = hA[p] + o->eps_h; wA[p] = c->w[A[p]]; }
@@ -405,17 +407,62 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
                     l1xs += fabs(x + s[p]);
                 }
                 double delta = ps + lam * (l1xs - l1x);              /* R9 */
+                /* pcd_snap (DESIGN Q27): z = the part of s that takes a coordinate exactly to 0 (x != 0, x + s = 0);
+                   line search along sigma(b) = b (s - z) + z, i.e. those coordinates are set to 0 for every b.
+                   q(sigma(b)) in closed form from Xz = X_A z and Hz = X_A^T D Xz + eps z. */
+                int nzero = 0;
+                double pz = 0.0, zHs = 0.0, zHz = 0.0, Z1 = 0.0;
+                if (o->pcd_snap) {
+                    for (int64_t p = 0; p < nA; ++p) {
+                        double x = wA[p] + d[p];
+                        u[p] = (x != 0.0 && x + s[p] == 0.0) ? s[p] : 0.0;   /* u holds z here */
+                        nzero += (u[p] != 0.0);
+                    }
+                    if (nzero) {
+                        apply_XC(c, A, nA, u, Xz);
+                        apply_XCt_D(c, A, nA, Xz, Hz);
+                        for (int64_t p = 0; p < nA; ++p) Hz[p] += o->eps_h * u[p];
+                        for (int64_t p = 0; p < nA; ++p) {
+                            pz += (gA[p] + Hd[p]) * u[p];
+                            zHs += u[p] * Hs[p];
+                            zHz += u[p] * Hz[p];
+                            Z1 += fabs(u[p]);
+                        }
+                    }
+                }
                 double beta = 1.0;                                   /* R10: Armijo on the model, b = 1, 1/2, ... */
-                int ok = 0;
-                for (int32_t t = 0; t < o->max_ls; ++t, beta *= o->beta) {
-                    double l1b = 0.0;
-                    for (int64_t p = 0; p < nA; ++p) l1b += fabs(wA[p] + d[p] + beta * s[p]);
-                    double dq = beta * ps + 0.5 * beta * beta * sHs + lam * (l1b - l1x);
-                    if (dq <= o->sigma_in * beta * delta) { ok = 1; break; }
+                int ok = 0, snapped = 0;
+                for (int pathk = (nzero ? 0 : 1); pathk < 2 && !ok; ++pathk) {   /* 0: snap path, 1: plain path */
+                    beta = 1.0;
+                    for (int32_t t = 0; t < o->max_ls; ++t, beta *= o->beta) {
+                        double l1b = 0.0;
+                        for (int64_t p = 0; p < nA; ++p) l1b += fabs(wA[p] + d[p] + beta * s[p]);
+                        double dq;
+                        if (pathk == 0) {
+                            /* sigma = b sn + z, sn = s - z: p^T sigma = b (ps - pz) + pz;
+                               sigma^T H sigma = b^2 (sHs - 2 zHs + zHz) + 2 b (zHs - zHz) + zHz;
+                               ||x + sigma||_1 - ||x||_1 = (l1b - l1x) - (1 - b) Z1 */
+                            double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
+                            dq = beta * (ps - pz) + pz + 0.5 * (beta * beta * snHsn + 2.0 * beta * snHz + zHz)
+                                 + lam * ((l1b - l1x) - (1.0 - beta) * Z1);
+                        } else {
+                            dq = beta * ps + 0.5 * beta * beta * sHs + lam * (l1b - l1x);
+                        }
+                        if (dq <= o->sigma_in * beta * delta) { ok = 1; snapped = (pathk == 0); break; }
+                    }
                 }
                 if (!ok) break;                                      /* R11 */
-                for (int64_t p = 0; p < nA; ++p) { d[p] += beta * s[p]; Hd[p] += beta * Hs[p]; } /* R12 */
-                for (int64_t i = 0; i < m; ++i) Xd[i] += beta * Xs[i];
+                if (snapped) {                                       /* R12 on the snap path */
+                    for (int64_t p = 0; p < nA; ++p) {
+                        double zp = u[p];
+                        d[p] = (zp != 0.0) ? -wA[p] : d[p] + beta * s[p];
+                        Hd[p] += beta * (Hs[p] - Hz[p]) + Hz[p];
+                    }
+                    for (int64_t i = 0; i < m; ++i) Xd[i] += beta * (Xs[i] - Xz[i]) + Xz[i];
+                } else {
+                    for (int64_t p = 0; p < nA; ++p) { d[p] += beta * s[p]; Hd[p] += beta * Hs[p]; } /* R12 */
+                    for (int64_t i = 0; i < m; ++i) Xd[i] += beta * Xs[i];
+                }
                 cg_restart = 1;
                 kinked = 0;
             } else {
@@ -471,7 +518,7 @@ static int relax_core(mlo_ctx *c, const int32_t *C, int64_t nC, double *gC, doub
         } else {
             row.outcome = MLO_R_NOSTEP;
         }
-        free(d); free(Hd); free(Xd); free(u); free(s); free(Hs); free(Xs); free(hh); free(wA);
+        free(d); free(Hd); free(Xd); free(u); free(s); free(Hs); free(Xs); free(Xz); free(Hz); free(hh); free(wA);
     }
 done:
     row.F_after = F_current(c);

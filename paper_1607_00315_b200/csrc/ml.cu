@@ -108,6 +108,9 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* Xs = cv.take<double>(mm);
     double* sv = cv.take<double>(mm);
     double* Xu = cv.take<double>(mm);
+    double* Xz = cv.take<double>(mm);
+    double* svz = cv.take<double>(mm);
+    double* Xzu = cv.take<double>(mm);
     double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
     double2* tilepart = cv.take<double2>(ntile_n + 1);
     unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
@@ -141,6 +144,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     for (int k = 0; k < 4; ++k) c->um[k] = um[k];
     Prm& P = c->P;
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
+    P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
 
@@ -226,6 +230,8 @@ __global__ void k_init_rows(Prm P, int m) {   // w = 0: z = 0, r = -y/2, D = 1/4
         P.Xs[i] = 0.0;
         P.Xd[i] = 0.0;
         P.Xu[i] = 0.0;
+        P.Xz[i] = 0.0;
+        P.Xzu[i] = 0.0;
     }
 }
 __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* npos) {
@@ -333,7 +339,7 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
                     double* out, const int* skip, const int* skip2, int mode = 0, const double* coef2 = nullptr) {
     Seg S = seg_cols(c, list);
     const int* use1 = &c->ctl->pcd_mode;   // relaxation (mode < 0): coef (s) on PCD steps, coef2 (u) on PCD-CG steps
-    if (c->sm_scatter) {
+    if (c->sm_scatter && mode == 0) {   // relaxations on small m run inside k_inner_small
         {
             PassScope ps(c, cls);
             Prm Pc = c->P;
@@ -358,6 +364,14 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
         ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, dst, skip, skip2,
                                        acc_of(c, cls), coef2, u1));
     }
+    if (mode && c->P.pcd_snap && coef2) {   // PCD snap (Q27): X_A z over the zeroing coordinates (z = AS.u = coef2)
+        PassScope ps(c, cls);
+        ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef2,
+                  c->P.Xzu, skip, &c->ctl->zscatter_skip, acc_of(c, cls), (const double*)nullptr, (const int*)nullptr);
+        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef2, c->P.Xzu,
+                                       skip, &c->ctl->zscatter_skip, acc_of(c, cls), (const double*)nullptr,
+                                       (const int*)nullptr));
+    }
     if (mode) { PassScope ps(c, CLS_MPASS); ML_LAUNCH(c, k_mpass, c->gM, c->P, mode); }
 }
 
@@ -368,19 +382,24 @@ void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int*
     PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
     const ASet A0 = AS ? *AS : c->coarse;
-    if (c->sm_gather) {
+    if (c->sm_gather && mode != 2) {
         k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out, s,
                                                                          eps, skip, skip2, acc_of(c, cls), c->P, A0,
                                                                          mode == 2 ? -1 : mode);
         c->launches++;
         return;
     }
+    if (mode == 2) {   // relaxation Hs gather; on a PCD snap step also X_A^T (D o Xz) (OpDot2, decided on the device)
+        const OpDot2 op{v, c->P.svz, &c->ctl->pcd_mode, &c->ctl->zsnap, 0};
+        ML_LAUNCH(c, (k_heavy<OpDot2, false>), c->gHeavy, S, units_of(c, slot), op, (const double*)nullptr,
+                  (double*)nullptr, skip, skip2, acc_of(c, cls));
+        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 2, OpDot2>), c->gSeg, S, op, nseg_dev, nseg_host, out,
+                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
+        return;
+    }
     ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
               (double*)nullptr, skip, skip2, acc_of(c, cls));
-    if (mode == 2) {
-        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 2, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
-                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
-    } else {
+    {
         ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
                                        (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
     }
@@ -442,6 +461,7 @@ void set_params(ml_ctx* c, const ml_solve_opts* o) {
     P.eta = o->eta;
     P.max_ls = std::max(1, std::min(o->max_ls, ML_MAXLS));
     P.inner_cg = o->inner_cg;
+    P.pcd_snap = o->pcd_snap;
 }
 
 // level sizes (P:194, P:602 via P:798; DESIGN section 3 S9-S10): k[0] = n, returns L
@@ -490,8 +510,9 @@ void ml_default_opts(ml_solve_opts* o) {
     o->max_ls = 40;
     o->eps_h = 1e-12;
     o->multilevel = 1;
-    o->inner_cg = 1;
+    o->inner_cg = 2;
     o->eta = 0.0;
+    o->pcd_snap = 1;
 }
 
 size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz) {

@@ -31,6 +31,9 @@ struct Ctl {
     int skipped, t_acc;
     int nC, pad0;
     int pend, pend_m, d_init, xd_init, acc_steps, combine, pcd_mode, next_pcd;
+    int zsnap, nzero;             // PCD step on the snap path (Q27); zeroing coordinates in the last PCD direction
+    int zscatter_skip, pad5;      // 1: no X_A z pass this iteration
+    double hs_beta, pz, Z1, zz;   // multiplier of Hs in the pending step; snap-path sums of the PCD direction
     unsigned grp_ctr[128];
     unsigned grp_done, pad4;
     const int* Cptr;            // current restriction list (nullptr = all columns)
@@ -73,12 +76,14 @@ struct Seg {
 // ------------------------------------------------------------------ per-element operations
 struct OpMargin {     // z_i = sum_k X_ik w_k, gathers gated by the support bitmap
     const double* w; const uint32_t* bits;
+    __device__ __forceinline__ void prepare() {}
     __device__ __forceinline__ void add(double& a0, double&, int c, float v) const {
         if ((__ldg(bits + (c >> 5)) >> (c & 31)) & 1u) a0 += (double)v * __ldg(w + c);
     }
 };
 struct OpGH {         // g_j = sum_i X_ij r_i ; h_j = sum_i X_ij^2 D_i
     const double2* rD;
+    __device__ __forceinline__ void prepare() {}
     __device__ __forceinline__ void add(double& a0, double& a1, int r, float v) const {
         double2 q = __ldg(rD + r);
         double x = (double)v;
@@ -88,7 +93,20 @@ struct OpGH {         // g_j = sum_i X_ij r_i ; h_j = sum_i X_ij^2 D_i   (P:792,
 };
 struct OpDot {        // acc = sum_i X_ij v_i
     const double* v;
+    __device__ __forceinline__ void prepare() {}
     __device__ __forceinline__ void add(double& a0, double&, int r, float x) const { a0 += (double)x * __ldg(v + r); }
+};
+struct OpDot2 {       // acc0 = sum_i X_ij v_i, acc1 = sum_i X_ij v2_i when dual (PCD snap step)
+    const double* v;
+    const double* v2;
+    const int* flag_pcd;
+    const int* flag_zsnap;
+    int dual;
+    __device__ __forceinline__ void prepare() { dual = (flag_pcd && flag_zsnap) ? (*flag_pcd && *flag_zsnap) : 0; }
+    __device__ __forceinline__ void add(double& a0, double& a1, int r, float x) const {
+        a0 += (double)x * __ldg(v + r);
+        if (dual) a1 += (double)x * __ldg(v2 + r);
+    }
 };
 
 // Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).  Each lane streams U 16-byte vectors of
@@ -243,6 +261,7 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
                                                   const double* coef2 = nullptr, const int* use_coef1 = nullptr) {
     if ((skip && *skip) || (skip2 && *skip2)) return;
     if (coef2 && use_coef1 && !*use_coef1) coef = coef2;
+    op.prepare();
     const int lane = threadIdx.x & 31;
     const int nunits = min(*U.n, U.cap);
     const int gw = (blockIdx.x * ML_NT + threadIdx.x) >> 5, nw = (gridDim.x * ML_NT) >> 5;
@@ -291,9 +310,10 @@ struct Prm {
     int m, n;
     const int8_t* y;
     double lam, eps_h, sigma_in, sigma_out, beta_ls, tol, eta;
-    int max_ls, inner_cg;
+    int max_ls, inner_cg, pcd_snap, pad_p;
     double* w; uint32_t* wbits; double* z; double2* rD;
     double* Xd; double* Xs; double* sv; double* Xu;   // Xu: scatter target of the atomic path (kept zero between uses)
+    double* Xz; double* svz; double* Xzu;             // snap path: X_A z, D o Xz; Xzu: atomic scatter target of z (kept zero)
     double* parts; int nparts;                        // small-m scatter: per-block partials (+ group partials)
     Ctl* ctl;
     double* part;              // reduction partials
@@ -309,20 +329,36 @@ struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd;
 // The inner step s accepted in iteration `it` (length beta, optional kink snap) is applied lazily: to d and Hd by the
 // next direction kernel (or the outer line search), to Xd by the next m-side pass (or the outer line search).
 // R6-R10, PCD: Armijo on the model over beta = 1, 1/2, ... with delta the model's linear part at beta = 1.
-__device__ __forceinline__ void decide_pcd(const Prm& P, Ctl* c, double sHs) {
+// With pcd_snap (DESIGN Q27) and zeroing coordinates z (x != 0, x + s = 0), the snap path sigma(b) = b (s - z) + z is
+// tried first; its model change in closed form: q = b (ps - pz) + pz + 1/2 (b^2 snHsn + 2 b snHz + zHz)
+// + lam (l1diff_b - (1 - b) Z1); otherwise the plain path b s.  sHs, zHs, zHz include the eps_h ridge.
+__device__ __forceinline__ void decide_pcd(const Prm& P, Ctl* c, double sHs, double zHs, double zHz) {
     c->sHs = sHs;
     const double delta = c->ps + P.lam * c->l1diff_out[0];
     double b = 1.0;
-    int ok = 0;
-    for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
-        const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
-        if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+    int ok = 0, snapped = 0;
+    if (c->nzero > 0) {
+        const double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
+        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+            const double dq = b * (c->ps - c->pz) + c->pz + 0.5 * (b * b * snHsn + 2.0 * b * snHz + zHz) +
+                              P.lam * (c->l1diff_out[t] - (1.0 - b) * c->Z1);
+            if (dq <= P.sigma_in * b * delta) { ok = 1; snapped = 1; break; }
+        }
+    }
+    if (!ok) {
+        b = 1.0;
+        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+            const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
+            if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+        }
     }
     c->cg_restart = 1;
     c->next_pcd = (P.inner_cg == 0);
     if (!ok) { c->inner_stop = 1; c->beta = 0.0; return; }
     c->beta = b;
     c->snap = 0;
+    c->zsnap = snapped;
+    c->hs_beta = 1.0;   // the Hs gather of a PCD iteration returns H sigma (the step), not H s
     c->pend = 1;
     c->pend_m = 1;
     c->acc_steps += 1;
@@ -336,6 +372,8 @@ __device__ __forceinline__ void decide_cg(const Prm& P, Ctl* c, double bk) {
     c->bq = bq;
     c->beta = bq < bk ? bq : bk;
     c->snap = (bk <= bq);
+    c->zsnap = 0;
+    c->hs_beta = c->beta;
     c->cg_restart = c->snap;
     c->next_pcd = (P.inner_cg == 2) && c->snap;   // inner_cg = 2: a shrinkage step after every kink (DESIGN Q9b)
     c->rz_prev = c->rz;
@@ -344,12 +382,17 @@ __device__ __forceinline__ void decide_cg(const Prm& P, Ctl* c, double bk) {
     c->acc_steps += 1;
 }
 struct Pending {   // a snapshot of the pending step, read once per kernel
-    int on, init, snap;
-    double beta, bk;
+    int on, init, snap, zsnap;
+    double beta, bk, hs_beta;
 };
-__device__ __forceinline__ Pending pending_A(const Ctl* c) { return Pending{c->pend, c->d_init, c->snap, c->beta, c->bk}; }
-__device__ __forceinline__ Pending pending_m(const Ctl* c) { return Pending{c->pend_m, c->xd_init, 0, c->beta, 0.0}; }
-// d (and Hd when Hs is valid) after the pending step at position p; writes them back
+__device__ __forceinline__ Pending pending_A(const Ctl* c) {
+    return Pending{c->pend, c->d_init, c->snap, c->zsnap, c->beta, c->bk, c->hs_beta};
+}
+__device__ __forceinline__ Pending pending_m(const Ctl* c) {
+    return Pending{c->pend_m, c->xd_init, 0, c->zsnap, c->beta, 0.0, 0.0};
+}
+// d (and Hd when Hs is valid) after the pending step at position p; writes them back.  A CG step snaps its first-kink
+// coordinates to 0; a PCD snap step (Q27) snaps its zeroing coordinates (z = AS.u != 0) to 0.
 __device__ __forceinline__ double apply_A(const Pending& q, const ASet& AS, int p, bool with_hd, double* Hd_out) {
     double d = q.init ? AS.d[p] : 0.0;
     double hd = (with_hd && q.init) ? AS.Hd[p] : 0.0;
@@ -357,12 +400,19 @@ __device__ __forceinline__ double apply_A(const Pending& q, const ASet& AS, int 
         const double sp = AS.s[p];
         const double x = AS.wA[p] + d;
         const bool kink = q.snap && x * sp < 0.0 && -x / sp == q.bk;
-        d = kink ? -AS.wA[p] : d + q.beta * sp;   // a coordinate reaching its kink becomes exactly 0
+        const bool zero = q.zsnap && AS.u[p] != 0.0;
+        d = (kink || zero) ? -AS.wA[p] : d + q.beta * sp;   // a snapped coordinate becomes exactly 0
         AS.d[p] = d;
-        if (with_hd) { hd += q.beta * AS.Hs[p]; AS.Hd[p] = hd; }
+        if (with_hd) { hd += q.hs_beta * AS.Hs[p]; AS.Hd[p] = hd; }
     }
     if (Hd_out) *Hd_out = hd;
     return d;
+}
+// Xd after the pending step: CG / PCD plain: + beta Xs; PCD snap: + beta Xs + (1 - beta) Xz
+__device__ __forceinline__ double apply_m(const Pending& q, const Prm& P, int i) {
+    double xd = q.init ? P.Xd[i] : 0.0;
+    if (q.on) xd += q.beta * P.Xs[i] + (q.zsnap ? (1.0 - q.beta) * P.Xz[i] : 0.0);
+    return xd;
 }
 __device__ __forceinline__ void consume_A(Ctl* c) { if (c->pend) { c->pend = 0; c->d_init = 1; } }
 __device__ __forceinline__ void consume_m(Ctl* c) { if (c->pend_m) { c->pend_m = 0; c->xd_init = 1; } }
@@ -552,12 +602,13 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
     __shared__ double2 res[TILE];
     __shared__ double smr[2 * ML_NW + 2];
     if ((skip && *skip) || (skip2 && *skip2)) return;
+    op.prepare();
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int ntiles = (nseg + TILE - 1) / TILE;
     long long streamed = 0, segs = 0;
-    double bcg = 0.0;
-    int pcdm = 0;
-    if (MODE == 2) { bcg = P.ctl->bcg; pcdm = P.ctl->pcd_mode; }
+    double bcg = 0.0, beta = 0.0;
+    int pcdm = 0, zs = 0;
+    if (MODE == 2) { bcg = P.ctl->bcg; pcdm = P.ctl->pcd_mode; beta = P.ctl->beta; zs = P.ctl->zsnap; }
     Red<0, 0, 1> r;
     r.zero();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -568,7 +619,11 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
             else if (MODE == 1) out0[p] = q.x + (s ? eps * s[p] : 0.0);
-            else if (pcdm) out0[p] = q.x + eps * s[p];
+            else if (pcdm) {   // PCD step (decided before this gather): Hs = H sigma, sigma = b s (+ snapped z)
+                const double zp = zs ? AS.u[p] : 0.0;
+                const double sg = (zp != 0.0) ? zp : beta * s[p];
+                out0[p] = beta * q.x + (zs ? (1.0 - beta) * q.y : 0.0) + eps * sg;
+            }
             else {
                 const double sp = AS.u[p] + bcg * AS.s[p];
                 AS.s[p] = sp;
@@ -832,7 +887,7 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         if (mode == 0) out_api[i] = xu;
         else {
             const double xs_old = P.Xs[i];
-            if (q.on) P.Xd[i] = (q.init ? P.Xd[i] : 0.0) + q.beta * xs_old;
+            if (q.on) P.Xd[i] = apply_m(q, P, i);
             const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
             P.Xs[i] = xs;
             const double D = P.rD[i].y;
@@ -858,7 +913,7 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
     if (threadIdx.x == 0) {
         consume_m(c);
         const double sHs = tot + P.eps_h * c->ss;
-        if (mode == 1) decide_pcd(P, c, sHs);
+        if (mode == 1) { c->nzero = 0; decide_pcd(P, c, sHs, 0.0, 0.0); }
         else c->sHs = sHs;
         c->grp_done = 0u;
     }
@@ -950,8 +1005,8 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
 // The relaxation state lives in registers/shared memory of every block; block 0 writes it back to ml::Ctl at the end
 // (the outer line search then applies any pending step).
 struct IState {
-    int pend, pend_m, d_init, xd_init, snap, cg_restart, next_pcd, acc_steps, stop, pcd;
-    double beta, bk, bq, bcg, rz, rz_prev, slope, ss, ps, sHs, vq;
+    int pend, pend_m, d_init, xd_init, snap, cg_restart, next_pcd, acc_steps, stop, pcd, zsnap, nzero;
+    double beta, bk, bq, bcg, rz, rz_prev, slope, ss, ps, sHs, vq, hs_beta, pz, Z1, zz;
 };
 
 // every block: sums of NV per-block partials part[b*NV + k] in block order -> out[k] (shared); warps own values
@@ -1085,7 +1140,9 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
     st.cg_restart = c->cg_restart; st.next_pcd = c->next_pcd; st.acc_steps = c->acc_steps; st.stop = c->inner_stop;
     st.pcd = c->pcd_mode; st.beta = c->beta; st.bk = c->bk; st.bq = c->bq; st.bcg = c->bcg; st.rz = c->rz;
     st.rz_prev = c->rz_prev; st.slope = c->slope; st.ss = c->ss; st.ps = c->ps; st.sHs = c->sHs; st.vq = c->vq;
+    st.zsnap = c->zsnap; st.hs_beta = c->hs_beta; st.nzero = 0; st.pz = 0.0; st.Z1 = 0.0; st.zz = 0.0;
     const double vmax_C = c->vmax;
+    double* svz_sh = reinterpret_cast<double*>(smraw + pw + stream_warp_bytes<IN_SCH, IN_NSTG>(0));   // warp 1's acc area
     long long nsc = 0, nhs = 0;
     double bt[ML_MAXLS];
     bt[0] = 1.0;
@@ -1095,12 +1152,12 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
         // ------------------------------------------------ D: pending step + direction on my positions
         ColStream<IN_SCH, IN_NSTG> csG;   // the Hs phase's stream (prefetched before the m-side barrier)
         const int pcd = st.next_pcd;
-        const Pending pq{st.pend, st.d_init, st.snap, st.beta, st.bk};
+        const Pending pq{st.pend, st.d_init, st.snap, st.zsnap, st.beta, st.bk, st.hs_beta};
         if (pcd) {
-            double v[ML_MAXLS + 2];
+            double v[ML_MAXLS + 6];   // ps, ss, l1 trial sums, pz, Z1, zz, #zeroing
             double vm0 = 0.0, vm1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < ML_MAXLS + 2; ++k) v[k] = 0.0;
+            for (int k = 0; k < ML_MAXLS + 6; ++k) v[k] = 0.0;
             for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
                 double Hd;
                 const double d = apply_A(pq, AS, p, true, &Hd);
@@ -1108,6 +1165,8 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 const double sp = soft(x - pj / hh, P.lam / hh) - x;
                 AS.s[p] = sp;
                 const double vv = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+                const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;   // zeroing part (Q27)
+                AS.u[p] = zp;
                 vm0 = fmax(vm0, fabs(sp));
                 vm1 = fmax(vm1, fabs(vv));
                 v[0] += pj * sp;
@@ -1115,18 +1174,22 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 const double ax = fabs(x);
 #pragma unroll
                 for (int t = 0; t < ML_MAXLS; ++t) v[2 + t] += fabs(x + bt[t] * sp) - ax;
+                v[ML_MAXLS + 2] += pj * zp;
+                v[ML_MAXLS + 3] += fabs(zp);
+                v[ML_MAXLS + 4] += zp * zp;
+                v[ML_MAXLS + 5] += (zp != 0.0) ? 1.0 : 0.0;
             }
-            blk_sums<ML_MAXLS + 2>(v, sh_w, sh_t);
+            blk_sums<ML_MAXLS + 6>(v, sh_w, sh_t);
             vm0 = warp_max(vm0);
             vm1 = warp_max(vm1);
             if (lane == 0) { sh_w[wid] = vm0; sh_w[16 + wid] = vm1; }
             __syncthreads();
-            if (threadIdx.x < ML_MAXLS + 2) part[(size_t)blockIdx.x * (ML_MAXLS + 4) + threadIdx.x] = sh_t[threadIdx.x];
+            if (threadIdx.x < ML_MAXLS + 6) part[(size_t)blockIdx.x * (ML_MAXLS + 8) + threadIdx.x] = sh_t[threadIdx.x];
             if (threadIdx.x == 0) {
                 double a = 0.0, b = 0.0;
                 for (int w = 0; w < W; ++w) { a = fmax(a, sh_w[w]); b = fmax(b, sh_w[16 + w]); }
-                part[(size_t)blockIdx.x * (ML_MAXLS + 4) + ML_MAXLS + 2] = a;
-                part[(size_t)blockIdx.x * (ML_MAXLS + 4) + ML_MAXLS + 3] = b;
+                part[(size_t)blockIdx.x * (ML_MAXLS + 8) + ML_MAXLS + 6] = a;
+                part[(size_t)blockIdx.x * (ML_MAXLS + 8) + ML_MAXLS + 7] = b;
             }
             PH_MARK(0);
         } else {
@@ -1209,7 +1272,7 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
             PH_MARK(3);
             // direction totals (identical in every block) and its stop tests
             {
-                const int NV = pcd ? ML_MAXLS + 4 : 8;
+                const int NV = pcd ? ML_MAXLS + 8 : 8;
                 grid_totals(part, NV, sh_t, false);
                 __shared__ double sh_mx[2];
                 if (threadIdx.x < 64) {   // maxima: PCD slots NV-2 (max|s|), NV-1 (vq); CG slot 6 (vq)
@@ -1225,6 +1288,10 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 if (pcd) {
                     st.ps = sh_t[0];
                     st.ss = sh_t[1];
+                    st.pz = sh_t[ML_MAXLS + 2];
+                    st.Z1 = sh_t[ML_MAXLS + 3];
+                    st.zz = sh_t[ML_MAXLS + 4];
+                    st.nzero = (int)sh_t[ML_MAXLS + 5];
                     st.vq = sh_mx[1];
                     stop = (it > 0 && P.eta > 0.0 && sh_mx[1] <= P.eta * vmax_C);
                     if (sh_mx[0] == 0.0) stop = 1;
@@ -1246,29 +1313,83 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 PH_MARK(1);
                 if (stop) break;
             }
+            const int withz = pcd && st.nzero > 0;
+            double* parts_z = parts + (size_t)gridDim.x * m + 8 * gridDim.x;   // after part2's 5 x grid scalars
+            if (withz) {   // S': X_A z over the zeroing columns only (AS.u holds z; zero coefficients are skipped)
+                for (int i = lane; i < m; i += 32) mine[i] = 0.0;
+                __syncwarp();
+                ColStream<IN_SCH, IN_NSTG> cz;
+                cz.streamed = 0;
+                cz.segs = 0;
+                stream_begin(cz, S, AS.u, p0, p1, base);
+                int stg = 0;
+                while (true) {
+                    const ChunkDesc d = cz.desc[stg];
+                    if (d.cf == 0.0) break;
+                    mbar_wait(cz.bar + stg, (phase >> stg) & 1u);
+                    phase ^= 1u << stg;
+                    const int* ci = cz.sidx + stg * IN_SCH - d.a;
+                    const float* cv = cz.sval + stg * IN_SCH - d.a;
+                    const int kend = min(d.ve, d.ce);
+                    int k2 = d.vb + lane;
+                    for (; k2 < kend; k2 += 32) { const int r = ci[k2]; mine[r] = fma((double)cv[k2], d.cf, mine[r]); }
+                    for (; k2 < d.ve; k2 += 32) { const int r = __ldg(S.idx + k2); mine[r] = fma((double)__ldg(S.val + k2), d.cf, mine[r]); }
+                    __syncwarp();
+                    ChunkDesc nd;
+                    const bool ok = cz.next(nd);
+                    if (lane == 0) {
+                        if (ok) { cz.desc[stg] = nd; cz.issue(stg, nd); }
+                        else cz.desc[stg].cf = 0.0;
+                    }
+                    __syncwarp();
+                    stg = (stg + 1) % IN_NSTG;
+                }
+                nsc += cz.streamed;
+                __syncthreads();
+                for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                    double t = 0.0;
+                    for (int w = 0; w < W; ++w) t += reinterpret_cast<const double*>(smraw + (size_t)w * pw + stream_warp_bytes<IN_SCH, IN_NSTG>(0))[i];
+                    parts_z[(size_t)blockIdx.x * m + i] = t;
+                }
+                __threadfence();
+                grid.sync();
+            }
             // my rows: combine the block partials (thread (row, group) split, groups in order)
             const int ng = max(1, (int)blockDim.x / max(R, 1));
             const int rr = threadIdx.x % max(R, 1), grp = threadIdx.x / max(R, 1);
-            double t = 0.0;
+            double t = 0.0, tz = 0.0;
             if (grp < ng && row0 + rr < row1)
-                for (int k2 = grp; k2 < (int)gridDim.x; k2 += ng) t += ld_cg(parts + (size_t)k2 * m + row0 + rr);
-            sh_w[threadIdx.x] = t;   // sh_w holds >= 16*(ML_MAXLS+4) >= blockDim doubles
+                for (int k2 = grp; k2 < (int)gridDim.x; k2 += ng) {
+                    t += ld_cg(parts + (size_t)k2 * m + row0 + rr);
+                    if (withz) tz += ld_cg(parts_z + (size_t)k2 * m + row0 + rr);
+                }
+            sh_w[threadIdx.x] = t;   // sh_w holds >= 16*(ML_MAXLS+4) >= 2*blockDim doubles
+            sh_w[blockDim.x + threadIdx.x] = tz;
             __syncthreads();
-            double a2 = 0.0;
+            double a2 = 0.0, a3 = 0.0, a4 = 0.0;
             if ((int)threadIdx.x < R && row0 + (int)threadIdx.x < row1) {
-                double xu = 0.0;
-                for (int g = 0; g < ng; ++g) xu += sh_w[g * R + threadIdx.x];
+                double xu = 0.0, xz = 0.0;
+                for (int g = 0; g < ng; ++g) { xu += sh_w[g * R + threadIdx.x]; xz += sh_w[blockDim.x + g * R + threadIdx.x]; }
                 const int i = row0 + threadIdx.x;
                 const double xs_old = P.Xs[i];
-                if (st.pend_m) P.Xd[i] = (st.xd_init ? P.Xd[i] : 0.0) + st.beta * xs_old;
+                if (st.pend_m)   // pending step: CG / PCD plain + beta Xs, PCD snap + beta Xs + (1 - beta) Xz
+                    P.Xd[i] = (st.xd_init ? P.Xd[i] : 0.0) + st.beta * xs_old + (st.zsnap ? (1.0 - st.beta) * P.Xz[i] : 0.0);
                 const double xs = pcd ? xu : xu + st.bcg * xs_old;
                 P.Xs[i] = xs;
                 const double D = P.rD[i].y;
                 P.sv[i] = D * xs;
                 a2 = D * xs * xs;
+                if (withz) {
+                    P.Xz[i] = xz;
+                    P.svz[i] = D * xz;
+                    a3 = D * xs * xz;
+                    a4 = D * xz * xz;
+                }
             }
             const double bs = block_sum_any(a2);
-            if (threadIdx.x == 0) part2[blockIdx.x] = bs;
+            const double bs3 = withz ? block_sum_any(a3) : 0.0;
+            const double bs4 = withz ? block_sum_any(a4) : 0.0;
+            if (threadIdx.x == 0) { part2[blockIdx.x] = bs; part2[3 * gridDim.x + blockIdx.x] = bs3; part2[4 * gridDim.x + blockIdx.x] = bs4; }
             // prefetch: start the Hs phase's TMA ring (X_A does not depend on sv) before the barrier
             if (it < K - 1) {
                 csG.streamed = 0;
@@ -1277,29 +1398,47 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
             }
             __threadfence();
             grid.sync();
-            if (threadIdx.x < 32) {
+            if (threadIdx.x < 96) {   // warps 0, 1, 2: s^T H s, z^T H s, z^T H z (without the ridge)
+                const int kk = threadIdx.x >> 5;
+                const int off = kk == 0 ? 0 : (kk + 2) * (int)gridDim.x;
                 double tt = 0.0;
-                for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) tt += ld_cg(part2 + b);
+                if (kk == 0 || withz)
+                    for (int b = lane; b < (int)gridDim.x; b += 32) tt += ld_cg(part2 + off + b);
                 tt = warp_sum(tt);
-                if (threadIdx.x == 0) sh_m[0] = tt;
+                if (lane == 0) sh_m[kk] = tt;
             }
             __syncthreads();
             PH_MARK(4);
             if (st.pend_m) { st.pend_m = 0; st.xd_init = 1; }
             const double sHs = sh_m[0] + P.eps_h * st.ss;
             st.sHs = sHs;
-            if (pcd) {   // R10: Armijo on the model (decide_pcd); sh_t[2 + t] still holds the l1 trial sums of D
+            if (pcd) {   // R10 (decide_pcd incl. the snap path, Q27); sh_t[2 + t] still holds the l1 trial sums of D
+                const double zHs = sh_m[1] + P.eps_h * st.zz, zHz = sh_m[2] + P.eps_h * st.zz;
                 const double delta = st.ps + P.lam * sh_t[2];
                 double b = 1.0;
-                int ok = 0;
-                for (int t2 = 0; t2 < P.max_ls; ++t2, b *= P.beta_ls) {
-                    const double dq = b * st.ps + 0.5 * b * b * sHs + P.lam * sh_t[2 + t2];
-                    if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+                int ok = 0, snapped = 0;
+                if (withz) {
+                    const double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
+                    for (int t2 = 0; t2 < P.max_ls; ++t2, b *= P.beta_ls) {
+                        const double dq = b * (st.ps - st.pz) + st.pz + 0.5 * (b * b * snHsn + 2.0 * b * snHz + zHz) +
+                                          P.lam * (sh_t[2 + t2] - (1.0 - b) * st.Z1);
+                        if (dq <= P.sigma_in * b * delta) { ok = 1; snapped = 1; break; }
+                    }
+                }
+                if (!ok) {
+                    b = 1.0;
+                    for (int t2 = 0; t2 < P.max_ls; ++t2, b *= P.beta_ls) {
+                        const double dq = b * st.ps + 0.5 * b * b * sHs + P.lam * sh_t[2 + t2];
+                        if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+                    }
                 }
                 st.cg_restart = 1;
                 st.next_pcd = (inner_cg == 0);
                 if (!ok) { st.stop = 1; st.beta = 0.0; }
-                else { st.beta = b; st.snap = 0; st.pend = 1; st.pend_m = 1; st.acc_steps += 1; }
+                else {
+                    st.beta = b; st.snap = 0; st.zsnap = snapped; st.hs_beta = 1.0;
+                    st.pend = 1; st.pend_m = 1; st.acc_steps += 1;
+                }
             }
         }
         if (st.stop) {
@@ -1313,11 +1452,15 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
         double bkmin = __longlong_as_double(0x7ff0000000000000LL);
         if (need_hs) {
             __syncthreads();
-            for (int i = threadIdx.x; i < m; i += blockDim.x) sv_sh[i] = ld_cg(P.sv + i);
+            const int dual = pcd && st.zsnap;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                sv_sh[i] = ld_cg(P.sv + i);
+                if (dual) svz_sh[i] = ld_cg(P.svz + i);
+            }
             __syncthreads();
             ColStream<IN_SCH, IN_NSTG>& cs = csG;
             int stg = 0;
-            double a = 0.0;
+            double a = 0.0, az = 0.0;
             while (true) {
                 const ChunkDesc d = cs.desc[stg];
                 if (d.cf == 0.0) break;
@@ -1327,21 +1470,39 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 const float* cv = cs.sval + stg * IN_SCH - d.a;
                 const int kend = min(d.ve, d.ce);
                 int k = d.vb + lane;
-                double a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                for (; k + 96 < kend; k += 128) {
-                    a = fma((double)cv[k], sv_sh[ci[k]], a);
-                    a1 = fma((double)cv[k + 32], sv_sh[ci[k + 32]], a1);
-                    a2 = fma((double)cv[k + 64], sv_sh[ci[k + 64]], a2);
-                    a3 = fma((double)cv[k + 96], sv_sh[ci[k + 96]], a3);
+                if (dual) {
+                    for (; k < kend; k += 32) {
+                        const int r = ci[k];
+                        a = fma((double)cv[k], sv_sh[r], a);
+                        az = fma((double)cv[k], svz_sh[r], az);
+                    }
+                    for (; k < d.ve; k += 32) {
+                        const int r = __ldg(S.idx + k);
+                        const double xv = (double)__ldg(S.val + k);
+                        a = fma(xv, sv_sh[r], a);
+                        az = fma(xv, svz_sh[r], az);
+                    }
+                } else {
+                    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    for (; k + 96 < kend; k += 128) {
+                        a = fma((double)cv[k], sv_sh[ci[k]], a);
+                        a1 = fma((double)cv[k + 32], sv_sh[ci[k + 32]], a1);
+                        a2 = fma((double)cv[k + 64], sv_sh[ci[k + 64]], a2);
+                        a3 = fma((double)cv[k + 96], sv_sh[ci[k + 96]], a3);
+                    }
+                    a += (a1 + a2) + a3;
+                    for (; k < kend; k += 32) a = fma((double)cv[k], sv_sh[ci[k]], a);
+                    for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[__ldg(S.idx + k)], a);
                 }
-                a += (a1 + a2) + a3;
-                for (; k < kend; k += 32) a = fma((double)cv[k], sv_sh[ci[k]], a);
-                for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[__ldg(S.idx + k)], a);
                 if (d.last) {
                     const double t = warp_sum(a);
+                    const double tz = dual ? warp_sum(az) : 0.0;
                     if (lane == 0) {
-                        if (pcd) AS.Hs[d.p] = t + P.eps_h * AS.s[d.p];
-                        else {
+                        if (pcd) {   // H sigma, sigma = b s (+ snapped z)
+                            const double zp = dual ? AS.u[d.p] : 0.0;
+                            const double sg = (zp != 0.0) ? zp : st.beta * AS.s[d.p];
+                            AS.Hs[d.p] = st.beta * t + (dual ? (1.0 - st.beta) * tz : 0.0) + P.eps_h * sg;
+                        } else {
                             const double sp = AS.u[d.p] + st.bcg * AS.s[d.p];
                             AS.s[d.p] = sp;
                             AS.Hs[d.p] = t + P.eps_h * sp;
@@ -1350,6 +1511,7 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                         }
                     }
                     a = 0.0;
+                    az = 0.0;
                 }
                 __syncwarp();
                 ChunkDesc nd;
@@ -1385,6 +1547,8 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
                 st.bq = bq;
                 st.beta = bq < bk ? bq : bk;
                 st.snap = (bk <= bq);
+                st.zsnap = 0;
+                st.hs_beta = st.beta;
                 st.cg_restart = st.snap;
                 st.next_pcd = (inner_cg == 2) && st.snap;
                 st.rz_prev = st.rz;
@@ -1411,6 +1575,7 @@ __global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, i
         c->cg_restart = st.cg_restart; c->next_pcd = st.next_pcd; c->acc_steps = st.acc_steps; c->inner_stop = st.stop;
         c->pcd_mode = st.pcd; c->beta = st.beta; c->bk = st.bk; c->bq = st.bq; c->bcg = st.bcg; c->rz = st.rz;
         c->rz_prev = st.rz_prev; c->slope = st.slope; c->ss = st.ss; c->ps = st.ps; c->sHs = st.sHs; c->vq = st.vq;
+        c->zsnap = st.zsnap; c->hs_beta = st.hs_beta;
     }
 }
 
@@ -1445,6 +1610,10 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
     c->acc_steps = 0;
     c->combine = 0;
     c->next_pcd = 1;
+    c->zsnap = 0;
+    c->nzero = 0;
+    c->zscatter_skip = 1;
+    c->hs_beta = 0.0;
     c->units_n[2] = 0;   // A-set units are rebuilt by the gather
     c->units_h[2] = 0;
     if (set_list) { c->Cptr = Cptr; c->nC = nC; }
@@ -1461,12 +1630,12 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
 //  Both: the model's min-norm subgradient (forcing, R13).
 __global__ void __launch_bounds__(ML_NT) k_dir_pcd(Prm P, ASet AS, int it) {
     constexpr int WANT = 1;
-    __shared__ double sm[(ML_MAXLS + 4) * ML_NW + ML_MAXLS + 4];
+    __shared__ double sm[(ML_MAXLS + 8) * ML_NW + ML_MAXLS + 8];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop || c->next_pcd != WANT) return;   // the iteration type is chosen on the device
     const int nA = c->nA;
     const Pending q = pending_A(c);
-    Red<ML_MAXLS + 2, 2> r;
+    Red<ML_MAXLS + 6, 2> r;   // ps, ss, l1 trial sums, pz, Z1, zz, #zeroing
     r.zero();
     double bt[ML_MAXLS];
     bt[0] = 1.0;
@@ -1479,6 +1648,8 @@ __global__ void __launch_bounds__(ML_NT) k_dir_pcd(Prm P, ASet AS, int it) {
         const double sp = soft(x - pj / hh, P.lam / hh) - x;
         AS.s[p] = sp;
         const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+        const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;   // zeroing part (Q27)
+        AS.u[p] = zp;
         r.mx[0] = fmax(r.mx[0], fabs(sp));
         r.mx[1] = fmax(r.mx[1], fabs(v));
         r.s[0] += pj * sp;
@@ -1486,10 +1657,18 @@ __global__ void __launch_bounds__(ML_NT) k_dir_pcd(Prm P, ASet AS, int it) {
         const double ax = fabs(x);
 #pragma unroll
         for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * sp) - ax;
+        r.s[ML_MAXLS + 2] += pj * zp;
+        r.s[ML_MAXLS + 3] += fabs(zp);
+        r.s[ML_MAXLS + 4] += zp * zp;
+        r.s[ML_MAXLS + 5] += (zp != 0.0) ? 1.0 : 0.0;
     }
     if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
         if (threadIdx.x == 0) {
             consume_A(c);
+            c->pz = r.s[ML_MAXLS + 2];
+            c->Z1 = r.s[ML_MAXLS + 3];
+            c->zz = r.s[ML_MAXLS + 4];
+            c->nzero = (int)r.s[ML_MAXLS + 5];
             c->vq = r.mx[1];
             int stop = (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax);   // R13 forcing
             c->ps = r.s[0];
@@ -1499,6 +1678,7 @@ __global__ void __launch_bounds__(ML_NT) k_dir_pcd(Prm P, ASet AS, int it) {
             c->combine = 0;
             c->bcg = 0.0;
             c->inner_stop = stop;
+            c->zscatter_skip = (c->nzero == 0) || stop;   // Xzu must stay zero: no z pass without its m-pass
             c->pcd_mode = 1;
             c->it = it;
         }
@@ -1546,6 +1726,7 @@ __global__ void __launch_bounds__(ML_NT) k_dir_cg(Prm P, ASet AS, int it) {
             c->combine = 1;
             c->inner_stop = stop;
             c->pcd_mode = 0;
+            c->zscatter_skip = 1;
             c->it = it;
         }
     }
@@ -1573,31 +1754,42 @@ __global__ void __launch_bounds__(ML_NT) k_cg_finish(Prm P, ASet AS) {
 // m-side pass of the atomic-scatter path: Xu -> (pending Xd += beta Xs) -> Xs = Xu (+ b Xs_prev) -> sv = D o Xs,
 // s^T H s; Xu is cleared for the next scatter; PCD decision (R10).
 __global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int mode) {
-    __shared__ double sm[2 * ML_NW + 2];
+    __shared__ double sm[4 * ML_NW + 4];
     Ctl* c = P.ctl;
     if (c->skip || c->inner_stop) return;
     if (mode < 0) mode = c->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
     const Pending q = pending_m(c);
     const double bcg = (mode == 2) ? c->bcg : 0.0;
-    Red<1> r;
+    const int withz = (mode == 1) && !c->zscatter_skip;
+    Red<3> r;
     r.zero();
     for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
         const double xu = P.Xu[i];
         P.Xu[i] = 0.0;
+        if (q.on) P.Xd[i] = apply_m(q, P, i);   // uses the previous Xs, Xz
         const double xs_old = P.Xs[i];
-        if (q.on) P.Xd[i] = (q.init ? P.Xd[i] : 0.0) + q.beta * xs_old;
         const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
         P.Xs[i] = xs;
         const double D = P.rD[i].y;
         P.sv[i] = D * xs;
         r.s[0] += D * xs * xs;
+        if (withz) {
+            const double xz = P.Xzu[i];
+            P.Xzu[i] = 0.0;
+            P.Xz[i] = xz;
+            P.svz[i] = D * xz;
+            r.s[1] += D * xs * xz;
+            r.s[2] += D * xz * xz;
+        }
     }
     if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
         if (threadIdx.x == 0) {
             consume_m(c);
             const double sHs = r.s[0] + P.eps_h * c->ss;
-            if (mode == 1) decide_pcd(P, c, sHs);
-            else c->sHs = sHs;
+            if (mode == 1) {
+                if (!withz) c->nzero = 0;
+                decide_pcd(P, c, sHs, r.s[1] + P.eps_h * c->zz, r.s[2] + P.eps_h * c->zz);
+            } else c->sHs = sHs;
         }
     }
 }
@@ -1647,7 +1839,7 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
         const Pending q = pending_m(c);
         for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
             double xd;
-            if (t0 == 0 && q.on) { xd = (q.init ? P.Xd[i] : 0.0) + q.beta * P.Xs[i]; P.Xd[i] = xd; }
+            if (t0 == 0 && q.on) { xd = apply_m(q, P, i); P.Xd[i] = xd; }
             else xd = P.Xd[i];
             const double y = (double)P.y[i];
             const double ti = y * P.z[i], yx = y * xd;
@@ -1730,7 +1922,7 @@ __global__ void __launch_bounds__(ML_NT) k_update(Prm P, ASet AS, int nblkA) {
             c->F = c->L + P.lam * c->l1;
             c->outcome = OUT_UPDATED;
             if (c->ntrace < c->trace_cap) {
-                TraceRow tr{c->level, OUT_UPDATED, 0, c->nA, (long long)c->nC, Fb, c->F, a};
+                TraceRow tr{c->level, OUT_UPDATED, c->acc_steps, c->nA, (long long)c->nC, Fb, c->F, a};
                 P.trace[c->ntrace] = tr;
             }
             c->ntrace += 1;
@@ -1743,7 +1935,7 @@ __global__ void k_relax_end(Prm P) {
     Ctl* c = P.ctl;
     if (c->outcome == OUT_UPDATED || c->skipped) return;
     if (c->ntrace < c->trace_cap) {
-        TraceRow tr{c->level, c->outcome, 0, c->nA, (long long)c->nC, c->F, c->F, 0.0};
+        TraceRow tr{c->level, c->outcome, c->outcome == OUT_CONVERGED ? 0 : c->acc_steps, c->nA, (long long)c->nC, c->F, c->F, 0.0};
         P.trace[c->ntrace] = tr;
     }
     c->ntrace += 1;

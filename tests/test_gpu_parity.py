@@ -254,11 +254,34 @@ def test_solve_parity_full_configs(name):
     _support_check(ds, ctx.ml_get_w().cpu().numpy(), w_o, g_o)
 
 
-@pytest.mark.parametrize("name,opts", [("cfg2s", {"inner_cg": 2}), ("cfg1", {"inner_cg": 2}), ("onehot", {"inner_cg": 2})])
+@pytest.mark.parametrize("name,opts", [("cfg2s", {"inner_cg": 1, "pcd_snap": 0}), ("cfg1", {"inner_cg": 1, "pcd_snap": 0}),
+                                       ("onehot", {"inner_cg": 1, "pcd_snap": 0}), ("cfg2s", {"pcd_snap": 0}),
+                                       ("cfg4s", {"pcd_snap": 0}), ("cfg4s", {}), ("cfg4s", {"inner_cg": 0})])
 def test_solve_parity_inner_variants(name, opts):
-    """The other inner solver (DESIGN Q9b): PCD-CG with a shrinkage step after every kink.  (Plain PCD is covered on
-    cfg 1 by test_solve_parity; it does not reach kappa <= 1e-6 on the Zipf designs in either implementation.)"""
+    """The other inner solvers (DESIGN Q9b, Q27): plain PCD-CG, PCD-CG with a shrinkage step after every kink without
+    the snap path, plain PCD with the snap path; small-m (persistent) and large-m (generic) relaxation paths."""
     test_solve_parity(name, opts)
+
+
+@pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("cfg2s", {"inner_cg": 0}),
+                                       ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0})])
+def test_trace_parity(name, opts):
+    """Relaxation by relaxation (Algorithm 1, DESIGN S1-S18/R1-R18): level, |A|, outcome, inner iterations and
+    F after each of the first relaxations agree with the oracle's trace (decisions identical while rounding
+    differences stay below the decision margins)."""
+    ds = dataset(name)
+    o = oracle.Oracle(ds)
+    o.solve(oracle.default_opts(max_cycles=3, **opts))
+    ctx = ml.Context(ds)
+    ctx.ml_solve(ml.default_opts(max_cycles=3, **opts))
+    to, tg = o.trace(), ctx.trace()
+    n = min(len(to), len(tg), 12)
+    assert n >= 5
+    for k in range(n):
+        a, b = to[k], tg[k]
+        for f in ("level", "nA", "outcome", "inner_iters"):
+            assert a[f] == b[f], (k, f, a, b)
+        assert abs(a["F_after"] - b["F_after"]) <= 1e-9 * abs(a["F_after"]), (k, a, b)
 
 
 @pytest.mark.parametrize("cfg", [4, 5])

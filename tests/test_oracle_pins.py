@@ -304,10 +304,16 @@ def _brute_force(X, y, lam):
     return best
 
 
+VARIANTS = [dict(), dict(pcd_snap=0), dict(inner_cg=1, pcd_snap=0), dict(inner_cg=0, pcd_snap=1),
+            dict(inner_cg=0, pcd_snap=0), dict(multilevel=0)]
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("variant", range(len(VARIANTS)))
 @pytest.mark.filterwarnings("ignore::RuntimeWarning")
-def test_brute_force_small(seed):
-    """Solver on general tiny data vs brute-force support/sign enumeration."""
+def test_brute_force_small(seed, variant):
+    """Solver on general tiny data vs brute-force support/sign enumeration, for every inner-solver
+    variant (DESIGN Q9b, Q27): all of them must reach the same unique minimiser."""
     rng = np.random.default_rng(100 + seed)
     m, n = 24, 6
     X = rng.standard_normal((m, n)).astype(np.float32)
@@ -316,11 +322,15 @@ def test_brute_force_small(seed):
     lam = 0.15 * lmax
     wref, Fref = _brute_force(X.astype(np.float64), y.astype(np.float64), lam)
     o = oracle.Oracle(mlgen.from_dense(X, y, lam))
-    rep = o.solve(_tight())
+    v = dict(VARIANTS[variant])
+    if v.get("inner_cg") == 0:   # plain PCD's model decrease hits rounding near kappa ~ 1e-10 (no step, not an error)
+        v["tol_kkt"] = 1e-9
+    rep = o.solve(oracle.default_opts(**{"tol_kkt": 1e-12, "max_cycles": 2000, **v}))
     w = o.get_w()
     assert rep["status"] == 0
     assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
     assert abs(rep["F"] - Fref) <= 1e-12 * Fref
+    assert np.max(np.abs(w - wref)) <= (1e-6 if v.get("inner_cg") == 0 else 1e-9) * max(1.0, np.max(np.abs(wref)))
 
 
 # ----------------------------------------------------------------------------- small-lambda limit
