@@ -72,7 +72,7 @@ struct ml_ctx {
     int scat_W = 0, scat_P = 0, gMP = 1;
     size_t scat_bytes = 0;
     bool sm_gather = false;
-    bool sm_inner = false;   // persistent cooperative inner solver (k_inner_small)
+    bool sm_inner = false;   // persistent cooperative inner solver (k_inner)
     int inner_W = 0, inner_P = 0;
     size_t inner_bytes = 0;
     int gath_W = 0, gath_P = 0;
@@ -116,6 +116,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
     double2* hres = cv.take<double2>(std::max(nn, mm));
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
+    double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -145,6 +146,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     Prm& P = c->P;
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
+    P.irpart = irpart;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
 
@@ -339,7 +341,7 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
                     double* out, const int* skip, const int* skip2, int mode = 0, const double* coef2 = nullptr) {
     Seg S = seg_cols(c, list);
     const int* use1 = &c->ctl->pcd_mode;   // relaxation (mode < 0): coef (s) on PCD steps, coef2 (u) on PCD-CG steps
-    if (c->sm_scatter && mode == 0) {   // relaxations on small m run inside k_inner_small
+    if (c->sm_scatter && mode == 0) {   // relaxations on small m run inside k_inner
         {
             PassScope ps(c, cls);
             Prm Pc = c->P;
@@ -422,8 +424,7 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
         long long* a1 = acc_of(c, CLS_SCATTER);
         long long* a2 = acc_of(c, CLS_HS);
         void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
-        cudaLaunchCooperativeKernel((const void*)k_inner_small, dim3(c->inner_P), dim3(32 * c->inner_W), args,
-                                    c->inner_bytes, c->st);
+        cudaLaunchCooperativeKernel((const void*)k_inner, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
         c->launches++;
     } else
     for (int it = 0; it < K; ++it) {
@@ -597,17 +598,15 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->gath_bytes = bytes;
             c->gath_P = SM_COUNT * bps;
         }
-        W = 8;
-        while (W > 1 && inner_smem_bytes(W, (int)X->m) > 196 * 1024) --W;
-        bytes = inner_smem_bytes(W, (int)X->m);
-        if (W >= 2 && cudaFuncSetAttribute(k_inner_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
+        bytes = inner_smem_bytes((int)X->m);
+        if (bytes <= 220 * 1024 && X->m <= 256LL * std::min(SM_COUNT, IR_GMAX) &&
+            cudaFuncSetAttribute(k_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
             int bps = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inner_small, 32 * W, bytes);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inner, 32 * IR_W, bytes);
             if (bps >= 1) {
-                c->sm_inner = c->sm_scatter && c->sm_gather;
-                c->inner_W = W;
+                c->sm_inner = true;
                 c->inner_bytes = bytes;
-                c->inner_P = SM_COUNT;
+                c->inner_P = std::min(SM_COUNT, IR_GMAX);
             }
         }
         cudaGetLastError();
@@ -929,8 +928,8 @@ ml_status ml_inner_phases(ml_ctx* c, uint64_t* ns_host, int reset) {
     if (!c) return ML_E_INVAL;
     ml_status s = sync_ctl(c);
     if (s != ML_OK) return s;
-    for (int k = 0; k < 8; ++k) if (ns_host) ns_host[k] = c->h.tph[k];
-    if (reset) { unsigned long long z[8] = {0}; cudaMemcpyAsync(c->ctl->tph, z, sizeof(z), cudaMemcpyHostToDevice, c->st); }
+    for (int k = 0; k < 12; ++k) if (ns_host) ns_host[k] = c->h.tph[k];
+    if (reset) { unsigned long long z[12] = {0}; cudaMemcpyAsync(c->ctl->tph, z, sizeof(z), cudaMemcpyHostToDevice, c->st); }
     return cuda_fail(c, "ml_inner_phases");
 }
 

@@ -1,0 +1,531 @@
+// Persistent small-m inner solver (A4-A6 for m <= SMALL_M).
+//
+// One cooperative launch per relaxation runs all K inner iterations (R4-R12) on the free set A.
+// Block b owns the contiguous free-set positions [b q, (b+1) q) and the contiguous rows [b R, (b+1) R).  Per inner
+// iteration, two grid barriers:
+//   D   my positions: direction (PCD Eq. 5 with the zeroing part z of Q27, or the PCD-CG residual u of Q9b), block
+//       partial sums;
+//   S   X_A coef over my columns into ONE shared m-vector per block: the block stages one column chunk at a time
+//       (TMA bulk copies, a 4-stage ring) and every warp takes a slice of it -- rows are distinct within a column, so
+//       there are no conflicts and no per-warp copies; zeroing columns also go to a second m-vector (X_A z);
+//       the m-vector(s) are written as this block's partials                                      -> barrier B1
+//   R   every block sums the direction partials (identical in every block: fixed order); my rows: X_A s = sum of the
+//       block partials in block order (PCD-CG: X_A u + b X s_prev), X_A z, D-weighted squares; PCD-CG: s = u + b s_prev
+//       and the first kink on my positions                                                         -> barrier B2
+//   G   totals; the step decision (model Armijo with the snap path, or the CG step truncated at the first kink) in
+//       every block; my rows Xd += X sigma; sv = D o X sigma for all rows into shared memory; my positions:
+//       H sigma = X_A^T sv + eps sigma through per-warp TMA rings (prefetched across B2), d += sigma, Hd += H sigma.
+// Partials are slot-major (part[slot * G + block]): a warp sums one slot with coalesced loads in a fixed order, so
+// every block takes bitwise identical decisions, and results are reproducible run to run.
+#pragma once
+
+constexpr int IR_W = 8;          // warps per block (launch with 256 threads)
+constexpr int IR_GMAX = 160;     // grid <= 160 blocks (5 partials per lane in the totals)
+constexpr int IR_NT0 = 4;        // l1 trial differences computed with the direction; the rest only if Armijo needs them
+constexpr int IR_SCH = 2048, IR_SST = 4;   // S phase: block-shared ring, chunk elements x stages
+constexpr int IN_GSCH = 512, IN_GST = 2;   // G phase: per-warp rings
+// partial slots: D (PCD) 0 ps, 1 ss, 2 pz, 3 Z1, 4 zz, 5 #zeroing, 6..9 l1 trials 0..3, 10 max|s|, 11 vq
+//                D (CG)  0 rz, 1 gx.u, 2 gx.s_prev, 3 u.u, 4 u.s_prev, 5 s_prev.s_prev, 11 vq
+//                R       12 D Xs^2, 13 D Xs Xz, 14 D Xz^2, 15 first kink (min);  lazy l1 trials 16 ..
+enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16, IR_NSLOT = 16 + ML_MAXLS - IR_NT0 };
+constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
+
+struct SChunk { int p, a, vb, ve, ce, zf; double cf; };   // copy [a, ce) of column p, valid [vb, ve)
+
+__host__ __device__ inline size_t ir_sring_bytes() {
+    return (size_t)8 * IR_SST * IR_SCH + 8 * IR_SST + sizeof(SChunk) * IR_SST;
+}
+__host__ __device__ inline size_t ir_ring_bytes() {
+    const size_t g = (size_t)IR_W * stream_warp_bytes<IN_GSCH, IN_GST>(0), s = ir_sring_bytes();
+    return ((g > s ? g : s) + 15) / 16 * 16;
+}
+// dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z)
+__host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes() + (size_t)16 * m; }
+
+// N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
+// block's own totals stay in sh_w[IR_W * N + k]
+template <int N>
+__device__ __forceinline__ void ir_block_partials(const double (&v)[N], unsigned maxmask, unsigned minmask,
+                                                  double* sh_w, double* part, int slot0) {
+    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double t = ((maxmask >> k) & 1u) ? warp_max(v[k]) : ((minmask >> k) & 1u) ? warp_min(v[k]) : warp_sum(v[k]);
+        if (lane == 0) sh_w[wid * N + k] = t;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        double t = sh_w[k];
+        for (int w = 1; w < W; ++w) {
+            const double x = sh_w[w * N + k];
+            t = ((maxmask >> k) & 1u) ? fmax(t, x) : ((minmask >> k) & 1u) ? fmin(t, x) : t + x;
+        }
+        part[(size_t)(slot0 + k) * gridDim.x + blockIdx.x] = t;
+        sh_w[IR_W * N + k] = t;
+    }
+    __syncthreads();
+}
+// grid total of one slot by one warp: op 0 sum, 1 max, 2 min (fixed order)
+__device__ __forceinline__ double ir_slot_total(const double* src, int op) {
+    const int lane = threadIdx.x & 31, G = gridDim.x;
+    const double idn = op == 2 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+    double v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int b = lane + 32 * j;
+        v[j] = b < G ? ld_cg(src + b) : idn;
+    }
+    double t = v[0];
+#pragma unroll
+    for (int j = 1; j < 5; ++j) t = op == 0 ? t + v[j] : op == 1 ? fmax(t, v[j]) : fmin(t, v[j]);
+    return op == 0 ? warp_sum(t) : op == 1 ? warp_max(t) : warp_min(t);
+}
+// slots [s0, s0 + n) -> out[0 .. n) in shared memory, every block identically
+__device__ __forceinline__ void ir_totals(const double* part, int s0, int n, unsigned maxmask, unsigned minmask,
+                                          double* out) {
+    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = wid; k < n; k += W) {
+        const int op = ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
+        const double t = ir_slot_total(part + (size_t)(s0 + k) * gridDim.x, op);
+        if (lane == 0) out[k] = t;
+    }
+    __syncthreads();
+}
+
+// S phase producer (thread 0): the next chunk of my columns with a nonzero coefficient
+struct SProducer {
+    int p, p1, noff, nnz4;
+    __device__ bool next(const Seg& S, const double* coef, const double* zc, SChunk& d) {
+        while (p < p1) {
+            const double cf = coef[p];
+            const int j = __ldg(S.list + p);
+            const int b = __ldg(S.ptr + j), e = __ldg(S.ptr + j + 1);
+            const int start = b + noff;
+            if (cf == 0.0 || start >= e) { ++p; noff = 0; continue; }
+            d.p = p;
+            d.a = start & ~3;
+            d.vb = start;
+            d.ve = min(e, d.a + IR_SCH);
+            d.ce = max(d.a, min((d.ve + 3) & ~3, nnz4));
+            d.cf = cf;
+            d.zf = zc ? (zc[p] != 0.0) : 0;
+            if (d.ve == e) { ++p; noff = 0; } else noff = d.ve - b;
+            return true;
+        }
+        return false;
+    }
+    __device__ void issue(const Seg& S, const SChunk& d, int st, int* s_idx, float* s_val, uint64_t* s_bar) const {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(s_bar + st, 8u * (uint32_t)(d.ce - d.a));
+        if (d.ce > d.a) {
+            bulk_g2s(s_idx + st * IR_SCH, S.idx + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
+            bulk_g2s(s_val + st * IR_SCH, S.val + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
+        }
+    }
+};
+
+// l1 trial differences for trials IR_NT0 .. ML_MAXLS - 1 on my positions -> block partials (rare: Armijo past 1/8)
+__device__ __noinline__ void ir_lazy_l1(const Prm& P, const ASet& AS, int p0, int p1, double b_last, double* sh_w,
+                                        double* part) {
+    double v[ML_MAXLS - IR_NT0];
+#pragma unroll
+    for (int k = 0; k < ML_MAXLS - IR_NT0; ++k) v[k] = 0.0;
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const double x = AS.wA[p] + AS.d[p], sp = AS.s[p], ax = fabs(x);
+        double b = b_last;
+#pragma unroll
+        for (int k = 0; k < ML_MAXLS - IR_NT0; ++k) {
+            b *= P.beta_ls;
+            v[k] += fabs(x + b * sp) - ax;
+        }
+    }
+    ir_block_partials<ML_MAXLS - IR_NT0>(v, 0u, 0u, sh_w, part, IR_SL1);
+}
+
+__global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
+                                                  long long* acc_hs) {
+    unsigned long long ph_t = gtimer(), ph_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ double sh_w[2 * 256 + 8];   // >= IR_W * N + N for every ir_block_partials<N>; 2 x 256 in R
+    __shared__ double sh_t[12], sh_r[4], sh_l1[ML_MAXLS];
+    cg::grid_group grid = cg::this_grid();
+    Ctl* c = P.ctl;
+    if (c->skip) return;   // grid-uniform
+    const int m = P.m, G = gridDim.x;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nA = c->nA;
+    const int q = (nA + G - 1) / G;
+    const int p0 = min(nA, (int)blockIdx.x * q), p1 = min(nA, p0 + q);
+    const int R = (m + G - 1) / G;
+    const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
+    double* part = P.irpart;
+    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes());   // X_A s of my columns, later sv
+    double* xz_sh = xs_sh + m;                                           // X_A z of my columns
+    double* parts = P.parts;                                              // [G][m] block partials of X_A s
+    double* zparts = P.parts + (size_t)G * m;                             // [G][m] block partials of X_A z
+    // S ring (block-shared)
+    int* s_idx = reinterpret_cast<int*>(smraw);
+    float* s_val = reinterpret_cast<float*>(smraw + (size_t)4 * IR_SST * IR_SCH);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smraw + (size_t)8 * IR_SST * IR_SCH);
+    SChunk* s_desc = reinterpret_cast<SChunk*>(s_bar + IR_SST);
+    // G rings (per warp; alias the S ring, used after it)
+    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<IN_GSCH, IN_GST>(0);
+    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * IN_GST * IN_GSCH);
+    uint32_t g_phase = 0u;
+    long long nsc = 0, nhs = 0;
+
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) { P.Xd[i] = 0.0; P.Xs[i] = 0.0; }
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) { AS.d[p] = 0.0; AS.Hd[p] = 0.0; }
+
+    int next_pcd = c->next_pcd, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;
+    double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = c->rz_prev, slope = 0.0, ss = 0.0, ps = 0.0;
+    double sHs = 0.0, vq = 0.0;
+    const double vmax_C = c->vmax;
+    double bt[IR_NT0];
+    bt[0] = 1.0;
+#pragma unroll
+    for (int t = 1; t < IR_NT0; ++t) bt[t] = bt[t - 1] * P.beta_ls;
+    for (int it = 0; it < K; ++it) {
+        pcd = next_pcd;
+        // ------------------------------------------------ D: direction on my positions
+        int my_z = 0;
+        {
+            double v[12];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) v[k] = 0.0;
+            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+                const double x = AS.wA[p] + AS.d[p], pj = AS.gA[p] + AS.Hd[p], hh = AS.hA[p];
+                if (pcd) {   // R6 (Eq. 5, D = diag H + eps) + the zeroing part z (Q27)
+                    const double sp = soft(x - pj / hh, P.lam / hh) - x;
+                    AS.s[p] = sp;
+                    const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;
+                    AS.u[p] = zp;
+                    const double vv = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
+                    v[0] += pj * sp;
+                    v[1] += sp * sp;
+                    v[2] += pj * zp;
+                    v[3] += fabs(zp);
+                    v[4] += zp * zp;
+                    v[5] += (zp != 0.0) ? 1.0 : 0.0;
+                    const double ax = fabs(x);
+#pragma unroll
+                    for (int t = 0; t < IR_NT0; ++t) v[6 + t] += fabs(x + bt[t] * sp) - ax;
+                    v[10] = fmax(v[10], fabs(sp));
+                    v[11] = fmax(v[11], fabs(vv));
+                } else {     // R6' (Q9b): orthant residual, preconditioned by diag H + eps
+                    const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;
+                    const double u = (x != 0.0) ? -gx / hh : 0.0;
+                    AS.u[p] = u;
+                    const double sp = AS.s[p];
+                    const double vv = (x != 0.0) ? gx : soft(pj, P.lam);
+                    v[0] += hh * u * u;
+                    v[1] += gx * u;
+                    v[2] += gx * sp;
+                    v[3] += u * u;
+                    v[4] += u * sp;
+                    v[5] += sp * sp;
+                    v[11] = fmax(v[11], fabs(vv));
+                }
+            }
+            ir_block_partials<12>(v, IR_DMAX, 0u, sh_w, part, IR_SD);
+            my_z = pcd && sh_w[IR_W * 12 + 5] > 0.0;
+        }
+        PH_MARK(0);
+        // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
+        {
+            const double* coef = pcd ? AS.s : AS.u;
+            const double* zc = my_z ? AS.u : nullptr;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                xs_sh[i] = 0.0;
+                if (my_z) xz_sh[i] = 0.0;
+            }
+            SProducer pr{p0, p1, 0, (int)(S.nnz & ~3LL)};
+            if (threadIdx.x == 0) {
+                for (int k = 0; k < IR_SST; ++k) mbar_init(s_bar + k, 1);
+                fence_mbar_init();
+                for (int k = 0; k < IR_SST; ++k) {
+                    SChunk d;
+                    if (pr.next(S, coef, zc, d)) { s_desc[k] = d; pr.issue(S, d, k, s_idx, s_val, s_bar); }
+                    else s_desc[k].cf = 0.0;
+                }
+            }
+            __syncthreads();
+            uint32_t s_phase = 0u;
+            for (int st = 0;; st = (st + 1) % IR_SST) {
+                const SChunk d = s_desc[st];
+                if (d.cf == 0.0) break;
+                mbar_wait(s_bar + st, (s_phase >> st) & 1u);
+                s_phase ^= 1u << st;
+                const int* ci = s_idx + st * IR_SCH - d.a;
+                const float* cv = s_val + st * IR_SCH - d.a;
+                const int kend = min(d.ve, d.ce);
+                for (int k = d.vb + threadIdx.x; k < d.ve; k += blockDim.x) {   // rows are distinct within a column
+                    const int r = k < kend ? ci[k] : __ldg(S.idx + k);
+                    const double xv = (double)(k < kend ? cv[k] : __ldg(S.val + k));
+                    xs_sh[r] = fma(xv, d.cf, xs_sh[r]);
+                    if (d.zf) xz_sh[r] = fma(xv, d.cf, xz_sh[r]);   // z_p = s_p on a zeroing column
+                }
+                if (threadIdx.x == 0) nsc += d.ve - d.vb;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    SChunk nd;
+                    if (pr.next(S, coef, zc, nd)) { s_desc[st] = nd; pr.issue(S, nd, st, s_idx, s_val, s_bar); }
+                    else s_desc[st].cf = 0.0;
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0)
+                for (int k = 0; k < IR_SST; ++k) mbar_inval(s_bar + k);
+            // my block partials (a block without zeroing columns writes zeros for X_A z)
+            const int zpart = pcd && P.pcd_snap;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                parts[(size_t)blockIdx.x * m + i] = xs_sh[i];
+                if (zpart) zparts[(size_t)blockIdx.x * m + i] = my_z ? xz_sh[i] : 0.0;
+            }
+        }
+        PH_MARK(1);
+        grid.sync();   // B1
+        ir_totals(part, IR_SD, 12, IR_DMAX, 0u, sh_t);
+        PH_MARK(2);
+        int nzero = 0;
+        double pz = 0.0, Z1 = 0.0, zz = 0.0;
+        if (pcd) {
+            ps = sh_t[0]; ss = sh_t[1]; pz = sh_t[2]; Z1 = sh_t[3]; zz = sh_t[4]; nzero = (int)sh_t[5]; vq = sh_t[11];
+            stop = (it > 0 && P.eta > 0.0 && vq <= P.eta * vmax_C) || sh_t[10] == 0.0;   // R13, R7
+            bcg = 0.0;
+        } else {
+            rz = sh_t[0]; vq = sh_t[11];
+            stop = (it > 0 && P.eta > 0.0 && vq <= P.eta * vmax_C) || rz == 0.0;
+            if (!stop) {
+                bcg = cg_restart ? 0.0 : rz / rz_prev;
+                slope = sh_t[1] + bcg * sh_t[2];
+                ss = sh_t[3] + 2.0 * bcg * sh_t[4] + bcg * bcg * sh_t[5];
+            }
+        }
+        if (stop) break;
+        const int dual = pcd && nzero > 0;
+        // ------------------------------------------------ R: my rows; PCD-CG: s and the first kink on my positions
+        {
+            double a_ss = 0.0, a_sz = 0.0, a_zz = 0.0;
+            const int nr = r1 - r0;
+            if (nr > 0) {   // thread (group g, row rr) sums blocks g, g + ng, ...; then the groups in order
+                const int ng = max(1, (int)blockDim.x / nr);
+                const int g = threadIdx.x / nr, rr = threadIdx.x % nr;
+                double t = 0.0, tz = 0.0;
+                if (g < ng) {
+                    const double* src = parts + r0 + rr;
+                    const double* srz = zparts + r0 + rr;
+                    int b = g;
+                    for (; b + 3 * ng < G; b += 4 * ng) {
+                        const double x0 = ld_cg(src + (size_t)b * m), x1 = ld_cg(src + (size_t)(b + ng) * m),
+                                     x2 = ld_cg(src + (size_t)(b + 2 * ng) * m), x3 = ld_cg(src + (size_t)(b + 3 * ng) * m);
+                        t += ((x0 + x1) + x2) + x3;
+                        if (dual) {
+                            const double z0 = ld_cg(srz + (size_t)b * m), z1 = ld_cg(srz + (size_t)(b + ng) * m),
+                                         z2 = ld_cg(srz + (size_t)(b + 2 * ng) * m), z3 = ld_cg(srz + (size_t)(b + 3 * ng) * m);
+                            tz += ((z0 + z1) + z2) + z3;
+                        }
+                    }
+                    for (; b < G; b += ng) {
+                        t += ld_cg(src + (size_t)b * m);
+                        if (dual) tz += ld_cg(srz + (size_t)b * m);
+                    }
+                    sh_w[threadIdx.x] = t;   // sh_w holds >= 2 * 256 doubles
+                    sh_w[blockDim.x + threadIdx.x] = tz;
+                }
+                __syncthreads();
+                for (int rr2 = threadIdx.x; rr2 < nr; rr2 += blockDim.x) {
+                    double xs = 0.0, xz = 0.0;
+                    for (int g2 = 0; g2 < ng; ++g2) {
+                        xs += sh_w[g2 * nr + rr2];
+                        xz += sh_w[blockDim.x + g2 * nr + rr2];
+                    }
+                    const int i = r0 + rr2;
+                    if (!pcd) xs += bcg * P.Xs[i];
+                    P.Xs[i] = xs;
+                    if (dual) P.Xz[i] = xz;
+                    const double D = P.rD[i].y;
+                    a_ss += D * xs * xs;
+                    a_sz += D * xs * xz;
+                    a_zz += D * xz * xz;
+                }
+                __syncthreads();   // group sums read before sh_w is reused by the block partials
+            }
+            double kmin = __longlong_as_double(0x7ff0000000000000LL);
+            if (!pcd)
+                for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+                    const double sp = AS.u[p] + bcg * AS.s[p];
+                    AS.s[p] = sp;
+                    const double x = AS.wA[p] + AS.d[p];
+                    if (x * sp < 0.0) kmin = fmin(kmin, -x / sp);
+                }
+            const double v[4] = {a_ss, a_sz, a_zz, kmin};
+            ir_block_partials<4>(v, 0u, 1u << 3, sh_w, part, IR_SR);
+        }
+        // prefetch the G rings (X_A's columns do not depend on the step) across the barrier
+        ColStream<IN_GSCH, IN_GST> csG;
+        const bool need_hs = it < K - 1;
+        if (need_hs) {
+            if (lane == 0) {
+                for (int k = 0; k < IN_GST; ++k) mbar_init(g_bar + k, 1);
+                fence_mbar_init();
+            }
+            __syncwarp();
+            g_phase = 0u;
+            csG.streamed = 0;
+            csG.segs = 0;
+            stream_begin(csG, S, nullptr, p0, p1, gbase);
+        }
+        PH_MARK(3);
+        grid.sync();   // B2
+        ir_totals(part, IR_SR, 4, 0u, 1u << 3, sh_r);
+        // ------------------------------------------------ step decision, identical in every block
+        int have_l1 = 0;
+        auto l1 = [&](int t) -> double {   // sum_p |x + beta^t s| - |x| (trials >= IR_NT0 on demand: one more barrier)
+            if (t < IR_NT0) return sh_t[6 + t];
+            if (!have_l1) {
+                ir_lazy_l1(P, AS, p0, p1, bt[IR_NT0 - 1], sh_w, part);
+                grid.sync();
+                ir_totals(part, IR_SL1, ML_MAXLS - IR_NT0, 0u, 0u, sh_l1);
+                have_l1 = 1;
+            }
+            return sh_l1[t - IR_NT0];
+        };
+        zs = 0;
+        ksnap = 0;
+        if (pcd) {   // R10: model Armijo, snap path first (Q27), then the plain path
+            sHs = sh_r[0] + P.eps_h * ss;
+            const double zHs = sh_r[1] + P.eps_h * zz, zHz = sh_r[2] + P.eps_h * zz;
+            const double delta = ps + P.lam * sh_t[6];
+            double b = 1.0;
+            int ok = 0;
+            if (dual) {
+                const double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
+                for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+                    const double dq = b * (ps - pz) + pz + 0.5 * (b * b * snHsn + 2.0 * b * snHz + zHz) +
+                                      P.lam * (l1(t) - (1.0 - b) * Z1);
+                    if (dq <= P.sigma_in * b * delta) { ok = 1; zs = 1; break; }
+                }
+            }
+            if (!ok) {
+                b = 1.0;
+                for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
+                    const double dq = b * ps + 0.5 * b * b * sHs + P.lam * l1(t);
+                    if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
+                }
+            }
+            cg_restart = 1;
+            next_pcd = (inner_cg == 0);
+            if (!ok) stop = 1;
+            else beta = b;
+        } else {     // R6': exact model step along s, truncated at the first kink
+            sHs = sh_r[0] + P.eps_h * ss;
+            bk = sh_r[3];
+            if (!(slope < 0.0) || !(sHs > 0.0)) stop = 1;
+            else {
+                bq = -slope / sHs;
+                beta = bq < bk ? bq : bk;
+                ksnap = (bk <= bq);
+                cg_restart = ksnap;
+                next_pcd = (inner_cg == 2) && ksnap;
+                rz_prev = rz;
+            }
+        }
+        PH_MARK(4);
+        if (stop) {
+            if (need_hs) {   // drain the prefetched rings
+                for (int stg2 = 0; stg2 < IN_GST; ++stg2)
+                    if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (g_phase >> stg2) & 1u); g_phase ^= 1u << stg2; }
+                __syncwarp();
+                if (lane == 0)
+                    for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+            }
+            break;
+        }
+        acc_steps += 1;
+        // R12, m side: Xd += X sigma on my rows (sigma = beta s, or beta s + (1 - beta) z on the snap path)
+        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+            P.Xd[i] += beta * P.Xs[i] + (zs ? (1.0 - beta) * P.Xz[i] : 0.0);
+        if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
+            double* sv_sh = xs_sh;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const double xsg = beta * ld_cg(P.Xs + i) + (zs ? (1.0 - beta) * ld_cg(P.Xz + i) : 0.0);
+                sv_sh[i] = P.rD[i].y * xsg;
+            }
+            __syncthreads();
+            PH_MARK(5);
+            ColStream<IN_GSCH, IN_GST>& cs = csG;
+            int stg = 0;
+            double a = 0.0;
+            while (true) {
+                const ChunkDesc dsc = cs.desc[stg];
+                if (dsc.cf == 0.0) break;
+                mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
+                g_phase ^= 1u << stg;
+                const int* ci = cs.sidx + stg * IN_GSCH - dsc.a;
+                const float* cv = cs.sval + stg * IN_GSCH - dsc.a;
+                const int kend = min(dsc.ve, dsc.ce);
+                int k = dsc.vb + lane;
+                double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                for (; k + 96 < kend; k += 128) {
+                    a = fma((double)cv[k], sv_sh[ci[k]], a);
+                    a1 = fma((double)cv[k + 32], sv_sh[ci[k + 32]], a1);
+                    a2 = fma((double)cv[k + 64], sv_sh[ci[k + 64]], a2);
+                    a3 = fma((double)cv[k + 96], sv_sh[ci[k + 96]], a3);
+                }
+                a += (a1 + a2) + a3;
+                for (; k < kend; k += 32) a = fma((double)cv[k], sv_sh[ci[k]], a);
+                for (; k < dsc.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[__ldg(S.idx + k)], a);
+                if (dsc.last) {
+                    const double t = warp_sum(a);
+                    if (lane == 0) {
+                        const int p = dsc.p;
+                        const double sp = AS.s[p], zp = zs ? AS.u[p] : 0.0;
+                        const double x = AS.wA[p] + AS.d[p];
+                        const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
+                        AS.Hd[p] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
+                        AS.d[p] = (zp != 0.0 || kink) ? -AS.wA[p] : AS.d[p] + beta * sp;   // snapped coordinates become 0
+                    }
+                    a = 0.0;
+                }
+                __syncwarp();
+                ChunkDesc nd;
+                const bool ok = cs.next(nd);
+                if (lane == 0) {
+                    if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
+                    else cs.desc[stg].cf = 0.0;
+                }
+                __syncwarp();
+                stg = (stg + 1) % IN_GST;
+            }
+            nhs += cs.streamed;
+            __syncwarp();
+            if (lane == 0)
+                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+            PH_MARK(6);
+        } else {   // last iteration: d only
+            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+                const double sp = AS.s[p], zp = zs ? AS.u[p] : 0.0;
+                const double x = AS.wA[p] + AS.d[p];
+                const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
+                AS.d[p] = (zp != 0.0 || kink) ? -AS.wA[p] : AS.d[p] + beta * sp;
+            }
+        }
+        __syncthreads();   // my positions' d, Hd and the shared rings before the next direction
+    }
+    // accounting: X_A s scatters, Hs gathers
+    {
+        const long long s1 = warp_sum_ll(lane == 0 ? nsc : 0), s2 = warp_sum_ll(lane == 0 ? nhs : 0);
+        if (lane == 0) {
+            if (s1) atomicAdd((unsigned long long*)acc_sc, (unsigned long long)s1);
+            if (s2) atomicAdd((unsigned long long*)acc_hs, (unsigned long long)s2);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int q2 = 0; q2 < 12; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
+        c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1; c->snap = 0; c->zsnap = 0;
+        c->cg_restart = cg_restart; c->next_pcd = next_pcd; c->acc_steps = acc_steps; c->inner_stop = stop;
+        c->pcd_mode = pcd; c->beta = beta; c->bk = bk; c->bq = bq; c->bcg = bcg; c->rz = rz;
+        c->rz_prev = rz_prev; c->slope = slope; c->ss = ss; c->ps = ps; c->sHs = sHs; c->vq = vq;
+    }
+}

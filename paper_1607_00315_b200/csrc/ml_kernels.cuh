@@ -49,7 +49,7 @@ struct Ctl {
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
     int ntrace, trace_cap, bad_y, level, it;
     int pad2[3];
-    unsigned long long tph[8];   // persistent inner solver: ns spent per phase (block 0), diagnostics
+    unsigned long long tph[12];  // persistent inner solver: ns spent per phase (block 0), diagnostics
 };
 
 // heavy-segment schedule for one segment list
@@ -315,6 +315,7 @@ struct Prm {
     double* Xd; double* Xs; double* sv; double* Xu;   // Xu: scatter target of the atomic path (kept zero between uses)
     double* Xz; double* svz; double* Xzu;             // snap path: X_A z, D o Xz; Xzu: atomic scatter target of z (kept zero)
     double* parts; int nparts;                        // small-m scatter: per-block partials (+ group partials)
+    double* irpart;                                   // persistent inner solver: slot-major block partials
     Ctl* ctl;
     double* part;              // reduction partials
     double2* tilepart;         // per-tile partials of the compaction kernels
@@ -992,68 +993,6 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
     }
 }
 
-// ------------------------------------------------------------------ persistent small-m inner solver (A4-A6)
-// One cooperative launch runs all K inner iterations of a relaxation when an m-vector fits in shared memory: one CTA
-// per SM, W warps, block b owning the contiguous free-set positions [b q, (b+1) q) in every phase.  Per iteration:
-//   D  direction (k_dir_* logic) on my positions -> block partials -> grid barrier -> every block sums the partials
-//      in block order (identical, deterministic totals in every block) and takes the same decisions;
-//   S  X_A coef streamed through the per-warp TMA rings into private shared m-vectors -> block partial -> barrier ->
-//      my slice of rows: pending Xd += beta Xs, Xs = Xu (+ b Xs_prev), sv = D o Xs, D Xs^2 partial -> barrier ->
-//      s^T H s; PCD decision;
-//   G  sv copied to shared memory, X_A^T sv streamed on my positions: Hs (+ s = u + b s_prev and the first kink for
-//      PCD-CG) -> barrier -> CG decision.
-// The relaxation state lives in registers/shared memory of every block; block 0 writes it back to ml::Ctl at the end
-// (the outer line search then applies any pending step).
-struct IState {
-    int pend, pend_m, d_init, xd_init, snap, cg_restart, next_pcd, acc_steps, stop, pcd, zsnap, nzero;
-    double beta, bk, bq, bcg, rz, rz_prev, slope, ss, ps, sHs, vq, hs_beta, pz, Z1, zz;
-};
-
-// every block: sums of NV per-block partials part[b*NV + k] in block order -> out[k] (shared); warps own values
-__device__ __forceinline__ void grid_totals(const double* part, int NV, double* out, bool is_max) {
-    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int k = wid; k < NV; k += W) {
-        double t = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) {
-            const double v = ld_cg(part + (size_t)b * NV + k);
-            t = is_max ? fmax(t, v) : t + v;
-        }
-        t = is_max ? warp_max(t) : warp_sum(t);
-        if (lane == 0) out[k] = t;
-    }
-    __syncthreads();
-}
-__device__ __forceinline__ double grid_min_total(const double* part) {
-    __shared__ double sh;
-    if (threadIdx.x < 32) {
-        double t = __longlong_as_double(0x7ff0000000000000LL);
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t = fmin(t, ld_cg(part + b));
-        t = warp_min(t);
-        if (threadIdx.x == 0) sh = t;
-    }
-    __syncthreads();
-    const double r = sh;
-    __syncthreads();
-    return r;
-}
-// block sum of NV per-thread values into sh_out[0..NV) (shared), via per-warp partials sh_w[32*NV]
-template <int NV>
-__device__ __forceinline__ void blk_sums(const double (&v)[NV], double* sh_w, double* sh_out) {
-    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const double t = warp_sum(v[k]);
-        if (lane == 0) sh_w[wid * NV + k] = t;
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < NV; k += blockDim.x) {
-        double t = 0.0;
-        for (int w = 0; w < W; ++w) t += sh_w[w * NV + k];
-        sh_out[k] = t;
-    }
-    __syncthreads();
-}
-
 template <int SCH, int NSTG>
 __device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG>& cs, const Seg& S, const double* coef, int p0, int p1,
                                              unsigned char* base) {
@@ -1087,8 +1026,6 @@ __device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG>& cs, const Seg
     __syncwarp();
 }
 
-constexpr int IN_SCH = 1024, IN_NSTG = 2;
-__host__ __device__ inline size_t inner_smem_bytes(int W, int m) { return (size_t)W * stream_warp_bytes<IN_SCH, IN_NSTG>(m); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -1104,480 +1041,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
         }                                                                           \
     } while (0)
 
-__global__ void __launch_bounds__(256, 1) k_inner_small(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
-                                                        long long* acc_hs) {
-    unsigned long long ph_t = gtimer(), ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ double sh_w[16 * (ML_MAXLS + 4)];
-    __shared__ double sh_t[ML_MAXLS + 8];
-    __shared__ double sh_m[4];
-    cg::grid_group grid = cg::this_grid();
-    Ctl* c = P.ctl;
-    if (c->skip) return;   // grid-uniform
-    const int m = P.m;
-    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t pw = stream_warp_bytes<IN_SCH, IN_NSTG>(m);
-    unsigned char* base = smraw + (size_t)wid * pw;
-    double* mine = reinterpret_cast<double*>(base + stream_warp_bytes<IN_SCH, IN_NSTG>(0));
-    double* sv_sh = reinterpret_cast<double*>(smraw + stream_warp_bytes<IN_SCH, IN_NSTG>(0));   // warp 0's acc area
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + 8 * IN_NSTG * IN_SCH);
-    if (lane == 0) {
-        for (int k = 0; k < IN_NSTG; ++k) mbar_init(bar + k, 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    uint32_t phase = 0u;
-    const int nA = c->nA;
-    const int q = (nA + gridDim.x - 1) / gridDim.x;
-    const int p0 = blockIdx.x * q, p1 = min(nA, p0 + q);
-    const int R = (m + gridDim.x - 1) / gridDim.x;
-    const int row0 = blockIdx.x * R, row1 = min(m, row0 + R);
-    double* part = P.part;                       // scalar partials [grid][NV]
-    double* parts = P.parts;                     // m-vector partials [grid][m]
-    double* part2 = P.parts + (size_t)gridDim.x * m;
-    IState st;
-    st.pend = c->pend; st.pend_m = c->pend_m; st.d_init = c->d_init; st.xd_init = c->xd_init; st.snap = c->snap;
-    st.cg_restart = c->cg_restart; st.next_pcd = c->next_pcd; st.acc_steps = c->acc_steps; st.stop = c->inner_stop;
-    st.pcd = c->pcd_mode; st.beta = c->beta; st.bk = c->bk; st.bq = c->bq; st.bcg = c->bcg; st.rz = c->rz;
-    st.rz_prev = c->rz_prev; st.slope = c->slope; st.ss = c->ss; st.ps = c->ps; st.sHs = c->sHs; st.vq = c->vq;
-    st.zsnap = c->zsnap; st.hs_beta = c->hs_beta; st.nzero = 0; st.pz = 0.0; st.Z1 = 0.0; st.zz = 0.0;
-    const double vmax_C = c->vmax;
-    double* svz_sh = reinterpret_cast<double*>(smraw + pw + stream_warp_bytes<IN_SCH, IN_NSTG>(0));   // warp 1's acc area
-    long long nsc = 0, nhs = 0;
-    double bt[ML_MAXLS];
-    bt[0] = 1.0;
-#pragma unroll
-    for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
-    for (int it = 0; it < K && !st.stop; ++it) {
-        // ------------------------------------------------ D: pending step + direction on my positions
-        ColStream<IN_SCH, IN_NSTG> csG;   // the Hs phase's stream (prefetched before the m-side barrier)
-        const int pcd = st.next_pcd;
-        const Pending pq{st.pend, st.d_init, st.snap, st.zsnap, st.beta, st.bk, st.hs_beta};
-        if (pcd) {
-            double v[ML_MAXLS + 6];   // ps, ss, l1 trial sums, pz, Z1, zz, #zeroing
-            double vm0 = 0.0, vm1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < ML_MAXLS + 6; ++k) v[k] = 0.0;
-            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                double Hd;
-                const double d = apply_A(pq, AS, p, true, &Hd);
-                const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-                const double sp = soft(x - pj / hh, P.lam / hh) - x;
-                AS.s[p] = sp;
-                const double vv = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
-                const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;   // zeroing part (Q27)
-                AS.u[p] = zp;
-                vm0 = fmax(vm0, fabs(sp));
-                vm1 = fmax(vm1, fabs(vv));
-                v[0] += pj * sp;
-                v[1] += sp * sp;
-                const double ax = fabs(x);
-#pragma unroll
-                for (int t = 0; t < ML_MAXLS; ++t) v[2 + t] += fabs(x + bt[t] * sp) - ax;
-                v[ML_MAXLS + 2] += pj * zp;
-                v[ML_MAXLS + 3] += fabs(zp);
-                v[ML_MAXLS + 4] += zp * zp;
-                v[ML_MAXLS + 5] += (zp != 0.0) ? 1.0 : 0.0;
-            }
-            blk_sums<ML_MAXLS + 6>(v, sh_w, sh_t);
-            vm0 = warp_max(vm0);
-            vm1 = warp_max(vm1);
-            if (lane == 0) { sh_w[wid] = vm0; sh_w[16 + wid] = vm1; }
-            __syncthreads();
-            if (threadIdx.x < ML_MAXLS + 6) part[(size_t)blockIdx.x * (ML_MAXLS + 8) + threadIdx.x] = sh_t[threadIdx.x];
-            if (threadIdx.x == 0) {
-                double a = 0.0, b = 0.0;
-                for (int w = 0; w < W; ++w) { a = fmax(a, sh_w[w]); b = fmax(b, sh_w[16 + w]); }
-                part[(size_t)blockIdx.x * (ML_MAXLS + 8) + ML_MAXLS + 6] = a;
-                part[(size_t)blockIdx.x * (ML_MAXLS + 8) + ML_MAXLS + 7] = b;
-            }
-            PH_MARK(0);
-        } else {
-            double v[6] = {0, 0, 0, 0, 0, 0};
-            double vm = 0.0;
-            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                double Hd;
-                const double d = apply_A(pq, AS, p, true, &Hd);
-                const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-                const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;
-                const double u = (x != 0.0) ? -gx / hh : 0.0;
-                AS.u[p] = u;
-                const double sp = AS.s[p];
-                const double vv = (x != 0.0) ? gx : soft(pj, P.lam);
-                v[0] += hh * u * u; v[1] += gx * u; v[2] += gx * sp; v[3] += u * u; v[4] += u * sp; v[5] += sp * sp;
-                vm = fmax(vm, fabs(vv));
-            }
-            blk_sums<6>(v, sh_w, sh_t);
-            vm = warp_max(vm);
-            if (lane == 0) sh_w[wid] = vm;
-            __syncthreads();
-            if (threadIdx.x < 6) part[(size_t)blockIdx.x * 8 + threadIdx.x] = sh_t[threadIdx.x];
-            if (threadIdx.x == 0) {
-                double a = 0.0;
-                for (int w = 0; w < W; ++w) a = fmax(a, sh_w[w]);
-                part[(size_t)blockIdx.x * 8 + 6] = a;
-                part[(size_t)blockIdx.x * 8 + 7] = 0.0;
-            }
-            PH_MARK(0);
-        }
-        if (st.pend) { st.pend = 0; st.d_init = 1; }
-        // ------------------------------------------------ S (the direction's block partials ride on its barrier): X_A coef into per-warp shared m-vectors
-        {
-            for (int i = lane; i < m; i += 32) mine[i] = 0.0;
-            __syncwarp();
-            ColStream<IN_SCH, IN_NSTG> cs;
-            cs.streamed = 0;
-            cs.segs = 0;
-            stream_begin(cs, S, pcd ? AS.s : AS.u, p0, p1, base);
-            int stg = 0;
-            while (true) {
-                const ChunkDesc d = cs.desc[stg];
-                if (d.cf == 0.0) break;
-                mbar_wait(cs.bar + stg, (phase >> stg) & 1u);
-                phase ^= 1u << stg;
-                const int* ci = cs.sidx + stg * IN_SCH - d.a;
-                const float* cv = cs.sval + stg * IN_SCH - d.a;
-                const int kend = min(d.ve, d.ce);
-                int k = d.vb + lane;
-                for (; k + 96 < kend; k += 128) {
-                    const int r0 = ci[k], r1 = ci[k + 32], r2 = ci[k + 64], r3 = ci[k + 96];
-                    const double x0 = mine[r0], x1 = mine[r1], x2 = mine[r2], x3 = mine[r3];
-                    mine[r0] = fma((double)cv[k], d.cf, x0);
-                    mine[r1] = fma((double)cv[k + 32], d.cf, x1);
-                    mine[r2] = fma((double)cv[k + 64], d.cf, x2);
-                    mine[r3] = fma((double)cv[k + 96], d.cf, x3);
-                }
-                for (; k < kend; k += 32) { const int r = ci[k]; mine[r] = fma((double)cv[k], d.cf, mine[r]); }
-                for (; k < d.ve; k += 32) { const int r = __ldg(S.idx + k); mine[r] = fma((double)__ldg(S.val + k), d.cf, mine[r]); }
-                __syncwarp();
-                ChunkDesc nd;
-                const bool ok = cs.next(nd);
-                if (lane == 0) {
-                    if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
-                    else cs.desc[stg].cf = 0.0;
-                }
-                __syncwarp();
-                stg = (stg + 1) % IN_NSTG;
-            }
-            nsc += cs.streamed;
-            __syncthreads();
-            PH_MARK(2);
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                double t = 0.0;
-                for (int w = 0; w < W; ++w) t += reinterpret_cast<const double*>(smraw + (size_t)w * pw + stream_warp_bytes<IN_SCH, IN_NSTG>(0))[i];
-                parts[(size_t)blockIdx.x * m + i] = t;
-            }
-            __threadfence();
-            grid.sync();
-            PH_MARK(3);
-            // direction totals (identical in every block) and its stop tests
-            {
-                const int NV = pcd ? ML_MAXLS + 8 : 8;
-                grid_totals(part, NV, sh_t, false);
-                __shared__ double sh_mx[2];
-                if (threadIdx.x < 64) {   // maxima: PCD slots NV-2 (max|s|), NV-1 (vq); CG slot 6 (vq)
-                    const int kk = threadIdx.x >> 5;
-                    const int slot = pcd ? NV - 2 + kk : 6;
-                    double t = 0.0;
-                    for (int b = lane; b < (int)gridDim.x; b += 32) t = fmax(t, ld_cg(part + (size_t)b * NV + slot));
-                    t = warp_max(t);
-                    if (lane == 0) sh_mx[kk] = t;
-                }
-                __syncthreads();
-                int stop;
-                if (pcd) {
-                    st.ps = sh_t[0];
-                    st.ss = sh_t[1];
-                    st.pz = sh_t[ML_MAXLS + 2];
-                    st.Z1 = sh_t[ML_MAXLS + 3];
-                    st.zz = sh_t[ML_MAXLS + 4];
-                    st.nzero = (int)sh_t[ML_MAXLS + 5];
-                    st.vq = sh_mx[1];
-                    stop = (it > 0 && P.eta > 0.0 && sh_mx[1] <= P.eta * vmax_C);
-                    if (sh_mx[0] == 0.0) stop = 1;
-                    st.bcg = 0.0;
-                    st.pcd = 1;
-                } else {
-                    const double rz = sh_t[0];
-                    stop = (it > 0 && P.eta > 0.0 && sh_mx[0] <= P.eta * vmax_C);
-                    if (rz == 0.0) stop = 1;
-                    const double b = st.cg_restart ? 0.0 : rz / st.rz_prev;
-                    st.bcg = b;
-                    st.rz = rz;
-                    st.slope = sh_t[1] + b * sh_t[2];
-                    st.ss = sh_t[3] + 2.0 * b * sh_t[4] + b * b * sh_t[5];
-                    st.vq = sh_mx[0];
-                    st.pcd = 0;
-                }
-                st.stop = stop;
-                PH_MARK(1);
-                if (stop) break;
-            }
-            const int withz = pcd && st.nzero > 0;
-            double* parts_z = parts + (size_t)gridDim.x * m + 8 * gridDim.x;   // after part2's 5 x grid scalars
-            if (withz) {   // S': X_A z over the zeroing columns only (AS.u holds z; zero coefficients are skipped)
-                for (int i = lane; i < m; i += 32) mine[i] = 0.0;
-                __syncwarp();
-                ColStream<IN_SCH, IN_NSTG> cz;
-                cz.streamed = 0;
-                cz.segs = 0;
-                stream_begin(cz, S, AS.u, p0, p1, base);
-                int stg = 0;
-                while (true) {
-                    const ChunkDesc d = cz.desc[stg];
-                    if (d.cf == 0.0) break;
-                    mbar_wait(cz.bar + stg, (phase >> stg) & 1u);
-                    phase ^= 1u << stg;
-                    const int* ci = cz.sidx + stg * IN_SCH - d.a;
-                    const float* cv = cz.sval + stg * IN_SCH - d.a;
-                    const int kend = min(d.ve, d.ce);
-                    int k2 = d.vb + lane;
-                    for (; k2 < kend; k2 += 32) { const int r = ci[k2]; mine[r] = fma((double)cv[k2], d.cf, mine[r]); }
-                    for (; k2 < d.ve; k2 += 32) { const int r = __ldg(S.idx + k2); mine[r] = fma((double)__ldg(S.val + k2), d.cf, mine[r]); }
-                    __syncwarp();
-                    ChunkDesc nd;
-                    const bool ok = cz.next(nd);
-                    if (lane == 0) {
-                        if (ok) { cz.desc[stg] = nd; cz.issue(stg, nd); }
-                        else cz.desc[stg].cf = 0.0;
-                    }
-                    __syncwarp();
-                    stg = (stg + 1) % IN_NSTG;
-                }
-                nsc += cz.streamed;
-                __syncthreads();
-                for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                    double t = 0.0;
-                    for (int w = 0; w < W; ++w) t += reinterpret_cast<const double*>(smraw + (size_t)w * pw + stream_warp_bytes<IN_SCH, IN_NSTG>(0))[i];
-                    parts_z[(size_t)blockIdx.x * m + i] = t;
-                }
-                __threadfence();
-                grid.sync();
-            }
-            // my rows: combine the block partials (thread (row, group) split, groups in order)
-            const int ng = max(1, (int)blockDim.x / max(R, 1));
-            const int rr = threadIdx.x % max(R, 1), grp = threadIdx.x / max(R, 1);
-            double t = 0.0, tz = 0.0;
-            if (grp < ng && row0 + rr < row1)
-                for (int k2 = grp; k2 < (int)gridDim.x; k2 += ng) {
-                    t += ld_cg(parts + (size_t)k2 * m + row0 + rr);
-                    if (withz) tz += ld_cg(parts_z + (size_t)k2 * m + row0 + rr);
-                }
-            sh_w[threadIdx.x] = t;   // sh_w holds >= 16*(ML_MAXLS+4) >= 2*blockDim doubles
-            sh_w[blockDim.x + threadIdx.x] = tz;
-            __syncthreads();
-            double a2 = 0.0, a3 = 0.0, a4 = 0.0;
-            if ((int)threadIdx.x < R && row0 + (int)threadIdx.x < row1) {
-                double xu = 0.0, xz = 0.0;
-                for (int g = 0; g < ng; ++g) { xu += sh_w[g * R + threadIdx.x]; xz += sh_w[blockDim.x + g * R + threadIdx.x]; }
-                const int i = row0 + threadIdx.x;
-                const double xs_old = P.Xs[i];
-                if (st.pend_m)   // pending step: CG / PCD plain + beta Xs, PCD snap + beta Xs + (1 - beta) Xz
-                    P.Xd[i] = (st.xd_init ? P.Xd[i] : 0.0) + st.beta * xs_old + (st.zsnap ? (1.0 - st.beta) * P.Xz[i] : 0.0);
-                const double xs = pcd ? xu : xu + st.bcg * xs_old;
-                P.Xs[i] = xs;
-                const double D = P.rD[i].y;
-                P.sv[i] = D * xs;
-                a2 = D * xs * xs;
-                if (withz) {
-                    P.Xz[i] = xz;
-                    P.svz[i] = D * xz;
-                    a3 = D * xs * xz;
-                    a4 = D * xz * xz;
-                }
-            }
-            const double bs = block_sum_any(a2);
-            const double bs3 = withz ? block_sum_any(a3) : 0.0;
-            const double bs4 = withz ? block_sum_any(a4) : 0.0;
-            if (threadIdx.x == 0) { part2[blockIdx.x] = bs; part2[3 * gridDim.x + blockIdx.x] = bs3; part2[4 * gridDim.x + blockIdx.x] = bs4; }
-            // prefetch: start the Hs phase's TMA ring (X_A does not depend on sv) before the barrier
-            if (it < K - 1) {
-                csG.streamed = 0;
-                csG.segs = 0;
-                stream_begin(csG, S, nullptr, p0, p1, base);
-            }
-            __threadfence();
-            grid.sync();
-            if (threadIdx.x < 96) {   // warps 0, 1, 2: s^T H s, z^T H s, z^T H z (without the ridge)
-                const int kk = threadIdx.x >> 5;
-                const int off = kk == 0 ? 0 : (kk + 2) * (int)gridDim.x;
-                double tt = 0.0;
-                if (kk == 0 || withz)
-                    for (int b = lane; b < (int)gridDim.x; b += 32) tt += ld_cg(part2 + off + b);
-                tt = warp_sum(tt);
-                if (lane == 0) sh_m[kk] = tt;
-            }
-            __syncthreads();
-            PH_MARK(4);
-            if (st.pend_m) { st.pend_m = 0; st.xd_init = 1; }
-            const double sHs = sh_m[0] + P.eps_h * st.ss;
-            st.sHs = sHs;
-            if (pcd) {   // R10 (decide_pcd incl. the snap path, Q27); sh_t[2 + t] still holds the l1 trial sums of D
-                const double zHs = sh_m[1] + P.eps_h * st.zz, zHz = sh_m[2] + P.eps_h * st.zz;
-                const double delta = st.ps + P.lam * sh_t[2];
-                double b = 1.0;
-                int ok = 0, snapped = 0;
-                if (withz) {
-                    const double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
-                    for (int t2 = 0; t2 < P.max_ls; ++t2, b *= P.beta_ls) {
-                        const double dq = b * (st.ps - st.pz) + st.pz + 0.5 * (b * b * snHsn + 2.0 * b * snHz + zHz) +
-                                          P.lam * (sh_t[2 + t2] - (1.0 - b) * st.Z1);
-                        if (dq <= P.sigma_in * b * delta) { ok = 1; snapped = 1; break; }
-                    }
-                }
-                if (!ok) {
-                    b = 1.0;
-                    for (int t2 = 0; t2 < P.max_ls; ++t2, b *= P.beta_ls) {
-                        const double dq = b * st.ps + 0.5 * b * b * sHs + P.lam * sh_t[2 + t2];
-                        if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
-                    }
-                }
-                st.cg_restart = 1;
-                st.next_pcd = (inner_cg == 0);
-                if (!ok) { st.stop = 1; st.beta = 0.0; }
-                else {
-                    st.beta = b; st.snap = 0; st.zsnap = snapped; st.hs_beta = 1.0;
-                    st.pend = 1; st.pend_m = 1; st.acc_steps += 1;
-                }
-            }
-        }
-        if (st.stop) {
-            if (it < K - 1)   // drain the prefetched ring
-                for (int stg2 = 0; stg2 < IN_NSTG; ++stg2)
-                    if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (phase >> stg2) & 1u); phase ^= 1u << stg2; }
-            break;
-        }
-        // ------------------------------------------------ G: Hs on my positions (+ CG epilogue and decision)
-        const bool need_hs = it < K - 1;
-        double bkmin = __longlong_as_double(0x7ff0000000000000LL);
-        if (need_hs) {
-            __syncthreads();
-            const int dual = pcd && st.zsnap;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                sv_sh[i] = ld_cg(P.sv + i);
-                if (dual) svz_sh[i] = ld_cg(P.svz + i);
-            }
-            __syncthreads();
-            ColStream<IN_SCH, IN_NSTG>& cs = csG;
-            int stg = 0;
-            double a = 0.0, az = 0.0;
-            while (true) {
-                const ChunkDesc d = cs.desc[stg];
-                if (d.cf == 0.0) break;
-                mbar_wait(cs.bar + stg, (phase >> stg) & 1u);
-                phase ^= 1u << stg;
-                const int* ci = cs.sidx + stg * IN_SCH - d.a;
-                const float* cv = cs.sval + stg * IN_SCH - d.a;
-                const int kend = min(d.ve, d.ce);
-                int k = d.vb + lane;
-                if (dual) {
-                    for (; k < kend; k += 32) {
-                        const int r = ci[k];
-                        a = fma((double)cv[k], sv_sh[r], a);
-                        az = fma((double)cv[k], svz_sh[r], az);
-                    }
-                    for (; k < d.ve; k += 32) {
-                        const int r = __ldg(S.idx + k);
-                        const double xv = (double)__ldg(S.val + k);
-                        a = fma(xv, sv_sh[r], a);
-                        az = fma(xv, svz_sh[r], az);
-                    }
-                } else {
-                    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                    for (; k + 96 < kend; k += 128) {
-                        a = fma((double)cv[k], sv_sh[ci[k]], a);
-                        a1 = fma((double)cv[k + 32], sv_sh[ci[k + 32]], a1);
-                        a2 = fma((double)cv[k + 64], sv_sh[ci[k + 64]], a2);
-                        a3 = fma((double)cv[k + 96], sv_sh[ci[k + 96]], a3);
-                    }
-                    a += (a1 + a2) + a3;
-                    for (; k < kend; k += 32) a = fma((double)cv[k], sv_sh[ci[k]], a);
-                    for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[__ldg(S.idx + k)], a);
-                }
-                if (d.last) {
-                    const double t = warp_sum(a);
-                    const double tz = dual ? warp_sum(az) : 0.0;
-                    if (lane == 0) {
-                        if (pcd) {   // H sigma, sigma = b s (+ snapped z)
-                            const double zp = dual ? AS.u[d.p] : 0.0;
-                            const double sg = (zp != 0.0) ? zp : st.beta * AS.s[d.p];
-                            AS.Hs[d.p] = st.beta * t + (dual ? (1.0 - st.beta) * tz : 0.0) + P.eps_h * sg;
-                        } else {
-                            const double sp = AS.u[d.p] + st.bcg * AS.s[d.p];
-                            AS.s[d.p] = sp;
-                            AS.Hs[d.p] = t + P.eps_h * sp;
-                            const double x = AS.wA[d.p] + AS.d[d.p];
-                            if (x * sp < 0.0) bkmin = fmin(bkmin, -x / sp);
-                        }
-                    }
-                    a = 0.0;
-                    az = 0.0;
-                }
-                __syncwarp();
-                ChunkDesc nd;
-                const bool ok = cs.next(nd);
-                if (lane == 0) {
-                    if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
-                    else cs.desc[stg].cf = 0.0;
-                }
-                __syncwarp();
-                stg = (stg + 1) % IN_NSTG;
-            }
-            nhs += cs.streamed;
-            PH_MARK(5);
-        } else if (!pcd) {   // last iteration of PCD-CG: s and the kink only
-            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                const double sp = AS.u[p] + st.bcg * AS.s[p];
-                AS.s[p] = sp;
-                const double x = AS.wA[p] + AS.d[p];
-                if (x * sp < 0.0) bkmin = fmin(bkmin, -x / sp);
-            }
-        }
-        if (!pcd) {   // R6': CG decision (decide_cg)
-            const double bmin = block_min_any(bkmin);
-            if (threadIdx.x == 0) part2[gridDim.x + blockIdx.x] = bmin;
-            __threadfence();
-            grid.sync();
-            const double bk = grid_min_total(part2 + gridDim.x);
-            PH_MARK(6);
-            st.bk = bk;
-            if (!(st.slope < 0.0) || !(st.sHs > 0.0)) { st.stop = 1; st.beta = 0.0; }
-            else {
-                const double bq = -st.slope / st.sHs;
-                st.bq = bq;
-                st.beta = bq < bk ? bq : bk;
-                st.snap = (bk <= bq);
-                st.zsnap = 0;
-                st.hs_beta = st.beta;
-                st.cg_restart = st.snap;
-                st.next_pcd = (inner_cg == 2) && st.snap;
-                st.rz_prev = st.rz;
-                st.pend = 1;
-                st.pend_m = 1;
-                st.acc_steps += 1;
-            }
-        } else {
-            grid.sync();   // Hs of this iteration complete before the next direction reads partials again
-        }
-    }
-    // per-warp streamed counts -> class counters
-    {
-        const long long s1 = warp_sum_ll(lane == 0 ? nsc : 0), s2 = warp_sum_ll(lane == 0 ? nhs : 0);
-        if (lane == 0) {
-            if (s1) atomicAdd((unsigned long long*)acc_sc, (unsigned long long)s1);
-            if (s2) atomicAdd((unsigned long long*)acc_hs, (unsigned long long)s2);
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        for (int q2 = 0; q2 < 8; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        c->pend = st.pend; c->pend_m = st.pend_m; c->d_init = st.d_init; c->xd_init = st.xd_init; c->snap = st.snap;
-        c->cg_restart = st.cg_restart; c->next_pcd = st.next_pcd; c->acc_steps = st.acc_steps; c->inner_stop = st.stop;
-        c->pcd_mode = st.pcd; c->beta = st.beta; c->bk = st.bk; c->bq = st.bq; c->bcg = st.bcg; c->rz = st.rz;
-        c->rz_prev = st.rz_prev; c->slope = st.slope; c->ss = st.ss; c->ps = st.ps; c->sHs = st.sHs; c->vq = st.vq;
-        c->zsnap = st.zsnap; c->hs_beta = st.hs_beta;
-    }
-}
+#include "ml_inner.cuh"
 
 // out[i] = sum_b parts[b][i] (block order)
 __global__ void k_parts_sum(const double* __restrict__ parts, int nparts, int m, double* out) {
