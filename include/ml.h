@@ -126,9 +126,9 @@ int64_t ml_kernel_launches(const ml_ctx *c);
    the passes launched, and the nonzeros streamed and segments (rows / columns) visited on the device. */
 ml_status ml_profile(ml_ctx *c, uint32_t class_mask);
 ml_status ml_profile_read(ml_ctx *c, double *ms_host, int64_t *passes_host, int64_t *nnz_host, int64_t *segs_host);
-/* Diagnostics: nanoseconds spent per phase of the persistent small-m inner solver, 12 entries (block 0; 0 row-copy
-   counts + barrier, 1 block offsets + barrier, 2 row pointers + fill, 3 direction, 4 barrier + totals, 5 row products,
-   6 barrier + totals + step decision, 7 D o X sigma to shared memory, 8 Hs stream + step, 9-11 unused). */
+/* Diagnostics: nanoseconds spent per phase of the persistent small-m inner solver, 16 entries (block 0): entries
+   0-6 for relaxations with |A| < 2048, 8-14 for larger ones: direction, X_A s scatter, barrier + totals, row sums,
+   barrier + totals + step decision, D o X sigma to shared memory, Hs stream + step; 7 and 15 unused. */
 ml_status ml_inner_phases(ml_ctx *c, uint64_t *ns_host, int reset);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */

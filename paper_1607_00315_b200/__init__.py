@@ -297,7 +297,7 @@ class Context:
                 for k, name in enumerate(self.CLASSES)}
 
     def ml_inner_phases(self, reset=True):
-        ns = (ctypes.c_uint64 * 12)()
+        ns = (ctypes.c_uint64 * 16)()
         self._check(load().ml_inner_phases(self.h, ns, int(reset)))
         return [int(x) for x in ns]
 

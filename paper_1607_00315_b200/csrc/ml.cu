@@ -74,6 +74,7 @@ struct ml_ctx {
     bool sm_gather = false;
     bool sm_inner = false;   // persistent cooperative inner solver (k_inner)
     int inner_W = 0, inner_P = 0;
+    const void* inner_fn = nullptr;   // k_inner<1024> or k_inner<512>
     size_t inner_bytes = 0;
     int gath_W = 0, gath_P = 0;
     size_t gath_bytes = 0;
@@ -424,7 +425,7 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
         long long* a1 = acc_of(c, CLS_SCATTER);
         long long* a2 = acc_of(c, CLS_HS);
         void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
-        cudaLaunchCooperativeKernel((const void*)k_inner, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
+        cudaLaunchCooperativeKernel(c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
         c->launches++;
     } else
     for (int it = 0; it < K; ++it) {
@@ -598,13 +599,17 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->gath_bytes = bytes;
             c->gath_P = SM_COUNT * bps;
         }
-        bytes = inner_smem_bytes((int)X->m);
+        // persistent inner solver: 1024-element G chunks when the m-vectors leave room, else 512
+        const bool big_g = inner_smem_bytes<1024>((int)X->m) <= 220 * 1024;
+        const void* kfn = big_g ? (const void*)k_inner<1024> : (const void*)k_inner<512>;
+        bytes = big_g ? inner_smem_bytes<1024>((int)X->m) : inner_smem_bytes<512>((int)X->m);
         if (bytes <= 220 * 1024 && X->m <= 256LL * std::min(SM_COUNT, IR_GMAX) &&
-            cudaFuncSetAttribute(k_inner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
             int bps = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inner, 32 * IR_W, bytes);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, bytes);
             if (bps >= 1) {
                 c->sm_inner = true;
+                c->inner_fn = kfn;
                 c->inner_bytes = bytes;
                 c->inner_P = std::min(SM_COUNT, IR_GMAX);
             }
@@ -928,8 +933,8 @@ ml_status ml_inner_phases(ml_ctx* c, uint64_t* ns_host, int reset) {
     if (!c) return ML_E_INVAL;
     ml_status s = sync_ctl(c);
     if (s != ML_OK) return s;
-    for (int k = 0; k < 12; ++k) if (ns_host) ns_host[k] = c->h.tph[k];
-    if (reset) { unsigned long long z[12] = {0}; cudaMemcpyAsync(c->ctl->tph, z, sizeof(z), cudaMemcpyHostToDevice, c->st); }
+    for (int k = 0; k < 16; ++k) if (ns_host) ns_host[k] = c->h.tph[k];
+    if (reset) { unsigned long long z[16] = {0}; cudaMemcpyAsync(c->ctl->tph, z, sizeof(z), cudaMemcpyHostToDevice, c->st); }
     return cuda_fail(c, "ml_inner_phases");
 }
 

@@ -22,25 +22,30 @@
 constexpr int IR_W = 8;          // warps per block (launch with 256 threads)
 constexpr int IR_GMAX = 160;     // grid <= 160 blocks (5 partials per lane in the totals)
 constexpr int IR_NT0 = 4;        // l1 trial differences computed with the direction; the rest only if Armijo needs them
-constexpr int IR_SCH = 2048, IR_SST = 4;   // S phase: block-shared ring, chunk elements x stages
-constexpr int IN_GSCH = 512, IN_GST = 2;   // G phase: per-warp rings
+constexpr int IR_SCH = 2048;               // S phase: block-shared ring of IR_SCH-element chunks, sst(GSCH) stages
+constexpr int IR_QC = 1024;                // column extents of up to IR_QC own positions cached in shared memory
+constexpr int IN_GST = 2;                  // G phase: per-warp rings of GSCH-element chunks (template)
 // partial slots: D (PCD) 0 ps, 1 ss, 2 pz, 3 Z1, 4 zz, 5 #zeroing, 6..9 l1 trials 0..3, 10 max|s|, 11 vq
 //                D (CG)  0 rz, 1 gx.u, 2 gx.s_prev, 3 u.u, 4 u.s_prev, 5 s_prev.s_prev, 11 vq
 //                R       12 D Xs^2, 13 D Xs Xz, 14 D Xz^2, 15 first kink (min);  lazy l1 trials 16 ..
 enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16, IR_NSLOT = 16 + ML_MAXLS - IR_NT0 };
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
-struct SChunk { int p, a, vb, ve, ce, zf; double cf; };   // copy [a, ce) of column p, valid [vb, ve)
+struct SChunk { int p, a, vb, ve, ce, ok; };   // copy [a, ce) of column p, valid [vb, ve); ok = 0: no chunk
 
-__host__ __device__ inline size_t ir_sring_bytes() {
-    return (size_t)8 * IR_SST * IR_SCH + 8 * IR_SST + sizeof(SChunk) * IR_SST;
+__host__ __device__ constexpr int ir_sst(int gsch) { return gsch >= 1024 ? 8 : 4; }   // the S ring fits the G rings
+__host__ __device__ inline size_t ir_sring_bytes(int sst) {
+    return (size_t)8 * sst * IR_SCH + 8 * sst + sizeof(SChunk) * sst;
 }
+template <int GSCH>
 __host__ __device__ inline size_t ir_ring_bytes() {
-    const size_t g = (size_t)IR_W * stream_warp_bytes<IN_GSCH, IN_GST>(0), s = ir_sring_bytes();
+    const size_t g = (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0), s = ir_sring_bytes(ir_sst(GSCH));
     return ((g > s ? g : s) + 15) / 16 * 16;
 }
+static_assert(sizeof(SChunk) == 24, "SChunk layout");
 // dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z)
-__host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes() + (size_t)16 * m; }
+template <int GSCH>
+__host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes<GSCH>() + (size_t)16 * m; }
 
 // N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
 // block's own totals stay in sh_w[IR_W * N + k]
@@ -65,50 +70,57 @@ __device__ __forceinline__ void ir_block_partials(const double (&v)[N], unsigned
     }
     __syncthreads();
 }
-// grid total of one slot by one warp: op 0 sum, 1 max, 2 min (fixed order)
-__device__ __forceinline__ double ir_slot_total(const double* src, int op) {
-    const int lane = threadIdx.x & 31, G = gridDim.x;
-    const double idn = op == 2 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
-    double v[5];
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-        const int b = lane + 32 * j;
-        v[j] = b < G ? ld_cg(src + b) : idn;
-    }
-    double t = v[0];
-#pragma unroll
-    for (int j = 1; j < 5; ++j) t = op == 0 ? t + v[j] : op == 1 ? fmax(t, v[j]) : fmin(t, v[j]);
-    return op == 0 ? warp_sum(t) : op == 1 ? warp_max(t) : warp_min(t);
-}
-// slots [s0, s0 + n) -> out[0 .. n) in shared memory, every block identically
+// slots [s0, s0 + n) -> out[0 .. n) in shared memory, every block identically; a warp loads its (up to 2) slots
+// before reducing them, so the totals cost one round trip for n <= 2 W
 __device__ __forceinline__ void ir_totals(const double* part, int s0, int n, unsigned maxmask, unsigned minmask,
                                           double* out) {
-    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int k = wid; k < n; k += W) {
-        const int op = ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
-        const double t = ir_slot_total(part + (size_t)(s0 + k) * gridDim.x, op);
-        if (lane == 0) out[k] = t;
+    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31, G = gridDim.x;
+    for (int k0 = wid; k0 < n; k0 += 2 * W) {
+        double v[2][5];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = k0 + h * W;
+            const int op = k >= n ? 0 : ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
+            const double idn = op == 2 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const int b = lane + 32 * j;
+                v[h][j] = (k < n && b < G) ? ld_cg(part + (size_t)(s0 + k) * G + b) : idn;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = k0 + h * W;
+            if (k >= n) break;
+            const int op = ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
+            double t = v[h][0];
+#pragma unroll
+            for (int j = 1; j < 5; ++j) t = op == 0 ? t + v[h][j] : op == 1 ? fmax(t, v[h][j]) : fmin(t, v[h][j]);
+            t = op == 0 ? warp_sum(t) : op == 1 ? warp_max(t) : warp_min(t);
+            if (lane == 0) out[k] = t;
+        }
     }
     __syncthreads();
 }
 
-// S phase producer (thread 0): the next chunk of my columns with a nonzero coefficient
+// S phase producer (thread 0): the next chunk of my columns; with coef, columns with a zero coefficient are skipped
+// (the first SST chunks are issued before the direction exists, without skipping)
 struct SProducer {
-    int p, p1, noff, nnz4;
-    __device__ bool next(const Seg& S, const double* coef, const double* zc, SChunk& d) {
+    int p, p0, p1, noff, nnz4;
+    const int2* ext;   // cached column extents of positions [p0, p0 + IR_QC)
+    __device__ bool next(const Seg& S, const double* coef, SChunk& d) {
         while (p < p1) {
-            const double cf = coef[p];
-            const int j = __ldg(S.list + p);
-            const int b = __ldg(S.ptr + j), e = __ldg(S.ptr + j + 1);
+            int b, e;
+            if (p - p0 < IR_QC) { const int2 x = ext[p - p0]; b = x.x; e = x.y; }
+            else { const int j = __ldg(S.list + p); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
             const int start = b + noff;
-            if (cf == 0.0 || start >= e) { ++p; noff = 0; continue; }
+            if ((coef && noff == 0 && coef[p] == 0.0) || start >= e) { ++p; noff = 0; continue; }
             d.p = p;
             d.a = start & ~3;
             d.vb = start;
             d.ve = min(e, d.a + IR_SCH);
             d.ce = max(d.a, min((d.ve + 3) & ~3, nnz4));
-            d.cf = cf;
-            d.zf = zc ? (zc[p] != 0.0) : 0;
+            d.ok = 1;
             if (d.ve == e) { ++p; noff = 0; } else noff = d.ve - b;
             return true;
         }
@@ -120,6 +132,18 @@ struct SProducer {
         if (d.ce > d.a) {
             bulk_g2s(s_idx + st * IR_SCH, S.idx + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
             bulk_g2s(s_val + st * IR_SCH, S.val + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
+        }
+    }
+    // the first sst chunks of my columns (no skipping: issued before the direction exists)
+    __device__ void prefetch(const Seg& S, int sst, SChunk* s_desc, int* s_idx, float* s_val, uint64_t* s_bar) {
+        p = p0;
+        noff = 0;
+        for (int k = 0; k < sst; ++k) mbar_init(s_bar + k, 1);
+        fence_mbar_init();
+        for (int k = 0; k < sst; ++k) {
+            SChunk d;
+            if (next(S, nullptr, d)) { s_desc[k] = d; issue(S, d, k, s_idx, s_val, s_bar); }
+            else s_desc[k].ok = 0;
         }
     }
 };
@@ -142,35 +166,39 @@ __device__ __noinline__ void ir_lazy_l1(const Prm& P, const ASet& AS, int p0, in
     ir_block_partials<ML_MAXLS - IR_NT0>(v, 0u, 0u, sh_w, part, IR_SL1);
 }
 
+template <int GSCH>
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
-    unsigned long long ph_t = gtimer(), ph_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph_t = gtimer(), ph_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ double sh_w[2 * 256 + 8];   // >= IR_W * N + N for every ir_block_partials<N>; 2 x 256 in R
     __shared__ double sh_t[12], sh_r[4], sh_l1[ML_MAXLS];
+    __shared__ int2 col_ext[IR_QC];
+    constexpr int SST = ir_sst(GSCH);
     cg::grid_group grid = cg::this_grid();
     Ctl* c = P.ctl;
     if (c->skip) return;   // grid-uniform
     const int m = P.m, G = gridDim.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nA = c->nA;
+    const int ph_off = nA < 2048 ? 0 : 8;
     const int q = (nA + G - 1) / G;
     const int p0 = min(nA, (int)blockIdx.x * q), p1 = min(nA, p0 + q);
     const int R = (m + G - 1) / G;
     const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
     double* part = P.irpart;
-    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes());   // X_A s of my columns, later sv
+    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes<GSCH>());   // X_A s of my columns, later sv
     double* xz_sh = xs_sh + m;                                           // X_A z of my columns
     double* parts = P.parts;                                              // [G][m] block partials of X_A s
     double* zparts = P.parts + (size_t)G * m;                             // [G][m] block partials of X_A z
     // S ring (block-shared)
     int* s_idx = reinterpret_cast<int*>(smraw);
-    float* s_val = reinterpret_cast<float*>(smraw + (size_t)4 * IR_SST * IR_SCH);
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smraw + (size_t)8 * IR_SST * IR_SCH);
-    SChunk* s_desc = reinterpret_cast<SChunk*>(s_bar + IR_SST);
+    float* s_val = reinterpret_cast<float*>(smraw + (size_t)4 * SST * IR_SCH);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smraw + (size_t)8 * SST * IR_SCH);
+    SChunk* s_desc = reinterpret_cast<SChunk*>(s_bar + SST);
     // G rings (per warp; alias the S ring, used after it)
-    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<IN_GSCH, IN_GST>(0);
-    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * IN_GST * IN_GSCH);
+    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<GSCH, IN_GST>(0);
+    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * IN_GST * GSCH);
     uint32_t g_phase = 0u;
     long long nsc = 0, nhs = 0;
 
@@ -185,8 +213,16 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     bt[0] = 1.0;
 #pragma unroll
     for (int t = 1; t < IR_NT0; ++t) bt[t] = bt[t - 1] * P.beta_ls;
+    for (int p = p0 + threadIdx.x; p < min(p1, p0 + IR_QC); p += blockDim.x) {
+        const int j = __ldg(S.list + p);
+        col_ext[p - p0] = make_int2(__ldg(S.ptr + j), __ldg(S.ptr + j + 1));
+    }
+    __syncthreads();
+    SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // thread 0's S-ring producer state
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
+        const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
+        if (producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
         // ------------------------------------------------ D: direction on my positions
         int my_z = 0;
         {
@@ -234,48 +270,60 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         {
             const double* coef = pcd ? AS.s : AS.u;
-            const double* zc = my_z ? AS.u : nullptr;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
                 xs_sh[i] = 0.0;
                 if (my_z) xz_sh[i] = 0.0;
             }
-            SProducer pr{p0, p1, 0, (int)(S.nnz & ~3LL)};
-            if (threadIdx.x == 0) {
-                for (int k = 0; k < IR_SST; ++k) mbar_init(s_bar + k, 1);
-                fence_mbar_init();
-                for (int k = 0; k < IR_SST; ++k) {
-                    SChunk d;
-                    if (pr.next(S, coef, zc, d)) { s_desc[k] = d; pr.issue(S, d, k, s_idx, s_val, s_bar); }
-                    else s_desc[k].cf = 0.0;
+            __syncthreads();
+            uint32_t s_phase = 0u;
+            for (int st = 0;; st = (st + 1) % SST) {
+                const SChunk d = s_desc[st];
+                if (!d.ok) break;
+                mbar_wait(s_bar + st, (s_phase >> st) & 1u);
+                s_phase ^= 1u << st;
+                const double cf = coef[d.p];
+                if (cf != 0.0) {
+                    const int zf = my_z && AS.u[d.p] != 0.0;   // z_p = s_p on a zeroing column
+                    const int* ci = s_idx + st * IR_SCH - d.a;
+                    const float* cv = s_val + st * IR_SCH - d.a;
+                    const int kend = min(d.ve, d.ce);
+                    // rows are distinct within a column: all loads of a batch are issued before its stores
+                    constexpr int UB = IR_SCH / 256;
+                    for (int k0 = d.vb + threadIdx.x; k0 < d.ve; k0 += UB * (int)blockDim.x) {
+                        int r[UB];
+                        double xv[UB], a[UB];
+#pragma unroll
+                        for (int u = 0; u < UB; ++u) {
+                            const int k = k0 + u * blockDim.x;
+                            r[u] = -1;
+                            if (k < kend) { r[u] = ci[k]; xv[u] = (double)cv[k]; }
+                            else if (k < d.ve) { r[u] = __ldg(S.idx + k); xv[u] = (double)__ldg(S.val + k); }
+                        }
+#pragma unroll
+                        for (int u = 0; u < UB; ++u) a[u] = r[u] >= 0 ? xs_sh[r[u]] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < UB; ++u)
+                            if (r[u] >= 0) xs_sh[r[u]] = fma(xv[u], cf, a[u]);
+                        if (zf) {
+#pragma unroll
+                            for (int u = 0; u < UB; ++u) a[u] = r[u] >= 0 ? xz_sh[r[u]] : 0.0;
+#pragma unroll
+                            for (int u = 0; u < UB; ++u)
+                                if (r[u] >= 0) xz_sh[r[u]] = fma(xv[u], cf, a[u]);
+                        }
+                    }
+                    if (threadIdx.x == 0) nsc += d.ve - d.vb;
+                }
+                __syncthreads();   // stage st consumed by every warp
+                if (producer) {
+                    SChunk nd;
+                    if (pr.next(S, coef, nd)) { s_desc[st] = nd; pr.issue(S, nd, st, s_idx, s_val, s_bar); }
+                    else s_desc[st].ok = 0;
                 }
             }
             __syncthreads();
-            uint32_t s_phase = 0u;
-            for (int st = 0;; st = (st + 1) % IR_SST) {
-                const SChunk d = s_desc[st];
-                if (d.cf == 0.0) break;
-                mbar_wait(s_bar + st, (s_phase >> st) & 1u);
-                s_phase ^= 1u << st;
-                const int* ci = s_idx + st * IR_SCH - d.a;
-                const float* cv = s_val + st * IR_SCH - d.a;
-                const int kend = min(d.ve, d.ce);
-                for (int k = d.vb + threadIdx.x; k < d.ve; k += blockDim.x) {   // rows are distinct within a column
-                    const int r = k < kend ? ci[k] : __ldg(S.idx + k);
-                    const double xv = (double)(k < kend ? cv[k] : __ldg(S.val + k));
-                    xs_sh[r] = fma(xv, d.cf, xs_sh[r]);
-                    if (d.zf) xz_sh[r] = fma(xv, d.cf, xz_sh[r]);   // z_p = s_p on a zeroing column
-                }
-                if (threadIdx.x == 0) nsc += d.ve - d.vb;
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    SChunk nd;
-                    if (pr.next(S, coef, zc, nd)) { s_desc[st] = nd; pr.issue(S, nd, st, s_idx, s_val, s_bar); }
-                    else s_desc[st].cf = 0.0;
-                }
-                __syncthreads();
-            }
-            if (threadIdx.x == 0)
-                for (int k = 0; k < IR_SST; ++k) mbar_inval(s_bar + k);
+            if (producer)
+                for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
             // my block partials (a block without zeroing columns writes zeros for X_A z)
             const int zpart = pcd && P.pcd_snap;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -315,20 +363,16 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (g < ng) {
                     const double* src = parts + r0 + rr;
                     const double* srz = zparts + r0 + rr;
-                    int b = g;
-                    for (; b + 3 * ng < G; b += 4 * ng) {
-                        const double x0 = ld_cg(src + (size_t)b * m), x1 = ld_cg(src + (size_t)(b + ng) * m),
-                                     x2 = ld_cg(src + (size_t)(b + 2 * ng) * m), x3 = ld_cg(src + (size_t)(b + 3 * ng) * m);
-                        t += ((x0 + x1) + x2) + x3;
-                        if (dual) {
-                            const double z0 = ld_cg(srz + (size_t)b * m), z1 = ld_cg(srz + (size_t)(b + ng) * m),
-                                         z2 = ld_cg(srz + (size_t)(b + 2 * ng) * m), z3 = ld_cg(srz + (size_t)(b + 3 * ng) * m);
-                            tz += ((z0 + z1) + z2) + z3;
+                    for (int b0 = g; b0 < G; b0 += 8 * ng) {   // 8 loads in flight, summed in block order
+                        double x[8], z[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int b = b0 + u * ng;
+                            x[u] = b < G ? ld_cg(src + (size_t)b * m) : 0.0;
+                            z[u] = (dual && b < G) ? ld_cg(srz + (size_t)b * m) : 0.0;
                         }
-                    }
-                    for (; b < G; b += ng) {
-                        t += ld_cg(src + (size_t)b * m);
-                        if (dual) tz += ld_cg(srz + (size_t)b * m);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) { t += x[u]; tz += z[u]; }
                     }
                     sh_w[threadIdx.x] = t;   // sh_w holds >= 2 * 256 doubles
                     sh_w[blockDim.x + threadIdx.x] = tz;
@@ -363,7 +407,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             ir_block_partials<4>(v, 0u, 1u << 3, sh_w, part, IR_SR);
         }
         // prefetch the G rings (X_A's columns do not depend on the step) across the barrier
-        ColStream<IN_GSCH, IN_GST> csG;
+        ColStream<GSCH, IN_GST> csG;
         const bool need_hs = it < K - 1;
         if (need_hs) {
             if (lane == 0) {
@@ -448,13 +492,24 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             P.Xd[i] += beta * P.Xs[i] + (zs ? (1.0 - beta) * P.Xz[i] : 0.0);
         if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
             double* sv_sh = xs_sh;
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                const double xsg = beta * ld_cg(P.Xs + i) + (zs ? (1.0 - beta) * ld_cg(P.Xz + i) : 0.0);
-                sv_sh[i] = P.rD[i].y * xsg;
+            for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 rows in flight per thread
+                double xs[8], xz[8], dd[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    xs[u] = i < m ? ld_cg(P.Xs + i) : 0.0;
+                    xz[u] = (zs && i < m) ? ld_cg(P.Xz + i) : 0.0;
+                    dd[u] = i < m ? P.rD[i].y : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < m) sv_sh[i] = dd[u] * (beta * xs[u] + (zs ? (1.0 - beta) * xz[u] : 0.0));
+                }
             }
             __syncthreads();
             PH_MARK(5);
-            ColStream<IN_GSCH, IN_GST>& cs = csG;
+            ColStream<GSCH, IN_GST>& cs = csG;
             int stg = 0;
             double a = 0.0;
             while (true) {
@@ -462,8 +517,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (dsc.cf == 0.0) break;
                 mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
                 g_phase ^= 1u << stg;
-                const int* ci = cs.sidx + stg * IN_GSCH - dsc.a;
-                const float* cv = cs.sval + stg * IN_GSCH - dsc.a;
+                const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                const float* cv = cs.sval + stg * GSCH - dsc.a;
                 const int kend = min(dsc.ve, dsc.ce);
                 int k = dsc.vb + lane;
                 double a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -522,7 +577,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int q2 = 0; q2 < 12; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
+        for (int q2 = 0; q2 < 16; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
         c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1; c->snap = 0; c->zsnap = 0;
         c->cg_restart = cg_restart; c->next_pcd = next_pcd; c->acc_steps = acc_steps; c->inner_stop = stop;
         c->pcd_mode = pcd; c->beta = beta; c->bk = bk; c->bq = bq; c->bcg = bcg; c->rz = rz;

@@ -49,7 +49,7 @@ struct Ctl {
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
     int ntrace, trace_cap, bad_y, level, it;
     int pad2[3];
-    unsigned long long tph[12];  // persistent inner solver: ns spent per phase (block 0), diagnostics
+    unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics
 };
 
 // heavy-segment schedule for one segment list
@@ -1036,7 +1036,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                                                                            \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                  \
             const unsigned long long t_ = gtimer();                                 \
-            ph_acc[k] += t_ - ph_t;                                                 \
+            ph_acc[(k) + ph_off] += t_ - ph_t;                                      \
             ph_t = t_;                                                              \
         }                                                                           \
     } while (0)
