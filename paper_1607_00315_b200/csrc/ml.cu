@@ -75,6 +75,8 @@ struct ml_ctx {
     bool sm_inner = false;   // persistent cooperative inner solver (k_inner)
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // k_inner<1024> or k_inner<512>
+    const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
+    size_t gsmall_bytes = 0;
     size_t inner_bytes = 0;
     int gath_W = 0, gath_P = 0;
     size_t gath_bytes = 0;
@@ -328,6 +330,16 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
     const int cls = finest ? CLS_GATHER_FINE : CLS_GATHER_COARSE;
     PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
+    if (c->sm_inner) {   // small m: one cooperative launch (k_gather_small), (r, D) in shared memory
+        Prm Pc = c->P;
+        ASet A2 = AS;
+        long long* ac = acc_of(c, cls);
+        void* args[] = {(void*)&Pc, (void*)&S, (void*)&A2, (void*)&ac};
+        cudaLaunchCooperativeKernel(finest ? c->gsmall_fn[1] : c->gsmall_fn[0], dim3(c->inner_P), dim3(32 * IR_W), args,
+                                    c->gsmall_bytes, c->st);
+        c->launches++;
+        return;
+    }
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
               (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
     const int grid = std::max(1, std::min(GRID_CAP, (nC_host + TILE - 1) / TILE));
@@ -607,11 +619,24 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, bytes);
-            if (bps >= 1) {
+            const void* g0 = big_g ? (const void*)k_gather_small<1024, false> : (const void*)k_gather_small<512, false>;
+            const void* g1 = big_g ? (const void*)k_gather_small<1024, true> : (const void*)k_gather_small<512, true>;
+            const size_t gb = big_g ? gather_small_smem_bytes<1024>((int)X->m) : gather_small_smem_bytes<512>((int)X->m);
+            int gps0 = 0, gps1 = 0;
+            if (gb <= 220 * 1024 &&
+                cudaFuncSetAttribute(g0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb) == cudaSuccess &&
+                cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb) == cudaSuccess) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gps0, g0, 32 * IR_W, gb);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gps1, g1, 32 * IR_W, gb);
+            }
+            if (bps >= 1 && gps0 >= 1 && gps1 >= 1) {
                 c->sm_inner = true;
                 c->inner_fn = kfn;
                 c->inner_bytes = bytes;
                 c->inner_P = std::min(SM_COUNT, IR_GMAX);
+                c->gsmall_fn[0] = g0;
+                c->gsmall_fn[1] = g1;
+                c->gsmall_bytes = gb;
             }
         }
         cudaGetLastError();
@@ -843,7 +868,7 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
                         const int* Cl = c->lvl + loff[l - 1];
                         const int nCl = (int)k[l];
                         ML_LAUNCH(c, k_set_C, 1, ctl, nCl, 1);
-                        launch_units_build(c, 1, Cl, nCl);
+                        if (!c->sm_inner) launch_units_build(c, 1, Cl, nCl);   // heavy units of the generic gathers
                         const int reps = (l == L) ? o.nu_c : o.nu;
                         const int K = (l == L) ? o.K_coarse : o.K_mid;
                         for (int r = 0; r < reps; ++r) {

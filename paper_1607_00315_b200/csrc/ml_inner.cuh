@@ -584,3 +584,177 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         c->rz_prev = rz_prev; c->slope = slope; c->ss = ss; c->ps = ps; c->sHs = sHs; c->vq = vq;
     }
 }
+
+// ------------------------------------------------------------------ A2 + A3 for small m: cooperative free-set gather
+// Block b owns the contiguous positions [b q, (b+1) q) of C (or of all columns at the finest level).  (r, D) of all rows
+// is staged in shared memory; each warp streams its columns through a TMA ring (as in k_inner's Hs phase):
+// g_j = sum_i X_ij r_i, h_j = sum_i X_ij^2 D_i into AS.s / AS.Hs (scratch, by position).  Then my
+// positions in order: v_j, free flag w_j != 0 or |g_j| > lam; block counts and partial sums -> one grid
+// barrier -> every block: its offset (counts of the blocks before it, in order), the totals; my free columns are
+// written IN ORDER into the ASet.  Block 0 takes the last-block decisions of k_gather_free (nA, vmax, F, R2).
+template <int GSCH>
+__host__ __device__ inline size_t gather_small_smem_bytes(int m) {
+    return (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0) + (size_t)16 * m;
+}
+template <int GSCH, bool FINEST>
+__global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, long long* acc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ double sh_w[2 * 256 + 8];
+    __shared__ double sh_t[4];
+    __shared__ int sh_cnt[IR_W + 1];
+    cg::grid_group grid = cg::this_grid();
+    Ctl* ctl = P.ctl;
+    if (ctl->skip) return;   // grid-uniform (coarse relaxations of a converged level)
+    const int m = P.m, G = gridDim.x;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nC = S.list ? ctl->nC : P.n;
+    const int q = (nC + G - 1) / G;
+    const int p0 = min(nC, (int)blockIdx.x * q), p1 = min(nC, p0 + q);
+    double2* rd_sh = reinterpret_cast<double2*>(smraw + (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0));
+    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<GSCH, IN_GST>(0);
+    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * IN_GST * GSCH);
+    if (lane == 0) {
+        for (int k = 0; k < IN_GST; ++k) mbar_init(g_bar + k, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    ColStream<GSCH, IN_GST> cs;
+    cs.streamed = 0;
+    cs.segs = 0;
+    stream_begin(cs, S, nullptr, p0, p1, gbase);   // X first: its latency overlaps the (r, D) staging
+    for (int i = threadIdx.x; i < m; i += blockDim.x) rd_sh[i] = P.rD[i];
+    __syncthreads();
+    {
+        uint32_t phase = 0u;
+        int stg = 0;
+        double a = 0.0, b = 0.0;
+        while (true) {
+            const ChunkDesc dsc = cs.desc[stg];
+            if (dsc.cf == 0.0) break;
+            mbar_wait(cs.bar + stg, (phase >> stg) & 1u);
+            phase ^= 1u << stg;
+            const int* ci = cs.sidx + stg * GSCH - dsc.a;
+            const float* cv = cs.sval + stg * GSCH - dsc.a;
+            const int kend = min(dsc.ve, dsc.ce);
+            int k = dsc.vb + lane;
+            double a1 = 0.0, b1 = 0.0;
+            for (; k + 32 < kend; k += 64) {
+                const double2 q0 = rd_sh[ci[k]], q1 = rd_sh[ci[k + 32]];
+                const double x0 = (double)cv[k], x1 = (double)cv[k + 32];
+                a = fma(x0, q0.x, a);
+                b = fma(x0 * x0, q0.y, b);
+                a1 = fma(x1, q1.x, a1);
+                b1 = fma(x1 * x1, q1.y, b1);
+            }
+            a += a1;
+            b += b1;
+            for (; k < kend; k += 32) {
+                const double2 q0 = rd_sh[ci[k]];
+                const double x0 = (double)cv[k];
+                a = fma(x0, q0.x, a);
+                b = fma(x0 * x0, q0.y, b);
+            }
+            for (; k < dsc.ve; k += 32) {
+                const double2 q0 = rd_sh[__ldg(S.idx + k)];
+                const double x0 = (double)__ldg(S.val + k);
+                a = fma(x0, q0.x, a);
+                b = fma(x0 * x0, q0.y, b);
+            }
+            if (dsc.last) {
+                const double g = warp_sum(a), h = warp_sum(b);
+                if (lane == 0) { AS.s[dsc.p] = g; AS.Hs[dsc.p] = h; }
+                a = 0.0;
+                b = 0.0;
+            }
+            __syncwarp();
+            ChunkDesc nd;
+            const bool ok = cs.next(nd);
+            if (lane == 0) {
+                if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
+                else cs.desc[stg].cf = 0.0;
+            }
+            __syncwarp();
+            stg = (stg + 1) % IN_GST;
+        }
+        __syncwarp();
+        if (lane == 0)
+            for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+    }
+    acc_add(acc, cs.streamed, cs.segs);   // (synchronises the block: g, h of my positions are visible)
+    // my positions in order: flags, block count, partial sums
+    double v1p = 0.0, l1p = 0.0, vmx = 0.0;
+    int cnt = 0;
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const int j = S.list ? __ldg(S.list + p) : p;
+        const double g = AS.s[p];
+        double wj = 0.0;
+        if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
+        const double v = (wj != 0.0) ? g + P.lam * sgn(wj) : soft(g, P.lam);
+        vmx = fmax(vmx, fabs(v));
+        v1p += fabs(v);
+        l1p += fabs(wj);
+        cnt += (wj != 0.0) || (fabs(g) > P.lam);
+    }
+    {
+        const double v[4] = {v1p, l1p, vmx, (double)cnt};
+        ir_block_partials<4>(v, 1u << 2, 0u, sh_w, P.irpart, 0);
+    }
+    grid.sync();
+    // totals (identical in every block) and my offset: the counts of the blocks before me, in order
+    ir_totals(P.irpart, 0, 3, 1u << 2, 0u, sh_t);
+    if (wid == 0) {
+        int off = 0, tot = 0;
+        for (int b0 = 0; b0 < G; b0 += 32) {
+            const int b = b0 + lane;
+            const int c = b < G ? (int)ld_cg(P.irpart + (size_t)3 * G + b) : 0;
+            const int before = (b < (int)blockIdx.x) ? c : 0;
+            off += __reduce_add_sync(0xffffffffu, before);
+            tot += __reduce_add_sync(0xffffffffu, c);
+        }
+        if (lane == 0) { sh_cnt[IR_W] = off; sh_cnt[0] = tot; }
+    }
+    __syncthreads();
+    const int my_off = sh_cnt[IR_W], nA = sh_cnt[0];
+    __syncthreads();
+    // my free columns, in position order
+    int base = my_off;
+    for (int p00 = p0; p00 < p1; p00 += blockDim.x) {
+        const int p = p00 + threadIdx.x;
+        int j = 0, flag = 0;
+        double g = 0.0, wj = 0.0;
+        if (p < p1) {
+            j = S.list ? __ldg(S.list + p) : p;
+            g = AS.s[p];
+            if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
+            flag = (wj != 0.0) || (fabs(g) > P.lam);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0) sh_cnt[wid] = __popc(bal);
+        __syncthreads();
+        int woff = 0, tot = 0;
+        for (int w = 0; w < IR_W; ++w) { if (w < wid) woff += sh_cnt[w]; tot += sh_cnt[w]; }
+        if (flag) {
+            const int o = base + woff + __popc(bal & ((1u << lane) - 1u));
+            AS.A[o] = j;
+            AS.gA[o] = g;
+            AS.hA[o] = AS.Hs[p] + P.eps_h;
+            AS.wA[o] = wj;
+        }
+        base += tot;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // the last-block decisions of k_gather_free
+        ctl->nA = nA;
+        const double vmax = sh_t[2];
+        ctl->vmax = vmax;
+        ctl->vmax_bits = 0ull;
+        if (FINEST) {
+            ctl->v1 = sh_t[0];
+            ctl->l1 = sh_t[1];
+            ctl->nAf = nA;
+            ctl->F = ctl->L + P.lam * ctl->l1;
+        }
+        ctl->F_before = ctl->F;
+        if (vmax / P.lam <= P.tol) { ctl->skip = 1; ctl->outcome = OUT_CONVERGED; ctl->level_conv = 1; }
+    }
+}
