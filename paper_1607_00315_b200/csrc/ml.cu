@@ -439,6 +439,7 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
         void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
         cudaLaunchCooperativeKernel(c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
         c->launches++;
+        return;   // k_inner also runs the outer line search and the update (R14-R18) and writes the trace row
     } else
     for (int it = 0; it < K; ++it) {
         {
@@ -611,11 +612,11 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->gath_bytes = bytes;
             c->gath_P = SM_COUNT * bps;
         }
-        // persistent inner solver: 1024-element G chunks when the m-vectors leave room, else 512
-        const bool big_g = inner_smem_bytes<1024>((int)X->m) <= 220 * 1024;
+        // persistent inner solver: 1024-element G chunks when the two m-vectors leave room, else 512
+        const bool big_g = inner_smem_bytes<1024>((int)X->m) <= IR_SMEM_MAX;
         const void* kfn = big_g ? (const void*)k_inner<1024> : (const void*)k_inner<512>;
         bytes = big_g ? inner_smem_bytes<1024>((int)X->m) : inner_smem_bytes<512>((int)X->m);
-        if (bytes <= 220 * 1024 && X->m <= 256LL * std::min(SM_COUNT, IR_GMAX) &&
+        if (bytes <= IR_SMEM_MAX && X->m <= (int64_t)IR_RS * std::min(SM_COUNT, IR_GMAX) &&
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, bytes);

@@ -28,9 +28,16 @@ constexpr int IN_GST = 2;                  // G phase: per-warp rings of GSCH-el
 // partial slots: D (PCD) 0 ps, 1 ss, 2 pz, 3 Z1, 4 zz, 5 #zeroing, 6..9 l1 trials 0..3, 10 max|s|, 11 vq
 //                D (CG)  0 rz, 1 gx.u, 2 gx.s_prev, 3 u.u, 4 u.s_prev, 5 s_prev.s_prev, 11 vq
 //                R       12 D Xs^2, 13 D Xs Xz, 14 D Xz^2, 15 first kink (min);  lazy l1 trials 16 ..
-enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16, IR_NSLOT = 16 + ML_MAXLS - IR_NT0 };
+enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
+// outer line search + update (R14-R18): 0 g.d, 1 max|d|, 2..5 l1 trials 0..3, 6..9 loss trials 0..3; the rest:
+// 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
+constexpr int IR_NLS = ML_MAXLS - 4;
+enum { IR_SO = 0, IR_SO2 = 10, IR_NSLOT = 10 + 2 * IR_NLS };
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
+// my positions' state, indexed by p - p0: shared memory when q <= IR_QS, else the ASet arrays (offset by p0)
+constexpr int IR_QS = 160, IR_RS = 64;   // cached positions / rows per block (rows: m <= IR_RS * G)
+struct PosState { const double* wA; const double* gA; const double* hA; double* d; double* Hd; double* s; double* u; };
 struct SChunk { int p, a, vb, ve, ce, ok; };   // copy [a, ce) of column p, valid [vb, ve); ok = 0: no chunk
 
 __host__ __device__ constexpr int ir_sst(int gsch) { return gsch >= 1024 ? 8 : 4; }   // the S ring fits the G rings
@@ -46,6 +53,7 @@ static_assert(sizeof(SChunk) == 24, "SChunk layout");
 // dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z)
 template <int GSCH>
 __host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes<GSCH>() + (size_t)16 * m; }
+constexpr size_t IR_SMEM_MAX = 196 * 1024;   // dynamic shared memory budget (the static part is ~30 KB)
 
 // N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
 // block's own totals stay in sh_w[IR_W * N + k]
@@ -114,7 +122,7 @@ struct SProducer {
             if (p - p0 < IR_QC) { const int2 x = ext[p - p0]; b = x.x; e = x.y; }
             else { const int j = __ldg(S.list + p); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
             const int start = b + noff;
-            if ((coef && noff == 0 && coef[p] == 0.0) || start >= e) { ++p; noff = 0; continue; }
+            if ((coef && noff == 0 && coef[p - p0] == 0.0) || start >= e) { ++p; noff = 0; continue; }
             d.p = p;
             d.a = start & ~3;
             d.vb = start;
@@ -149,13 +157,13 @@ struct SProducer {
 };
 
 // l1 trial differences for trials IR_NT0 .. ML_MAXLS - 1 on my positions -> block partials (rare: Armijo past 1/8)
-__device__ __noinline__ void ir_lazy_l1(const Prm& P, const ASet& AS, int p0, int p1, double b_last, double* sh_w,
+__device__ __noinline__ void ir_lazy_l1(const Prm& P, const PosState& X, int q0, double b_last, double* sh_w,
                                         double* part) {
     double v[ML_MAXLS - IR_NT0];
 #pragma unroll
     for (int k = 0; k < ML_MAXLS - IR_NT0; ++k) v[k] = 0.0;
-    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-        const double x = AS.wA[p] + AS.d[p], sp = AS.s[p], ax = fabs(x);
+    for (int k0 = threadIdx.x; k0 < q0; k0 += blockDim.x) {
+        const double x = X.wA[k0] + X.d[k0], sp = X.s[k0], ax = fabs(x);
         double b = b_last;
 #pragma unroll
         for (int k = 0; k < ML_MAXLS - IR_NT0; ++k) {
@@ -166,18 +174,55 @@ __device__ __noinline__ void ir_lazy_l1(const Prm& P, const ASet& AS, int p0, in
     ir_block_partials<ML_MAXLS - IR_NT0>(v, 0u, 0u, sh_w, part, IR_SL1);
 }
 
+// R14-R18 second batch: l1 and loss differences of trials 4 .. max_ls - 1 (rare) -> block partials
+__device__ __noinline__ void ir_outer_batch2(const Prm& P, const PosState& X, int q0, int r0, int r1, const double* xd_r,
+                                             double* sh_w, double* part) {
+    double v[2 * IR_NLS];
+#pragma unroll
+    for (int k = 0; k < 2 * IR_NLS; ++k) v[k] = 0.0;
+    double a4 = 1.0;
+    for (int t = 0; t < 4; ++t) a4 *= P.beta_ls;
+    for (int k0 = threadIdx.x; k0 < q0; k0 += blockDim.x) {
+        const double d = X.d[k0], w = X.wA[k0], aw = fabs(w);
+        double a = a4;
+#pragma unroll
+        for (int k = 0; k < IR_NLS; ++k) { v[k] += fabs(w + a * d) - aw; a *= P.beta_ls; }
+    }
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const double y = (double)P.y[i];
+        const double ti = y * P.z[i], yx = y * xd_r[i - r0];
+        double a = a4;
+#pragma unroll
+        for (int k = 0; k < IR_NLS; ++k) { v[IR_NLS + k] += dloss(ti, a * yx); a *= P.beta_ls; }
+    }
+    ir_block_partials<2 * IR_NLS>(v, 0u, 0u, sh_w, part, IR_SO2);
+}
+__device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int steps, double Fb, double Fa, double a) {
+    if (c->ntrace < c->trace_cap) {
+        TraceRow tr{c->level, outcome, steps, c->nA, (long long)c->nC, Fb, Fa, a};
+        P.trace[c->ntrace] = tr;
+    }
+    c->ntrace += 1;
+}
+
 template <int GSCH>
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
     unsigned long long ph_t = gtimer(), ph_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ double sh_w[2 * 256 + 8];   // >= IR_W * N + N for every ir_block_partials<N>; 2 x 256 in R
-    __shared__ double sh_t[12], sh_r[4], sh_l1[ML_MAXLS];
+    __shared__ double sh_w[IR_W * 2 * IR_NLS + 2 * IR_NLS];   // >= IR_W * N + N for every ir_block_partials<N>
+    __shared__ double sh_t[12], sh_r[4], sh_l1[2 * IR_NLS];
     __shared__ int2 col_ext[IR_QC];
+    __shared__ double pos_sh[7][IR_QS];   // wA gA hA d Hd s u of my positions (q <= IR_QS)
+    __shared__ double row_sh[4][IR_RS];   // D, X s, X z, X d of my rows
     constexpr int SST = ir_sst(GSCH);
     cg::grid_group grid = cg::this_grid();
     Ctl* c = P.ctl;
-    if (c->skip) return;   // grid-uniform
+    if (c->skip) {   // grid-uniform: converged at R2 (or a converged level): the relaxation's trace row
+        if (blockIdx.x == 0 && threadIdx.x == 0 && !c->skipped)
+            ir_trace(P, c, c->outcome, 0, c->F, c->F, 0.0);
+        return;
+    }
     const int m = P.m, G = gridDim.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nA = c->nA;
@@ -188,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
     double* part = P.irpart;
     double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes<GSCH>());   // X_A s of my columns, later sv
-    double* xz_sh = xs_sh + m;                                           // X_A z of my columns
+    double* xz_sh = xs_sh + m;                                                 // X_A z of my columns
     double* parts = P.parts;                                              // [G][m] block partials of X_A s
     double* zparts = P.parts + (size_t)G * m;                             // [G][m] block partials of X_A z
     // S ring (block-shared)
@@ -202,8 +247,29 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     uint32_t g_phase = 0u;
     long long nsc = 0, nhs = 0;
 
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) { P.Xd[i] = 0.0; P.Xs[i] = 0.0; }
-    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) { AS.d[p] = 0.0; AS.Hd[p] = 0.0; }
+    const int q0 = p1 - p0;
+    PosState X;
+    if (q0 <= IR_QS) {
+        X = PosState{pos_sh[0], pos_sh[1], pos_sh[2], pos_sh[3], pos_sh[4], pos_sh[5], pos_sh[6]};
+        for (int k = threadIdx.x; k < q0; k += blockDim.x) {
+            pos_sh[0][k] = AS.wA[p0 + k];
+            pos_sh[1][k] = AS.gA[p0 + k];
+            pos_sh[2][k] = AS.hA[p0 + k];
+        }
+    } else {
+        X = PosState{AS.wA + p0, AS.gA + p0, AS.hA + p0, AS.d + p0, AS.Hd + p0, AS.s + p0, AS.u + p0};
+    }
+    for (int k = threadIdx.x; k < q0; k += blockDim.x) { X.d[k] = 0.0; X.Hd[k] = 0.0; }
+    double* rD_r = row_sh[0];
+    double* xs_r = row_sh[1];
+    double* xz_r = row_sh[2];
+    double* xd_r = row_sh[3];
+    for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) {
+        rD_r[k] = P.rD[r0 + k].y;
+        xs_r[k] = 0.0;
+        xz_r[k] = 0.0;
+        xd_r[k] = 0.0;
+    }
 
     int next_pcd = c->next_pcd, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;
     double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = c->rz_prev, slope = 0.0, ss = 0.0, ps = 0.0;
@@ -218,7 +284,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         col_ext[p - p0] = make_int2(__ldg(S.ptr + j), __ldg(S.ptr + j + 1));
     }
     __syncthreads();
-    SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // thread 0's S-ring producer state
+    SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
         const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
@@ -229,13 +295,13 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             double v[12];
 #pragma unroll
             for (int k = 0; k < 12; ++k) v[k] = 0.0;
-            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                const double x = AS.wA[p] + AS.d[p], pj = AS.gA[p] + AS.Hd[p], hh = AS.hA[p];
+            for (int k = threadIdx.x; k < q0; k += blockDim.x) {
+                const double x = X.wA[k] + X.d[k], pj = X.gA[k] + X.Hd[k], hh = X.hA[k];
                 if (pcd) {   // R6 (Eq. 5, D = diag H + eps) + the zeroing part z (Q27)
                     const double sp = soft(x - pj / hh, P.lam / hh) - x;
-                    AS.s[p] = sp;
+                    X.s[k] = sp;
                     const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;
-                    AS.u[p] = zp;
+                    X.u[k] = zp;
                     const double vv = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
                     v[0] += pj * sp;
                     v[1] += sp * sp;
@@ -251,8 +317,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 } else {     // R6' (Q9b): orthant residual, preconditioned by diag H + eps
                     const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;
                     const double u = (x != 0.0) ? -gx / hh : 0.0;
-                    AS.u[p] = u;
-                    const double sp = AS.s[p];
+                    X.u[k] = u;
+                    const double sp = X.s[k];
                     const double vv = (x != 0.0) ? gx : soft(pj, P.lam);
                     v[0] += hh * u * u;
                     v[1] += gx * u;
@@ -269,7 +335,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         PH_MARK(0);
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         {
-            const double* coef = pcd ? AS.s : AS.u;
+            const double* coef = pcd ? X.s : X.u;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
                 xs_sh[i] = 0.0;
                 if (my_z) xz_sh[i] = 0.0;
@@ -281,9 +347,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (!d.ok) break;
                 mbar_wait(s_bar + st, (s_phase >> st) & 1u);
                 s_phase ^= 1u << st;
-                const double cf = coef[d.p];
+                const double cf = coef[d.p - p0];
                 if (cf != 0.0) {
-                    const int zf = my_z && AS.u[d.p] != 0.0;   // z_p = s_p on a zeroing column
+                    const int zf = my_z && X.u[d.p - p0] != 0.0;   // z_p = s_p on a zeroing column
                     const int* ci = s_idx + st * IR_SCH - d.a;
                     const float* cv = s_val + st * IR_SCH - d.a;
                     const int kend = min(d.ve, d.ce);
@@ -385,10 +451,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         xz += sh_w[blockDim.x + g2 * nr + rr2];
                     }
                     const int i = r0 + rr2;
-                    if (!pcd) xs += bcg * P.Xs[i];
+                    if (!pcd) xs += bcg * xs_r[rr2];
+                    xs_r[rr2] = xs;
                     P.Xs[i] = xs;
-                    if (dual) P.Xz[i] = xz;
-                    const double D = P.rD[i].y;
+                    if (dual) { xz_r[rr2] = xz; P.Xz[i] = xz; }
+                    const double D = rD_r[rr2];
                     a_ss += D * xs * xs;
                     a_sz += D * xs * xz;
                     a_zz += D * xz * xz;
@@ -397,10 +464,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             double kmin = __longlong_as_double(0x7ff0000000000000LL);
             if (!pcd)
-                for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                    const double sp = AS.u[p] + bcg * AS.s[p];
-                    AS.s[p] = sp;
-                    const double x = AS.wA[p] + AS.d[p];
+                for (int k = threadIdx.x; k < q0; k += blockDim.x) {
+                    const double sp = X.u[k] + bcg * X.s[k];
+                    X.s[k] = sp;
+                    const double x = X.wA[k] + X.d[k];
                     if (x * sp < 0.0) kmin = fmin(kmin, -x / sp);
                 }
             const double v[4] = {a_ss, a_sz, a_zz, kmin};
@@ -418,7 +485,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             g_phase = 0u;
             csG.streamed = 0;
             csG.segs = 0;
-            stream_begin(csG, S, nullptr, p0, p1, gbase);
+            stream_begin(csG, S, nullptr, p0, p1, gbase, col_ext, IR_QC);
         }
         PH_MARK(3);
         grid.sync();   // B2
@@ -428,7 +495,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         auto l1 = [&](int t) -> double {   // sum_p |x + beta^t s| - |x| (trials >= IR_NT0 on demand: one more barrier)
             if (t < IR_NT0) return sh_t[6 + t];
             if (!have_l1) {
-                ir_lazy_l1(P, AS, p0, p1, bt[IR_NT0 - 1], sh_w, part);
+                ir_lazy_l1(P, X, q0, bt[IR_NT0 - 1], sh_w, part);
                 grid.sync();
                 ir_totals(part, IR_SL1, ML_MAXLS - IR_NT0, 0u, 0u, sh_l1);
                 have_l1 = 1;
@@ -488,8 +555,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         acc_steps += 1;
         // R12, m side: Xd += X sigma on my rows (sigma = beta s, or beta s + (1 - beta) z on the snap path)
-        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-            P.Xd[i] += beta * P.Xs[i] + (zs ? (1.0 - beta) * P.Xz[i] : 0.0);
+        for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x)
+            xd_r[k] += beta * xs_r[k] + (zs ? (1.0 - beta) * xz_r[k] : 0.0);
         if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
             double* sv_sh = xs_sh;
             for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 rows in flight per thread
@@ -534,12 +601,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (dsc.last) {
                     const double t = warp_sum(a);
                     if (lane == 0) {
-                        const int p = dsc.p;
-                        const double sp = AS.s[p], zp = zs ? AS.u[p] : 0.0;
-                        const double x = AS.wA[p] + AS.d[p];
+                        const int k = dsc.p - p0;
+                        const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
+                        const double x = X.wA[k] + X.d[k];
                         const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
-                        AS.Hd[p] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
-                        AS.d[p] = (zp != 0.0 || kink) ? -AS.wA[p] : AS.d[p] + beta * sp;   // snapped coordinates become 0
+                        X.Hd[k] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
+                        X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;   // snapped coordinates become 0
                     }
                     a = 0.0;
                 }
@@ -559,11 +626,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
             PH_MARK(6);
         } else {   // last iteration: d only
-            for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-                const double sp = AS.s[p], zp = zs ? AS.u[p] : 0.0;
-                const double x = AS.wA[p] + AS.d[p];
+            for (int k = threadIdx.x; k < q0; k += blockDim.x) {
+                const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
+                const double x = X.wA[k] + X.d[k];
                 const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
-                AS.d[p] = (zp != 0.0 || kink) ? -AS.wA[p] : AS.d[p] + beta * sp;
+                X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;
             }
         }
         __syncthreads();   // my positions' d, Hd and the shared rings before the next direction
@@ -577,11 +644,104 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int q2 = 0; q2 < 16; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
         c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1; c->snap = 0; c->zsnap = 0;
         c->cg_restart = cg_restart; c->next_pcd = next_pcd; c->acc_steps = acc_steps; c->inner_stop = stop;
         c->pcd_mode = pcd; c->beta = beta; c->bk = bk; c->bq = bq; c->bcg = bcg; c->rz = rz;
         c->rz_prev = rz_prev; c->slope = slope; c->ss = ss; c->ps = ps; c->sHs = sHs; c->vq = vq;
+    }
+    // ------------------------------------------------ R14-R18: outer line search on F and the update
+    PH_MARK(7);
+    const double F0 = c->F;
+    if (acc_steps == 0) {   // R14: d = 0
+        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, 0, F0, F0, 0.0); }
+        return;
+    }
+    double at[4];
+    at[0] = 1.0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k) at[k] = at[k - 1] * P.beta_ls;
+    {   // first batch {1, 1/2, 1/4, 1/8} (Eq. 4; Armijo Q7; term-by-term differences Q26)
+        double v[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) v[k] = 0.0;
+        for (int k0 = threadIdx.x; k0 < q0; k0 += blockDim.x) {
+            const double d = X.d[k0], w = X.wA[k0], aw = fabs(w);
+            v[0] += X.gA[k0] * d;
+            v[1] = fmax(v[1], fabs(d));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[2 + k] += fabs(w + at[k] * d) - aw;
+        }
+        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            const double y = (double)P.y[i];
+            const double ti = y * P.z[i], yx = y * xd_r[i - r0];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[6 + k] += dloss(ti, at[k] * yx);
+        }
+        ir_block_partials<10>(v, 1u << 1, 0u, sh_w, part, IR_SO);
+    }
+    grid.sync();
+    ir_totals(part, IR_SO, 10, 1u << 1, 0u, sh_t);
+    const double Delta = sh_t[0] + P.lam * sh_t[2];
+    if (sh_t[1] == 0.0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, acc_steps, F0, F0, 0.0); }
+        return;
+    }
+    int t_acc = -1;
+    double alpha = 0.0, l1d = 0.0;
+    for (int k = 0; k < 4 && k < P.max_ls; ++k)
+        if (sh_t[6 + k] + P.lam * sh_t[2 + k] <= P.sigma_out * at[k] * Delta) { t_acc = k; alpha = at[k]; l1d = sh_t[2 + k]; break; }
+    if (t_acc < 0 && P.max_ls > 4) {   // rare: the remaining trials
+        ir_outer_batch2(P, X, q0, r0, r1, xd_r, sh_w, part);
+        grid.sync();
+        ir_totals(part, IR_SO2, 2 * IR_NLS, 0u, 0u, sh_l1);
+        double a = at[3];
+        for (int k = 0; k + 4 < P.max_ls; ++k) {
+            a *= P.beta_ls;
+            if (sh_l1[IR_NLS + k] + P.lam * sh_l1[k] <= P.sigma_out * a * Delta) { t_acc = 4 + k; alpha = a; l1d = sh_l1[k]; break; }
+        }
+    }
+    if (t_acc < 0) {   // R17
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            c->skip = 1; c->outcome = OUT_STAGNATION; c->alpha = 0.0;
+            ir_trace(P, c, OUT_STAGNATION, acc_steps, F0, F0, 0.0);
+        }
+        return;
+    }
+    {   // R18: w_A += a d (bitmap, support count), z += a Xd with the per-sample refresh, L, F
+        double v[2] = {0.0, 0.0};
+        for (int k0 = threadIdx.x; k0 < q0; k0 += blockDim.x) {
+            const double w0 = X.wA[k0], w1 = w0 + alpha * X.d[k0];
+            const int j = AS.A[p0 + k0];
+            P.w[j] = w1;
+            const int nz0 = (w0 != 0.0), nz1 = (w1 != 0.0);
+            if (nz0 != nz1) { atomicXor(P.wbits + (j >> 5), 1u << (j & 31)); v[1] += nz1 - nz0; }
+        }
+        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            const double z = P.z[i] + alpha * xd_r[i - r0];
+            P.z[i] = z;
+            const RowState st = row_state(z, (double)P.y[i]);
+            P.rD[i] = make_double2(st.r, st.D);
+            v[0] += st.ell;
+        }
+        ir_block_partials<2>(v, 0u, 0u, sh_w, part, IR_SO);
+    }
+    grid.sync();
+    PH_MARK(7);
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0)
+            for (int q2 = 0; q2 < 16; ++q2) atomicAdd(&c->tph[q2], ph_acc[q2]);
+        ir_totals(part, IR_SO, 2, 0u, 0u, sh_t);
+        if (threadIdx.x == 0) {
+            c->nS += (int)sh_t[1];
+            c->L = sh_t[0];
+            c->l1 += l1d;
+            c->alpha = alpha;
+            c->t_acc = t_acc;
+            c->ls_ok = 1;
+            c->F = c->L + P.lam * c->l1;
+            c->outcome = OUT_UPDATED;
+            ir_trace(P, c, OUT_UPDATED, acc_steps, F0, c->F, alpha);
+        }
     }
 }
 

@@ -686,6 +686,7 @@ struct ColStream {
     const Seg* S;
     const double* coef;
     int* sidx; float* sval; uint64_t* bar; ChunkDesc* desc;
+    const int2* ext; int ext_p0, ext_n;   // optional cached segment extents of positions [ext_p0, ext_p0 + ext_n)
 
     __device__ void load_batch() {
         const int p = p0 + wid + W * (batch * 32 + lane);
@@ -693,9 +694,15 @@ struct ColStream {
         if (p < p1) {
             mcf = coef ? coef[p] : 1.0;
             if (mcf != 0.0) {
-                const int j = S->list ? __ldg(S->list + p) : p;
-                mb = __ldg(S->ptr + j);
-                me = __ldg(S->ptr + j + 1);
+                if (ext && p - ext_p0 < ext_n) {
+                    const int2 x = ext[p - ext_p0];
+                    mb = x.x;
+                    me = x.y;
+                } else {
+                    const int j = S->list ? __ldg(S->list + p) : p;
+                    mb = __ldg(S->ptr + j);
+                    me = __ldg(S->ptr + j + 1);
+                }
             }
         }
         kk = 0;
@@ -759,6 +766,8 @@ __host__ __device__ inline size_t gather_smem_bytes(int W, int m) {
 template <int SCH, int NSTG>
 __device__ __forceinline__ void stream_setup(ColStream<SCH, NSTG>& cs, unsigned char* base, const Seg& S, const double* coef, int nseg,
                                              int m_acc) {
+    cs.ext = nullptr;
+    cs.ext_n = 0;
     cs.W = blockDim.x >> 5;
     cs.wid = threadIdx.x >> 5;
     cs.lane = threadIdx.x & 31;
@@ -995,7 +1004,10 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
 
 template <int SCH, int NSTG>
 __device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG>& cs, const Seg& S, const double* coef, int p0, int p1,
-                                             unsigned char* base) {
+                                             unsigned char* base, const int2* ext = nullptr, int ext_n = 0) {
+    cs.ext = ext;
+    cs.ext_p0 = p0;
+    cs.ext_n = ext_n;
     cs.W = blockDim.x >> 5;
     cs.wid = threadIdx.x >> 5;
     cs.lane = threadIdx.x & 31;

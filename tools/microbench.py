@@ -61,7 +61,7 @@ def main():
     ctx.ml_inner_phases(reset=True)
     t = timeit(lambda: ctx.ml_solve(), 3, st)
     ph = ctx.ml_inner_phases(reset=True)
-    out["solve"] = {"ms": t, "inner_phase_ms_small_A": [round(x / 6e6, 3) for x in ph[:7]], "inner_phase_ms_large_A": [round(x / 6e6, 3) for x in ph[8:15]]}
+    out["solve"] = {"ms": t, "inner_phase_ms_small_A": [round(x / 6e6, 3) for x in ph[:8]], "inner_phase_ms_large_A": [round(x / 6e6, 3) for x in ph[8:16]]}
     print(json.dumps({"config": a.config, "ncols": len(C), "flush": a.flush, **out}))
 
 
