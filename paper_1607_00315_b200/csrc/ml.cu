@@ -77,6 +77,8 @@ struct ml_ctx {
     const void* inner_fn = nullptr;   // k_inner<1024> or k_inner<512>
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
     size_t gsmall_bytes = 0;
+    const void* msmall_fn = nullptr;   // k_margins_small<GSCH>
+    int* slist = nullptr;
     size_t inner_bytes = 0;
     int gath_W = 0, gath_P = 0;
     size_t gath_bytes = 0;
@@ -120,6 +122,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double2* hres = cv.take<double2>(std::max(nn, mm));
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
+    int* slist = cv.take<int>(mm <= SMALL_M ? nn + 1 : 1);   // k_margins_small: supp(w) in column order
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -150,6 +153,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
     P.irpart = irpart;
+    c->slist = slist;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
 
@@ -318,6 +322,16 @@ void launch_units_build(ml_ctx* c, int slot, const int* list, int nlist_host) {
 // A1: heavy rows, then the light row kernel with the fused epilogue
 void launch_margins(ml_ctx* c) {
     PassScope ps(c, CLS_MARGINS);
+    if (c->sm_inner) {   // small m: z = X_S w_S over the support's columns, one cooperative launch
+        Prm Pc = c->P;
+        Seg S = seg_cols(c, nullptr);
+        int* sl = c->slist;
+        long long* ac = acc_of(c, CLS_MARGINS);
+        void* args[] = {(void*)&Pc, (void*)&S, (void*)&sl, (void*)&ac};
+        cudaLaunchCooperativeKernel(c->msmall_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
+        c->launches++;
+        return;
+    }
     Seg S = seg_rows(c);
     ML_LAUNCH(c, (k_heavy<OpMargin, false>), c->gHeavy, S, units_of(c, 3), OpMargin{c->P.w, c->P.wbits},
               (const double*)nullptr, (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_MARGINS));
@@ -623,14 +637,18 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             const void* g0 = big_g ? (const void*)k_gather_small<1024, false> : (const void*)k_gather_small<512, false>;
             const void* g1 = big_g ? (const void*)k_gather_small<1024, true> : (const void*)k_gather_small<512, true>;
             const size_t gb = big_g ? gather_small_smem_bytes<1024>((int)X->m) : gather_small_smem_bytes<512>((int)X->m);
-            int gps0 = 0, gps1 = 0;
+            const void* mf = big_g ? (const void*)k_margins_small<1024> : (const void*)k_margins_small<512>;
+            int gps0 = 0, gps1 = 0, mps = 0;
             if (gb <= 220 * 1024 &&
                 cudaFuncSetAttribute(g0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb) == cudaSuccess &&
-                cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb) == cudaSuccess) {
+                cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb) == cudaSuccess &&
+                cudaFuncSetAttribute(mf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gps0, g0, 32 * IR_W, gb);
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gps1, g1, 32 * IR_W, gb);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mps, mf, 32 * IR_W, bytes);
             }
-            if (bps >= 1 && gps0 >= 1 && gps1 >= 1) {
+            if (bps >= 1 && gps0 >= 1 && gps1 >= 1 && mps >= 1) {
+                c->msmall_fn = mf;
                 c->sm_inner = true;
                 c->inner_fn = kfn;
                 c->inner_bytes = bytes;

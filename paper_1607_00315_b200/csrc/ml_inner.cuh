@@ -119,7 +119,7 @@ struct SProducer {
     __device__ bool next(const Seg& S, const double* coef, SChunk& d) {
         while (p < p1) {
             int b, e;
-            if (p - p0 < IR_QC) { const int2 x = ext[p - p0]; b = x.x; e = x.y; }
+            if (ext && p - p0 < IR_QC) { const int2 x = ext[p - p0]; b = x.x; e = x.y; }
             else { const int j = __ldg(S.list + p); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
             const int start = b + noff;
             if ((coef && noff == 0 && coef[p - p0] == 0.0) || start >= e) { ++p; noff = 0; continue; }
@@ -916,5 +916,172 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         }
         ctl->F_before = ctl->F;
         if (vmax / P.lam <= P.tol) { ctl->skip = 1; ctl->outcome = OUT_CONVERGED; ctl->level_conv = 1; }
+    }
+}
+
+// ------------------------------------------------------------------ A1 for small m: margins from the support's columns
+// z = X_S w_S (S = supp(w)) by the same block-cooperative column scatter as k_inner's S phase, instead of streaming all
+// of X by rows: (1) the support list in column order from the support bitmap (block counts -> barrier -> in-order
+// write), barrier; (2) my support columns (TMA ring, one shared m-vector) -> block partial, barrier; (3) my rows:
+// z_i = sum of the block partials in block order, t, ell, r, D; L = sum ell, F = L + lam ||w||_1.
+template <int GSCH>
+__global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* slist, long long* acc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ double sh_w[IR_W * 4 + 8];
+    __shared__ double sh_t[2];
+    __shared__ double gsum[256];
+    __shared__ int sh_cnt[IR_W + 2];
+    constexpr int SST = ir_sst(GSCH);
+    cg::grid_group grid = cg::this_grid();
+    Ctl* c = P.ctl;
+    const int m = P.m, G = gridDim.x;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* part = P.irpart;
+    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes<GSCH>());
+    int* s_idx = reinterpret_cast<int*>(smraw);
+    float* s_val = reinterpret_cast<float*>(smraw + (size_t)4 * SST * IR_SCH);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smraw + (size_t)8 * SST * IR_SCH);
+    SChunk* s_desc = reinterpret_cast<SChunk*>(s_bar + SST);
+    // (1) support list, in column order
+    const int nw = (P.n >> 5) + 1;
+    const int wq = (nw + G - 1) / G;
+    const int w0 = min(nw, (int)blockIdx.x * wq), w1 = min(nw, w0 + wq);
+    int cnt = 0;
+    for (int k = w0 + threadIdx.x; k < w1; k += blockDim.x) cnt += __popc(P.wbits[k]);
+    {
+        const double v[1] = {(double)cnt};
+        ir_block_partials<1>(v, 0u, 0u, sh_w, part, 0);
+    }
+    grid.sync();
+    if (wid == 0) {
+        int off = 0, tot = 0;
+        for (int b0 = 0; b0 < G; b0 += 32) {
+            const int b = b0 + lane;
+            const int x = b < G ? (int)ld_cg(part + b) : 0;
+            off += __reduce_add_sync(0xffffffffu, b < (int)blockIdx.x ? x : 0);
+            tot += __reduce_add_sync(0xffffffffu, x);
+        }
+        if (lane == 0) { sh_cnt[IR_W] = off; sh_cnt[IR_W + 1] = tot; }
+    }
+    __syncthreads();
+    const int nS = sh_cnt[IR_W + 1];
+    {
+        int base = sh_cnt[IR_W];
+        for (int k00 = w0; k00 < w1; k00 += blockDim.x) {
+            const int k = k00 + threadIdx.x;
+            const unsigned bits = k < w1 ? P.wbits[k] : 0u;
+            const int pc = __popc(bits);
+            int incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) sh_cnt[wid] = incl;
+            __syncthreads();
+            int woff = 0, tot = 0;
+            for (int w = 0; w < IR_W; ++w) { if (w < wid) woff += sh_cnt[w]; tot += sh_cnt[w]; }
+            int o = base + woff + incl - pc;
+            for (unsigned b = bits; b; b &= b - 1) slist[o++] = (k << 5) + __ffs(b) - 1;
+            base += tot;
+            __syncthreads();
+        }
+    }
+    fence_proxy_async_global();
+    grid.sync();
+    // (2) my support columns -> one shared m-vector -> my block partial
+    const int q = (nS + G - 1) / G;
+    const int p0 = min(nS, (int)blockIdx.x * q), p1 = min(nS, p0 + q);
+    Seg SS = S;
+    SS.list = slist;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) xs_sh[i] = 0.0;
+    const bool producer = threadIdx.x == blockDim.x - 32;
+    SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), nullptr};
+    if (producer) pr.prefetch(SS, SST, s_desc, s_idx, s_val, s_bar);
+    __syncthreads();
+    long long nsc = 0;
+    uint32_t s_phase = 0u;
+    for (int st = 0;; st = (st + 1) % SST) {
+        const SChunk d = s_desc[st];
+        if (!d.ok) break;
+        mbar_wait(s_bar + st, (s_phase >> st) & 1u);
+        s_phase ^= 1u << st;
+        const double cf = P.w[__ldg(slist + d.p)];
+        const int* ci = s_idx + st * IR_SCH - d.a;
+        const float* cv = s_val + st * IR_SCH - d.a;
+        const int kend = min(d.ve, d.ce);
+        constexpr int UB = IR_SCH / 256;
+        for (int k0 = d.vb + threadIdx.x; k0 < d.ve; k0 += UB * (int)blockDim.x) {   // rows distinct within a column
+            int r[UB];
+            double xv[UB], a[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int k = k0 + u * blockDim.x;
+                r[u] = -1;
+                if (k < kend) { r[u] = ci[k]; xv[u] = (double)cv[k]; }
+                else if (k < d.ve) { r[u] = __ldg(S.idx + k); xv[u] = (double)__ldg(S.val + k); }
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) a[u] = r[u] >= 0 ? xs_sh[r[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < UB; ++u)
+                if (r[u] >= 0) xs_sh[r[u]] = fma(xv[u], cf, a[u]);
+        }
+        if (threadIdx.x == 0) nsc += d.ve - d.vb;
+        __syncthreads();
+        if (producer) {
+            SChunk nd;
+            if (pr.next(SS, nullptr, nd)) { s_desc[st] = nd; pr.issue(SS, nd, st, s_idx, s_val, s_bar); }
+            else s_desc[st].ok = 0;
+        }
+    }
+    __syncthreads();
+    if (producer)
+        for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) P.parts[(size_t)blockIdx.x * m + i] = xs_sh[i];
+    acc_add(acc, nsc, threadIdx.x == 0 ? (long long)(p1 - p0) : 0);
+    grid.sync();
+    // (3) my rows
+    const int R = (m + G - 1) / G;
+    const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
+    const int nr = r1 - r0;
+    double lsum = 0.0;
+    if (nr > 0) {
+        const int ng = max(1, (int)blockDim.x / nr);
+        const int g = threadIdx.x / nr, rr = threadIdx.x % nr;
+        double t = 0.0;
+        if (g < ng) {
+            const double* src = P.parts + r0 + rr;
+            for (int b0 = g; b0 < G; b0 += 8 * ng) {
+                double x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int b = b0 + u * ng;
+                    x[u] = b < G ? ld_cg(src + (size_t)b * m) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t += x[u];
+            }
+            gsum[threadIdx.x] = t;
+        }
+        __syncthreads();
+        for (int rr2 = threadIdx.x; rr2 < nr; rr2 += blockDim.x) {
+            double z = 0.0;
+            for (int g2 = 0; g2 < ng; ++g2) z += gsum[g2 * nr + rr2];
+            const int i = r0 + rr2;
+            const RowState st = row_state(z, (double)P.y[i]);
+            P.z[i] = z;
+            P.rD[i] = make_double2(st.r, st.D);
+            lsum += st.ell;
+        }
+    }
+    {
+        const double v[1] = {lsum};
+        ir_block_partials<1>(v, 0u, 0u, sh_w, part, 1);
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {
+        ir_totals(part, 1, 1, 0u, 0u, sh_t);
+        if (threadIdx.x == 0) { c->L = sh_t[0]; c->F = sh_t[0] + P.lam * c->l1; }
     }
 }
