@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
     for (int u = gw; u < nunits; u += nw) {
         const int4 un = U.u[u];
         const int p = un.x;
+        if (SCATTER && coef[p] == 0.0) continue;   // (z pass: most units have a zero coefficient)
         const int j = S.list ? __ldg(S.list + p) : p;
         const int b0 = __ldg(S.ptr + j), e0 = __ldg(S.ptr + j + 1);
         const int b = b0 + un.y * CHUNK;
@@ -277,7 +278,16 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
             const double cf = coef[p];
             if (cf == 0.0) continue;
             if (lane == 0) streamed += e - b;
-            for (int k = b + lane; k < e; k += 32) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
+            int k = b + lane;
+            for (; k + 96 < e; k += 128) {   // loads of 4 elements in flight before their reductions
+                int r[4];
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { r[u] = __ldg(S.idx + k + 32 * u); v[u] = __ldg(S.val + k + 32 * u); }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) atomicAdd(out + r[u], (double)v[u] * cf);
+            }
+            for (; k < e; k += 32) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
         } else {
             if (lane == 0) streamed += e - b;
             double a0 = 0.0, a1 = 0.0;
@@ -1239,23 +1249,26 @@ __global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int mode) {
     const int withz = (mode == 1) && !c->zscatter_skip;
     Red<3> r;
     r.zero();
+    // all loads of a row first (the arrays are distinct; the compiler cannot know), then the stores
     for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
         const double xu = P.Xu[i];
-        P.Xu[i] = 0.0;
-        if (q.on) P.Xd[i] = apply_m(q, P, i);   // uses the previous Xs, Xz
+        const double xzu = withz ? P.Xzu[i] : 0.0;
         const double xs_old = P.Xs[i];
+        const double xz_old = (q.on && q.zsnap) ? P.Xz[i] : 0.0;
+        const double xd_old = q.init ? P.Xd[i] : 0.0;
+        const double D = P.rD[i].y;
+        P.Xu[i] = 0.0;
+        if (q.on) P.Xd[i] = xd_old + q.beta * xs_old + (q.zsnap ? (1.0 - q.beta) * xz_old : 0.0);   // apply_m
         const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
         P.Xs[i] = xs;
-        const double D = P.rD[i].y;
         P.sv[i] = D * xs;
         r.s[0] += D * xs * xs;
         if (withz) {
-            const double xz = P.Xzu[i];
             P.Xzu[i] = 0.0;
-            P.Xz[i] = xz;
-            P.svz[i] = D * xz;
-            r.s[1] += D * xs * xz;
-            r.s[2] += D * xz * xz;
+            P.Xz[i] = xzu;
+            P.svz[i] = D * xzu;
+            r.s[1] += D * xs * xzu;
+            r.s[2] += D * xzu * xzu;
         }
     }
     if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
