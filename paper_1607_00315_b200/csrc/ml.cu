@@ -72,7 +72,8 @@ struct ml_ctx {
     int scat_W = 0, scat_P = 0, gMP = 1;
     size_t scat_bytes = 0;
     bool sm_gather = false;
-    bool sm_inner = false;   // persistent cooperative inner solver (k_inner)
+    bool sm_inner = false;   // persistent cooperative inner solver (k_inner), m-vectors in shared memory
+    bool big_inner = false;  // k_inner<., true>: the same with the m-vectors in global memory (m > SMALL_M)
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // k_inner<1024> or k_inner<512>
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
@@ -123,6 +124,11 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
     int* slist = cv.take<int>(mm <= SMALL_M ? nn + 1 : 1);   // k_margins_small: supp(w) in column order
+    const size_t ucap2 = mm > SMALL_M ? nn + (size_t)nnz / IR_UNIT + 64 : 1;   // k_inner<., true>: column units
+    int2* uext = cv.take<int2>(ucap2);
+    int* upos = cv.take<int>(ucap2);
+    double2* upart = cv.take<double2>(ucap2);
+    int* ustart = cv.take<int>(mm > SMALL_M ? nn + 1 : 1);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -153,6 +159,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
     P.irpart = irpart;
+    P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart;
     c->slist = slist;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
@@ -442,7 +449,7 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
     // A-side grids sized by this level's |C| (>= |A|): fewer idle blocks in the grid reductions at coarse levels
     const int gAl = std::max(1, std::min(c->gA, (nC_host + ML_NT - 1) / ML_NT));
     const int nblkA = gAl;
-    if (c->sm_inner) {   // one persistent cooperative launch for all K inner iterations
+    if (c->sm_inner || c->big_inner) {   // one persistent cooperative launch: K inner iterations, line search, update
         PassScope ps(c, CLS_INNER);
         Prm Pc = c->P;
         ASet A2 = AS;
@@ -628,7 +635,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
         }
         // persistent inner solver: 1024-element G chunks when the two m-vectors leave room, else 512
         const bool big_g = inner_smem_bytes<1024>((int)X->m) <= IR_SMEM_MAX;
-        const void* kfn = big_g ? (const void*)k_inner<1024> : (const void*)k_inner<512>;
+        const void* kfn = big_g ? (const void*)k_inner<1024, false> : (const void*)k_inner<512, false>;
         bytes = big_g ? inner_smem_bytes<1024>((int)X->m) : inner_smem_bytes<512>((int)X->m);
         if (bytes <= IR_SMEM_MAX && X->m <= (int64_t)IR_RS * std::min(SM_COUNT, IR_GMAX) &&
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
@@ -659,6 +666,20 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             }
         }
         cudaGetLastError();
+    }
+    if (!c->sm_inner) {   // large m: the persistent solver with global m-vectors
+        const void* kfn = (const void*)k_inner<1024, true>;
+        const size_t b = inner_big_smem_bytes<1024>();
+        int bps = 0;
+        if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) == cudaSuccess)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, b);
+        cudaGetLastError();
+        if (bps >= 1) {
+            c->big_inner = true;
+            c->inner_fn = kfn;
+            c->inner_bytes = b;
+            c->inner_P = std::min(SM_COUNT, IR_GMAX);
+        }
     }
     // zero the control block, trace, bitmap, iterate and the heavy-unit counters
     cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st);

@@ -32,7 +32,8 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 // outer line search + update (R14-R18): 0 g.d, 1 max|d|, 2..5 l1 trials 0..3, 6..9 loss trials 0..3; the rest:
 // 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
 constexpr int IR_NLS = ML_MAXLS - 4;
-enum { IR_SO = 0, IR_SO2 = 10, IR_NSLOT = 10 + 2 * IR_NLS };
+enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 1 };   // IR_SU: unit counts (BIG)
+constexpr int IR_UNIT = 2048;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
 // my positions' state, indexed by p - p0: shared memory when q <= IR_QS, else the ASet arrays (offset by p0)
@@ -50,9 +51,11 @@ __host__ __device__ inline size_t ir_ring_bytes() {
     return ((g > s ? g : s) + 15) / 16 * 16;
 }
 static_assert(sizeof(SChunk) == 24, "SChunk layout");
-// dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z)
+// dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z); BIG: rings only
 template <int GSCH>
 __host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes<GSCH>() + (size_t)16 * m; }
+template <int GSCH>
+__host__ __device__ inline size_t inner_big_smem_bytes() { return ir_ring_bytes<GSCH>(); }
 constexpr size_t IR_SMEM_MAX = 196 * 1024;   // dynamic shared memory budget (the static part is ~30 KB)
 
 // N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
@@ -205,7 +208,10 @@ __device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int 
     c->ntrace += 1;
 }
 
-template <int GSCH>
+// BIG (m > SMALL_M): the m-vectors live in global memory: S scatters with fp64 reductions into Xu (Xzu) through
+// per-warp TMA column rings, R takes my rows of Xu directly (and clears them), G gathers D o Xs (D o Xz) from L2 and
+// applies beta at each column end.  The iteration structure, barriers, decisions and the tail are the same.
+template <int GSCH, bool BIG>
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
     unsigned long long ph_t = gtimer(), ph_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 
     const int q0 = p1 - p0;
     PosState X;
-    if (q0 <= IR_QS) {
+    if (!BIG && q0 <= IR_QS) {
         X = PosState{pos_sh[0], pos_sh[1], pos_sh[2], pos_sh[3], pos_sh[4], pos_sh[5], pos_sh[6]};
         for (int k = threadIdx.x; k < q0; k += blockDim.x) {
             pos_sh[0][k] = AS.wA[p0 + k];
@@ -260,12 +266,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         X = PosState{AS.wA + p0, AS.gA + p0, AS.hA + p0, AS.d + p0, AS.Hd + p0, AS.s + p0, AS.u + p0};
     }
     for (int k = threadIdx.x; k < q0; k += blockDim.x) { X.d[k] = 0.0; X.Hd[k] = 0.0; }
-    double* rD_r = row_sh[0];
-    double* xs_r = row_sh[1];
-    double* xz_r = row_sh[2];
-    double* xd_r = row_sh[3];
+    double* rD_r = row_sh[0];   // (not used when BIG: D from P.rD)
+    double* xs_r = BIG ? P.Xs + r0 : row_sh[1];
+    double* xz_r = BIG ? P.Xz + r0 : row_sh[2];
+    double* xd_r = BIG ? P.Xd + r0 : row_sh[3];
     for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) {
-        rD_r[k] = P.rD[r0 + k].y;
+        if (!BIG) rD_r[k] = P.rD[r0 + k].y;
         xs_r[k] = 0.0;
         xz_r[k] = 0.0;
         xd_r[k] = 0.0;
@@ -285,10 +291,74 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     }
     __syncthreads();
     SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
+    int u0 = 0, u1 = 0;   // BIG: my range of column units (balanced by nonzeros across blocks)
+    if constexpr (BIG) {
+        int nu_loc = 0;
+        for (int k = threadIdx.x; k < q0; k += blockDim.x) {
+            int b, e;
+            if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
+            else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
+            nu_loc += max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
+        }
+        {
+            const double v[1] = {(double)nu_loc};
+            ir_block_partials<1>(v, 0u, 0u, sh_w, part, IR_SU);
+        }
+        grid.sync();
+        __shared__ int s_uoff[2];
+        if (wid == 0) {
+            int off = 0, tot = 0;
+            for (int b0 = 0; b0 < G; b0 += 32) {
+                const int b = b0 + lane;
+                const int x = b < G ? (int)ld_cg(part + (size_t)IR_SU * G + b) : 0;
+                off += __reduce_add_sync(0xffffffffu, b < (int)blockIdx.x ? x : 0);
+                tot += __reduce_add_sync(0xffffffffu, x);
+            }
+            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; }
+        }
+        __syncthreads();
+        int base = s_uoff[0];
+        const int NU = s_uoff[1];
+        for (int k00 = 0; k00 < q0; k00 += blockDim.x) {   // my positions in order: their units
+            const int k = k00 + threadIdx.x;
+            int b = 0, e = 0, nu = 0;
+            if (k < q0) {
+                if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
+                else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
+                nu = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
+            }
+            int incl = nu;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            __shared__ int s_wsum[IR_W];
+            if (lane == 31) s_wsum[wid] = incl;
+            __syncthreads();
+            int woff = 0, wtot = 0;
+            for (int w = 0; w < IR_W; ++w) { if (w < wid) woff += s_wsum[w]; wtot += s_wsum[w]; }
+            if (k < q0) {
+                const int us = base + woff + incl - nu;
+                P.ustart[p0 + k] = us;
+                for (int c2 = 0; c2 < nu; ++c2) {
+                    P.uext[us + c2] = make_int2(b + c2 * IR_UNIT, min(e, b + (c2 + 1) * IR_UNIT));
+                    P.upos[us + c2] = p0 + k;
+                }
+            }
+            base += wtot;
+            __syncthreads();
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) P.ustart[nA] = NU;
+        const int uq = (NU + G - 1) / G;
+        u0 = min(NU, (int)blockIdx.x * uq);
+        u1 = min(NU, u0 + uq);
+        grid.sync();
+    }
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
         const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
-        if (producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
+        if (!BIG && producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
         // ------------------------------------------------ D: direction on my positions
         int my_z = 0;
         {
@@ -333,8 +403,62 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             my_z = pcd && sh_w[IR_W * 12 + 5] > 0.0;
         }
         PH_MARK(0);
+        if (BIG) grid.sync();   // the units of my stream may belong to other blocks' positions
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
-        {
+        if constexpr (BIG) {   // per-warp rings, fp64 reductions into Xu / Xzu (kept zero between uses)
+            const double* coef = pcd ? AS.s : AS.u;
+            if (lane == 0) {
+                for (int k = 0; k < IN_GST; ++k) mbar_init(g_bar + k, 1);
+                fence_mbar_init();
+            }
+            __syncwarp();
+            g_phase = 0u;   // fresh barriers
+            ColStream<GSCH, IN_GST> cs;
+            cs.streamed = 0;
+            cs.segs = 0;
+            stream_begin(cs, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            int stg = 0;
+            while (true) {
+                const ChunkDesc dsc = cs.desc[stg];
+                if (dsc.cf == 0.0) break;
+                mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
+                g_phase ^= 1u << stg;
+                const int pu = __ldg(P.upos + dsc.p);
+                const double cf = ld_cg(coef + pu);
+                if (cf != 0.0) {
+                    const int zf = pcd && P.pcd_snap && ld_cg(AS.u + pu) != 0.0;   // z_p = s_p on a zeroing column
+                    const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                    const float* cv = cs.sval + stg * GSCH - dsc.a;
+                    const int kend = min(dsc.ve, dsc.ce);
+                    int k = dsc.vb + lane;
+                    for (; k < kend; k += 32) {
+                        const int r = ci[k];
+                        const double xv = (double)cv[k] * cf;
+                        red_add_global(P.Xu + r, xv);
+                        if (zf) red_add_global(P.Xzu + r, xv);
+                    }
+                    for (; k < dsc.ve; k += 32) {
+                        const int r = __ldg(S.idx + k);
+                        const double xv = (double)__ldg(S.val + k) * cf;
+                        red_add_global(P.Xu + r, xv);
+                        if (zf) red_add_global(P.Xzu + r, xv);
+                    }
+                }
+                __syncwarp();
+                ChunkDesc nd;
+                const bool ok = cs.next(nd);
+                if (lane == 0) {
+                    if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
+                    else cs.desc[stg].cf = 0.0;
+                }
+                __syncwarp();
+                stg = (stg + 1) % IN_GST;
+            }
+            nsc += cs.streamed;
+            __syncwarp();
+            if (lane == 0)
+                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+        } else {
             const double* coef = pcd ? X.s : X.u;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
                 xs_sh[i] = 0.0;
@@ -416,13 +540,47 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 ss = sh_t[3] + 2.0 * bcg * sh_t[4] + bcg * bcg * sh_t[5];
             }
         }
-        if (stop) break;
+        if (stop) {
+            if (BIG)   // the scatter of this iteration is complete (B1): clear my rows for the next relaxation
+                for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) { P.Xu[r0 + k] = 0.0; P.Xzu[r0 + k] = 0.0; }
+            break;
+        }
         const int dual = pcd && nzero > 0;
         // ------------------------------------------------ R: my rows; PCD-CG: s and the first kink on my positions
         {
             double a_ss = 0.0, a_sz = 0.0, a_zz = 0.0;
             const int nr = r1 - r0;
-            if (nr > 0) {   // thread (group g, row rr) sums blocks g, g + ng, ...; then the groups in order
+            if (BIG) {   // my rows of Xu (Xzu), cleared for the next scatter; sv = D o Xs, svz = D o Xz for the G phase
+                for (int k0 = threadIdx.x; k0 < nr; k0 += 4 * blockDim.x) {
+                    double xu[4], xzu[4], xo[4], dd[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = k0 + u * blockDim.x;
+                        const bool in = k < nr;
+                        xu[u] = in ? ld_cg(P.Xu + r0 + k) : 0.0;
+                        xzu[u] = (in && dual) ? ld_cg(P.Xzu + r0 + k) : 0.0;
+                        xo[u] = (in && !pcd) ? xs_r[k] : 0.0;
+                        dd[u] = in ? P.rD[r0 + k].y : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = k0 + u * blockDim.x;
+                        if (k >= nr) break;
+                        const double xs = pcd ? xu[u] : xu[u] + bcg * xo[u];
+                        P.Xu[r0 + k] = 0.0;
+                        xs_r[k] = xs;
+                        P.sv[r0 + k] = dd[u] * xs;
+                        if (dual) {
+                            P.Xzu[r0 + k] = 0.0;
+                            xz_r[k] = xzu[u];
+                            P.svz[r0 + k] = dd[u] * xzu[u];
+                        }
+                        a_ss += dd[u] * xs * xs;
+                        a_sz += dd[u] * xs * xzu[u];
+                        a_zz += dd[u] * xzu[u] * xzu[u];
+                    }
+                }
+            } else if (nr > 0) {   // thread (group g, row rr) sums blocks g, g + ng, ...; then the groups in order
                 const int ng = max(1, (int)blockDim.x / nr);
                 const int g = threadIdx.x / nr, rr = threadIdx.x % nr;
                 double t = 0.0, tz = 0.0;
@@ -485,7 +643,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             g_phase = 0u;
             csG.streamed = 0;
             csG.segs = 0;
-            stream_begin(csG, S, nullptr, p0, p1, gbase, col_ext, IR_QC);
+            if (BIG) stream_begin(csG, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            else stream_begin(csG, S, nullptr, p0, p1, gbase, col_ext, IR_QC);
         }
         PH_MARK(3);
         grid.sync();   // B2
@@ -557,7 +716,82 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         // R12, m side: Xd += X sigma on my rows (sigma = beta s, or beta s + (1 - beta) z on the snap path)
         for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x)
             xd_r[k] += beta * xs_r[k] + (zs ? (1.0 - beta) * xz_r[k] : 0.0);
-        if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
+        if (BIG && need_hs) {   // G from L2: Hsigma = beta X^T (D o Xs) (+ (1 - beta) X^T (D o Xz)) + eps sigma
+            __syncthreads();
+            PH_MARK(5);
+            ColStream<GSCH, IN_GST>& cs = csG;
+            int stg = 0;
+            double a = 0.0, az = 0.0;
+            while (true) {
+                const ChunkDesc dsc = cs.desc[stg];
+                if (dsc.cf == 0.0) break;
+                mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
+                g_phase ^= 1u << stg;
+                const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                const float* cv = cs.sval + stg * GSCH - dsc.a;
+                const int kend = min(dsc.ve, dsc.ce);
+                int k = dsc.vb + lane;
+                if (zs) {
+                    for (; k < kend; k += 32) {
+                        const int r = ci[k];
+                        const double xv = (double)cv[k];
+                        a = fma(xv, ld_cg(P.sv + r), a);
+                        az = fma(xv, ld_cg(P.svz + r), az);
+                    }
+                } else {
+                    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    for (; k + 96 < kend; k += 128) {
+                        const int q0r = ci[k], q1r = ci[k + 32], q2r = ci[k + 64], q3r = ci[k + 96];
+                        const double s0 = ld_cg(P.sv + q0r), s1 = ld_cg(P.sv + q1r), s2 = ld_cg(P.sv + q2r),
+                                     s3 = ld_cg(P.sv + q3r);
+                        a = fma((double)cv[k], s0, a);
+                        a1 = fma((double)cv[k + 32], s1, a1);
+                        a2 = fma((double)cv[k + 64], s2, a2);
+                        a3 = fma((double)cv[k + 96], s3, a3);
+                    }
+                    a += (a1 + a2) + a3;
+                    for (; k < kend; k += 32) a = fma((double)cv[k], ld_cg(P.sv + ci[k]), a);
+                }
+                for (; k < dsc.ve; k += 32) {
+                    const int r = __ldg(S.idx + k);
+                    const double xv = (double)__ldg(S.val + k);
+                    a = fma(xv, ld_cg(P.sv + r), a);
+                    if (zs) az = fma(xv, ld_cg(P.svz + r), az);
+                }
+                if (dsc.last) {   // unit end: its partial (combined per column after the barrier)
+                    const double t = warp_sum(a), tz = zs ? warp_sum(az) : 0.0;
+                    if (lane == 0) P.upart[dsc.p] = make_double2(t, tz);
+                    a = 0.0;
+                    az = 0.0;
+                }
+                __syncwarp();
+                ChunkDesc nd;
+                const bool ok = cs.next(nd);
+                if (lane == 0) {
+                    if (ok) { cs.desc[stg] = nd; cs.issue(stg, nd); }
+                    else cs.desc[stg].cf = 0.0;
+                }
+                __syncwarp();
+                stg = (stg + 1) % IN_GST;
+            }
+            nhs += cs.streamed;
+            __syncwarp();
+            if (lane == 0)
+                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+            grid.sync();   // every unit's partial
+            for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
+                const int p = p0 + k;
+                const int ua = ld_cg(P.ustart + p), ub = ld_cg(P.ustart + p + 1);
+                double t = 0.0, tz = 0.0;
+                for (int u = ua; u < ub; ++u) { const double2 q2 = ld_cg(P.upart + u); t += q2.x; tz += q2.y; }
+                const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
+                const double x = X.wA[k] + X.d[k];
+                const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
+                X.Hd[k] += beta * t + (zs ? (1.0 - beta) * tz : 0.0) + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
+                X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;
+            }
+            PH_MARK(6);
+        } else if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
             double* sv_sh = xs_sh;
             for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 rows in flight per thread
                 double xs[8], xz[8], dd[8];
