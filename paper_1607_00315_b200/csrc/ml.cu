@@ -129,6 +129,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     int* upos = cv.take<int>(ucap2);
     double2* upart = cv.take<double2>(ucap2);
     int* ustart = cv.take<int>(mm > SMALL_M ? nn + 1 : 1);
+    long long* unz = cv.take<long long>(ucap2 + 1);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
     coarse.A = cv.take<int>(nn); coarse.gA = cv.take<double>(nn); coarse.hA = cv.take<double>(nn); coarse.wA = cv.take<double>(nn);
@@ -159,7 +160,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
     P.irpart = irpart;
-    P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart;
+    P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.unz = unz;
     c->slist = slist;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }

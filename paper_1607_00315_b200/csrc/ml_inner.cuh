@@ -32,7 +32,7 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 // outer line search + update (R14-R18): 0 g.d, 1 max|d|, 2..5 l1 trials 0..3, 6..9 loss trials 0..3; the rest:
 // 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
 constexpr int IR_NLS = ML_MAXLS - 4;
-enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 1 };   // IR_SU: unit counts (BIG)
+enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 };   // IR_SU, +1: unit counts, nnz (BIG)
 constexpr int IR_UNIT = 2048;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
@@ -293,32 +293,38 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
     int u0 = 0, u1 = 0;   // BIG: my range of column units (balanced by nonzeros across blocks)
     if constexpr (BIG) {
-        int nu_loc = 0;
+        int nu_loc = 0, nz_loc = 0;
         for (int k = threadIdx.x; k < q0; k += blockDim.x) {
             int b, e;
             if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
             else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
             nu_loc += max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
+            nz_loc += e - b;
         }
         {
-            const double v[1] = {(double)nu_loc};
-            ir_block_partials<1>(v, 0u, 0u, sh_w, part, IR_SU);
+            const double v[2] = {(double)nu_loc, (double)nz_loc};
+            ir_block_partials<2>(v, 0u, 0u, sh_w, part, IR_SU);
         }
         grid.sync();
-        __shared__ int s_uoff[2];
-        if (wid == 0) {
-            int off = 0, tot = 0;
+        __shared__ long long s_uoff[4];
+        if (wid == 0) {   // my offsets in the unit and nonzero sequences, and their totals
+            long long off = 0, tot = 0, zoff = 0, ztot = 0;
             for (int b0 = 0; b0 < G; b0 += 32) {
                 const int b = b0 + lane;
-                const int x = b < G ? (int)ld_cg(part + (size_t)IR_SU * G + b) : 0;
-                off += __reduce_add_sync(0xffffffffu, b < (int)blockIdx.x ? x : 0);
-                tot += __reduce_add_sync(0xffffffffu, x);
+                const long long x = b < G ? (long long)ld_cg(part + (size_t)IR_SU * G + b) : 0;
+                const long long z = b < G ? (long long)ld_cg(part + (size_t)(IR_SU + 1) * G + b) : 0;
+                off += __reduce_add_sync(0xffffffffu, (unsigned)(b < (int)blockIdx.x ? x : 0));
+                tot += __reduce_add_sync(0xffffffffu, (unsigned)x);
+                zoff += warp_sum_ll(b < (int)blockIdx.x ? z : 0);
+                ztot += warp_sum_ll(z);
             }
-            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; }
+            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; s_uoff[2] = zoff; s_uoff[3] = ztot; }
         }
         __syncthreads();
-        int base = s_uoff[0];
-        const int NU = s_uoff[1];
+        int base = (int)s_uoff[0];
+        long long zbase = s_uoff[2];
+        const int NU = (int)s_uoff[1];
+        const long long NZ = s_uoff[3];
         for (int k00 = 0; k00 < q0; k00 += blockDim.x) {   // my positions in order: their units
             const int k = k00 + threadIdx.x;
             int b = 0, e = 0, nu = 0;
@@ -328,32 +334,55 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 nu = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
             }
             int incl = nu;
+            long long zincl = e - b;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
+                const long long tz = __shfl_up_sync(0xffffffffu, zincl, o);
+                if (lane >= o) { incl += t; zincl += tz; }
             }
             __shared__ int s_wsum[IR_W];
-            if (lane == 31) s_wsum[wid] = incl;
+            __shared__ long long s_zsum[IR_W];
+            if (lane == 31) { s_wsum[wid] = incl; s_zsum[wid] = zincl; }
             __syncthreads();
             int woff = 0, wtot = 0;
-            for (int w = 0; w < IR_W; ++w) { if (w < wid) woff += s_wsum[w]; wtot += s_wsum[w]; }
+            long long zwoff = 0, zwtot = 0;
+            for (int w = 0; w < IR_W; ++w) {
+                if (w < wid) { woff += s_wsum[w]; zwoff += s_zsum[w]; }
+                wtot += s_wsum[w];
+                zwtot += s_zsum[w];
+            }
             if (k < q0) {
                 const int us = base + woff + incl - nu;
+                const long long zs0 = zbase + zwoff + zincl - (e - b);
                 P.ustart[p0 + k] = us;
                 for (int c2 = 0; c2 < nu; ++c2) {
                     P.uext[us + c2] = make_int2(b + c2 * IR_UNIT, min(e, b + (c2 + 1) * IR_UNIT));
                     P.upos[us + c2] = p0 + k;
+                    P.unz[us + c2] = zs0 + (long long)c2 * IR_UNIT;   // nonzeros before this unit
                 }
             }
             base += wtot;
+            zbase += zwtot;
             __syncthreads();
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) P.ustart[nA] = NU;
-        const int uq = (NU + G - 1) / G;
-        u0 = min(NU, (int)blockIdx.x * uq);
-        u1 = min(NU, u0 + uq);
+        if (blockIdx.x == 0 && threadIdx.x == 0) { P.ustart[nA] = NU; P.unz[NU] = NZ; }
         grid.sync();
+        if (threadIdx.x == 0) {   // my units: those starting in my share [b T, (b+1) T) of the nonzeros
+            const long long T = (NZ + G - 1) / G;
+            for (int h = 0; h < 2; ++h) {
+                const long long target = (long long)(blockIdx.x + h) * T;
+                int lo = 0, hi = NU;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ld_cg(P.unz + mid) >= target) hi = mid; else lo = mid + 1;
+                }
+                s_uoff[h] = (blockIdx.x + h == G) ? NU : lo;
+            }
+        }
+        __syncthreads();
+        u0 = (int)s_uoff[0];
+        u1 = (int)s_uoff[1];
     }
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
