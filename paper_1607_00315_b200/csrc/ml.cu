@@ -369,123 +369,59 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
     else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
 }
 
-// X_A coef scatter (A5).  mode 0 (API): the result lands in `out` (atomic path: out zeroed by the caller; small-m
-// path: partials summed by k_parts_sum).  mode 1/2 (relaxation, PCD / PCD-CG): small m -> k_scatter_smem with its
-// fused m-side pass; otherwise atomics into P.Xu followed by k_mpass.
+// X_C coef scatter for the API (A5): the result lands in `out` (atomic path: out zeroed by the caller; small-m path:
+// per-block shared-memory m-vectors, partials summed in block order).
 void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* coef,
-                    double* out, const int* skip, const int* skip2, int mode = 0, const double* coef2 = nullptr) {
+                    double* out) {
     Seg S = seg_cols(c, list);
-    const int* use1 = &c->ctl->pcd_mode;   // relaxation (mode < 0): coef (s) on PCD steps, coef2 (u) on PCD-CG steps
-    if (c->sm_scatter && mode == 0) {   // relaxations on small m run inside k_inner
-        {
-            PassScope ps(c, cls);
-            Prm Pc = c->P;
-            int m = (int)c->X.m;
-            long long* ac = acc_of(c, cls);
-            double* parts = c->parts;
-            void* args[] = {(void*)&S, (void*)&nseg_dev, (void*)&nseg_host, (void*)&coef, (void*)&parts, (void*)&m,
-                            (void*)&skip, (void*)&skip2, (void*)&ac, (void*)&Pc, (void*)&mode, (void*)&out,
-                            (void*)&coef2};
-            cudaLaunchCooperativeKernel((const void*)k_scatter_smem, dim3(c->scat_P), dim3(32 * c->scat_W), args,
-                                        c->scat_bytes, c->st);
-            c->launches++;
-        }
-        return;
-    }
-    double* dst = mode ? c->P.Xu : out;
-    const int* u1 = mode ? use1 : nullptr;
-    {
-        PassScope ps(c, cls);
-        ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, dst, skip, skip2,
-                  acc_of(c, cls), coef2, u1);
-        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, dst, skip, skip2,
-                                       acc_of(c, cls), coef2, u1));
-    }
-    if (mode && c->P.pcd_snap && coef2) {   // PCD snap (Q27): X_A z over the zeroing coordinates (z = AS.u = coef2)
-        PassScope ps(c, cls);
-        ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef2,
-                  c->P.Xzu, skip, &c->ctl->zscatter_skip, acc_of(c, cls), (const double*)nullptr, (const int*)nullptr);
-        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef2, c->P.Xzu,
-                                       skip, &c->ctl->zscatter_skip, acc_of(c, cls), (const double*)nullptr,
-                                       (const int*)nullptr));
-    }
-    if (mode) { PassScope ps(c, CLS_MPASS); ML_LAUNCH(c, k_mpass, c->gM, c->P, mode); }
-}
-
-// out = X_C^T v (+ eps s); mode 2: the PCD-CG epilogue and step decision (see k_gather_out / k_gather_smem)
-void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
-                       double* out, const double* s, double eps, const int* skip, const int* skip2, int mode = 1,
-                       const ASet* AS = nullptr) {
     PassScope ps(c, cls);
-    Seg S = seg_cols(c, list);
-    const ASet A0 = AS ? *AS : c->coarse;
-    if (c->sm_gather && mode != 2) {
-        k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out, s,
-                                                                         eps, skip, skip2, acc_of(c, cls), c->P, A0,
-                                                                         mode == 2 ? -1 : mode);
+    if (c->sm_scatter) {
+        Prm Pc = c->P;
+        int m = (int)c->X.m;
+        long long* ac = acc_of(c, cls);
+        double* parts = c->parts;
+        void* args[] = {(void*)&S, (void*)&nseg_dev, (void*)&nseg_host, (void*)&coef, (void*)&parts, (void*)&m,
+                        (void*)&ac, (void*)&Pc, (void*)&out};
+        cudaLaunchCooperativeKernel((const void*)k_scatter_smem, dim3(c->scat_P), dim3(32 * c->scat_W), args,
+                                    c->scat_bytes, c->st);
         c->launches++;
         return;
     }
-    if (mode == 2) {   // relaxation Hs gather; on a PCD snap step also X_A^T (D o Xz) (OpDot2, decided on the device)
-        const OpDot2 op{v, c->P.svz, &c->ctl->pcd_mode, &c->ctl->zsnap, 0};
-        ML_LAUNCH(c, (k_heavy<OpDot2, false>), c->gHeavy, S, units_of(c, slot), op, (const double*)nullptr,
-                  (double*)nullptr, skip, skip2, acc_of(c, cls));
-        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 2, OpDot2>), c->gSeg, S, op, nseg_dev, nseg_host, out,
-                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
+    ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, out,
+              (const int*)nullptr, (const int*)nullptr, acc_of(c, cls));
+    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, out, acc_of(c, cls)));
+}
+
+// out = X_C^T v for the API (mode 0: out0 = g, out1 = h via OpGH is api_gather; here mode 1: dot products)
+void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int* nseg_dev, int nseg_host, const double* v,
+                       double* out) {
+    PassScope ps(c, cls);
+    Seg S = seg_cols(c, list);
+    if (c->sm_gather) {
+        k_gather_smem<<<c->gath_P, 32 * c->gath_W, c->gath_bytes, c->st>>>(S, nseg_dev, nseg_host, v, (int)c->X.m, out,
+                                                                         acc_of(c, cls));
+        c->launches++;
         return;
     }
     ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
-              (double*)nullptr, skip, skip2, acc_of(c, cls));
-    {
-        ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
-                                       (double*)nullptr, s, eps, skip, skip2, acc_of(c, cls), c->P, A0));
-    }
+              (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, cls));
+    ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
+                                   (double*)nullptr, acc_of(c, cls)));
 }
 
-// R3-R18 on the free set in AS (its gather already ran): K inner iterations, outer line search, update.
-// Per inner iteration: direction kernel (applies the previous step), scatter X_A s (+ m-side pass and, for PCD, the
-// step decision), Hs gather (+ for PCD-CG the step decision).  Steps are applied lazily (see decide_pcd).
-void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg, int nC_host) {
-    Ctl* ctl = c->ctl;
-    // A-side grids sized by this level's |C| (>= |A|): fewer idle blocks in the grid reductions at coarse levels
-    const int gAl = std::max(1, std::min(c->gA, (nC_host + ML_NT - 1) / ML_NT));
-    const int nblkA = gAl;
-    if (c->sm_inner || c->big_inner) {   // one persistent cooperative launch: K inner iterations, line search, update
-        PassScope ps(c, CLS_INNER);
-        Prm Pc = c->P;
-        ASet A2 = AS;
-        Seg S = seg_cols(c, AS.A);
-        int Kk = K, icg = inner_cg;
-        long long* a1 = acc_of(c, CLS_SCATTER);
-        long long* a2 = acc_of(c, CLS_HS);
-        void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
-        cudaLaunchCooperativeKernel(c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
-        c->launches++;
-        return;   // k_inner also runs the outer line search and the update (R14-R18) and writes the trace row
-    } else
-    for (int it = 0; it < K; ++it) {
-        {
-            // inner_cg 0 / 1: the iteration type is known here (PCD at it = 0 / always); inner_cg = 2 decides on
-            // the device after a kink, so both kernels are launched and one returns immediately
-            PassScope ps(c, CLS_DIR);
-            const bool may_pcd = !inner_cg || it == 0 || inner_cg == 2;
-            const bool may_cg = inner_cg && it > 0;
-            if (may_pcd) ML_LAUNCH(c, k_dir_pcd, gAl, c->P, AS, it);
-            if (may_cg) ML_LAUNCH(c, k_dir_cg, gAl, c->P, AS, it);
-        }
-        launch_scatter(c, CLS_SCATTER, AS.A, 2, &ctl->nA, 0, AS.s, nullptr, &ctl->skip, &ctl->inner_stop, -1, AS.u);
-        if (it < K - 1)
-            launch_gather_dot(c, CLS_HS, AS.A, 2, &ctl->nA, 0, c->P.sv, AS.Hs, AS.s, c->P.eps_h, &ctl->skip,
-                              &ctl->inner_stop, 2, &AS);
-        else if (inner_cg) { PassScope ps(c, CLS_DIR); ML_LAUNCH(c, k_cg_finish, gAl, c->P, AS); }
-    }
-    {
-        PassScope ps(c, CLS_OUTER);
-        ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
-        ML_LAUNCH(c, k_outer_ls<ML_MAXLS - 4>, nblkA + c->gM, c->P, AS, 4, nblkA);
-    }
-    { PassScope ps(c, CLS_UPDATE); ML_LAUNCH(c, k_update, nblkA + c->gM, c->P, AS, nblkA); }
-    { PassScope ps(c, CLS_BOOK); ML_LAUNCH(c, k_relax_end, 1, c->P); }
+// R3-R18 on the free set in AS (its gather already ran): one cooperative launch of the persistent inner solver runs
+// the K inner iterations, the outer line search and the update, and writes the relaxation's trace row.
+void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
+    PassScope ps(c, CLS_INNER);
+    Prm Pc = c->P;
+    ASet A2 = AS;
+    Seg S = seg_cols(c, AS.A);
+    int Kk = K, icg = inner_cg;
+    long long* a1 = acc_of(c, CLS_SCATTER);
+    long long* a2 = acc_of(c, CLS_HS);
+    void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
+    cudaLaunchCooperativeKernel(c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
+    c->launches++;
 }
 
 void set_params(ml_ctx* c, const ml_solve_opts* o) {
@@ -763,8 +699,7 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
               (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_API));
     const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,
-                                   g_C, h_C, (const double*)nullptr, 0.0, (const int*)nullptr, (const int*)nullptr,
-                                   acc_of(c, CLS_API), c->P, c->coarse));
+                                   g_C, h_C, acc_of(c, CLS_API)));
 }
 
 ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host, double* g_C, double* h_C) {
@@ -794,9 +729,9 @@ ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C,
         launch_units_build(c, 1, C, (int)nC);
     }
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
-    launch_scatter(c, CLS_API, C, slot, nullptr, (int)nC, v_C, c->P.Xs, nullptr, nullptr);   // X_C v
+    launch_scatter(c, CLS_API, C, slot, nullptr, (int)nC, v_C, c->P.Xs);   // X_C v
     ML_LAUNCH(c, k_dmul, c->gM, c->P, (int)c->X.m);                                   // D o X_C v
-    launch_gather_dot(c, CLS_API, C, slot, nullptr, (int)nC, c->P.sv, Hv_C, nullptr, 0.0, nullptr, nullptr, 0);
+    launch_gather_dot(c, CLS_API, C, slot, nullptr, (int)nC, c->P.sv, Hv_C);
     cudaMemsetAsync(c->P.Xs, 0, sizeof(double) * c->X.m, c->st);
     return cuda_fail(c, "ml_hessvec");
 }
@@ -819,7 +754,7 @@ ml_status ml_shrink_linesearch(ml_ctx* c, const int32_t* C, int64_t nC, const do
             launch_units_build(c, 1, C, n);
         }
         cudaMemsetAsync(c->P.Xd, 0, sizeof(double) * c->X.m, c->st);
-        launch_scatter(c, CLS_API, C, slot, nullptr, n, AS.d, c->P.Xd, nullptr, nullptr);
+        launch_scatter(c, CLS_API, C, slot, nullptr, n, AS.d, c->P.Xd);
     }
     const int nblkA = c->gA;
     ML_LAUNCH(c, k_outer_ls<4>, nblkA + c->gM, c->P, AS, 0, nblkA);
@@ -878,11 +813,11 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
         launch_margins(c);
         launch_gather_free(c, nullptr, n, c->fine, true);
         if (relax) {
-            launch_relax_body(c, c->fine, o.K_fine, o.inner_cg, n);
+            launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             for (int it = 1; it < o.nu; ++it) {
                 ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1, 1);
                 launch_gather_free(c, nullptr, n, c->fine, true);
-                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg, n);
+                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             }
         }
     };
@@ -915,7 +850,7 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
                         for (int r = 0; r < reps; ++r) {
                             ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1, 0);
                             launch_gather_free(c, Cl, nCl, c->coarse, false);
-                            launch_relax_body(c, c->coarse, K, o.inner_cg, nCl);
+                            launch_relax_body(c, c->coarse, K, o.inner_cg);
                         }
                     }
                 }

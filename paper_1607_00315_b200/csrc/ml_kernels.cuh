@@ -96,19 +96,6 @@ struct OpDot {        // acc = sum_i X_ij v_i
     __device__ __forceinline__ void prepare() {}
     __device__ __forceinline__ void add(double& a0, double&, int r, float x) const { a0 += (double)x * __ldg(v + r); }
 };
-struct OpDot2 {       // acc0 = sum_i X_ij v_i, acc1 = sum_i X_ij v2_i when dual (PCD snap step)
-    const double* v;
-    const double* v2;
-    const int* flag_pcd;
-    const int* flag_zsnap;
-    int dual;
-    __device__ __forceinline__ void prepare() { dual = (flag_pcd && flag_zsnap) ? (*flag_pcd && *flag_zsnap) : 0; }
-    __device__ __forceinline__ void add(double& a0, double& a1, int r, float x) const {
-        a0 += (double)x * __ldg(v + r);
-        if (dual) a1 += (double)x * __ldg(v2 + r);
-    }
-};
-
 // Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).  Each lane streams U 16-byte vectors of
 // indices and U of values per iteration (all loads issued before use), peeling the unaligned ends.
 template <int G, int U = 2, class Op>
@@ -206,35 +193,6 @@ __device__ __forceinline__ double block_sum_any(double v) {
     __syncthreads();
     return t;
 }
-__device__ __forceinline__ double block_min_any(double v) {
-    __shared__ double sh[32];
-    v = warp_min(v);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double t = sh[0];
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) t = fmin(t, sh[k]);
-    __syncthreads();
-    return t;
-}
-// Grid-wide min through per-block partials and the last-arriving block (any blockDim); true in the last block.
-__device__ bool grid_min_any(double& v, double* part, unsigned* ctr) {
-    __shared__ bool s_last;
-    const double b = block_min_any(v);
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = b;
-        __threadfence();
-        s_last = (atomicAdd(ctr, 1u) == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return false;
-    __threadfence();
-    double t = __longlong_as_double(0x7ff0000000000000LL);
-    for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) t = fmin(t, ld_cg(part + k));
-    v = block_min_any(t);
-    if (threadIdx.x == 0) *ctr = 0u;
-    return true;
-}
-
 // ------------------------------------------------------------------ heavy units
 // Build the heavy-unit schedule of a segment list: every segment longer than SPLIT gets ceil(len/CHUNK) units.
 // Unit order is arbitrary (atomics); results do not depend on it.
@@ -257,10 +215,8 @@ __global__ void k_units_build(const int* __restrict__ ptr, const int* __restrict
 // combination by the segment's last-arriving warp into S.hres[p].
 template <class Op, bool SCATTER>
 __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const double* coef, double* out,
-                                                  const int* skip, const int* skip2, long long* nnz_acc,
-                                                  const double* coef2 = nullptr, const int* use_coef1 = nullptr) {
+                                                  const int* skip, const int* skip2, long long* nnz_acc) {
     if ((skip && *skip) || (skip2 && *skip2)) return;
-    if (coef2 && use_coef1 && !*use_coef1) coef = coef2;
     op.prepare();
     const int lane = threadIdx.x & 31;
     const int nunits = min(*U.n, U.cap);
@@ -336,98 +292,6 @@ struct Prm {
 // free-set buffers of one relaxation (fine or coarse set)
 struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd; double* s; double* Hs; double* u; };
 
-
-// ------------------------------------------------------------------ inner-step decisions and deferred application
-// The inner step s accepted in iteration `it` (length beta, optional kink snap) is applied lazily: to d and Hd by the
-// next direction kernel (or the outer line search), to Xd by the next m-side pass (or the outer line search).
-// R6-R10, PCD: Armijo on the model over beta = 1, 1/2, ... with delta the model's linear part at beta = 1.
-// With pcd_snap (DESIGN Q27) and zeroing coordinates z (x != 0, x + s = 0), the snap path sigma(b) = b (s - z) + z is
-// tried first; its model change in closed form: q = b (ps - pz) + pz + 1/2 (b^2 snHsn + 2 b snHz + zHz)
-// + lam (l1diff_b - (1 - b) Z1); otherwise the plain path b s.  sHs, zHs, zHz include the eps_h ridge.
-__device__ __forceinline__ void decide_pcd(const Prm& P, Ctl* c, double sHs, double zHs, double zHz) {
-    c->sHs = sHs;
-    const double delta = c->ps + P.lam * c->l1diff_out[0];
-    double b = 1.0;
-    int ok = 0, snapped = 0;
-    if (c->nzero > 0) {
-        const double snHsn = sHs - 2.0 * zHs + zHz, snHz = zHs - zHz;
-        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
-            const double dq = b * (c->ps - c->pz) + c->pz + 0.5 * (b * b * snHsn + 2.0 * b * snHz + zHz) +
-                              P.lam * (c->l1diff_out[t] - (1.0 - b) * c->Z1);
-            if (dq <= P.sigma_in * b * delta) { ok = 1; snapped = 1; break; }
-        }
-    }
-    if (!ok) {
-        b = 1.0;
-        for (int t = 0; t < P.max_ls; ++t, b *= P.beta_ls) {
-            const double dq = b * c->ps + 0.5 * b * b * sHs + P.lam * c->l1diff_out[t];
-            if (dq <= P.sigma_in * b * delta) { ok = 1; break; }
-        }
-    }
-    c->cg_restart = 1;
-    c->next_pcd = (P.inner_cg == 0);
-    if (!ok) { c->inner_stop = 1; c->beta = 0.0; return; }
-    c->beta = b;
-    c->snap = 0;
-    c->zsnap = snapped;
-    c->hs_beta = 1.0;   // the Hs gather of a PCD iteration returns H sigma (the step), not H s
-    c->pend = 1;
-    c->pend_m = 1;
-    c->acc_steps += 1;
-}
-// R6', PCD-CG: exact step on the quadratic piece, truncated at the first kink (b_k), kink coordinates snapped to 0.
-__device__ __forceinline__ void decide_cg(const Prm& P, Ctl* c, double bk) {
-    c->bk = bk;
-    const double sHs = c->sHs;
-    if (!(c->slope < 0.0) || !(sHs > 0.0)) { c->inner_stop = 1; c->beta = 0.0; return; }
-    const double bq = -c->slope / sHs;
-    c->bq = bq;
-    c->beta = bq < bk ? bq : bk;
-    c->snap = (bk <= bq);
-    c->zsnap = 0;
-    c->hs_beta = c->beta;
-    c->cg_restart = c->snap;
-    c->next_pcd = (P.inner_cg == 2) && c->snap;   // inner_cg = 2: a shrinkage step after every kink (DESIGN Q9b)
-    c->rz_prev = c->rz;
-    c->pend = 1;
-    c->pend_m = 1;
-    c->acc_steps += 1;
-}
-struct Pending {   // a snapshot of the pending step, read once per kernel
-    int on, init, snap, zsnap;
-    double beta, bk, hs_beta;
-};
-__device__ __forceinline__ Pending pending_A(const Ctl* c) {
-    return Pending{c->pend, c->d_init, c->snap, c->zsnap, c->beta, c->bk, c->hs_beta};
-}
-__device__ __forceinline__ Pending pending_m(const Ctl* c) {
-    return Pending{c->pend_m, c->xd_init, 0, c->zsnap, c->beta, 0.0, 0.0};
-}
-// d (and Hd when Hs is valid) after the pending step at position p; writes them back.  A CG step snaps its first-kink
-// coordinates to 0; a PCD snap step (Q27) snaps its zeroing coordinates (z = AS.u != 0) to 0.
-__device__ __forceinline__ double apply_A(const Pending& q, const ASet& AS, int p, bool with_hd, double* Hd_out) {
-    double d = q.init ? AS.d[p] : 0.0;
-    double hd = (with_hd && q.init) ? AS.Hd[p] : 0.0;
-    if (q.on) {
-        const double sp = AS.s[p];
-        const double x = AS.wA[p] + d;
-        const bool kink = q.snap && x * sp < 0.0 && -x / sp == q.bk;
-        const bool zero = q.zsnap && AS.u[p] != 0.0;
-        d = (kink || zero) ? -AS.wA[p] : d + q.beta * sp;   // a snapped coordinate becomes exactly 0
-        AS.d[p] = d;
-        if (with_hd) { hd += q.hs_beta * AS.Hs[p]; AS.Hd[p] = hd; }
-    }
-    if (Hd_out) *Hd_out = hd;
-    return d;
-}
-// Xd after the pending step: CG / PCD plain: + beta Xs; PCD snap: + beta Xs + (1 - beta) Xz
-__device__ __forceinline__ double apply_m(const Pending& q, const Prm& P, int i) {
-    double xd = q.init ? P.Xd[i] : 0.0;
-    if (q.on) xd += q.beta * P.Xs[i] + (q.zsnap ? (1.0 - q.beta) * P.Xz[i] : 0.0);
-    return xd;
-}
-__device__ __forceinline__ void consume_A(Ctl* c) { if (c->pend) { c->pend = 0; c->d_init = 1; } }
-__device__ __forceinline__ void consume_m(Ctl* c) { if (c->pend_m) { c->pend_m = 0; c->xd_init = 1; } }
 
 // ------------------------------------------------------------------ A1: margins (full CSR pass)
 // z = Xw (CSR, support-bitmap-gated gathers of w), then per row: t, ell, r, D; L = sum ell.
@@ -609,20 +473,12 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
 //         last block: the CG step decision (R6')
 template <int G, int MODE, class Op>
 __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* nseg_dev, int nseg_host, double* out0,
-                                                      double* out1, const double* s, double eps, const int* skip,
-                                                      const int* skip2, long long* nnz_acc, Prm P, ASet AS) {
+                                                      double* out1, long long* nnz_acc) {
     __shared__ double2 res[TILE];
-    __shared__ double smr[2 * ML_NW + 2];
-    if ((skip && *skip) || (skip2 && *skip2)) return;
     op.prepare();
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int ntiles = (nseg + TILE - 1) / TILE;
     long long streamed = 0, segs = 0;
-    double bcg = 0.0, beta = 0.0;
-    int pcdm = 0, zs = 0;
-    if (MODE == 2) { bcg = P.ctl->bcg; pcdm = P.ctl->pcd_mode; beta = P.ctl->beta; zs = P.ctl->zsnap; }
-    Red<0, 0, 1> r;
-    r.zero();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         seg_tile<G>(S, op, nseg, tile, res, streamed, segs);
         __syncthreads();
@@ -630,36 +486,17 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
         if (p < nseg) {
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
-            else if (MODE == 1) out0[p] = q.x + (s ? eps * s[p] : 0.0);
-            else if (pcdm) {   // PCD step (decided before this gather): Hs = H sigma, sigma = b s (+ snapped z)
-                const double zp = zs ? AS.u[p] : 0.0;
-                const double sg = (zp != 0.0) ? zp : beta * s[p];
-                out0[p] = beta * q.x + (zs ? (1.0 - beta) * q.y : 0.0) + eps * sg;
-            }
-            else {
-                const double sp = AS.u[p] + bcg * AS.s[p];
-                AS.s[p] = sp;
-                out0[p] = q.x + eps * sp;
-                const double x = AS.wA[p] + AS.d[p];
-                if (x * sp < 0.0) r.mn[0] = fmin(r.mn[0], -x / sp);
-            }
+            else out0[p] = q.x;
         }
         __syncthreads();
     }
     acc_add(nnz_acc, streamed, segs);
-    if (MODE == 2 && !pcdm) {
-        if (grid_reduce(r, P.part, &P.ctl->red_ctr[3], smr))
-            if (threadIdx.x == 0) decide_cg(P, P.ctl, r.mn[0]);
-    }
 }
 
 // ------------------------------------------------------------------ A5: X_A s scatter (light segments)
 template <int G>
 __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, int nseg_host, const double* coef,
-                                                   double* out, const int* skip, const int* skip2, long long* nnz_acc,
-                                                   const double* coef2, const int* use_coef1) {
-    if ((skip && *skip) || (skip2 && *skip2)) return;
-    if (coef2 && use_coef1 && !*use_coef1) coef = coef2;
+                                                   double* out, long long* nnz_acc) {
     const int nseg = nseg_dev ? *nseg_dev : nseg_host;
     const int grp = (blockIdx.x * ML_NT + threadIdx.x) / G, lane = threadIdx.x % G;
     const int ngrp = gridDim.x * (ML_NT / G);
@@ -826,12 +663,8 @@ __device__ __forceinline__ void stream_setup(ColStream<SCH, NSTG>& cs, unsigned 
 // PCD-CG relaxation step): pending Xd += beta Xs, Xs = Xu (+ b Xs_prev for CG), sv = D o Xs, and s^T H s summed in
 // block order by the last block, which also takes the PCD decision.
 __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const double* coef, double* parts,
-                               int m, const int* skip, const int* skip2, long long* acc, Prm P, int mode, double* out_api,
-                               const double* coef2) {
+                               int m, long long* acc, Prm P, double* out) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    if ((skip && *skip) || (skip2 && *skip2)) return;
-    if (mode < 0) mode = P.ctl->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
-    if (mode == 2 && coef2) coef = coef2;   // PCD-CG scatters u (Xs = Xu + b Xs_prev)
     constexpr int SCH = SC_SCH, NSTG = SC_NSTG;
     const size_t pw = stream_warp_bytes<SCH, NSTG>(m);
     unsigned char* base = smraw + (size_t)(threadIdx.x >> 5) * pw;
@@ -888,7 +721,6 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
     cg::this_grid().sync();
     // block b combines rows [b*R, b*R + R) over all partials: thread t sums the partials k = g, g + ng, ... of row
     // t % R (g = t / R); groups are combined in order -> deterministic
-    Ctl* c = P.ctl;
     const int R = (m + gridDim.x - 1) / gridDim.x;
     const int ng = max(1, (int)blockDim.x / max(R, 1));
     const int row0 = blockIdx.x * R, rr = threadIdx.x % max(R, 1), grp = threadIdx.x / max(R, 1);
@@ -898,58 +730,19 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         for (int k = grp; k < (int)gridDim.x; k += ng) t += ld_cg(parts + (size_t)k * m + row0 + rr);
     red[threadIdx.x] = t;
     __syncthreads();
-    double a2 = 0.0;
-    const Pending q = pending_m(c);
-    const double bcg = (mode == 2) ? c->bcg : 0.0;
     if ((int)threadIdx.x < R && row0 + (int)threadIdx.x < m) {
         double xu = 0.0;
         for (int g = 0; g < ng; ++g) xu += red[g * R + threadIdx.x];
-        const int i = row0 + threadIdx.x;
-        if (mode == 0) out_api[i] = xu;
-        else {
-            const double xs_old = P.Xs[i];
-            if (q.on) P.Xd[i] = apply_m(q, P, i);
-            const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
-            P.Xs[i] = xs;
-            const double D = P.rD[i].y;
-            P.sv[i] = D * xs;
-            a2 = D * xs * xs;
-        }
+        out[row0 + threadIdx.x] = xu;
     }
-    if (mode == 0) return;
-    // grid sum of D Xs^2 through per-block partials and the last block (block order)
-    __shared__ bool s_last;
-    const double bs = block_sum_any(a2);
-    if (threadIdx.x == 0) {
-        parts[(size_t)gridDim.x * m + blockIdx.x] = bs;
-        __threadfence();
-        s_last = (atomicAdd(&c->grp_done, 1u) == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double tt = 0.0;
-    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) tt += ld_cg(parts + (size_t)gridDim.x * m + k);
-    const double tot = block_sum_any(tt);
-    if (threadIdx.x == 0) {
-        consume_m(c);
-        const double sHs = tot + P.eps_h * c->ss;
-        if (mode == 1) { c->nzero = 0; decide_pcd(P, c, sHs, 0.0, 0.0); }
-        else c->sHs = sHs;
-        c->grp_done = 0u;
-    }
+    (void)P;
 }
 
-// Hs_p = sum_i X_ij sv_i + eps s_p over the positions of A, with sv staged once per block in shared memory and the
-// columns streamed through the TMA ring; one warp per column, lane partials reduced at the column's last chunk.
-// mode 0/1: out_p = acc (+ eps s_p); mode 2: PCD-CG epilogue (s_p = u_p + b s_prev_p, Hs_p = acc + eps s_p, first kink)
-// and the CG decision in the last block.
+// out_p = sum_i X_ij v_i over the positions of C (API Hessian-vector product), with v staged once per block in shared
+// memory and the columns streamed through the TMA ring; one warp per column, lane partials reduced at its last chunk.
 __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const double* __restrict__ v, int m, double* out,
-                              const double* s, double eps, const int* skip, const int* skip2, long long* acc, Prm P,
-                              ASet AS, int mode) {
+                              long long* acc) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    if ((skip && *skip) || (skip2 && *skip2)) return;
-    if (mode < 0) mode = P.ctl->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
     constexpr int SCH = GA_SCH, NSTG = GA_NSTG;
     const int W = blockDim.x >> 5;
     double* sv = reinterpret_cast<double*>(smraw + (size_t)W * stream_warp_bytes<SCH, NSTG>(0));
@@ -962,8 +755,6 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
     uint32_t phase = 0u;
     int st = 0;
     double a = 0.0;
-    const double bcg = (mode == 2) ? P.ctl->bcg : 0.0;
-    double bkmin = __longlong_as_double(0x7ff0000000000000LL);
     while (true) {
         const ChunkDesc d = cs.desc[st];
         if (d.cf == 0.0) break;
@@ -985,15 +776,7 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv[__ldg(S.idx + k)], a);
         if (d.last) {
             const double t = warp_sum(a);
-            if (cs.lane == 0) {
-                if (mode == 2) {
-                    const double sp = AS.u[d.p] + bcg * AS.s[d.p];
-                    AS.s[d.p] = sp;
-                    out[d.p] = t + eps * sp;
-                    const double x = AS.wA[d.p] + AS.d[d.p];
-                    if (x * sp < 0.0) bkmin = fmin(bkmin, -x / sp);
-                } else out[d.p] = t + (s ? eps * s[d.p] : 0.0);
-            }
+            if (cs.lane == 0) out[d.p] = t;
             a = 0.0;
         }
         __syncwarp();
@@ -1007,10 +790,6 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         st = (st + 1) % NSTG;
     }
     acc_add(acc, cs.streamed, cs.segs);
-    if (mode == 2) {
-        if (grid_min_any(bkmin, P.part, &P.ctl->red_ctr[3]))
-            if (threadIdx.x == 0) decide_cg(P, P.ctl, bkmin);
-    }
 }
 
 template <int SCH, int NSTG>
@@ -1066,15 +845,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 #include "ml_inner.cuh"
 
-// out[i] = sum_b parts[b][i] (block order)
-__global__ void k_parts_sum(const double* __restrict__ parts, int nparts, int m, double* out) {
-    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
-        double t = 0.0;
-        for (int b = 0; b < nparts; ++b) t += parts[(size_t)b * m + i];
-        out[i] = t;
-    }
-}
-
 // ------------------------------------------------------------------ relaxation bookkeeping
 // Start of RELAX(C): reset per-relaxation flags; first == 1 starts a new level (clears level_conv).
 __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* Cptr, int nC, int set_list, int finest) {
@@ -1107,188 +877,11 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
     (void)finest;
 }
 
-// Inner direction (R5-R7 / R6'), one kernel for both iteration types; the type is chosen on the device (ctl->next_pcd:
-// a PCD step at it = 0, after every kink with inner_cg = 2, and always with inner_cg = 0).  First the pending step of the
-// previous iteration is applied to d and Hd; x = w_A + d, p = g_A + Hd.
-//  PCD (Eq. 5 with D = diag(H) + eps_h): s = Sh_{lam/h}(x - p/h) - x; reduce p^T s, ||s||^2, the l1 trial
-//      differences sum(|x + b_t s| - |x|) for all max_ls trials b_t = beta^t (R10), max|s|.
-//  PCD-CG: u_j = -(p_j + lam sign x_j)/h_j on F = {x != 0}, 0 elsewhere; reduce rz = sum h u^2 and the pieces of the
-//      slope and squared norm of s = u + b s_prev (formed later, in the Hs gather).
-//  Both: the model's min-norm subgradient (forcing, R13).
-__global__ void __launch_bounds__(ML_NT) k_dir_pcd(Prm P, ASet AS, int it) {
-    constexpr int WANT = 1;
-    __shared__ double sm[(ML_MAXLS + 8) * ML_NW + ML_MAXLS + 8];
-    Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop || c->next_pcd != WANT) return;   // the iteration type is chosen on the device
-    const int nA = c->nA;
-    const Pending q = pending_A(c);
-    Red<ML_MAXLS + 6, 2> r;   // ps, ss, l1 trial sums, pz, Z1, zz, #zeroing
-    r.zero();
-    double bt[ML_MAXLS];
-    bt[0] = 1.0;
-#pragma unroll
-    for (int t = 1; t < ML_MAXLS; ++t) bt[t] = bt[t - 1] * P.beta_ls;
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        double Hd;
-        const double d = apply_A(q, AS, p, true, &Hd);
-        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-        const double sp = soft(x - pj / hh, P.lam / hh) - x;
-        AS.s[p] = sp;
-        const double v = (x != 0.0) ? pj + P.lam * sgn(x) : soft(pj, P.lam);
-        const double zp = (P.pcd_snap && x != 0.0 && x + sp == 0.0) ? sp : 0.0;   // zeroing part (Q27)
-        AS.u[p] = zp;
-        r.mx[0] = fmax(r.mx[0], fabs(sp));
-        r.mx[1] = fmax(r.mx[1], fabs(v));
-        r.s[0] += pj * sp;
-        r.s[1] += sp * sp;
-        const double ax = fabs(x);
-#pragma unroll
-        for (int t = 0; t < ML_MAXLS; ++t) r.s[2 + t] += fabs(x + bt[t] * sp) - ax;
-        r.s[ML_MAXLS + 2] += pj * zp;
-        r.s[ML_MAXLS + 3] += fabs(zp);
-        r.s[ML_MAXLS + 4] += zp * zp;
-        r.s[ML_MAXLS + 5] += (zp != 0.0) ? 1.0 : 0.0;
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
-        if (threadIdx.x == 0) {
-            consume_A(c);
-            c->pz = r.s[ML_MAXLS + 2];
-            c->Z1 = r.s[ML_MAXLS + 3];
-            c->zz = r.s[ML_MAXLS + 4];
-            c->nzero = (int)r.s[ML_MAXLS + 5];
-            c->vq = r.mx[1];
-            int stop = (it > 0 && P.eta > 0.0 && r.mx[1] <= P.eta * c->vmax);   // R13 forcing
-            c->ps = r.s[0];
-            c->ss = r.s[1];
-            for (int t = 0; t < ML_MAXLS; ++t) c->l1diff_out[t] = r.s[2 + t];   // inner l1 trial differences
-            if (r.mx[0] == 0.0) stop = 1;                                        // R7
-            c->combine = 0;
-            c->bcg = 0.0;
-            c->inner_stop = stop;
-            c->zscatter_skip = (c->nzero == 0) || stop;   // Xzu must stay zero: no z pass without its m-pass
-            c->pcd_mode = 1;
-            c->it = it;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(ML_NT) k_dir_cg(Prm P, ASet AS, int it) {
-    constexpr int WANT = 0;
-    __shared__ double sm[8 * ML_NW + 8];
-    Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop || c->next_pcd != WANT) return;   // the iteration type is chosen on the device
-    const int nA = c->nA;
-    const Pending q = pending_A(c);
-    Red<6, 1> r;
-    r.zero();
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        double Hd;
-        const double d = apply_A(q, AS, p, true, &Hd);
-        const double x = AS.wA[p] + d, pj = AS.gA[p] + Hd, hh = AS.hA[p];
-        const double gx = (x != 0.0) ? pj + P.lam * sgn(x) : 0.0;   // gradient of the model on the orthant
-        const double u = (x != 0.0) ? -gx / hh : 0.0;
-        AS.u[p] = u;
-        const double sp = AS.s[p];
-        const double v = (x != 0.0) ? gx : soft(pj, P.lam);
-        r.s[0] += hh * u * u;   // rz
-        r.s[1] += gx * u;       // slope part of u
-        r.s[2] += gx * sp;      // slope part of s_prev
-        r.s[3] += u * u;
-        r.s[4] += u * sp;
-        r.s[5] += sp * sp;
-        r.mx[0] = fmax(r.mx[0], fabs(v));
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[1], sm)) {
-        if (threadIdx.x == 0) {
-            consume_A(c);
-            c->vq = r.mx[0];
-            int stop = (it > 0 && P.eta > 0.0 && r.mx[0] <= P.eta * c->vmax);
-            const double rz = r.s[0];
-            if (rz == 0.0) stop = 1;
-            const double b = c->cg_restart ? 0.0 : rz / c->rz_prev;
-            c->bcg = b;
-            c->rz = rz;
-            c->slope = r.s[1] + b * r.s[2];
-            c->ss = r.s[3] + 2.0 * b * r.s[4] + b * b * r.s[5];
-            c->combine = 1;
-            c->inner_stop = stop;
-            c->pcd_mode = 0;
-            c->zscatter_skip = 1;
-            c->it = it;
-        }
-    }
-}
-
-// Last inner iteration of PCD-CG (no Hs needed): s = u + b s_prev, first kink, decision.
-__global__ void __launch_bounds__(ML_NT) k_cg_finish(Prm P, ASet AS) {
-    __shared__ double sm[2 * ML_NW + 2];
-    Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop || c->pcd_mode) return;
-    const int nA = c->nA;
-    const double bcg = c->bcg;
-    Red<0, 0, 1> r;
-    r.zero();
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += gridDim.x * ML_NT) {
-        const double sp = AS.u[p] + bcg * AS.s[p];
-        AS.s[p] = sp;
-        const double x = AS.wA[p] + AS.d[p];
-        if (x * sp < 0.0) r.mn[0] = fmin(r.mn[0], -x / sp);
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[3], sm))
-        if (threadIdx.x == 0) decide_cg(P, c, r.mn[0]);
-}
-
-// m-side pass of the atomic-scatter path: Xu -> (pending Xd += beta Xs) -> Xs = Xu (+ b Xs_prev) -> sv = D o Xs,
-// s^T H s; Xu is cleared for the next scatter; PCD decision (R10).
-__global__ void __launch_bounds__(ML_NT) k_mpass(Prm P, int mode) {
-    __shared__ double sm[4 * ML_NW + 4];
-    Ctl* c = P.ctl;
-    if (c->skip || c->inner_stop) return;
-    if (mode < 0) mode = c->pcd_mode ? 1 : 2;   // relaxation: iteration type chosen on the device
-    const Pending q = pending_m(c);
-    const double bcg = (mode == 2) ? c->bcg : 0.0;
-    const int withz = (mode == 1) && !c->zscatter_skip;
-    Red<3> r;
-    r.zero();
-    // all loads of a row first (the arrays are distinct; the compiler cannot know), then the stores
-    for (int i = blockIdx.x * ML_NT + threadIdx.x; i < P.m; i += gridDim.x * ML_NT) {
-        const double xu = P.Xu[i];
-        const double xzu = withz ? P.Xzu[i] : 0.0;
-        const double xs_old = P.Xs[i];
-        const double xz_old = (q.on && q.zsnap) ? P.Xz[i] : 0.0;
-        const double xd_old = q.init ? P.Xd[i] : 0.0;
-        const double D = P.rD[i].y;
-        P.Xu[i] = 0.0;
-        if (q.on) P.Xd[i] = xd_old + q.beta * xs_old + (q.zsnap ? (1.0 - q.beta) * xz_old : 0.0);   // apply_m
-        const double xs = (mode == 2) ? xu + bcg * xs_old : xu;
-        P.Xs[i] = xs;
-        P.sv[i] = D * xs;
-        r.s[0] += D * xs * xs;
-        if (withz) {
-            P.Xzu[i] = 0.0;
-            P.Xz[i] = xzu;
-            P.svz[i] = D * xzu;
-            r.s[1] += D * xs * xzu;
-            r.s[2] += D * xzu * xzu;
-        }
-    }
-    if (grid_reduce(r, P.part, &c->red_ctr[4], sm)) {
-        if (threadIdx.x == 0) {
-            consume_m(c);
-            const double sHs = r.s[0] + P.eps_h * c->ss;
-            if (mode == 1) {
-                if (!withz) c->nzero = 0;
-                decide_pcd(P, c, sHs, r.s[1] + P.eps_h * c->zz, r.s[2] + P.eps_h * c->zz);
-            } else c->sHs = sHs;
-        }
-    }
-}
-
-// R14-R16: one batch of trials [t0, t0 + NT1) of the outer line search (Eq. 4; Armijo DESIGN Q7, Q26).
-// The first batch first applies the pending inner step (d, Xd).  A-range blocks reduce the l1 trial differences
-// sum(|w + a_t d| - |w|) of the batch (and, in the first batch, g^T d and max|d|); m-range blocks reduce
-// sum_i dloss(t_i, a_t y_i Xd_i).  Last block: Delta, decision.  First batch {1, 1/2, 1/4, 1/8}; the second (rare)
-// covers the remaining trials up to max_ls.
+// R14-R16 for the API (ml_shrink_linesearch; the solver runs them inside k_inner): one batch of trials [t0, t0 + NT1)
+// of the line search on F (Eq. 4; Armijo DESIGN Q7, Q26) for the step d = AS.d with Xd = P.Xd.  A-range
+// blocks reduce the l1 trial differences sum(|w + a_t d| - |w|) of the batch (and, in the first batch, g^T d and
+// max|d|); m-range blocks reduce sum_i dloss(t_i, a_t y_i Xd_i).  Last block: Delta, decision.  First batch
+// {1, 1/2, 1/4, 1/8}; the second (rare) covers the remaining trials up to max_ls.
 template <int NT1>
 __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int nblkA) {
     constexpr int NS = 1 + 2 * NT1;
@@ -1313,9 +906,8 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     }
     if ((int)blockIdx.x < nblkA) {
         const int nA = c->nA;
-        const Pending q = pending_A(c);
         for (int p = blockIdx.x * ML_NT + threadIdx.x; p < nA; p += nblkA * ML_NT) {
-            const double d = (t0 == 0) ? apply_A(q, AS, p, false, nullptr) : AS.d[p];
+            const double d = AS.d[p];
             const double w = AS.wA[p], aw = fabs(w);
             if (t0 == 0) {
                 r.s[0] += AS.gA[p] * d;
@@ -1326,11 +918,8 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
         }
     } else {
         const int nb = gridDim.x - nblkA;
-        const Pending q = pending_m(c);
         for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
-            double xd;
-            if (t0 == 0 && q.on) { xd = apply_m(q, P, i); P.Xd[i] = xd; }
-            else xd = P.Xd[i];
+            const double xd = P.Xd[i];
             const double y = (double)P.y[i];
             const double ti = y * P.z[i], yx = y * xd;
 #pragma unroll
@@ -1341,8 +930,6 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     if (grid_reduce(r, P.part, &c->red_ctr[5], sm)) {
         if (threadIdx.x == 0) {
             if (t0 == 0) {
-                consume_A(c);
-                consume_m(c);
                 c->gd = r.s[0];
                 c->Delta = r.s[0] + P.lam * r.s[1];
                 if (r.mx[0] == 0.0) { c->skip = 1; c->outcome = OUT_NOSTEP; return; }
@@ -1418,17 +1005,6 @@ __global__ void __launch_bounds__(ML_NT) k_update(Prm P, ASet AS, int nblkA) {
             c->ntrace += 1;
         }
     }
-}
-
-// End of a relaxation that did not update (converged / no step / stagnation): trace row.
-__global__ void k_relax_end(Prm P) {
-    Ctl* c = P.ctl;
-    if (c->outcome == OUT_UPDATED || c->skipped) return;
-    if (c->ntrace < c->trace_cap) {
-        TraceRow tr{c->level, c->outcome, c->outcome == OUT_CONVERGED ? 0 : c->acc_steps, c->nA, (long long)c->nC, c->F, c->F, 0.0};
-        P.trace[c->ntrace] = tr;
-    }
-    c->ntrace += 1;
 }
 
 }  // namespace ml
