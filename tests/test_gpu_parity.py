@@ -327,3 +327,19 @@ def test_full_size_solve_kkt_by_oracle(cfg):
     assert np.max(np.abs(g_o[~S])) <= lam * (1 + 1e-6)
     assert np.max(np.abs(g_o[S] + lam * np.sign(w[S]))) <= 1e-6 * lam
     assert abs(F_o - r["F"]) <= 1e-9 * abs(F_o)
+
+
+@pytest.mark.parametrize("name", ["cfg2s", "cfg1", "sparse_edges"])
+def test_small_m_solve_bitwise_reproducible(name):
+    """The small-m persistent path reduces in fixed orders only (slot-major partials, block-ordered row sums,
+    position-ordered compaction): two solves from w = 0 return bitwise identical w and F (DESIGN 8.2, Determinism)."""
+    ds = dataset(name)
+    ctx = ml.Context(ds)
+    r1 = ctx.ml_solve()
+    w1 = ctx.ml_get_w().cpu().numpy().copy()
+    ctx.ml_set_w(torch.zeros(ds.n, dtype=torch.float64, device="cuda"))
+    r2 = ctx.ml_solve()
+    w2 = ctx.ml_get_w().cpu().numpy()
+    assert r1["status"] == 0 and r2["status"] == 0
+    assert r1["F"] == r2["F"] and r1["cycles"] == r2["cycles"]
+    assert np.array_equal(w1, w2)
