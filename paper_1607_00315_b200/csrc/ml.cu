@@ -63,7 +63,6 @@ struct ml_ctx {
     int* lvl;          // level lists
     size_t lvl_cap;
     unsigned char* lev;
-    int* emit_cnt;
     UnitsMem um[4];    // 0: all columns, 1: C list, 2: free set A, 3: rows
     int Gr, Gc;
     int gA, gM, gSeg, gHeavy;
@@ -142,7 +141,6 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     size_t lvl_cap = 2 * nn + 2 * SEL_LMAX + 64;
     int* lvl = cv.take<int>(lvl_cap);
     unsigned char* lev = cv.take<unsigned char>(nn);
-    int* emit_cnt = cv.take<int>((ntile_n + 1) * SEL_LMAX);
     UnitsMem um[4];
     for (int k = 0; k < 4; ++k) {
         um[k].u = cv.take<int4>(ucap);
@@ -153,7 +151,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     }
     if (!c) return;
     c->ctl = ctl; c->sel = sel; c->trace = trace; c->hres = hres;
-    c->lvl = lvl; c->lvl_cap = lvl_cap; c->lev = lev; c->emit_cnt = emit_cnt; c->parts = parts;
+    c->lvl = lvl; c->lvl_cap = lvl_cap; c->lev = lev; c->parts = parts;
     c->fine = fine; c->coarse = coarse;
     for (int k = 0; k < 4; ++k) c->um[k] = um[k];
     Prm& P = c->P;
@@ -452,15 +450,15 @@ void launch_select(ml_ctx* c, SelIn in, int nin_host, int L, const std::vector<i
                    const std::vector<int64_t>& loff) {
     I64x32 T{}, O{};
     for (int l = 0; l < L; ++l) { T.v[l] = targets[l]; O.v[l] = loff[l]; }
-    // targets / offsets travel as kernel arguments (no host->device copies)
-    const int grid = std::max(1, std::min(GRID_CAP, (nin_host + ML_NT - 1) / ML_NT));
+    // targets / offsets travel as kernel arguments (no host->device copies); one cooperative launch, a block per
+    // 256 candidates (at most one per SM)
     PassScope ps(c, CLS_SELECT);
-    ML_LAUNCH(c, k_sel_init_v, 1, c->sel, L, T);
-    for (int d = 0; d < 12; ++d) ML_LAUNCH(c, k_sel_pass, grid, in, c->sel, d);
-    ML_LAUNCH(c, k_sel_mark, grid, in, c->sel);
-    ML_LAUNCH(c, k_emit_count, grid, in, L, c->emit_cnt);
-    ML_LAUNCH(c, k_emit_scan, L, in, L, c->emit_cnt);
-    ML_LAUNCH(c, k_emit_write_v, grid, in, L, c->emit_cnt, out, O);
+    int G = std::max(1, std::min(SM_COUNT, (nin_host + ML_NT - 1) / ML_NT));
+    SelState* stp = c->sel;
+    int Lv = L;
+    void* args[] = {(void*)&in, (void*)&stp, (void*)&Lv, (void*)&T, (void*)&out, (void*)&O};
+    cudaLaunchCooperativeKernel((const void*)k_select_coop, dim3(G), dim3(ML_NT), args, 0, c->st);
+    c->launches++;
 }
 
 }  // namespace

@@ -5,7 +5,7 @@
 // of 8-bit digits, each pass building one 256-bin histogram per level in shared memory (integer atomics only).
 // Because keys are unique, the T_l-th largest key K_l splits the candidates exactly, and K_1 <= K_2 <= ...
 // (T_l non-increasing), so a candidate's level is the number of thresholds it reaches.  The level lists are then
-// emitted in ascending index order by a tile count / scan / write pass.
+// emitted in ascending index order.  One cooperative launch (k_select_coop) does all of it.
 #pragma once
 #include "ml_common.cuh"
 
@@ -14,14 +14,9 @@ namespace ml {
 constexpr int SEL_LMAX = 32;
 struct I64x32 { long long v[SEL_LMAX]; };
 
-struct SelState {
-    unsigned long long pre_hi[SEL_LMAX];
-    unsigned pre_lo[SEL_LMAX];
-    long long rank[SEL_LMAX];   // remaining 1-based rank inside the current prefix group
-    long long target[SEL_LMAX]; // T_l
-    unsigned ghist[SEL_LMAX][256];
-    unsigned done;
-    int L;
+struct SelState {   // global scratch of k_select_coop
+    unsigned ghist3[3][SEL_LMAX][256];   // pass d uses buffer d % 3
+    int ecnt[160][SEL_LMAX];              // per-block level counts (emission)
 };
 
 struct SelIn {
@@ -50,170 +45,150 @@ __device__ __forceinline__ unsigned sel_digit(unsigned long long hi, unsigned lo
     return (lo >> (24 - 8 * (d - 8))) & 255u;
 }
 
-// One digit pass for every level.  Levels whose prefixes coincide share one histogram (rep[l]); counting is
-// warp-aggregated (__match_any_sync) to keep shared-memory atomics off the hot bins.
-__global__ void __launch_bounds__(ML_NT) k_sel_pass(SelIn in, SelState* st, int d) {
+// All of A8 in one cooperative launch (grid <= 160 blocks; block b owns the contiguous candidates [b q, (b+1) q)):
+// the 12 digit passes (block histograms in shared memory -> integer atomics into a triple-buffered global histogram
+// -> one grid barrier -> every block derives the same digits, one warp per level), the level marks, and the in-order
+// emission (per-block level counts -> barrier -> offsets in block order -> block-local ordered writes).  Same keys,
+// digits and order as the k_sel_* / k_emit_* sequence.
+__global__ void __launch_bounds__(ML_NT) k_select_coop(SelIn in, SelState* st, int L, I64x32 T, int* out, I64x32 O) {
     __shared__ unsigned h[SEL_LMAX][256];
     __shared__ unsigned long long s_hi[SEL_LMAX];
     __shared__ unsigned s_lo[SEL_LMAX];
+    __shared__ long long s_rank[SEL_LMAX];
     __shared__ int s_rep[SEL_LMAX];
-    __shared__ bool s_last;
-    const int L = st->L;
-    const int lane = threadIdx.x & 31;
-    for (int k = threadIdx.x; k < L * 256; k += ML_NT) h[k / 256][k % 256] = 0u;
-    if (threadIdx.x < L) {
-        s_hi[threadIdx.x] = st->pre_hi[threadIdx.x];
-        s_lo[threadIdx.x] = st->pre_lo[threadIdx.x];
-    }
-    __syncthreads();
-    if (threadIdx.x < L) {
-        const int l = threadIdx.x;
-        int rep = -1;
-        if (st->target[l] > 0) {
-            rep = l;
-            for (int k = 0; k < l; ++k)
-                if (st->target[k] > 0 && s_hi[k] == s_hi[l] && s_lo[k] == s_lo[l]) { rep = k; break; }
-        }
-        s_rep[l] = rep;
-    }
-    __syncthreads();
+    __shared__ int wc[ML_NW][SEL_LMAX];
+    __shared__ int s_base[SEL_LMAX];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int G = gridDim.x;
     const int n = in.count_dev ? *in.count_dev : in.count_host;
-    const int stride = gridDim.x * ML_NT;
-    for (int base = blockIdx.x * ML_NT + (threadIdx.x & ~31); base < n; base += stride) {
-        const int p = base + lane;
-        unsigned long long hi = 0ull;
-        unsigned lo = 0u;
-        int col = 0;
-        bool cand = false;
-        if (p < n) {
-            sel_key(in, p, hi, lo, col);
-            cand = (in.w[col] == 0.0);   // support members are not candidates
-        }
-        const unsigned dg = sel_digit(hi, lo, d);
-        for (int l = 0; l < L; ++l) {
-            if (s_rep[l] != l) continue;   // inactive or shares a histogram
-            const bool mt = cand && sel_match(hi, lo, d, s_hi[l], s_lo[l]);
-            const unsigned mm = __ballot_sync(0xffffffffu, mt);
-            if (mt) {
-                const unsigned grp = __match_any_sync(mm, dg);
-                if (lane == __ffs(grp) - 1) atomicAdd(&h[l][dg], (unsigned)__popc(grp));
+    const int q = (n + G - 1) / G;
+    const int p0 = min(n, (int)blockIdx.x * q), p1 = min(n, p0 + q);
+    if (threadIdx.x < SEL_LMAX) {
+        s_hi[threadIdx.x] = 0ull;
+        s_lo[threadIdx.x] = 0u;
+        s_rank[threadIdx.x] = threadIdx.x < L ? T.v[threadIdx.x] : 0;
+    }
+    if (blockIdx.x == 0)
+        for (int k = threadIdx.x; k < 2 * SEL_LMAX * 256; k += blockDim.x) (&st->ghist3[0][0][0])[k] = 0u;
+    __syncthreads();
+    grid.sync();
+    for (int d = 0; d < 12; ++d) {
+        unsigned (*gh)[256] = st->ghist3[d % 3];
+        if (blockIdx.x == 0 && d >= 1)   // buffer (d + 1) % 3: pass d - 2's, read by everyone before the last barrier
+            for (int k = threadIdx.x; k < SEL_LMAX * 256; k += blockDim.x) (&st->ghist3[(d + 1) % 3][0][0])[k] = 0u;
+        for (int k = threadIdx.x; k < L * 256; k += ML_NT) h[k / 256][k % 256] = 0u;
+        if (threadIdx.x < L) {   // levels with equal prefixes share one histogram
+            const int l = threadIdx.x;
+            int rep = -1;
+            if (T.v[l] > 0) {
+                rep = l;
+                for (int k = 0; k < l; ++k)
+                    if (T.v[k] > 0 && s_hi[k] == s_hi[l] && s_lo[k] == s_lo[l]) { rep = k; break; }
             }
+            s_rep[l] = rep;
         }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < L * 256; k += ML_NT)
-        if (h[k / 256][k % 256]) atomicAdd(&st->ghist[k / 256][k % 256], h[k / 256][k % 256]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&st->done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x < L && s_rep[threadIdx.x] >= 0) {
-        const int l = threadIdx.x, src = s_rep[l];
-        long long r = st->rank[l];
-        int b = 255;
-        for (; b >= 0; --b) {
-            const long long c = (long long)ld_cg(&st->ghist[src][b]);
-            if (r <= c) break;
-            r -= c;
-        }
-        if (b < 0) b = 0;   // (cannot happen when T_l <= #candidates)
-        if (d < 8) st->pre_hi[l] = (st->pre_hi[l] << 8) | (unsigned long long)b;
-        else st->pre_lo[l] = (st->pre_lo[l] << 8) | (unsigned)b;
-        st->rank[l] = r;
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < L * 256; k += ML_NT) st->ghist[k / 256][k % 256] = 0u;
-    if (threadIdx.x == 0) st->done = 0u;
-}
-
-// level mark: 255 for support members, else the number of thresholds the key reaches (0 = not selected)
-__global__ void __launch_bounds__(ML_NT) k_sel_mark(SelIn in, const SelState* st) {
-    const int n = in.count_dev ? *in.count_dev : in.count_host;
-    const int L = st->L;
-    for (int p = blockIdx.x * ML_NT + threadIdx.x; p < n; p += gridDim.x * ML_NT) {
-        unsigned long long hi;
-        unsigned lo;
-        int col;
-        sel_key(in, p, hi, lo, col);
-        unsigned char lv = 0;
-        if (in.w[col] != 0.0) lv = 255;
-        else
+        __syncthreads();
+        for (int base = p0 + (threadIdx.x & ~31); base < p1; base += ML_NT) {
+            const int p = base + lane;
+            unsigned long long hi = 0ull;
+            unsigned lo = 0u;
+            int col = 0;
+            bool cand = false;
+            if (p < p1) {
+                sel_key(in, p, hi, lo, col);
+                cand = (in.w[col] == 0.0);
+            }
+            const unsigned dg = sel_digit(hi, lo, d);
             for (int l = 0; l < L; ++l) {
-                if (st->target[l] <= 0) break;
-                const unsigned long long th = st->pre_hi[l];
-                const unsigned tl = st->pre_lo[l];
-                if (hi > th || (hi == th && lo >= tl)) lv = (unsigned char)(l + 1);
-                else break;
+                if (s_rep[l] != l) continue;
+                const bool mt = cand && sel_match(hi, lo, d, s_hi[l], s_lo[l]);
+                const unsigned mm = __ballot_sync(0xffffffffu, mt);
+                if (mt) {
+                    const unsigned grp = __match_any_sync(mm, dg);
+                    if (lane == __ffs(grp) - 1) atomicAdd(&h[l][dg], (unsigned)__popc(grp));
+                }
             }
-        in.lev[p] = lv;
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < L * 256; k += ML_NT)
+            if (h[k / 256][k % 256]) atomicAdd(&gh[k / 256][k % 256], h[k / 256][k % 256]);
+        grid.sync();
+        for (int l = wid; l < L; l += ML_NW) {   // the digit of the rank-th largest key (identical in every block)
+            if (s_rep[l] < 0) continue;
+            const int src = s_rep[l];
+            const long long r = s_rank[l];
+            unsigned c[8];
+            long long tot = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { c[k] = ld_cg(&gh[src][255 - (lane * 8 + k)]); tot += c[k]; }
+            long long incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const long long before = incl - tot;
+            int bsel = -1;
+            long long rr = 0;
+            if (before < r && r <= incl) {
+                long long acc = before;
+                for (int k = 0; k < 8; ++k) {
+                    if (r <= acc + (long long)c[k]) { bsel = 255 - (lane * 8 + k); rr = r - acc; break; }
+                    acc += c[k];
+                }
+            }
+            const unsigned who = __ballot_sync(0xffffffffu, bsel >= 0);
+            const int sl = who ? __ffs(who) - 1 : 0;
+            const int b = max(0, __shfl_sync(0xffffffffu, bsel, sl));
+            const long long rn = __shfl_sync(0xffffffffu, rr, sl);
+            __syncwarp();
+            if (lane == 0) {
+                if (d < 8) s_hi[l] = (s_hi[l] << 8) | (unsigned long long)b;
+                else s_lo[l] = (s_lo[l] << 8) | (unsigned)b;
+                s_rank[l] = who ? rn : r;
+            }
+        }
+        __syncthreads();
     }
-}
-
-// emission: tile counts per level
-__global__ void __launch_bounds__(ML_NT) k_emit_count(SelIn in, int L, int* cnt /*[ntiles][L]*/) {
-    __shared__ int wc[ML_NW][SEL_LMAX];
-    const int n = in.count_dev ? *in.count_dev : in.count_host;
-    const int ntiles = (n + ML_NT - 1) / ML_NT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int p = t * ML_NT + threadIdx.x;
-        const int lv = (p < n) ? (int)in.lev[p] : 0;
+    // level marks and per-block level counts
+    for (int k = threadIdx.x; k < SEL_LMAX; k += ML_NT) s_base[k] = 0;
+    __syncthreads();
+    for (int base = p0; base < p1; base += ML_NT) {
+        const int p = base + threadIdx.x;
+        int lv = 0;
+        if (p < p1) {
+            unsigned long long hi;
+            unsigned lo;
+            int col;
+            sel_key(in, p, hi, lo, col);
+            if (in.w[col] != 0.0) lv = 255;
+            else
+                for (int l = 0; l < L; ++l) {
+                    if (T.v[l] <= 0) break;
+                    if (hi > s_hi[l] || (hi == s_hi[l] && lo >= s_lo[l])) lv = l + 1;
+                    else break;
+                }
+            in.lev[p] = (unsigned char)lv;
+        }
         for (int l = 0; l < L; ++l) {
-            const unsigned b = __ballot_sync(0xffffffffu, lv >= l + 1);
-            if (lane == 0) wc[wid][l] = __popc(b);
+            const unsigned b = __ballot_sync(0xffffffffu, p < p1 && lv >= l + 1);
+            if (lane == 0 && b) atomicAdd(&s_base[l], __popc(b));
         }
-        __syncthreads();
-        if (threadIdx.x < L) {
-            int s = 0;
-            for (int k = 0; k < ML_NW; ++k) s += wc[k][threadIdx.x];
-            cnt[(size_t)t * L + threadIdx.x] = s;
-        }
-        __syncthreads();
-    }
-}
-// one block per level: exclusive scan over tiles (in place)
-__global__ void __launch_bounds__(ML_NT) k_emit_scan(SelIn in, int L, int* cnt) {
-    __shared__ int part[ML_NT];
-    const int l = blockIdx.x;
-    const int n = in.count_dev ? *in.count_dev : in.count_host;
-    const int ntiles = (n + ML_NT - 1) / ML_NT;
-    const int per = (ntiles + ML_NT - 1) / ML_NT;
-    const int t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-    int s = 0;
-    for (int t = t0; t < t1; ++t) s += cnt[(size_t)t * L + l];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int a = 0;
-        for (int k = 0; k < ML_NT; ++k) { int v = part[k]; part[k] = a; a += v; }
     }
     __syncthreads();
-    int a = part[threadIdx.x];
-    for (int t = t0; t < t1; ++t) { int v = cnt[(size_t)t * L + l]; cnt[(size_t)t * L + l] = a; a += v; }
-}
-// by-value variants of the selection kernels' small arrays
-__global__ void k_sel_init_v(SelState* st, int L, I64x32 T) {
-    const int l = threadIdx.x;
-    if (l == 0) { st->L = L; st->done = 0u; }
-    if (l < SEL_LMAX) {
-        st->pre_hi[l] = 0ull;
-        st->pre_lo[l] = 0u;
-        st->target[l] = (l < L) ? T.v[l] : 0;
-        st->rank[l] = st->target[l];
+    for (int l = threadIdx.x; l < L; l += ML_NT) st->ecnt[blockIdx.x][l] = s_base[l];
+    grid.sync();
+    for (int l = threadIdx.x; l < L; l += ML_NT) {   // my offset per level: the counts of the blocks before me
+        int o = 0;
+        for (int b = 0; b < (int)blockIdx.x; ++b) o += ld_cg(&st->ecnt[b][l]);
+        s_base[l] = o;
     }
-    for (int k = threadIdx.x; k < SEL_LMAX * 256; k += blockDim.x) st->ghist[k / 256][k % 256] = 0u;
-}
-__global__ void __launch_bounds__(ML_NT) k_emit_write_v(SelIn in, int L, const int* off, int* out, I64x32 O) {
-    __shared__ int wc[ML_NW][SEL_LMAX];
-    const int n = in.count_dev ? *in.count_dev : in.count_host;
-    const int ntiles = (n + ML_NT - 1) / ML_NT;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int p = t * ML_NT + threadIdx.x;
-        const int lv = (p < n) ? (int)in.lev[p] : 0;
-        const int col = (p < n) ? (in.list ? in.list[p] : p) : 0;
+    __syncthreads();
+    for (int base = p0; base < p1; base += ML_NT) {   // in-order writes
+        const int p = base + threadIdx.x;
+        const int lv = (p < p1) ? (int)in.lev[p] : 0;
+        const int col = (p < p1) ? (in.list ? in.list[p] : p) : 0;
         for (int l = 0; l < L; ++l) {
             const unsigned b = __ballot_sync(0xffffffffu, lv >= l + 1);
             if (lane == 0) wc[wid][l] = __popc(b);
@@ -222,11 +197,17 @@ __global__ void __launch_bounds__(ML_NT) k_emit_write_v(SelIn in, int L, const i
         for (int l = 0; l < L; ++l) {
             const unsigned b = __ballot_sync(0xffffffffu, lv >= l + 1);
             if (lv >= l + 1) {
-                int o = off[(size_t)t * L + l];
+                int o = s_base[l];
                 for (int k = 0; k < wid; ++k) o += wc[k][l];
                 o += __popc(b & ((1u << lane) - 1u));
                 out[O.v[l] + o] = col;
             }
+        }
+        __syncthreads();
+        for (int l = threadIdx.x; l < L; l += ML_NT) {
+            int t = 0;
+            for (int k = 0; k < ML_NW; ++k) t += wc[k][l];
+            s_base[l] += t;
         }
         __syncthreads();
     }
