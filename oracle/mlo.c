@@ -56,7 +56,7 @@ double mlo_weight(double t) {                            /* D = tau(t)(1-tau(t))
 void mlo_default_opts(mlo_opts *o) {
     memset(o, 0, sizeof(*o));
     o->tol_kkt = 1e-6; o->max_cycles = 1000; o->nu = 1; o->nu_c = 5;
-    o->K_fine = 2; o->K_mid = 3; o->K_coarse = 10;   /* tuned with this oracle, DESIGN "Defaults" */
+    o->K_fine = 2; o->K_mid = 3; o->K_coarse = 5;    /* tuned with this oracle, DESIGN "Defaults" */
     o->sigma_out = 1e-2; o->sigma_in = 1e-2; o->beta = 0.5; o->max_ls = 40;
     o->eps_h = 1e-12; o->multilevel = 1; o->inner_cg = 2; o->eta = 0.0; o->pcd_snap = 1;
 }

@@ -474,7 +474,7 @@ void ml_default_opts(ml_solve_opts* o) {
     o->nu_c = 5;
     o->K_fine = 2;
     o->K_mid = 3;
-    o->K_coarse = 10;
+    o->K_coarse = 5;
     o->sigma_out = 1e-2;
     o->sigma_in = 1e-2;
     o->beta = 0.5;

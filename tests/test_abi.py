@@ -49,7 +49,7 @@ def test_workspace_and_validation_host_only():
     assert L.ml_create(ctypes.byref(d), 1.0, None, None, 10, ctypes.byref(h)) == ml.ML_E_WORKSPACE
     assert L.ml_status_str(ml.ML_E_STAGNATION) == b"line search stagnation"
     o = ml.default_opts()
-    assert o.tol_kkt == 1e-6 and o.K_fine == 2 and o.K_mid == 3 and o.K_coarse == 10 and o.inner_cg == 2 and o.pcd_snap == 1
+    assert o.tol_kkt == 1e-6 and o.K_fine == 2 and o.K_mid == 3 and o.K_coarse == 5 and o.inner_cg == 2 and o.pcd_snap == 1
 
 
 def test_defaults_match_oracle():
