@@ -74,7 +74,7 @@ struct ml_ctx {
     bool sm_inner = false;   // persistent cooperative inner solver (k_inner), m-vectors in shared memory
     bool big_inner = false;  // k_inner<., true>: the same with the m-vectors in global memory (m > SMALL_M)
     int inner_W = 0, inner_P = 0;
-    const void* inner_fn = nullptr;   // k_inner<1024> or k_inner<512>
+    const void* inner_fn = nullptr;   // the k_inner instantiation in use
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
     size_t gsmall_bytes = 0;
     const void* msmall_fn = nullptr;   // k_margins_small<GSCH>
@@ -570,7 +570,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
         }
         // persistent inner solver: 1024-element G chunks when the two m-vectors leave room, else 512
         const bool big_g = inner_smem_bytes<1024>((int)X->m) <= IR_SMEM_MAX;
-        const void* kfn = big_g ? (const void*)k_inner<1024, false> : (const void*)k_inner<512, false>;
+        const void* kfn = big_g ? (const void*)k_inner<1024, IN_GST, false> : (const void*)k_inner<512, IN_GST, false>;
         bytes = big_g ? inner_smem_bytes<1024>((int)X->m) : inner_smem_bytes<512>((int)X->m);
         if (bytes <= IR_SMEM_MAX && X->m <= (int64_t)IR_RS * std::min(SM_COUNT, IR_GMAX) &&
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
@@ -603,8 +603,9 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
         cudaGetLastError();
     }
     if (!c->sm_inner) {   // large m: the persistent solver with global m-vectors
-        const void* kfn = (const void*)k_inner<1024, true>;
-        const size_t b = inner_big_smem_bytes<1024>();
+        // (measured: <256, 8> and <512, 4> rings were slower on cfg 3-4)
+        const void* kfn = (const void*)k_inner<1024, IN_GST, true>;
+        const size_t b = inner_big_smem_bytes<1024, IN_GST>();
         int bps = 0;
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) == cudaSuccess)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, b);

@@ -34,6 +34,7 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 constexpr int IR_NLS = ML_MAXLS - 4;
 enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 };   // IR_SU, +1: unit counts, nnz (BIG)
 constexpr int IR_UNIT = 2048;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
+constexpr int IR_UCOST = 1024;   // BIG: a unit's fixed cost in nonzeros (TMA issue, barrier wait) for the balance
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
 // my positions' state, indexed by p - p0: shared memory when q <= IR_QS, else the ASet arrays (offset by p0)
@@ -45,17 +46,17 @@ __host__ __device__ constexpr int ir_sst(int gsch) { return gsch >= 1024 ? 8 : 4
 __host__ __device__ inline size_t ir_sring_bytes(int sst) {
     return (size_t)8 * sst * IR_SCH + 8 * sst + sizeof(SChunk) * sst;
 }
-template <int GSCH>
+template <int GSCH, int GST = IN_GST>
 __host__ __device__ inline size_t ir_ring_bytes() {
-    const size_t g = (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0), s = ir_sring_bytes(ir_sst(GSCH));
+    const size_t g = (size_t)IR_W * stream_warp_bytes<GSCH, GST>(0), s = ir_sring_bytes(ir_sst(GSCH));
     return ((g > s ? g : s) + 15) / 16 * 16;
 }
 static_assert(sizeof(SChunk) == 24, "SChunk layout");
 // dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z); BIG: rings only
 template <int GSCH>
 __host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes<GSCH>() + (size_t)16 * m; }
-template <int GSCH>
-__host__ __device__ inline size_t inner_big_smem_bytes() { return ir_ring_bytes<GSCH>(); }
+template <int GSCH, int GST>
+__host__ __device__ inline size_t inner_big_smem_bytes() { return ir_ring_bytes<GSCH, GST>(); }
 constexpr size_t IR_SMEM_MAX = 196 * 1024;   // dynamic shared memory budget (the static part is ~30 KB)
 
 // N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
@@ -211,7 +212,7 @@ __device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int 
 // BIG (m > SMALL_M): the m-vectors live in global memory: S scatters with fp64 reductions into Xu (Xzu) through
 // per-warp TMA column rings, R takes my rows of Xu directly (and clears them), G gathers D o Xs (D o Xz) from L2 and
 // applies beta at each column end.  The iteration structure, barriers, decisions and the tail are the same.
-template <int GSCH, bool BIG>
+template <int GSCH, int GST, bool BIG>
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
     unsigned long long ph_t = gtimer(), ph_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     const int R = (m + G - 1) / G;
     const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
     double* part = P.irpart;
-    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes<GSCH>());   // X_A s of my columns, later sv
+    double* xs_sh = reinterpret_cast<double*>(smraw + ir_ring_bytes<GSCH, GST>());   // X_A s of my columns, later sv
     double* xz_sh = xs_sh + m;                                                 // X_A z of my columns
     double* parts = P.parts;                                              // [G][m] block partials of X_A s
     double* zparts = P.parts + (size_t)G * m;                             // [G][m] block partials of X_A z
@@ -248,8 +249,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smraw + (size_t)8 * SST * IR_SCH);
     SChunk* s_desc = reinterpret_cast<SChunk*>(s_bar + SST);
     // G rings (per warp; alias the S ring, used after it)
-    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<GSCH, IN_GST>(0);
-    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * IN_GST * GSCH);
+    unsigned char* gbase = smraw + (size_t)wid * stream_warp_bytes<GSCH, GST>(0);
+    uint64_t* g_bar = reinterpret_cast<uint64_t*>(gbase + 8 * GST * GSCH);
     uint32_t g_phase = 0u;
     long long nsc = 0, nhs = 0;
 
@@ -298,8 +299,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             int b, e;
             if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
             else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
-            nu_loc += max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
-            nz_loc += e - b;
+            const int nu1 = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
+            nu_loc += nu1;
+            nz_loc += e - b + IR_UCOST * nu1;
         }
         {
             const double v[2] = {(double)nu_loc, (double)nz_loc};
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 nu = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
             }
             int incl = nu;
-            long long zincl = e - b;
+            long long zincl = (long long)(e - b) + (long long)IR_UCOST * nu;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -354,12 +356,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             if (k < q0) {
                 const int us = base + woff + incl - nu;
-                const long long zs0 = zbase + zwoff + zincl - (e - b);
+                const long long zs0 = zbase + zwoff + zincl - ((long long)(e - b) + (long long)IR_UCOST * nu);
                 P.ustart[p0 + k] = us;
                 for (int c2 = 0; c2 < nu; ++c2) {
                     P.uext[us + c2] = make_int2(b + c2 * IR_UNIT, min(e, b + (c2 + 1) * IR_UNIT));
                     P.upos[us + c2] = p0 + k;
-                    P.unz[us + c2] = zs0 + (long long)c2 * IR_UNIT;   // nonzeros before this unit
+                    P.unz[us + c2] = zs0 + (long long)c2 * (IR_UNIT + IR_UCOST);   // weighted cost before this unit
                 }
             }
             base += wtot;
@@ -437,12 +439,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if constexpr (BIG) {   // per-warp rings, fp64 reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
             if (lane == 0) {
-                for (int k = 0; k < IN_GST; ++k) mbar_init(g_bar + k, 1);
+                for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
                 fence_mbar_init();
             }
             __syncwarp();
             g_phase = 0u;   // fresh barriers
-            ColStream<GSCH, IN_GST> cs;
+            ColStream<GSCH, GST> cs;
             cs.streamed = 0;
             cs.segs = 0;
             stream_begin(cs, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
@@ -481,12 +483,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     else cs.desc[stg].cf = 0.0;
                 }
                 __syncwarp();
-                stg = (stg + 1) % IN_GST;
+                stg = (stg + 1) % GST;
             }
             nsc += cs.streamed;
             __syncwarp();
             if (lane == 0)
-                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+                for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
         } else {
             const double* coef = pcd ? X.s : X.u;
             for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -661,11 +663,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             ir_block_partials<4>(v, 0u, 1u << 3, sh_w, part, IR_SR);
         }
         // prefetch the G rings (X_A's columns do not depend on the step) across the barrier
-        ColStream<GSCH, IN_GST> csG;
+        ColStream<GSCH, GST> csG;
         const bool need_hs = it < K - 1;
         if (need_hs) {
             if (lane == 0) {
-                for (int k = 0; k < IN_GST; ++k) mbar_init(g_bar + k, 1);
+                for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
                 fence_mbar_init();
             }
             __syncwarp();
@@ -733,11 +735,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         PH_MARK(4);
         if (stop) {
             if (need_hs) {   // drain the prefetched rings
-                for (int stg2 = 0; stg2 < IN_GST; ++stg2)
+                for (int stg2 = 0; stg2 < GST; ++stg2)
                     if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (g_phase >> stg2) & 1u); g_phase ^= 1u << stg2; }
                 __syncwarp();
                 if (lane == 0)
-                    for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+                    for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
             }
             break;
         }
@@ -748,7 +750,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (BIG && need_hs) {   // G from L2: Hsigma = beta X^T (D o Xs) (+ (1 - beta) X^T (D o Xz)) + eps sigma
             __syncthreads();
             PH_MARK(5);
-            ColStream<GSCH, IN_GST>& cs = csG;
+            ColStream<GSCH, GST>& cs = csG;
             int stg = 0;
             double a = 0.0, az = 0.0;
             while (true) {
@@ -801,12 +803,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     else cs.desc[stg].cf = 0.0;
                 }
                 __syncwarp();
-                stg = (stg + 1) % IN_GST;
+                stg = (stg + 1) % GST;
             }
             nhs += cs.streamed;
             __syncwarp();
             if (lane == 0)
-                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+                for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
             grid.sync();   // every unit's partial
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
                 const int p = p0 + k;
@@ -839,7 +841,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             __syncthreads();
             PH_MARK(5);
-            ColStream<GSCH, IN_GST>& cs = csG;
+            ColStream<GSCH, GST>& cs = csG;
             int stg = 0;
             double a = 0.0;
             while (true) {
@@ -881,12 +883,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     else cs.desc[stg].cf = 0.0;
                 }
                 __syncwarp();
-                stg = (stg + 1) % IN_GST;
+                stg = (stg + 1) % GST;
             }
             nhs += cs.streamed;
             __syncwarp();
             if (lane == 0)
-                for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
+                for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
             PH_MARK(6);
         } else {   // last iteration: d only
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {
