@@ -593,6 +593,7 @@ int mlo_solve(mlo_ctx *c, const mlo_opts *o, mlo_report *rep) {
     int64_t minpm = npos < c->m - npos ? npos : c->m - npos;
     int st = MLO_OK;
     int32_t outcome;
+    const int64_t nnz_touched0 = c->nnz_touched, x_passes0 = c->x_passes;   /* the report counts this solve only */
 
     /* S1-S2: w = 0, z = 0, EVAL_ALL */
     memset(c->w, 0, sizeof(double) * (size_t)n);
@@ -686,8 +687,8 @@ int mlo_solve(mlo_ctx *c, const mlo_opts *o, mlo_report *rep) {
     for (int l = 0; l < 32; ++l) rep->relaxations += rep->relax_per_level[l];
     rep->nnz_w = nnz_w(c);
     if (rep->nnz_w > rep->max_supp) rep->max_supp = rep->nnz_w;
-    rep->nnz_touched = c->nnz_touched;
-    rep->x_passes = c->x_passes;
+    rep->nnz_touched = c->nnz_touched - nnz_touched0;
+    rep->x_passes = c->x_passes - x_passes0;
     if (st == MLO_OK && !converged) st = MLO_E_NOT_CONVERGED;
     rep->status = st;
     free(g); free(h); free(Af); free(gAf); free(R);
