@@ -363,8 +363,8 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
               (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
     const int grid = std::max(1, std::min(GRID_CAP, (nC_host + TILE - 1) / TILE));
-    if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
-    else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, units_of(c, 2), acc_of(c, cls))); }
+    if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, acc_of(c, cls))); }
+    else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, acc_of(c, cls))); }
 }
 
 // X_C coef scatter for the API (A5): the result lands in `out` (atomic path: out zeroed by the caller; small-m path:

@@ -327,20 +327,22 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
 // ------------------------------------------------------------------ A2 + A3: gather over C with free-set compaction
 // For each position p of C (j = C[p], or p when C is all columns): g_j, h_j; v_j (min-norm subgradient,
 // P:248-256); free flag w_j != 0 or |g_j| > lam (P:459-461 via P:790).  Free columns are compacted IN ORDER into
-// the ASet (A, gA, hA + eps_h, wA) with a decoupled look-back scan over dynamically claimed tiles; heavy free
-// columns get their heavy units appended to UA.  FINEST additionally computes ||w||_1 and sum |v| exactly.
+// the ASet (A, gA, hA + eps_h, wA) with a decoupled look-back scan over dynamically claimed groups of SUP tiles
+// (one look-back per group).  FINEST additionally computes ||w||_1 and sum |v| exactly.
 // The last block to finish: nA, vmax, the convergence decision (R2), counters reset, epoch advance.
 template <int G, bool FINEST>
-__global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Units UA, long long* acc) {
+__global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, long long* acc) {
+    constexpr int SUP = 4;   // tiles per claim: one look-back per SUP tiles
     __shared__ double2 res[TILE];
     __shared__ int s_tile, s_excl;
-    __shared__ int s_wcnt[ML_NW];
+    __shared__ int s_wcnt[SUP][ML_NW];
     __shared__ double s_red[2 * ML_NW];
     __shared__ bool s_last;
     Ctl* ctl = P.ctl;
     if (ctl->skip) return;   // (not used at the finest level; coarse relaxations of a converged level)
     const int nC = S.list ? ctl->nC : P.n;
     const int ntiles = (nC + TILE - 1) / TILE;
+    const int nsup = (ntiles + SUP - 1) / SUP;
     const unsigned epoch = ctl->epoch;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     OpGH op{P.rD};
@@ -349,53 +351,61 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&ctl->tile_ctr, 1u);
         __syncthreads();
-        const int tile = s_tile;
-        if (tile >= ntiles) break;
-        seg_tile<G>(S, op, nC, tile, res, streamed, segs);
-        __syncthreads();
-        const int p = tile * TILE + threadIdx.x;
-        int j = 0, flag = 0, len = 0;
-        double g = 0.0, h = 0.0, wj = 0.0, av = 0.0;
-        if (p < nC) {
-            j = S.list ? S.list[p] : p;
-            g = res[threadIdx.x].x;
-            h = res[threadIdx.x].y;
-            if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
-            const double v = (wj != 0.0) ? g + P.lam * sgn(wj) : soft(g, P.lam);
-            av = fabs(v);
-            flag = (wj != 0.0) || (fabs(g) > P.lam);
-            if (flag) len = S.ptr[j + 1] - S.ptr[j];
-        }
-        vmax_loc = fmax(vmax_loc, av);
-        // block-exclusive ranks of the flags
-        const unsigned bal = __ballot_sync(0xffffffffu, flag);
-        const int rank_in_warp = __popc(bal & ((1u << lane) - 1u));
-        if (lane == 0) s_wcnt[wid] = __popc(bal);
+        const int sup = s_tile;
+        if (sup >= nsup) break;
+        int jj[SUP], flag[SUP];
+        double gg[SUP], hh[SUP], ww[SUP];
         double v1p = 0.0, l1p = 0.0;
+#pragma unroll
+        for (int t = 0; t < SUP; ++t) {
+            const int tile = sup * SUP + t;
+            jj[t] = 0; flag[t] = 0; gg[t] = 0.0; hh[t] = 0.0; ww[t] = 0.0;
+            if (tile < ntiles) {   // (uniform over the block)
+                seg_tile<G>(S, op, nC, tile, res, streamed, segs);
+                __syncthreads();
+                const int p = tile * TILE + threadIdx.x;
+                if (p < nC) {
+                    const int j = S.list ? S.list[p] : p;
+                    jj[t] = j;
+                    gg[t] = res[threadIdx.x].x;
+                    hh[t] = res[threadIdx.x].y;
+                    if ((P.wbits[j >> 5] >> (j & 31)) & 1u) ww[t] = P.w[j];
+                    const double v = (ww[t] != 0.0) ? gg[t] + P.lam * sgn(ww[t]) : soft(gg[t], P.lam);
+                    vmax_loc = fmax(vmax_loc, fabs(v));
+                    v1p += fabs(v);
+                    l1p += fabs(ww[t]);
+                    flag[t] = (ww[t] != 0.0) || (fabs(gg[t]) > P.lam);
+                }
+                __syncthreads();
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, flag[t]);
+            if (lane == 0) s_wcnt[t][wid] = __popc(bal);
+        }
         if (FINEST) {
-            v1p = warp_sum(av);
-            l1p = warp_sum(fabs(wj));
+            v1p = warp_sum(v1p);
+            l1p = warp_sum(l1p);
             if (lane == 0) { s_red[wid] = v1p; s_red[ML_NW + wid] = l1p; }
         }
         __syncthreads();
-        int woff = 0, total = 0;
-        for (int k = 0; k < ML_NW; ++k) { if (k < wid) woff += s_wcnt[k]; total += s_wcnt[k]; }
+        int total = 0;
+        for (int t = 0; t < SUP; ++t)
+            for (int k = 0; k < ML_NW; ++k) total += s_wcnt[t][k];
         if (threadIdx.x == 0) {
             if (FINEST) {
                 double a = 0.0, b = 0.0;
                 for (int k = 0; k < ML_NW; ++k) { a += s_red[k]; b += s_red[ML_NW + k]; }
-                P.tilepart[tile] = make_double2(a, b);
+                P.tilepart[sup] = make_double2(a, b);
             }
             // publish and look back (epoch-tagged status words: epoch<<34 | flag<<32 | count)
             const unsigned long long e34 = (unsigned long long)epoch << 34;
             int excl = 0;
-            if (tile == 0) {
+            if (sup == 0) {
                 __threadfence();
                 atomicExch(P.status + 0, e34 | (2ull << 32) | (unsigned)total);
             } else {
                 __threadfence();
-                atomicExch(P.status + tile, e34 | (1ull << 32) | (unsigned)total);
-                int pred = tile - 1;
+                atomicExch(P.status + sup, e34 | (1ull << 32) | (unsigned)total);
+                int pred = sup - 1;
                 while (true) {
                     unsigned long long st = *((volatile unsigned long long*)(P.status + pred));
                     if ((st >> 34) != epoch || ((st >> 32) & 3ull) == 0) continue;
@@ -404,23 +414,25 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
                     --pred;
                 }
                 __threadfence();
-                atomicExch(P.status + tile, e34 | (2ull << 32) | (unsigned)(excl + total));
+                atomicExch(P.status + sup, e34 | (2ull << 32) | (unsigned)(excl + total));
             }
             s_excl = excl;
         }
         __syncthreads();
-        if (flag) {
-            const int o = s_excl + woff + rank_in_warp;
-            AS.A[o] = j;
-            AS.gA[o] = g;
-            AS.hA[o] = h + P.eps_h;
-            AS.wA[o] = wj;
-            if (len > S.split) {   // heavy free column: schedule its units for the Hessian-vector passes over A
-                const int nch = (len + CHUNK - 1) / CHUNK;
-                const int hs = atomicAdd(UA.h, 1);
-                const int base = atomicAdd(UA.n, nch);
-                for (int c = 0; c < nch && base + c < UA.cap; ++c) UA.u[base + c] = make_int4(o, c, hs, base);
+        int base = s_excl;
+#pragma unroll
+        for (int t = 0; t < SUP; ++t) {   // in order: tile t after the tiles before it, warps, lanes
+            int woff = 0, ttot = 0;
+            for (int k = 0; k < ML_NW; ++k) { if (k < wid) woff += s_wcnt[t][k]; ttot += s_wcnt[t][k]; }
+            const unsigned bal = __ballot_sync(0xffffffffu, flag[t]);
+            if (flag[t]) {
+                const int o = base + woff + __popc(bal & ((1u << lane) - 1u));
+                AS.A[o] = jj[t];
+                AS.gA[o] = gg[t];
+                AS.hA[o] = hh[t] + P.eps_h;
+                AS.wA[o] = ww[t];
             }
+            base += ttot;
         }
         __syncthreads();
     }
@@ -443,7 +455,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
     __threadfence();
     if (FINEST) {   // exact sum |v| and ||w||_1 over all columns, in tile order
         double a = 0.0, b = 0.0;
-        for (int t = threadIdx.x; t < ntiles; t += ML_NT) { double2 q = ld_cg(P.tilepart + t); a += q.x; b += q.y; }
+        for (int t = threadIdx.x; t < nsup; t += ML_NT) { double2 q = ld_cg(P.tilepart + t); a += q.x; b += q.y; }
         Red<2> r;
         r.s[0] = a; r.s[1] = b;
         __shared__ double smr[2 * ML_NW + 2];
@@ -451,8 +463,8 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, Un
         if (threadIdx.x == 0) { ctl->v1 = r.s[0]; ctl->l1 = r.s[1]; }
     }
     if (threadIdx.x == 0) {
-        const unsigned long long st = ntiles ? *((volatile unsigned long long*)(P.status + ntiles - 1)) : 0ull;
-        const int nA = ntiles ? (int)(st & 0xffffffffull) : 0;
+        const unsigned long long st = nsup ? *((volatile unsigned long long*)(P.status + nsup - 1)) : 0ull;
+        const int nA = nsup ? (int)(st & 0xffffffffull) : 0;
         ctl->nA = nA;
         const double vmax = __longlong_as_double((long long)ctl->vmax_bits);
         ctl->vmax = vmax;
@@ -871,8 +883,6 @@ __global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* C
     c->nzero = 0;
     c->zscatter_skip = 1;
     c->hs_beta = 0.0;
-    c->units_n[2] = 0;   // A-set units are rebuilt by the gather
-    c->units_h[2] = 0;
     if (set_list) { c->Cptr = Cptr; c->nC = nC; }
     (void)finest;
 }
