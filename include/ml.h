@@ -20,8 +20,8 @@
  *   - ML_E_CUDA: a CUDA runtime error (message in ml_last_error).
  *   - ML_E_STAGNATION: no trial step passed the line search; the iterate is unchanged.
  *   - ML_E_NOT_CONVERGED: ml_solve hit max_cycles; w holds the last evaluated iterate.
- * Determinism: all reductions are fixed-shape trees (no floating-point atomics) except the Hessian-vector scatter
- *   X_A s, which adds with fp64 atomics (results reproducible to rounding, not bitwise).
+ * Determinism: for m <= 8192 every reduction has a fixed order (ml_solve is bitwise reproducible); for larger m the
+ *   Hessian-vector scatter X_A s (and the API's ml_hessvec) add with fp64 atomics: reproducible to rounding only.
  */
 #ifndef ML_H
 #define ML_H
