@@ -21,7 +21,7 @@ using namespace ml;
 
 namespace {
 
-constexpr int SM_COUNT = 148;
+constexpr int SM_COUNT = 148;   // B200; cooperative grids use the device's own count (ml_ctx::sms)
 constexpr int GRID_CAP = SM_COUNT * 4;
 constexpr int TRACE_CAP = 1 << 16;
 constexpr int NV_MAX = 96;   // widest reduction payload (doubles per block)
@@ -75,6 +75,7 @@ struct ml_ctx {
     bool big_inner = false;  // k_inner<., true>: the same with the m-vectors in global memory (m > SMALL_M)
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // the k_inner instantiation in use
+    int sms = SM_COUNT;               // the device's SM count (cooperative grids: one CTA per SM)
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
     size_t gsmall_bytes = 0;
     const void* msmall_fn = nullptr;   // k_margins_small<GSCH>
@@ -453,7 +454,7 @@ void launch_select(ml_ctx* c, SelIn in, int nin_host, int L, const std::vector<i
     // targets / offsets travel as kernel arguments (no host->device copies); one cooperative launch, a block per
     // 256 candidates (at most one per SM)
     PassScope ps(c, CLS_SELECT);
-    int G = std::max(1, std::min(SM_COUNT, (nin_host + ML_NT - 1) / ML_NT));
+    int G = std::max(1, std::min(c->sms, (nin_host + ML_NT - 1) / ML_NT));
     SelState* stp = c->sel;
     int Lv = L;
     void* args[] = {(void*)&in, (void*)&stp, (void*)&Lv, (void*)&T, (void*)&out, (void*)&O};
@@ -523,6 +524,11 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     c->X = *X;
     c->lam = lambda;
     c->st = (cudaStream_t)cuda_stream;
+    {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            c->sms = std::min(sms, SM_COUNT);   // (the partial buffers are sized for at most SM_COUNT blocks)
+    }
     c->ws = (char*)align_up((size_t)ws);
     c->ws_bytes = ws_bytes;
     Carve cv{c->ws};
@@ -553,7 +559,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->sm_scatter = bps >= 1;
             c->scat_W = W;
             c->scat_bytes = bytes;
-            c->scat_P = SM_COUNT * bps;
+            c->scat_P = c->sms * bps;
             c->gMP = std::max(1, std::min(GRID_CAP, (int)((X->m + 15) / 16)));
             c->gMP = std::max(c->gMP, (int)((X->m + ML_NT - 1) / ML_NT));
         }
@@ -566,13 +572,13 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->sm_gather = true;
             c->gath_W = W;
             c->gath_bytes = bytes;
-            c->gath_P = SM_COUNT * bps;
+            c->gath_P = c->sms * bps;
         }
         // persistent inner solver: 1024-element G chunks when the two m-vectors leave room, else 512
         const bool big_g = inner_smem_bytes<1024>((int)X->m) <= IR_SMEM_MAX;
         const void* kfn = big_g ? (const void*)k_inner<1024, IN_GST, false> : (const void*)k_inner<512, IN_GST, false>;
         bytes = big_g ? inner_smem_bytes<1024>((int)X->m) : inner_smem_bytes<512>((int)X->m);
-        if (bytes <= IR_SMEM_MAX && X->m <= (int64_t)IR_RS * std::min(SM_COUNT, IR_GMAX) &&
+        if (bytes <= IR_SMEM_MAX && X->m <= (int64_t)IR_RS * std::min(c->sms, IR_GMAX) &&
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, bytes);
@@ -594,7 +600,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
                 c->sm_inner = true;
                 c->inner_fn = kfn;
                 c->inner_bytes = bytes;
-                c->inner_P = std::min(SM_COUNT, IR_GMAX);
+                c->inner_P = std::min(c->sms, IR_GMAX);
                 c->gsmall_fn[0] = g0;
                 c->gsmall_fn[1] = g1;
                 c->gsmall_bytes = gb;
@@ -614,7 +620,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
             c->big_inner = true;
             c->inner_fn = kfn;
             c->inner_bytes = b;
-            c->inner_P = std::min(SM_COUNT, IR_GMAX);
+            c->inner_P = std::min(c->sms, IR_GMAX);
         }
     }
     // zero the control block, trace, bitmap, iterate and the heavy-unit counters
