@@ -313,8 +313,8 @@ __global__ void k_ls_prep(Prm P, ASet AS, const int* C, int nC, const double* g,
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Ctl* c = P.ctl;
-        c->nA = nC; c->nC = nC; c->skip = 0; c->ls_ok = 0; c->napply = 1; c->outcome = OUT_NOSTEP; c->level = -1;
-        c->acc_steps = 1; c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1;
+        c->nA = nC; c->nC = nC; c->skip = 0; c->ls_ok = 0; c->outcome = OUT_NOSTEP; c->level = -1;
+        c->acc_steps = 1;
         c->F_before = c->F;
     }
 }
@@ -634,7 +634,6 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     init.trace_cap = TRACE_CAP;
     init.L = (double)X->m * std::log(2.0);
     init.F = init.L;
-    init.cg_restart = 1;
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);
@@ -814,13 +813,13 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     }
     auto eval_and_fine_relax = [&](bool relax) {
         // S2/S15 EVAL_ALL (margins from scratch + full gather with the free set), then S4/S17 RELAX(C0, E)
-        ML_LAUNCH(c, k_relax_begin, 1, c->P, 1, 0, (const int*)nullptr, n, 1, 1);
+        ML_LAUNCH(c, k_relax_begin, 1, c->P, 1, 0, (const int*)nullptr, n, 1);
         launch_margins(c);
         launch_gather_free(c, nullptr, n, c->fine, true);
         if (relax) {
             launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             for (int it = 1; it < o.nu; ++it) {
-                ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1, 1);
+                ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1);
                 launch_gather_free(c, nullptr, n, c->fine, true);
                 launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             }
@@ -853,7 +852,7 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
                         const int reps = (l == L) ? o.nu_c : o.nu;
                         const int K = (l == L) ? o.K_coarse : o.K_mid;
                         for (int r = 0; r < reps; ++r) {
-                            ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1, 0);
+                            ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1);
                             launch_gather_free(c, Cl, nCl, c->coarse, false);
                             launch_relax_body(c, c->coarse, K, o.inner_cg);
                         }

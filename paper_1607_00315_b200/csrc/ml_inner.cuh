@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         xd_r[k] = 0.0;
     }
 
-    int next_pcd = c->next_pcd, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;
-    double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = c->rz_prev, slope = 0.0, ss = 0.0, ps = 0.0;
+    int next_pcd = 1, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;   // R6: PCD first
+    double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = 0.0, slope = 0.0, ss = 0.0, ps = 0.0;
     double sHs = 0.0, vq = 0.0;
     const double vmax_C = c->vmax;
     double bt[IR_NT0];
@@ -908,12 +908,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             if (s2) atomicAdd((unsigned long long*)acc_hs, (unsigned long long)s2);
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        c->pend = 0; c->pend_m = 0; c->d_init = 1; c->xd_init = 1; c->snap = 0; c->zsnap = 0;
-        c->cg_restart = cg_restart; c->next_pcd = next_pcd; c->acc_steps = acc_steps; c->inner_stop = stop;
-        c->pcd_mode = pcd; c->beta = beta; c->bk = bk; c->bq = bq; c->bcg = bcg; c->rz = rz;
-        c->rz_prev = rz_prev; c->slope = slope; c->ss = ss; c->ps = ps; c->sHs = sHs; c->vq = vq;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->acc_steps = acc_steps;
+    (void)bq; (void)vq; (void)sHs;
     // ------------------------------------------------ R14-R18: outer line search on F and the update
     PH_MARK(7);
     const double F0 = c->F;

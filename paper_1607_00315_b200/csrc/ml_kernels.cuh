@@ -26,19 +26,10 @@ struct TraceRow { int level, outcome, inner_iters, nA; long long nC; double F_be
 
 struct Ctl {
     // relaxation state
-    int nA, skip, level_conv, inner_stop, outcome, napply, cg_restart, snap;
-    int ls_ok, scattered, nS, nAf;
-    int skipped, t_acc;
-    int nC, pad0;
-    int pend, pend_m, d_init, xd_init, acc_steps, combine, pcd_mode, next_pcd;
-    int zsnap, nzero;             // PCD step on the snap path (Q27); zeroing coordinates in the last PCD direction
-    int zscatter_skip, pad5;      // 1: no X_A z pass this iteration
-    double hs_beta, pz, Z1, zz;   // multiplier of Hs in the pending step; snap-path sums of the PCD direction
-    unsigned grp_ctr[128];
-    unsigned grp_done, pad4;
+    int nA, skip, level_conv, outcome, ls_ok, nS, nAf, skipped, t_acc, nC, acc_steps, level;
     const int* Cptr;            // current restriction list (nullptr = all columns)
     double vmax, v1, l1, L, F, F_before;
-    double beta, alpha, rz, rz_prev, bcg, slope, ss, ps, delta, bk, bq, sHs, Delta, gd, vq;
+    double alpha, Delta, gd;
     double l1diff_out[ML_MAXLS];
     // counters
     unsigned red_ctr[8];
@@ -47,8 +38,7 @@ struct Ctl {
     long long cls[2][16];         // per pass class: [0] nonzeros streamed, [1] segments (rows/columns) visited
     long long dsupp;
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
-    int ntrace, trace_cap, bad_y, level, it;
-    int pad2[3];
+    int ntrace, trace_cap, bad_y, pad2;
     unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics
 };
 
@@ -859,32 +849,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // ------------------------------------------------------------------ relaxation bookkeeping
 // Start of RELAX(C): reset per-relaxation flags; first == 1 starts a new level (clears level_conv).
-__global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* Cptr, int nC, int set_list, int finest) {
+__global__ void k_relax_begin(Prm P, int first_of_level, int level, const int* Cptr, int nC, int set_list) {
     Ctl* c = P.ctl;
     if (first_of_level) c->level_conv = 0;
     c->skip = c->level_conv;
     c->skipped = c->level_conv;
     c->outcome = c->level_conv ? OUT_CONVERGED : OUT_NOSTEP;
-    c->inner_stop = 0;
-    c->napply = 0;
-    c->cg_restart = 1;
-    c->scattered = 0;
     c->ls_ok = 0;
     c->level = level;
-    c->it = 0;
-    c->pend = 0;
-    c->pend_m = 0;
-    c->d_init = 0;
-    c->xd_init = 0;
     c->acc_steps = 0;
-    c->combine = 0;
-    c->next_pcd = 1;
-    c->zsnap = 0;
-    c->nzero = 0;
-    c->zscatter_skip = 1;
-    c->hs_beta = 0.0;
     if (set_list) { c->Cptr = Cptr; c->nC = nC; }
-    (void)finest;
 }
 
 // R14-R16 for the API (ml_shrink_linesearch; the solver runs them inside k_inner): one batch of trials [t0, t0 + NT1)
