@@ -121,15 +121,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nv else "nvidia-smi"}
 
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, backend="nccl"):
+    """One process per GPU (torchrun env); replicas only: the collectives are the timing barrier and reductions."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     return rank, ws, local
 
 
@@ -147,6 +151,13 @@ def allreduce(vals, op, ws, device):
     t = torch.tensor(vals, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return t.tolist()
+
+
+def aggregate(bytes_local, t_ms_local, ws, device):
+    """Whole-job throughput of N replicas: bytes summed over ranks / the slowest rank's time (max over ranks)."""
+    t_max, = allreduce([t_ms_local], "max", ws, device)
+    bytes_all, = allreduce([bytes_local], "sum", ws, device)
+    return bytes_all / (t_max * 1e-3) / 1e9, t_max
 
 
 def parse_opts(text):
@@ -226,9 +237,7 @@ def run_ours(args):
     ok = all(r["status"] == 0 and r["kappa"] <= 1e-6 for r in reps)
     nnz_total = sum(r["nnz_touched"] for r in reps)
     bytes_total = 8.0 * nnz_total
-    t_max, = allreduce([t_ms], "max", ws, device)
-    bytes_all, = allreduce([bytes_total], "sum", ws, device)
-    value = bytes_all / (t_max * 1e-3) / 1e9
+    value, t_max = aggregate(bytes_total, t_ms, ws, device)
 
     # roofline of the dominant pass class, measured in the timed region
     peak, peak_kind = peaks()
