@@ -50,6 +50,8 @@ def dataset(name):
         ds = mlgen.make(3)
     elif name == "cfg4s":
         ds = mlgen.make(4, m=20000, n=40000)
+    elif name == "mid6k":      # 6000 rows: the small-m solver with 512-element column chunks (the 1024 rings do not fit)
+        ds = mlgen.make(3, m=6000, n=12000)
     elif name == "sparse_edges":   # empty rows and columns, ragged
         ds = mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40)
     elif name == "onehot":
@@ -256,14 +258,15 @@ def test_solve_parity_full_configs(name):
 
 @pytest.mark.parametrize("name,opts", [("cfg2s", {"inner_cg": 1, "pcd_snap": 0}), ("cfg1", {"inner_cg": 1, "pcd_snap": 0}),
                                        ("onehot", {"inner_cg": 1, "pcd_snap": 0}), ("cfg2s", {"pcd_snap": 0}),
-                                       ("cfg4s", {"pcd_snap": 0}), ("cfg4s", {}), ("cfg4s", {"inner_cg": 0})])
+                                       ("cfg4s", {"pcd_snap": 0}), ("cfg4s", {}), ("cfg4s", {"inner_cg": 0}),
+                                       ("mid6k", {}), ("mid6k", {"inner_cg": 1, "pcd_snap": 0})])
 def test_solve_parity_inner_variants(name, opts):
     """The other inner solvers (DESIGN Q9b, Q27): plain PCD-CG, PCD-CG with a shrinkage step after every kink without
     the snap path, plain PCD with the snap path; small-m (persistent) and large-m (generic) relaxation paths."""
     test_solve_parity(name, opts)
 
 
-@pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("cfg2s", {"inner_cg": 0}),
+@pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("mid6k", {}), ("cfg2s", {"inner_cg": 0}),
                                        ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0})])
 def test_trace_parity(name, opts):
     """Relaxation by relaxation (Algorithm 1, DESIGN S1-S18/R1-R18): level, |A|, outcome, inner iterations and
@@ -329,7 +332,7 @@ def test_full_size_solve_kkt_by_oracle(cfg):
     assert abs(F_o - r["F"]) <= 1e-9 * abs(F_o)
 
 
-@pytest.mark.parametrize("name", ["cfg2s", "cfg1", "sparse_edges"])
+@pytest.mark.parametrize("name", ["cfg2s", "cfg1", "sparse_edges", "mid6k"])
 def test_small_m_solve_bitwise_reproducible(name):
     """The small-m persistent path reduces in fixed orders only (slot-major partials, block-ordered row sums,
     position-ordered compaction): two solves from w = 0 return bitwise identical w and F (DESIGN 8.2, Determinism)."""
