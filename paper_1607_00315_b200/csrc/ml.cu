@@ -347,7 +347,11 @@ void launch_margins(ml_ctx* c) {
 }
 
 // A2 + A3 over C (list == nullptr: all columns, finest) into the ASet
-void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool finest) {
+// RELAX(C) start + A2/A3 over C.  Small m: one cooperative launch (k_gather_small also does k_relax_begin's work);
+// large m: k_relax_begin, then the segment-engine gather.
+void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* list, int nC_host, ASet& AS) {
+    const bool finest = list == nullptr;
+    if (!c->sm_inner) ML_LAUNCH(c, k_relax_begin, 1, c->P, first_of_level, level, list, nC_host, 1);
     const int cls = finest ? CLS_GATHER_FINE : CLS_GATHER_COARSE;
     PassScope ps(c, cls);
     Seg S = seg_cols(c, list);
@@ -355,7 +359,8 @@ void launch_gather_free(ml_ctx* c, const int* list, int nC_host, ASet& AS, bool 
         Prm Pc = c->P;
         ASet A2 = AS;
         long long* ac = acc_of(c, cls);
-        void* args[] = {(void*)&Pc, (void*)&S, (void*)&A2, (void*)&ac};
+        int fl = first_of_level, lv = level, nl = nC_host;
+        void* args[] = {(void*)&Pc, (void*)&S, (void*)&A2, (void*)&ac, (void*)&fl, (void*)&lv, (void*)&nl};
         cudaLaunchCooperativeKernel(finest ? c->gsmall_fn[1] : c->gsmall_fn[0], dim3(c->inner_P), dim3(32 * IR_W), args,
                                     c->gsmall_bytes, c->st);
         c->launches++;
@@ -813,14 +818,12 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     }
     auto eval_and_fine_relax = [&](bool relax) {
         // S2/S15 EVAL_ALL (margins from scratch + full gather with the free set), then S4/S17 RELAX(C0, E)
-        ML_LAUNCH(c, k_relax_begin, 1, c->P, 1, 0, (const int*)nullptr, n, 1);
         launch_margins(c);
-        launch_gather_free(c, nullptr, n, c->fine, true);
+        launch_relax_start(c, 1, 0, nullptr, n, c->fine);
         if (relax) {
             launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             for (int it = 1; it < o.nu; ++it) {
-                ML_LAUNCH(c, k_relax_begin, 1, c->P, 0, 0, (const int*)nullptr, n, 1);
-                launch_gather_free(c, nullptr, n, c->fine, true);
+                launch_relax_start(c, 0, 0, nullptr, n, c->fine);
                 launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
             }
         }
@@ -852,8 +855,7 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
                         const int reps = (l == L) ? o.nu_c : o.nu;
                         const int K = (l == L) ? o.K_coarse : o.K_mid;
                         for (int r = 0; r < reps; ++r) {
-                            ML_LAUNCH(c, k_relax_begin, 1, c->P, r == 0 ? 1 : 0, l, Cl, nCl, 1);
-                            launch_gather_free(c, Cl, nCl, c->coarse, false);
+                            launch_relax_start(c, r == 0 ? 1 : 0, l, Cl, nCl, c->coarse);
                             launch_relax_body(c, c->coarse, K, o.inner_cg);
                         }
                     }

@@ -1018,17 +1018,31 @@ __host__ __device__ inline size_t gather_small_smem_bytes(int m) {
     return (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0) + (size_t)16 * m;
 }
 template <int GSCH, bool FINEST>
-__global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, long long* acc) {
+// It also starts the relaxation (what k_relax_begin does on the large-m path): a relaxation of a level that already
+// converged is skipped; block 0 resets the per-relaxation flags.
+__global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, long long* acc, int first_of_level,
+                                                         int level, int nC_list) {
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ double sh_w[2 * 256 + 8];
     __shared__ double sh_t[4];
     __shared__ int sh_cnt[IR_W + 1];
     cg::grid_group grid = cg::this_grid();
     Ctl* ctl = P.ctl;
-    if (ctl->skip) return;   // grid-uniform (coarse relaxations of a converged level)
+    const int conv = first_of_level ? 0 : ctl->level_conv;   // (only written at the end of this kernel, by block 0)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (first_of_level) ctl->level_conv = 0;
+        ctl->skip = conv;
+        ctl->skipped = conv;
+        ctl->outcome = conv ? OUT_CONVERGED : OUT_NOSTEP;
+        ctl->ls_ok = 0;
+        ctl->level = level;
+        ctl->acc_steps = 0;
+        if (S.list) { ctl->Cptr = S.list; ctl->nC = nC_list; }
+    }
+    if (conv) return;   // grid-uniform (coarse relaxations of a converged level)
     const int m = P.m, G = gridDim.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nC = S.list ? ctl->nC : P.n;
+    const int nC = S.list ? nC_list : P.n;
     const int q = (nC + G - 1) / G;
     const int p0 = min(nC, (int)blockIdx.x * q), p1 = min(nC, p0 + q);
     double2* rd_sh = reinterpret_cast<double2*>(smraw + (size_t)IR_W * stream_warp_bytes<GSCH, IN_GST>(0));
