@@ -16,7 +16,8 @@
  *   - Index lists C are int32, strictly ascending, in [0, n).  C == NULL with nC == n means all columns.
  * Errors
  *   - Every call returns ml_status; nothing throws or exits across the ABI; ml_last_error gives detail.
- *   - ML_E_INVAL: m, n < 1, nnz >= 2^31, lambda <= 0 or non-finite, y not in {-1,+1}, bad C, too small workspace.
+ *   - ML_E_INVAL: m, n < 1, nnz >= 2^31, lambda <= 0 or non-finite, y not in {-1,+1}, bad C, too small workspace,
+ *     malformed X (pointers not from 0 to nnz, indices out of range or not strictly ascending inside a row/column).
  *   - ML_E_CUDA: a CUDA runtime error (message in ml_last_error).
  *   - ML_E_STAGNATION: no trial step passed the line search; the iterate is unchanged.
  *   - ML_E_NOT_CONVERGED: ml_solve hit max_cycles; w holds the last evaluated iterate.

@@ -261,6 +261,22 @@ __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* 
     pos = (unsigned long long)warp_sum_ll((long long)pos);
     if ((threadIdx.x & 31) == 0 && pos) atomicAdd(npos, pos);
 }
+// X's index structure: pointers non-decreasing with ptr[0] = 0, ptr[len] = nnz; indices in [0, bound) and strictly
+// ascending inside every segment (the column passes rely on distinct rows within a column); flags ctl->bad_y |= 2
+__global__ void k_check_index(const int* ptr, const int* idx, int len, int bound, long long nnz, Ctl* ctl) {
+    int bad = 0;
+    for (int s = blockIdx.x * ML_NT + threadIdx.x; s < len; s += gridDim.x * ML_NT) {
+        const int b = ptr[s], e = ptr[s + 1];
+        if (b > e || (s == 0 && b != 0) || (s == len - 1 && (long long)e != nnz)) { bad = 1; continue; }
+        int prev = -1;
+        for (int k = b; k < e; ++k) {
+            const int r = idx[k];
+            bad |= (r <= prev) || (r >= bound);
+            prev = r;
+        }
+    }
+    if (bad) atomicOr(&ctl->bad_y, 2);
+}
 // support bitmap, |supp| and ||w||_1 from w (deterministic: per-block partials + last block)
 __global__ void __launch_bounds__(ML_NT) k_w_stats(Prm P, int n) {
     __shared__ double sm[3 * ML_NW + 3];
@@ -642,6 +658,8 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);
+    ML_LAUNCH(c, k_check_index, c->gSeg, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
+    ML_LAUNCH(c, k_check_index, c->gM, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
@@ -652,7 +670,12 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     }
     ml_status s = sync_ctl(c);
     if (s != ML_OK) { *out = c; return s; }
-    if (c->h.bad_y) { delete c; return ML_E_INVAL; }
+    if (c->h.bad_y) {   // bit 0: labels not +-1; bit 1: malformed CSR / CSC index structure
+        c->err = (c->h.bad_y & 2) ? "X: pointers or indices malformed (indices must be in range and strictly ascending per segment)"
+                                  : "y: labels must be -1 or +1";
+        delete c;
+        return ML_E_INVAL;
+    }
     c->npos = (long long)c->h.dsupp;
     long long zero = 0;
     cudaMemcpyAsync(&c->ctl->dsupp, &zero, sizeof(long long), cudaMemcpyHostToDevice, c->st);

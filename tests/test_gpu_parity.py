@@ -346,3 +346,19 @@ def test_small_m_solve_bitwise_reproducible(name):
     assert r1["status"] == 0 and r2["status"] == 0
     assert r1["F"] == r2["F"] and r1["cycles"] == r2["cycles"]
     assert np.array_equal(w1, w2)
+
+
+def test_create_rejects_malformed_index():
+    """ABI error behaviour (include/ml.h): unsorted rows inside a CSC column and out-of-range CSR columns are rejected
+    by ml_create with ML_E_INVAL (the column passes rely on distinct rows within a column)."""
+    import dataclasses
+    good = mlgen.from_dense(np.eye(4, 3, dtype=np.float32) + 1.0, np.array([1, -1, 1, -1], np.int8), 0.1)
+    ml.Context(good)   # well formed: accepted
+    row = good.csc_row.copy()
+    row[0], row[1] = row[1], row[0]   # column 0's rows out of order
+    col = good.csr_col.copy()
+    col[-1] = good.n                  # a CSR column index out of range
+    for bad in (dataclasses.replace(good, csc_row=row), dataclasses.replace(good, csr_col=col)):
+        with pytest.raises(ml.MLError) as e:
+            ml.Context(bad)
+        assert "status 1" in str(e.value), str(e.value)
