@@ -264,15 +264,18 @@ __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* 
 // X's index structure: pointers non-decreasing with ptr[0] = 0, ptr[len] = nnz; indices in [0, bound) and strictly
 // ascending inside every segment (the column passes rely on distinct rows within a column); flags ctl->bad_y |= 2
 __global__ void k_check_index(const int* ptr, const int* idx, int len, int bound, long long nnz, Ctl* ctl) {
+    // one warp per segment, lanes over adjacent pairs (coalesced)
+    const int lane = threadIdx.x & 31;
     int bad = 0;
-    for (int s = blockIdx.x * ML_NT + threadIdx.x; s < len; s += gridDim.x * ML_NT) {
+    for (int s = (blockIdx.x * ML_NT + threadIdx.x) >> 5; s < len; s += (gridDim.x * ML_NT) >> 5) {
         const int b = ptr[s], e = ptr[s + 1];
-        if (b > e || (s == 0 && b != 0) || (s == len - 1 && (long long)e != nnz)) { bad = 1; continue; }
-        int prev = -1;
-        for (int k = b; k < e; ++k) {
+        if (b > e || b < 0 || (long long)e > nnz || (s == 0 && b != 0) || (s == len - 1 && (long long)e != nnz)) {
+            bad = 1;
+            continue;
+        }
+        for (int k = b + lane; k < e; k += 32) {
             const int r = idx[k];
-            bad |= (r <= prev) || (r >= bound);
-            prev = r;
+            bad |= (r < 0) || (r >= bound) || (k + 1 < e && idx[k + 1] <= r);
         }
     }
     if (bad) atomicOr(&ctl->bad_y, 2);
@@ -658,8 +661,8 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);
-    ML_LAUNCH(c, k_check_index, c->gSeg, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
-    ML_LAUNCH(c, k_check_index, c->gM, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
+    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
+    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
