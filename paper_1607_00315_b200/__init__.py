@@ -82,7 +82,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or _SO
+    p = path or os.environ.get("ML_LIB") or _SO   # ML_LIB: an alternative build of the same library (tools)
     if not os.path.exists(p):
         raise OSError(f"libml.so not built ({p}); run paper_1607_00315_b200.build()")
     L = ctypes.CDLL(p)

@@ -23,7 +23,32 @@ constexpr int IR_W = 8;          // warps per block (launch with 256 threads)
 constexpr int IR_GMAX = 160;     // grid <= 160 blocks (5 partials per lane in the totals)
 constexpr int IR_NT0 = 4;        // l1 trial differences computed with the direction; the rest only if Armijo needs them
 constexpr int IR_SCH = 2048;               // S phase: block-shared ring of IR_SCH-element chunks, sst(GSCH) stages
-constexpr int IR_QC = 1024;                // column extents of up to IR_QC own positions cached in shared memory
+#ifndef IR_RL
+#define IR_RL 12   // R phase: partial loads in flight per thread (m = 2000, G = 148: one round)
+#endif
+constexpr int IR_QC = 1024;               // column extents of up to IR_QC own positions cached in shared memory
+// phase timers (block 0, thread 0): 8 phases for small |A| and 8 for large |A|.  Debug builds: IR_PHDBG puts
+// sub-phases of the small-|A| iteration in slots 8..15 (large |A| relaxations are then not timed) and the kernel time
+// and iterations run in the trace rows (F_before, alpha); GS_PHDBG puts k_gather_small's phases in slots 8..15
+#if defined(IR_PHDBG) || defined(GS_PHDBG)
+constexpr int IR_PHN = 32;
+#else
+constexpr int IR_PHN = 16;
+#endif
+#ifdef IR_PHDBG
+#define PH_SUB(k) PH_MARK(8 + (k))
+#define IR_FB(x) ((double)(gtimer() - ph_k0))
+#define IR_AL(x) ((double)ph_its)
+#else
+#define PH_SUB(k) do {} while (0)
+#define IR_FB(x) (x)
+#define IR_AL(x) (x)
+#endif
+#ifdef GS_PHDBG
+#define GS_MARK(k) PH_MARK(8 + (k))
+#else
+#define GS_MARK(k) do {} while (0)
+#endif
 constexpr int IN_GST = 2;                  // G phase: per-warp rings of GSCH-element chunks (template)
 // partial slots: D (PCD) 0 ps, 1 ss, 2 pz, 3 Z1, 4 zz, 5 #zeroing, 6..9 l1 trials 0..3, 10 max|s|, 11 vq
 //                D (CG)  0 rz, 1 gx.u, 2 gx.s_prev, 3 u.u, 4 u.s_prev, 5 s_prev.s_prev, 11 vq
@@ -59,58 +84,104 @@ template <int GSCH, int GST>
 __host__ __device__ inline size_t inner_big_smem_bytes() { return ir_ring_bytes<GSCH, GST>(); }
 constexpr size_t IR_SMEM_MAX = 196 * 1024;   // dynamic shared memory budget (the static part is ~30 KB)
 
+// The transposed warp butterfly: NP (a power of 2, <= 32) values per lane are reduced across the warp with
+// NP - 1 + (5 - log2 NP) shuffles instead of 5 NP (the shuffle pipe, not latency, bounds the plain form).  At each
+// offset a lane keeps one half of its slots and sends the other half to its partner, so every slot is combined in
+// the same tree as warp_sum / warp_max: the results are bitwise those of the per-slot butterflies.  On return a[0]
+// holds slot (lane >> (5 - log2 NP)).
+template <int NP>
+__device__ __forceinline__ void warp_reduce_slots(double (&a)[NP], unsigned maxmask, unsigned minmask) {
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int o = 16 >> s;
+        const int c = NP >> s;   // slots still held (compile time after unrolling)
+        if (c >= 2) {
+            const int h = c >> 1;
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const double send = up ? a[i] : a[i + h];
+                const double keep = up ? a[i + h] : a[i];
+                const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+                const int slot = base + (up ? h : 0) + i;
+                a[i] = ((maxmask >> slot) & 1u) ? fmax(keep, recv) : ((minmask >> slot) & 1u) ? fmin(keep, recv) : keep + recv;
+            }
+            if (up) base += h;
+        } else {
+            const double recv = __shfl_xor_sync(0xffffffffu, a[0], o);
+            a[0] = ((maxmask >> base) & 1u) ? fmax(a[0], recv) : ((minmask >> base) & 1u) ? fmin(a[0], recv) : a[0] + recv;
+        }
+    }
+}
+template <int N> struct SlotPad { static constexpr int NP = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+                                  static constexpr int SH = NP == 1 ? 5 : NP == 2 ? 4 : NP == 4 ? 3 : NP == 8 ? 2 : NP == 16 ? 1 : 0; };
+
 // N values per thread -> per-block totals in part[(slot0 + k) * G + block] (sum, or max / min per mask bit); the
-// block's own totals stay in sh_w[IR_W * N + k]
+// block's own totals stay in sh_w[IR_W * N + k].  Launch with IR_W warps.
 template <int N>
 __device__ __forceinline__ void ir_block_partials(const double (&v)[N], unsigned maxmask, unsigned minmask,
                                                   double* sh_w, double* part, int slot0) {
-    const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if constexpr (N <= 32) {
+        constexpr int NP = SlotPad<N>::NP, SH = SlotPad<N>::SH;
+        double a[NP];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const double t = ((maxmask >> k) & 1u) ? warp_max(v[k]) : ((minmask >> k) & 1u) ? warp_min(v[k]) : warp_sum(v[k]);
-        if (lane == 0) sh_w[wid * N + k] = t;
+        for (int k = 0; k < NP; ++k) a[k] = k < N ? v[k] : 0.0;
+        warp_reduce_slots<NP>(a, maxmask, minmask);
+        const int slot = lane >> SH;
+        if ((lane & ((1 << SH) - 1)) == 0 && slot < N) sh_w[wid * N + slot] = a[0];
+    } else {   // (cold paths: the lazy line-search trials)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const double t = ((maxmask >> k) & 1u) ? warp_max(v[k]) : ((minmask >> k) & 1u) ? warp_min(v[k]) : warp_sum(v[k]);
+            if (lane == 0) sh_w[wid * N + k] = t;
+        }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
-        double t = sh_w[k];
-        for (int w = 1; w < W; ++w) {
-            const double x = sh_w[w * N + k];
-            t = ((maxmask >> k) & 1u) ? fmax(t, x) : ((minmask >> k) & 1u) ? fmin(t, x) : t + x;
-        }
+        double x[IR_W];
+#pragma unroll
+        for (int w = 0; w < IR_W; ++w) x[w] = sh_w[w * N + k];   // all loads first, then the sums in warp order
+        double t = x[0];
+#pragma unroll
+        for (int w = 1; w < IR_W; ++w) t = ((maxmask >> k) & 1u) ? fmax(t, x[w]) : ((minmask >> k) & 1u) ? fmin(t, x[w]) : t + x[w];
         part[(size_t)(slot0 + k) * gridDim.x + blockIdx.x] = t;
         sh_w[IR_W * N + k] = t;
     }
     __syncthreads();
 }
 // slots [s0, s0 + n) -> out[0 .. n) in shared memory, every block identically; a warp loads its (up to 2) slots
-// before reducing them, so the totals cost one round trip for n <= 2 W
+// before reducing them (one transposed butterfly for both), so the totals cost one round trip for n <= 2 W
 __device__ __forceinline__ void ir_totals(const double* part, int s0, int n, unsigned maxmask, unsigned minmask,
                                           double* out) {
     const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31, G = gridDim.x;
     for (int k0 = wid; k0 < n; k0 += 2 * W) {
         double v[2][5];
+        int op[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int k = k0 + h * W;
-            const int op = k >= n ? 0 : ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
-            const double idn = op == 2 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+            op[h] = k >= n ? 0 : ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
+            const double idn = op[h] == 2 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
 #pragma unroll
             for (int j = 0; j < 5; ++j) {
                 const int b = lane + 32 * j;
                 v[h][j] = (k < n && b < G) ? ld_cg(part + (size_t)(s0 + k) * G + b) : idn;
             }
         }
+        double a[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int k = k0 + h * W;
-            if (k >= n) break;
-            const int op = ((maxmask >> k) & 1u) ? 1 : ((minmask >> k) & 1u) ? 2 : 0;
             double t = v[h][0];
 #pragma unroll
-            for (int j = 1; j < 5; ++j) t = op == 0 ? t + v[h][j] : op == 1 ? fmax(t, v[h][j]) : fmin(t, v[h][j]);
-            t = op == 0 ? warp_sum(t) : op == 1 ? warp_max(t) : warp_min(t);
-            if (lane == 0) out[k] = t;
+            for (int j = 1; j < 5; ++j) t = op[h] == 0 ? t + v[h][j] : op[h] == 1 ? fmax(t, v[h][j]) : fmin(t, v[h][j]);
+            a[h] = t;
         }
+        warp_reduce_slots<2>(a, (op[0] == 1 ? 1u : 0u) | (op[1] == 1 ? 2u : 0u), (op[0] == 2 ? 1u : 0u) | (op[1] == 2 ? 2u : 0u));
+        const int k = k0 + (lane >> 4) * W;
+        if ((lane & 15) == 0 && k < n) out[k] = a[0];
     }
     __syncthreads();
 }
@@ -215,7 +286,9 @@ __device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int 
 template <int GSCH, int GST, bool BIG>
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
-    unsigned long long ph_t = gtimer(), ph_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph_t = gtimer(), ph_acc[IR_PHN] = {};
+    const unsigned long long ph_k0 = ph_t;
+    int ph_its = 0;
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ double sh_w[IR_W * 2 * IR_NLS + 2 * IR_NLS];   // >= IR_W * N + N for every ir_block_partials<N>
     __shared__ double sh_t[12], sh_r[4], sh_l1[2 * IR_NLS];
@@ -233,7 +306,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     const int m = P.m, G = gridDim.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nA = c->nA;
-    const int ph_off = nA < 2048 ? 0 : 8;
+    const int ph_off = nA < 2048 ? 0 : IR_PHN / 2;
     const int q = (nA + G - 1) / G;
     const int p0 = min(nA, (int)blockIdx.x * q), p1 = min(nA, p0 + q);
     const int R = (m + G - 1) / G;
@@ -388,8 +461,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     }
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
+        ph_its += 1;
         const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
         if (!BIG && producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
+        PH_SUB(0);
         // ------------------------------------------------ D: direction on my positions
         int my_z = 0;
         {
@@ -430,6 +505,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     v[11] = fmax(v[11], fabs(vv));
                 }
             }
+            PH_SUB(1);
             ir_block_partials<12>(v, IR_DMAX, 0u, sh_w, part, IR_SD);
             my_z = pcd && sh_w[IR_W * 12 + 5] > 0.0;
         }
@@ -496,11 +572,14 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (my_z) xz_sh[i] = 0.0;
             }
             __syncthreads();
+            PH_SUB(2);
             uint32_t s_phase = 0u;
             for (int st = 0;; st = (st + 1) % SST) {
                 const SChunk d = s_desc[st];
                 if (!d.ok) break;
+                PH_SUB(3);
                 mbar_wait(s_bar + st, (s_phase >> st) & 1u);
+                PH_SUB(7);
                 s_phase ^= 1u << st;
                 const double cf = coef[d.p - p0];
                 if (cf != 0.0) {
@@ -508,17 +587,19 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     const int* ci = s_idx + st * IR_SCH - d.a;
                     const float* cv = s_val + st * IR_SCH - d.a;
                     const int kend = min(d.ve, d.ce);
-                    // rows are distinct within a column: all loads of a batch are issued before its stores
+                    // rows are distinct within a column: all loads of a batch are issued before its stores.  The
+                    // staged part [vb, kend) has branch-free (predicated) loads; the global tail past the last
+                    // 16-byte boundary of X (at most 3 nonzeros) is a separate loop
                     constexpr int UB = IR_SCH / 256;
-                    for (int k0 = d.vb + threadIdx.x; k0 < d.ve; k0 += UB * (int)blockDim.x) {
+                    for (int k0 = d.vb + threadIdx.x; k0 < kend; k0 += UB * (int)blockDim.x) {
                         int r[UB];
                         double xv[UB], a[UB];
 #pragma unroll
                         for (int u = 0; u < UB; ++u) {
                             const int k = k0 + u * blockDim.x;
                             r[u] = -1;
+                            xv[u] = 0.0;
                             if (k < kend) { r[u] = ci[k]; xv[u] = (double)cv[k]; }
-                            else if (k < d.ve) { r[u] = __ldg(S.idx + k); xv[u] = (double)__ldg(S.val + k); }
                         }
 #pragma unroll
                         for (int u = 0; u < UB; ++u) a[u] = r[u] >= 0 ? xs_sh[r[u]] : 0.0;
@@ -533,16 +614,26 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                                 if (r[u] >= 0) xz_sh[r[u]] = fma(xv[u], cf, a[u]);
                         }
                     }
+                    for (int k = kend + threadIdx.x; k < d.ve; k += blockDim.x) {
+                        const int r = __ldg(S.idx + k);
+                        const double xv = (double)__ldg(S.val + k);
+                        xs_sh[r] = fma(xv, cf, xs_sh[r]);
+                        if (zf) xz_sh[r] = fma(xv, cf, xz_sh[r]);
+                    }
                     if (threadIdx.x == 0) nsc += d.ve - d.vb;
                 }
+                PH_SUB(4);
                 __syncthreads();   // stage st consumed by every warp
+                PH_SUB(5);
                 if (producer) {
                     SChunk nd;
                     if (pr.next(S, coef, nd)) { s_desc[st] = nd; pr.issue(S, nd, st, s_idx, s_val, s_bar); }
                     else s_desc[st].ok = 0;
                 }
+                PH_SUB(6);
             }
             __syncthreads();
+            PH_SUB(3);
             if (producer)
                 for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
             // my block partials (a block without zeroing columns writes zeros for X_A z)
@@ -618,16 +709,16 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (g < ng) {
                     const double* src = parts + r0 + rr;
                     const double* srz = zparts + r0 + rr;
-                    for (int b0 = g; b0 < G; b0 += 8 * ng) {   // 8 loads in flight, summed in block order
-                        double x[8], z[8];
+                    for (int b0 = g; b0 < G; b0 += IR_RL * ng) {   // IR_RL loads in flight, summed in block order
+                        double x[IR_RL], z[IR_RL];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < IR_RL; ++u) {
                             const int b = b0 + u * ng;
                             x[u] = b < G ? ld_cg(src + (size_t)b * m) : 0.0;
                             z[u] = (dual && b < G) ? ld_cg(srz + (size_t)b * m) : 0.0;
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) { t += x[u]; tz += z[u]; }
+                        for (int u = 0; u < IR_RL; ++u) { t += x[u]; tz += z[u]; }
                     }
                     sh_w[threadIdx.x] = t;   // sh_w holds >= 2 * 256 doubles
                     sh_w[blockDim.x + threadIdx.x] = tz;
@@ -914,7 +1005,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     PH_MARK(7);
     const double F0 = c->F;
     if (acc_steps == 0) {   // R14: d = 0
-        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, 0, F0, F0, 0.0); }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, 0, IR_FB(F0), F0, IR_AL(0.0)); }
         return;
     }
     double at[4];
@@ -944,7 +1035,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     ir_totals(part, IR_SO, 10, 1u << 1, 0u, sh_t);
     const double Delta = sh_t[0] + P.lam * sh_t[2];
     if (sh_t[1] == 0.0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, acc_steps, F0, F0, 0.0); }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, acc_steps, IR_FB(F0), F0, IR_AL(0.0)); }
         return;
     }
     int t_acc = -1;
@@ -964,7 +1055,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     if (t_acc < 0) {   // R17
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             c->skip = 1; c->outcome = OUT_STAGNATION; c->alpha = 0.0;
-            ir_trace(P, c, OUT_STAGNATION, acc_steps, F0, F0, 0.0);
+            ir_trace(P, c, OUT_STAGNATION, acc_steps, IR_FB(F0), F0, IR_AL(0.0));
         }
         return;
     }
@@ -1001,7 +1092,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             c->ls_ok = 1;
             c->F = c->L + P.lam * c->l1;
             c->outcome = OUT_UPDATED;
-            ir_trace(P, c, OUT_UPDATED, acc_steps, F0, c->F, alpha);
+            ir_trace(P, c, OUT_UPDATED, acc_steps, IR_FB(F0), c->F, IR_AL(alpha));
         }
     }
 }
@@ -1040,6 +1131,10 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         if (S.list) { ctl->Cptr = S.list; ctl->nC = nC_list; }
     }
     if (conv) return;   // grid-uniform (coarse relaxations of a converged level)
+#ifdef GS_PHDBG
+    unsigned long long ph_t = gtimer(), ph_acc[IR_PHN] = {};
+    const int ph_off = FINEST ? 16 : 0;   // coarse-level launches only
+#endif
     const int m = P.m, G = gridDim.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nC = S.list ? nC_list : P.n;
@@ -1057,8 +1152,21 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
     cs.streamed = 0;
     cs.segs = 0;
     stream_begin(cs, S, nullptr, p0, p1, gbase);   // X first: its latency overlaps the (r, D) staging
-    for (int i = threadIdx.x; i < m; i += blockDim.x) rd_sh[i] = P.rD[i];
+    for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 loads in flight per thread
+        double2 t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            t[u] = i < m ? P.rD[i] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < m) rd_sh[i] = t[u];
+        }
+    }
     __syncthreads();
+    GS_MARK(0);
     {
         uint32_t phase = 0u;
         int stg = 0;
@@ -1066,7 +1174,9 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         while (true) {
             const ChunkDesc dsc = cs.desc[stg];
             if (dsc.cf == 0.0) break;
+            GS_MARK(1);
             mbar_wait(cs.bar + stg, (phase >> stg) & 1u);
+            GS_MARK(6);
             phase ^= 1u << stg;
             const int* ci = cs.sidx + stg * GSCH - dsc.a;
             const float* cv = cs.sval + stg * GSCH - dsc.a;
@@ -1115,13 +1225,18 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         if (lane == 0)
             for (int k = 0; k < IN_GST; ++k) mbar_inval(g_bar + k);
     }
+    GS_MARK(1);
     acc_add(acc, cs.streamed, cs.segs);   // (synchronises the block: g, h of my positions are visible)
     // my positions in order: flags, block count, partial sums
     double v1p = 0.0, l1p = 0.0, vmx = 0.0;
     int cnt = 0;
+    const bool one_pass = p1 - p0 <= (int)blockDim.x;   // then my position's (j, g, w_j) stay in registers
+    int j1 = 0;
+    double g1 = 0.0, w1 = 0.0, h1 = 0.0;
     for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int j = S.list ? __ldg(S.list + p) : p;
         const double g = AS.s[p];
+        h1 = AS.Hs[p];
         double wj = 0.0;
         if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
         const double v = (wj != 0.0) ? g + P.lam * sgn(wj) : soft(g, P.lam);
@@ -1129,12 +1244,15 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         v1p += fabs(v);
         l1p += fabs(wj);
         cnt += (wj != 0.0) || (fabs(g) > P.lam);
+        j1 = j; g1 = g; w1 = wj;
     }
     {
         const double v[4] = {v1p, l1p, vmx, (double)cnt};
         ir_block_partials<4>(v, 1u << 2, 0u, sh_w, P.irpart, 0);
     }
+    GS_MARK(2);
     grid.sync();
+    GS_MARK(3);
     // totals (identical in every block) and my offset: the counts of the blocks before me, in order
     ir_totals(P.irpart, 0, 3, 1u << 2, 0u, sh_t);
     if (wid == 0) {
@@ -1151,6 +1269,7 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
     __syncthreads();
     const int my_off = sh_cnt[IR_W], nA = sh_cnt[0];
     __syncthreads();
+    GS_MARK(4);
     // my free columns, in position order
     int base = my_off;
     for (int p00 = p0; p00 < p1; p00 += blockDim.x) {
@@ -1158,9 +1277,12 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         int j = 0, flag = 0;
         double g = 0.0, wj = 0.0;
         if (p < p1) {
-            j = S.list ? __ldg(S.list + p) : p;
-            g = AS.s[p];
-            if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
+            if (one_pass) { j = j1; g = g1; wj = w1; }
+            else {
+                j = S.list ? __ldg(S.list + p) : p;
+                g = AS.s[p];
+                if ((P.wbits[j >> 5] >> (j & 31)) & 1u) wj = P.w[j];
+            }
             flag = (wj != 0.0) || (fabs(g) > P.lam);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, flag);
@@ -1172,12 +1294,17 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
             const int o = base + woff + __popc(bal & ((1u << lane) - 1u));
             AS.A[o] = j;
             AS.gA[o] = g;
-            AS.hA[o] = AS.Hs[p] + P.eps_h;
+            AS.hA[o] = (one_pass ? h1 : AS.Hs[p]) + P.eps_h;
             AS.wA[o] = wj;
         }
         base += tot;
         __syncthreads();
     }
+    GS_MARK(5);
+#ifdef GS_PHDBG
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q2 = 0; q2 < 16; ++q2) atomicAdd(&ctl->tph[q2], ph_acc[q2]);
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) {   // the last-block decisions of k_gather_free
         ctl->nA = nA;
         const double vmax = sh_t[2];
