@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     unsigned long long ph_t = gtimer(), ph_acc[IR_PHN] = {};
     const unsigned long long ph_k0 = ph_t;
     int ph_its = 0;
+    (void)ph_k0;
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ double sh_w[IR_W * 2 * IR_NLS + 2 * IR_NLS];   // >= IR_W * N + N for every ir_block_partials<N>
     __shared__ double sh_t[12], sh_r[4], sh_l1[2 * IR_NLS];
