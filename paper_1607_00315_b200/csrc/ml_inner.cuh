@@ -186,6 +186,27 @@ __device__ __forceinline__ void ir_totals(const double* part, int s0, int n, uns
     __syncthreads();
 }
 
+// Split grid barrier (the cooperative-groups algorithm with the arrival and the wait apart, so that block-local work
+// overlaps the wait): block 0 adds 2^31 - (G - 1), every other block 1, so the counter's top bit flips exactly when the
+// last block arrives; its low 31 bits return to their value (0) after every barrier.  Release fence before the
+// arrival, acquire load in the wait, the block barrier on both sides.
+__device__ __forceinline__ unsigned gbar_arrive(unsigned* ctr) {
+    __syncthreads();
+    unsigned old = 0u;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        old = atomicAdd(ctr, blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u);
+    }
+    return old;   // (thread 0)
+}
+__device__ __forceinline__ void gbar_wait(const unsigned* ctr, unsigned old) {
+    if (threadIdx.x == 0) {
+        unsigned v;
+        do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory"); } while (((v ^ old) & 0x80000000u) == 0u);
+    }
+    __syncthreads();
+}
+
 // S phase producer (thread 0): the next chunk of my columns; with coef, columns with a zero coefficient are skipped
 // (the first SST chunks are issued before the direction exists, without skipping)
 struct SProducer {
@@ -462,6 +483,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     }
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
+        ColStream<GSCH, GST> csG;   // the G rings: prefetched during B1 (small m) or B2 (BIG)
+        const bool need_hs = it < K - 1;
         ph_its += 1;
         const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
         if (!BIG && producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
@@ -645,7 +668,22 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
         }
         PH_MARK(1);
-        grid.sync();   // B1
+        if constexpr (BIG) grid.sync();   // B1
+        else {   // B1, split: the G rings (aliasing the consumed S ring) are set up and issued while it completes
+            const unsigned bar_old = gbar_arrive(&c->gbar);
+            if (need_hs) {
+                if (lane == 0) {
+                    for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
+                    fence_mbar_init();
+                }
+                __syncwarp();
+                g_phase = 0u;
+                csG.streamed = 0;
+                csG.segs = 0;
+                stream_begin(csG, S, nullptr, p0, p1, gbase, col_ext, IR_QC);
+            }
+            gbar_wait(&c->gbar, bar_old);
+        }
         ir_totals(part, IR_SD, 12, IR_DMAX, 0u, sh_t);
         PH_MARK(2);
         int nzero = 0;
@@ -666,6 +704,13 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (stop) {
             if (BIG)   // the scatter of this iteration is complete (B1): clear my rows for the next relaxation
                 for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) { P.Xu[r0 + k] = 0.0; P.Xzu[r0 + k] = 0.0; }
+            else if (need_hs) {   // drain the prefetched G rings
+                for (int stg2 = 0; stg2 < GST; ++stg2)
+                    if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (g_phase >> stg2) & 1u); g_phase ^= 1u << stg2; }
+                __syncwarp();
+                if (lane == 0)
+                    for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
+            }
             break;
         }
         const int dual = pcd && nzero > 0;
@@ -754,10 +799,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             const double v[4] = {a_ss, a_sz, a_zz, kmin};
             ir_block_partials<4>(v, 0u, 1u << 3, sh_w, part, IR_SR);
         }
-        // prefetch the G rings (X_A's columns do not depend on the step) across the barrier
-        ColStream<GSCH, GST> csG;
-        const bool need_hs = it < K - 1;
-        if (need_hs) {
+        // BIG: prefetch the G rings (X_A's columns do not depend on the step) across the barrier
+        if (BIG && need_hs) {
             if (lane == 0) {
                 for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
                 fence_mbar_init();
@@ -766,8 +809,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             g_phase = 0u;
             csG.streamed = 0;
             csG.segs = 0;
-            if (BIG) stream_begin(csG, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
-            else stream_begin(csG, S, nullptr, p0, p1, gbase, col_ext, IR_QC);
+            stream_begin(csG, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
         }
         PH_MARK(3);
         grid.sync();   // B2

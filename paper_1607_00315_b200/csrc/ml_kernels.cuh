@@ -33,7 +33,7 @@ struct Ctl {
     double l1diff_out[ML_MAXLS];
     // counters
     unsigned red_ctr[8];
-    unsigned tile_ctr, done_ctr, epoch, pad1;
+    unsigned tile_ctr, done_ctr, epoch, gbar;   // gbar: k_inner's split grid barrier (top bit flips per barrier)
     unsigned long long vmax_bits;
     long long cls[2][16];         // per pass class: [0] nonzeros streamed, [1] segments (rows/columns) visited
     long long dsupp;
