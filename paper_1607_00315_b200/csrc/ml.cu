@@ -262,23 +262,31 @@ __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* 
     if ((threadIdx.x & 31) == 0 && pos) atomicAdd(npos, pos);
 }
 // X's index structure: pointers non-decreasing with ptr[0] = 0, ptr[len] = nnz; indices in [0, bound) and strictly
-// ascending inside every segment (the column passes rely on distinct rows within a column); flags ctl->bad_y |= 2
+// ascending inside every segment (the column passes rely on distinct rows within a column); flags ctl->bad_y |= 2.
+// Element-parallel (long rows of a dense X are not one warp's serial loop): a descent idx[k] <= idx[k-1] is legal only
+// at a segment start, so the descents counted over all k >= 1 minus those at the starts of non-empty segments
+// (each start counted once) must be 0; the difference is summed into ctl->idx_desc (>= 0 per array).
 __global__ void k_check_index(const int* ptr, const int* idx, int len, int bound, long long nnz, Ctl* ctl) {
-    // one warp per segment, lanes over adjacent pairs (coalesced)
     const int lane = threadIdx.x & 31;
+    const long long T = (long long)gridDim.x * blockDim.x, t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int bad = 0;
-    for (int s = (blockIdx.x * ML_NT + threadIdx.x) >> 5; s < len; s += (gridDim.x * ML_NT) >> 5) {
+    long long net = 0;
+    for (long long s = t0; s < len; s += T) {   // pointers; descents at segment starts (subtracted)
         const int b = ptr[s], e = ptr[s + 1];
         if (b > e || b < 0 || (long long)e > nnz || (s == 0 && b != 0) || (s == len - 1 && (long long)e != nnz)) {
             bad = 1;
             continue;
         }
-        for (int k = b + lane; k < e; k += 32) {
-            const int r = idx[k];
-            bad |= (r < 0) || (r >= bound) || (k + 1 < e && idx[k + 1] <= r);
-        }
+        if (b < e && b > 0 && idx[b] <= idx[b - 1]) net -= 1;
+    }
+    for (long long k = t0; k < nnz; k += T) {   // ranges; every descent (added)
+        const int r = idx[k];
+        bad |= (r < 0) || (r >= bound);
+        if (k > 0 && r <= idx[k - 1]) net += 1;
     }
     if (bad) atomicOr(&ctl->bad_y, 2);
+    net = warp_sum_ll(net);
+    if (lane == 0 && net != 0) atomicAdd((unsigned long long*)&ctl->idx_desc, (unsigned long long)net);
 }
 // support bitmap, |supp| and ||w||_1 from w (deterministic: per-block partials + last block)
 __global__ void __launch_bounds__(ML_NT) k_w_stats(Prm P, int n) {
@@ -673,8 +681,9 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     }
     ml_status s = sync_ctl(c);
     if (s != ML_OK) { *out = c; return s; }
-    if (c->h.bad_y) {   // bit 0: labels not +-1; bit 1: malformed CSR / CSC index structure
-        c->err = (c->h.bad_y & 2) ? "X: pointers or indices malformed (indices must be in range and strictly ascending per segment)"
+    if (c->h.bad_y || c->h.idx_desc != 0) {   // bit 0: labels not +-1; bit 1 / descents: malformed CSR / CSC
+        c->err = ((c->h.bad_y & 2) || c->h.idx_desc != 0)
+                     ? "X: pointers or indices malformed (indices must be in range and strictly ascending per segment)"
                                   : "y: labels must be -1 or +1";
         delete c;
         return ML_E_INVAL;

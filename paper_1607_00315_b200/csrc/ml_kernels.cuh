@@ -37,6 +37,7 @@ struct Ctl {
     unsigned long long vmax_bits;
     long long cls[2][16];         // per pass class: [0] nonzeros streamed, [1] segments (rows/columns) visited
     long long dsupp;
+    long long idx_desc;           // k_check_index: index descents not at a segment start (0 for a valid X)
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
     int ntrace, trace_cap, bad_y, pad2;
     unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics

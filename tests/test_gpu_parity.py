@@ -358,7 +358,16 @@ def test_create_rejects_malformed_index():
     row[0], row[1] = row[1], row[0]   # column 0's rows out of order
     col = good.csr_col.copy()
     col[-1] = good.n                  # a CSR column index out of range
-    for bad in (dataclasses.replace(good, csc_row=row), dataclasses.replace(good, csr_col=col)):
+    dup = good.csc_row.copy()
+    dup[1] = dup[0]                   # a repeated row inside column 0
+    last = good.csc_row.copy()
+    last[3], last[2] = last[2], last[3]   # the descent at a column's last element (next to a legal one at its end)
+    for bad in (dataclasses.replace(good, csc_row=row), dataclasses.replace(good, csr_col=col),
+                dataclasses.replace(good, csc_row=dup), dataclasses.replace(good, csc_row=last)):
         with pytest.raises(ml.MLError) as e:
             ml.Context(bad)
         assert "status 1" in str(e.value), str(e.value)
+    # empty rows and columns (equal consecutive pointers) are well formed
+    a = np.zeros((5, 4), np.float32)
+    a[0, 1], a[3, 1], a[3, 3] = 1.0, 2.0, 3.0
+    ml.Context(mlgen.from_dense(a, np.array([1, -1, 1, -1, 1], np.int8), 0.1))
