@@ -26,6 +26,9 @@ constexpr int IR_SCH = 2048;               // S phase: block-shared ring of IR_S
 #ifndef IR_RL
 #define IR_RL 12   // R phase: partial loads in flight per thread (m = 2000, G = 148: one round)
 #endif
+#ifndef IR_GU
+#define IR_GU 8   // BIG G phase: L2 gathers in flight per lane (multiple of 4)
+#endif
 constexpr int IR_QC = 1024;               // column extents of up to IR_QC own positions cached in shared memory
 // phase timers (block 0, thread 0): 8 phases for small |A| and 8 for large |A|.  Debug builds: IR_PHDBG puts
 // sub-phases of the small-|A| iteration in slots 8..15 (large |A| relaxations are then not timed) and the kernel time
@@ -562,6 +565,17 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     const float* cv = cs.sval + stg * GSCH - dsc.a;
                     const int kend = min(dsc.ve, dsc.ce);
                     int k = dsc.vb + lane;
+                    for (; k + 96 < kend; k += 128) {   // 4 reductions per lane issued back to back
+                        int r[4];
+                        double xv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) { r[u] = ci[k + 32 * u]; xv[u] = (double)cv[k + 32 * u] * cf; }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            red_add_global(P.Xu + r[u], xv[u]);
+                            if (zf) red_add_global(P.Xzu + r[u], xv[u]);
+                        }
+                    }
                     for (; k < kend; k += 32) {
                         const int r = ci[k];
                         const double xv = (double)cv[k] * cf;
@@ -896,7 +910,26 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 const float* cv = cs.sval + stg * GSCH - dsc.a;
                 const int kend = min(dsc.ve, dsc.ce);
                 int k = dsc.vb + lane;
+                // the L2 gathers of D o X sigma are latency-bound: IR_GU gathers in flight per lane
                 if (zs) {
+                    double a1 = 0.0, az1 = 0.0;
+                    for (; k + 32 * (IR_GU / 2) - 32 < kend; k += 32 * (IR_GU / 2)) {
+                        int q[IR_GU / 2];
+                        double sa[IR_GU / 2], sz[IR_GU / 2];
+#pragma unroll
+                        for (int u = 0; u < IR_GU / 2; ++u) q[u] = ci[k + 32 * u];
+#pragma unroll
+                        for (int u = 0; u < IR_GU / 2; ++u) { sa[u] = ld_cg(P.sv + q[u]); sz[u] = ld_cg(P.svz + q[u]); }
+#pragma unroll
+                        for (int u = 0; u < IR_GU / 2; u += 2) {
+                            a = fma((double)cv[k + 32 * u], sa[u], a);
+                            az = fma((double)cv[k + 32 * u], sz[u], az);
+                            a1 = fma((double)cv[k + 32 * u + 32], sa[u + 1], a1);
+                            az1 = fma((double)cv[k + 32 * u + 32], sz[u + 1], az1);
+                        }
+                    }
+                    a += a1;
+                    az += az1;
                     for (; k < kend; k += 32) {
                         const int r = ci[k];
                         const double xv = (double)cv[k];
@@ -905,6 +938,21 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     }
                 } else {
                     double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    for (; k + 32 * IR_GU - 32 < kend; k += 32 * IR_GU) {
+                        int q[IR_GU];
+                        double sa[IR_GU];
+#pragma unroll
+                        for (int u = 0; u < IR_GU; ++u) q[u] = ci[k + 32 * u];
+#pragma unroll
+                        for (int u = 0; u < IR_GU; ++u) sa[u] = ld_cg(P.sv + q[u]);
+#pragma unroll
+                        for (int u = 0; u < IR_GU; u += 4) {
+                            a = fma((double)cv[k + 32 * u], sa[u], a);
+                            a1 = fma((double)cv[k + 32 * u + 32], sa[u + 1], a1);
+                            a2 = fma((double)cv[k + 32 * u + 64], sa[u + 2], a2);
+                            a3 = fma((double)cv[k + 32 * u + 96], sa[u + 3], a3);
+                        }
+                    }
                     for (; k + 96 < kend; k += 128) {
                         const int q0r = ci[k], q1r = ci[k + 32], q2r = ci[k + 64], q3r = ci[k + 96];
                         const double s0 = ld_cg(P.sv + q0r), s1 = ld_cg(P.sv + q1r), s2 = ld_cg(P.sv + q2r),

@@ -43,6 +43,7 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ph = ctx.ml_inner_phases(reset=True)
+    prof = ctx.ml_profile_read()   # nonzeros streamed per pass class (device counters, all solves since create)
     tr = ctx.trace()
     its = [0, 0]
     rel = [0, 0]
@@ -52,7 +53,9 @@ def main():
         k = 0 if r["nA"] < 2048 else 1
         its[k] += r["inner_iters"]
         rel[k] += 1
-    out = {"config": a.config, "tag": a.tag, "ms": sorted(ts)[len(ts) // 2], "cycles": rep["cycles"]}
+    out = {"config": a.config, "tag": a.tag, "ms": sorted(ts)[len(ts) // 2], "cycles": rep["cycles"], "nnz_touched": rep["nnz_touched"],
+           "nnz_per_solve": {k: prof[k]["nnz"] // (a.reps + 1) for k in ("scatter_XAs", "gather_Hs", "gather_fine",
+                                                                    "gather_coarse", "margins") if prof[k]["nnz"]}}
     if a.gather:   # k_gather_small phases (slots 8..13), per launch (relaxations incl. converged-level skips)
         nl = sum(1 for r in tr if r["level"] > 0) or 1   # coarse-level launches only
         names = ["setup+rD", "stream", "flags+partials", "grid.sync", "totals+offsets", "compaction", "stream:tma-wait"]
