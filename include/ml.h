@@ -64,7 +64,9 @@ typedef struct {                  /* defaults: ml_default_opts (DESIGN.md sectio
     double eta;                   /* inner forcing (0 = off) */
     int32_t pcd_snap;             /* 1 (default): a PCD step first tries the path that sets the coordinates its shrinkage
                                      sends to 0 exactly to 0 for every step length (DESIGN Q27); 0: plain PCD steps */
-    int32_t pad;
+    int32_t continuation;         /* 1: first one finest relaxation at each of lambda_4 > lambda_3 > lambda_2, lambda_4 =
+                                     (lambda_max + lambda) / 2, linearly spaced down to lambda (DESIGN Q28),
+                                     then the solve at lambda from that warm start; 0 (default): from w = 0 */
 } ml_solve_opts;
 
 typedef struct {

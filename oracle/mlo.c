@@ -604,6 +604,23 @@ int mlo_solve(mlo_ctx *c, const mlo_opts *o, mlo_report *rep) {
     v1_0 = v1;
     int converged = (vinf / c->lam <= o->tol_kkt);                  /* S3 (lambda >= lambda_max) */
     int cycle = 0;
+    if (!converged && o->continuation) {
+        /* Continuation (DESIGN Q28): lambda_4 = (lambda_max + lambda) / 2 and lambda_3, lambda_2 linearly
+           spaced between lambda_4 and lambda_1 = lambda; one finest relaxation (one proximal-Newton outer iteration on
+           the free set) at each of lambda_4, lambda_3, lambda_2 in decreasing order, then the solve at lambda from that
+           warm start.  At w = 0, vinf = max_j (|g_j| - lambda), so lambda_max = vinf + lambda. */
+        const double lam1 = c->lam, lam4 = 0.5 * ((vinf + lam1) + lam1);
+        for (int kk = 4; kk >= 2 && st == MLO_OK; --kk) {
+            c->lam = lam1 + (lam4 - lam1) * (double)(kk - 1) / 3.0;
+            st = relax_core(c, NULL, n, NULL, NULL, o->K_fine, o, 0, Af, &nAf, gAf, &outcome);
+            rep->relax_per_level[0]++;
+        }
+        c->lam = lam1;
+        /* S2 again at the warm start: EVAL_ALL with margins from scratch */
+        mlo_eval_f_grad(c, NULL, n, &F, g, h);
+        kkt_all(c, g, &vinf, &v1);
+        converged = (vinf / c->lam <= o->tol_kkt);
+    }
     if (!converged) {
         /* S4: initial finest relaxation so that a finest gradient exists */
         st = relax_core(c, NULL, n, g, h, o->K_fine, o, 0, Af, &nAf, gAf, &outcome);

@@ -39,7 +39,8 @@ typedef struct {
     int32_t inner_cg;    /* 2: PCD-CG + a PCD step after every kink (default); 1: PCD-CG; 0: plain PCD (DESIGN Q9b) */
     double eta;          /* inner forcing: stop when the model's min-norm subgradient <= eta * its value at d = 0 (0 = off) */
     int32_t pcd_snap;    /* 1 (default): PCD steps set coordinates whose shrinkage target is 0 exactly to 0 for every step length (Q27) */
-    int32_t pad;
+    int32_t continuation; /* 1: before the solve, one finest relaxation at each of lambda_4 > lambda_3 > lambda_2 (
+                             DESIGN Q28), then the solve at lambda from that warm start; 0 (default): start at w = 0 */
 } mlo_opts;
 
 typedef struct {

@@ -50,7 +50,7 @@ class SolveOpts(ctypes.Structure):
                 ("K_coarse", ctypes.c_int32), ("sigma_out", ctypes.c_double), ("sigma_in", ctypes.c_double),
                 ("beta", ctypes.c_double), ("max_ls", ctypes.c_int32), ("eps_h", ctypes.c_double),
                 ("multilevel", ctypes.c_int32), ("inner_cg", ctypes.c_int32), ("eta", ctypes.c_double),
-                ("pcd_snap", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("pcd_snap", ctypes.c_int32), ("continuation", ctypes.c_int32)]
 
 
 class SolveReport(ctypes.Structure):

@@ -517,6 +517,7 @@ void ml_default_opts(ml_solve_opts* o) {
     o->inner_cg = 2;
     o->eta = 0.0;
     o->pcd_snap = 1;
+    o->continuation = 0;
 }
 
 size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz) {
@@ -863,10 +864,30 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
             }
         }
     };
+    double v1_0 = -1.0;
+    if (o.continuation) {
+        // Continuation (DESIGN Q28): EVAL_ALL at w = 0 gives lambda_max = vmax + lambda; one finest
+        // relaxation at each of lambda_4 = (lambda_max + lambda) / 2 > lambda_3 > lambda_2 (linearly spaced down to
+        // lambda), each with its own free-set gather; then the solve at lambda from that warm start.
+        launch_margins(c);
+        launch_relax_start(c, 1, 0, nullptr, n, c->fine);
+        ml_status s0 = sync_ctl(c);
+        if (s0 != ML_OK) return s0;
+        v1_0 = c->h.v1;
+        if (c->h.vmax / c->lam > o.tol_kkt) {
+            const double lam1 = c->lam, lam4 = 0.5 * ((c->h.vmax + lam1) + lam1);
+            for (int kk = 4; kk >= 2; --kk) {
+                c->P.lam = lam1 + (lam4 - lam1) * (double)(kk - 1) / 3.0;
+                launch_relax_start(c, 1, 0, nullptr, n, c->fine);
+                launch_relax_body(c, c->fine, o.K_fine, o.inner_cg);
+            }
+            c->P.lam = lam1;
+        }
+    }
     eval_and_fine_relax(true);
     ml_status s = sync_ctl(c);
     if (s != ML_OK) return s;
-    const double v1_0 = c->h.v1;
+    if (v1_0 < 0.0) v1_0 = c->h.v1;
     bool converged = c->h.vmax / c->lam <= o.tol_kkt;
     int cycle = 0;
     int64_t max_supp = c->h.nS;

@@ -195,7 +195,9 @@ def _support_check(ds, w_g, w_o, g_o):
 @pytest.mark.parametrize("name,opts", [("cfg1", {}), ("cfg2s", {}), ("cfg3s", {}), ("sparse_edges", {}),
                                        ("onehot", {}), ("n1", {}), ("m1", {}),
                                        ("cfg3s", {"multilevel": 0, "K_fine": 10}),
-                                       ("cfg1", {"inner_cg": 0, "K_mid": 2, "K_coarse": 5})])
+                                       ("cfg1", {"inner_cg": 0, "K_mid": 2, "K_coarse": 5}),
+                                       ("cfg2s", {"continuation": 1}), ("cfg3s", {"continuation": 1}),
+                                       ("mid6k", {"continuation": 1}), ("onehot", {"continuation": 1})])
 def test_solve_parity(name, opts):
     """A9: ml_solve vs the oracle's solve (Algorithm 1 P:155-173 per P:798), both to kappa <= 1e-6."""
     ds = dataset(name)
@@ -267,7 +269,8 @@ def test_solve_parity_inner_variants(name, opts):
 
 
 @pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("mid6k", {}), ("cfg2s", {"inner_cg": 0}),
-                                       ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0})])
+                                       ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0}),
+                                       ("cfg2s", {"continuation": 1}), ("cfg4s", {"continuation": 1})])
 def test_trace_parity(name, opts):
     """Relaxation by relaxation (Algorithm 1, DESIGN S1-S18/R1-R18): level, |A|, outcome, inner iterations and
     F after each of the first relaxations agree with the oracle's trace (decisions identical while rounding

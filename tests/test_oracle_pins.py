@@ -305,7 +305,8 @@ def _brute_force(X, y, lam):
 
 
 VARIANTS = [dict(), dict(pcd_snap=0), dict(inner_cg=1, pcd_snap=0), dict(inner_cg=0, pcd_snap=1),
-            dict(inner_cg=0, pcd_snap=0), dict(multilevel=0)]
+            dict(inner_cg=0, pcd_snap=0), dict(multilevel=0), dict(continuation=1),
+            dict(continuation=1, multilevel=0)]
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
@@ -487,3 +488,31 @@ def test_linesearch_armijo_decision():
     assert F(w + 2 * alpha * d) - F(w) > 1e-2 * 2 * alpha * Delta
     assert np.allclose(o.get_w(), w + alpha * d, rtol=0, atol=1e-15)
     assert abs(Fn - F(w + alpha * d)) <= 1e-12 * Fn
+
+
+# ----------------------------------------------------------------------------- continuation (Q28)
+@pytest.mark.parametrize("multilevel", [1, 0])
+def test_continuation_onehot_closed_form(multilevel):
+    """Continuation (one finest relaxation at each of lambda_4 > lambda_3 > lambda_2, then the solve at lambda from
+    that warm start) reaches the one-hot closed form; its first three relaxations start at
+    F(0) = m log 2 and decrease F (Lemma P:207-243 holds at every lambda_k)."""
+    ds, a, p, q = mlgen.onehot(400, 5)
+    lam = ds.lam
+    d = np.abs(p - q).astype(np.float64)
+    act = lam < a * d / 2
+    wref = np.zeros(ds.n)
+    big, small = np.maximum(p, q).astype(np.float64), np.minimum(p, q).astype(np.float64)
+    wref[act] = np.sign(p - q)[act] / a[act] * np.log((a[act] * big[act] - lam) / (a[act] * small[act] + lam))
+    o = oracle.Oracle(ds)
+    rep = o.solve(oracle.default_opts(tol_kkt=1e-12, continuation=1, multilevel=multilevel))
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    nz = wref != 0
+    assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-9
+    tr = o.trace()
+    assert tr[0]["level"] == 0 and abs(tr[0]["F_before"] - ds.m * np.log(2.0)) <= 1e-12 * ds.m
+    assert all(r["level"] == 0 for r in tr[:3])
+    # the continuation stages use lambda_k > lambda: each stage's free set is no larger than the next stage's
+    assert tr[0]["nA"] <= tr[1]["nA"] <= tr[2]["nA"] <= tr[3]["nA"]
+    assert rep["relax_per_level"][0] >= 4
