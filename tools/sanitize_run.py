@@ -38,3 +38,5 @@ if __name__ == "__main__":
     run(mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40))
     run(mlgen.onehot(3000, 3)[0])
     run(mlgen.make(1), ml.default_opts(inner_cg=2))
+    run(mlgen.make(2, m=300, n=3000), ml.default_opts(continuation=1))
+    run(mlgen.make(3, m=20000, n=30000), ml.default_opts(continuation=1))
