@@ -88,6 +88,12 @@ size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz);
 /* Bind X, y, lambda (> 0) to a context; w = 0.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
    Validates sizes, lambda and y (one device pass).  Builds the static heavy-row schedule (one pass over rowptr). */
 ml_status ml_create(const ml_data *X, double lambda, void *cuda_stream, void *ws, size_t ws_bytes, ml_ctx **out);
+/* The squared-loss instance of Eq. 1: the LASSO of Eq. 2 with H = X^T X and g = -X^T b, i.e.
+   F(w) = sum_i (x_i^T w - b_i)^2 / 2 + lambda ||w||_1 (DESIGN Q29).  b: [m] targets (device, fp64, borrowed like X);
+   X->y is not read and may be NULL.  Every other entry point works unchanged on the context (r_i = z_i - b_i,
+   D_i = 1); ML_E_INVAL if b is NULL. */
+ml_status ml_create_lasso(const ml_data *X, const double *b, double lambda, void *cuda_stream, void *ws, size_t ws_bytes,
+                          ml_ctx **out);
 ml_status ml_destroy(ml_ctx *c);
 
 /* w <- w_dev[n] (device); margins are recomputed at the next evaluation. */

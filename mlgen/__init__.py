@@ -89,6 +89,7 @@ class Dataset:
     wstar_idx: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     wstar_val: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float64))
     name: str = ""
+    b: np.ndarray | None = None   # squared-loss (LASSO) targets [m], fp64; None = logistic labels y
 
     @property
     def nnz(self) -> int:
@@ -214,3 +215,31 @@ def onehot(n: int, seed: int, rows_per_col=(2, 12), lam: float | None = None) ->
                  csc_colptr=colptr.astype(np.int32), csc_row=corder.astype(np.int32),
                  csc_val=vals[corder], y=lab.astype(np.int8), lam=float(lam), name=f"onehot{n}s{seed}")
     return ds, a32, p, q
+
+
+# ----------------------------------------------------------------- squared-loss (LASSO) instances
+def lasso(base: Dataset, seed: int, k: int = 10, noise: float = 0.1, lam_factor: float = 0.1) -> Dataset:
+    """The LASSO instance of Eq. 2 on the design of `base`: targets b = X w* + noise, with w* holding k
+    N(0, 1) values at uniform random columns; lambda = lam_factor * lambda_max, lambda_max = ||X^T b||_inf (w = 0 is
+    optimal iff lambda >= lambda_max).  Targets and lambda are inputs: no solver arithmetic here."""
+    import copy
+    rng = np.random.default_rng(seed)
+    wi = np.sort(rng.choice(base.n, min(k, base.n), replace=False)).astype(np.int32)
+    wv = rng.standard_normal(len(wi))
+    w = np.zeros(base.n)
+    w[wi] = wv
+    rp, ci, cv = base.csr_rowptr, base.csr_col, base.csr_val.astype(np.float64)
+    rows = np.repeat(np.arange(base.m), np.diff(rp))
+    z = np.zeros(base.m)
+    np.add.at(z, rows, cv * w[ci])
+    b = z + noise * rng.standard_normal(base.m)
+    g0 = np.zeros(base.n)
+    np.add.at(g0, ci, cv * b[rows])
+    lmax = float(np.max(np.abs(g0))) if base.nnz else 1.0
+    d = copy.copy(base)
+    d.b = b
+    d.lambda_max = lmax
+    d.lam = lam_factor * lmax if lmax > 0 else 1.0
+    d.wstar_idx, d.wstar_val = wi, wv
+    d.name = base.name + f"-lasso{seed}"
+    return d

@@ -72,6 +72,8 @@ def _load():
     L.mlo_default_opts.argtypes = [ctypes.POINTER(Opts)]
     L.mlo_create.restype = _P
     L.mlo_create.argtypes = [i64, i64, i64, _P, _P, _P, _P, _P, _P, _P, d]
+    L.mlo_create_lasso.restype = _P
+    L.mlo_create_lasso.argtypes = [i64, i64, i64, _P, _P, _P, _P, _P, _P, _P, d]
     L.mlo_destroy.argtypes = [_P]
     L.mlo_set_w.argtypes = [_P, _P]
     L.mlo_get_w.argtypes = [_P, _P]
@@ -141,7 +143,11 @@ class Oracle:
                                                          ds.csc_row, ds.csc_val, ds.y)]
         k = self._keep
         self.m, self.n = ds.m, ds.n
-        self.h = L.mlo_create(ds.m, ds.n, ds.nnz, *[_ptr(a) for a in k], float(ds.lam))
+        if getattr(ds, "b", None) is not None:   # squared loss (LASSO): targets b in place of the labels
+            k[-1] = np.ascontiguousarray(ds.b, np.float64)
+            self.h = L.mlo_create_lasso(ds.m, ds.n, ds.nnz, *[_ptr(a) for a in k], float(ds.lam))
+        else:
+            self.h = L.mlo_create(ds.m, ds.n, ds.nnz, *[_ptr(a) for a in k], float(ds.lam))
         if not self.h:
             raise ValueError("mlo_create rejected the input")
 

@@ -21,7 +21,8 @@ struct mlo_ctx {
     int64_t m, n, nnz;
     const int32_t *rp, *ci; const float *cv;  /* CSR */
     const int32_t *cp, *ri; const float *rv;  /* CSC */
-    const int8_t *y;
+    const int8_t *y;                /* logistic labels (NULL for the squared loss) */
+    const double *b;                /* squared-loss (LASSO) targets, Eq. 2 with H = X^T X, g = -X^T b (NULL = logistic) */
     double lam;
     double *w;                      /* [n] */
     double *z, *r, *D, *ell;        /* [m] per-sample state */
@@ -65,6 +66,14 @@ void mlo_default_opts(mlo_opts *o) {
 static void refresh_rows(mlo_ctx *c) {  /* per-sample quantities at the current z, then L */
     double L = 0.0;
     for (int64_t i = 0; i < c->m; ++i) {
+        if (c->b) {                                       /* squared loss: ell = (z - b)^2 / 2, r = ell', D = ell'' = 1 */
+            double r = c->z[i] - c->b[i];
+            c->ell[i] = 0.5 * r * r;
+            c->r[i] = r;
+            c->D[i] = 1.0;
+            L += c->ell[i];
+            continue;
+        }
         double t = (double)c->y[i] * c->z[i];
         c->ell[i] = mlo_logloss(t);
         c->r[i] = -(double)c->y[i] * mlo_tau(-t);      /* (tau(t)-1) y = -y tau(-t) */
@@ -89,17 +98,17 @@ static double l1_all(const mlo_ctx *c) {
 }
 static double F_current(const mlo_ctx *c) { return c->L + c->lam * l1_all(c); }
 
-mlo_ctx *mlo_create(int64_t m, int64_t n, int64_t nnz,
-                    const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
-                    const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
-                    const int8_t *y, double lambda) {
+static mlo_ctx *create_impl(int64_t m, int64_t n, int64_t nnz,
+                            const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
+                            const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
+                            const int8_t *y, const double *b, double lambda) {
     if (m < 1 || n < 1 || nnz < 0 || !(lambda > 0.0) || !isfinite(lambda)) return NULL;
-    for (int64_t i = 0; i < m; ++i) if (y[i] != 1 && y[i] != -1) return NULL;
+    if (!b) for (int64_t i = 0; i < m; ++i) if (y[i] != 1 && y[i] != -1) return NULL;
     mlo_ctx *c = (mlo_ctx *)calloc(1, sizeof(mlo_ctx));
     c->m = m; c->n = n; c->nnz = nnz;
     c->rp = csr_rowptr; c->ci = csr_col; c->cv = csr_val;
     c->cp = csc_colptr; c->ri = csc_row; c->rv = csc_val;
-    c->y = y; c->lam = lambda;
+    c->y = b ? NULL : y; c->b = b; c->lam = lambda;
     c->w = (double *)calloc((size_t)n, sizeof(double));
     c->z = (double *)calloc((size_t)m, sizeof(double));
     c->r = (double *)calloc((size_t)m, sizeof(double));
@@ -107,6 +116,19 @@ mlo_ctx *mlo_create(int64_t m, int64_t n, int64_t nnz,
     c->ell = (double *)calloc((size_t)m, sizeof(double));
     refresh_rows(c);   /* w = 0, z = 0 */
     return c;
+}
+mlo_ctx *mlo_create(int64_t m, int64_t n, int64_t nnz,
+                    const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
+                    const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
+                    const int8_t *y, double lambda) {
+    return create_impl(m, n, nnz, csr_rowptr, csr_col, csr_val, csc_colptr, csc_row, csc_val, y, NULL, lambda);
+}
+mlo_ctx *mlo_create_lasso(int64_t m, int64_t n, int64_t nnz,
+                          const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
+                          const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
+                          const double *b, double lambda) {
+    if (!b) return NULL;
+    return create_impl(m, n, nnz, csr_rowptr, csr_col, csr_val, csc_colptr, csc_row, csc_val, NULL, b, lambda);
 }
 void mlo_destroy(mlo_ctx *c) {
     if (!c) return;
@@ -224,6 +246,11 @@ static int outer_linesearch(mlo_ctx *c, const int32_t *A, int64_t nA, const doub
     for (int32_t t = 0; t < o->max_ls; ++t, alpha *= o->beta) {
         double dL = 0.0;
         for (int64_t i = 0; i < c->m; ++i) {
+            if (c->b) {   /* (z + delta - b)^2/2 - (z - b)^2/2 = delta (z - b + delta/2), exact algebra (as Q26) */
+                double delta = alpha * Xd[i];
+                dL += delta * ((c->z[i] - c->b[i]) + 0.5 * delta);
+                continue;
+            }
             double ti = (double)c->y[i] * c->z[i];
             dL += dloss(ti, alpha * (double)c->y[i] * Xd[i]);
         }
@@ -589,7 +616,7 @@ int mlo_solve(mlo_ctx *c, const mlo_opts *o, mlo_report *rep) {
     int32_t *R = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     int64_t nAf = 0;
     int64_t npos = 0;
-    for (int64_t i = 0; i < c->m; ++i) npos += (c->y[i] > 0);
+    for (int64_t i = 0; i < c->m && c->y; ++i) npos += (c->y[i] > 0);   /* (squared loss: no labels) */
     int64_t minpm = npos < c->m - npos ? npos : c->m - npos;
     int st = MLO_OK;
     int32_t outcome;

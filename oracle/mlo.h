@@ -65,6 +65,12 @@ mlo_ctx *mlo_create(int64_t m, int64_t n, int64_t nnz,
                     const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
                     const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
                     const int8_t *y, double lambda);
+/* The squared-loss instance (LASSO, Eq. 2 P:49-53 with H = X^T X, g = -X^T b): ell_i = (x_i^T w - b_i)^2 / 2, r_i =
+   x_i^T w - b_i, D_i = 1 (DESIGN Q29).  b: [m] targets. */
+mlo_ctx *mlo_create_lasso(int64_t m, int64_t n, int64_t nnz,
+                          const int32_t *csr_rowptr, const int32_t *csr_col, const float *csr_val,
+                          const int32_t *csc_colptr, const int32_t *csc_row, const float *csc_val,
+                          const double *b, double lambda);
 void mlo_destroy(mlo_ctx *c);
 
 void mlo_set_w(mlo_ctx *c, const double *w);   /* [n]; recomputes margins from scratch */

@@ -13,6 +13,8 @@ import ctypes
 import os
 import subprocess
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libml.so")
 _SRC = os.path.join(_HERE, "csrc")
@@ -69,7 +71,7 @@ class TraceRow(ctypes.Structure):
                 ("F_after", ctypes.c_double), ("alpha", ctypes.c_double)]
 
 
-EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
+EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_create_lasso", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
            "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
            "ml_profile_read", "ml_inner_phases"]
@@ -92,6 +94,8 @@ def load(path: str | None = None):
     L.ml_workspace_bytes.argtypes = [i64, i64, i64]
     L.ml_create.restype = i32
     L.ml_create.argtypes = [ctypes.POINTER(MLData), d, P, P, ctypes.c_size_t, ctypes.POINTER(P)]
+    L.ml_create_lasso.restype = i32
+    L.ml_create_lasso.argtypes = [ctypes.POINTER(MLData), P, d, P, P, ctypes.c_size_t, ctypes.POINTER(P)]
     for f in ("ml_destroy",):
         getattr(L, f).restype = i32
         getattr(L, f).argtypes = [P]
@@ -187,8 +191,14 @@ class Context:
         self.data = MLData(self.m, self.n, self.nnz, *[t.data_ptr() for t in (
             self.csr_rowptr, self.csr_col, self.csr_val, self.csc_colptr, self.csc_row, self.csc_val, self.y)])
         h = ctypes.c_void_p()
-        st = L.ml_create(ctypes.byref(self.data), self.lam, ctypes.c_void_p(self.stream.cuda_stream),
-                         ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(), ctypes.byref(h))
+        self.b = None if getattr(ds, "b", None) is None else torch.from_numpy(np.asarray(ds.b, np.float64)).to(dev)
+        if self.b is not None:   # the squared-loss (LASSO) instance
+            st = L.ml_create_lasso(ctypes.byref(self.data), ctypes.c_void_p(self.b.data_ptr()), self.lam,
+                                   ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(self.ws.data_ptr()),
+                                   self.ws.numel(), ctypes.byref(h))
+        else:
+            st = L.ml_create(ctypes.byref(self.data), self.lam, ctypes.c_void_p(self.stream.cuda_stream),
+                             ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(), ctypes.byref(h))
         if st != ML_OK:
             raise MLError(st, L.ml_status_str(st).decode())
         self.h = h

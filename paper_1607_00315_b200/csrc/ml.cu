@@ -241,7 +241,7 @@ ml_status sync_ctl(ml_ctx* c) {
 __global__ void k_init_rows(Prm P, int m) {   // w = 0: z = 0, r = -y/2, D = 1/4, L = m log 2
     for (int i = blockIdx.x * ML_NT + threadIdx.x; i < m; i += gridDim.x * ML_NT) {
         P.z[i] = 0.0;
-        RowState s = row_state(0.0, (double)P.y[i]);
+        RowState s = row_state_i(P.y, P.b, i, 0.0);
         P.rD[i] = make_double2(s.r, s.D);
         P.Xs[i] = 0.0;
         P.Xd[i] = 0.0;
@@ -543,13 +543,14 @@ const char* ml_status_str(ml_status s) {
 const char* ml_last_error(const ml_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int64_t ml_kernel_launches(const ml_ctx* c) { return c ? c->launches : 0; }
 
-ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws, size_t ws_bytes, ml_ctx** out) {
+static ml_status create_impl(const ml_data* X, const double* b, double lambda, void* cuda_stream, void* ws,
+                             size_t ws_bytes, ml_ctx** out) {
     if (!X || !out) return ML_E_INVAL;
     *out = nullptr;
     if (X->m < 1 || X->n < 1 || X->nnz < 0 || X->nnz >= 2147483647LL || X->m >= 2147483647LL || X->n >= 2147483647LL)
         return ML_E_INVAL;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return ML_E_INVAL;
-    if (!X->csr_rowptr || !X->csc_colptr || !X->y || (X->nnz > 0 && (!X->csr_col || !X->csr_val || !X->csc_row || !X->csc_val)))
+    if (!X->csr_rowptr || !X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csr_col || !X->csr_val || !X->csc_row || !X->csc_val)))
         return ML_E_INVAL;
     const size_t need = ml_workspace_bytes(X->m, X->n, X->nnz);
     if (!ws || ws_bytes < need) return ML_E_WORKSPACE;
@@ -570,6 +571,7 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     P.m = (int)X->m;
     P.n = (int)X->n;
     P.y = X->y;
+    P.b = b;
     P.lam = lambda;
     ml_solve_opts o;
     ml_default_opts(&o);
@@ -665,11 +667,11 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     Ctl init;
     std::memset(&init, 0, sizeof(init));
     init.trace_cap = TRACE_CAP;
-    init.L = (double)X->m * std::log(2.0);
+    init.L = b ? 0.0 : (double)X->m * std::log(2.0);   // (the first margins pass recomputes L)
     init.F = init.L;
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
-    ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);
+    if (!b) ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);   // (squared loss: no labels)
     ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
     ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
@@ -696,6 +698,15 @@ ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws
     s = sync_ctl(c);
     *out = c;
     return s;
+}
+
+ml_status ml_create(const ml_data* X, double lambda, void* cuda_stream, void* ws, size_t ws_bytes, ml_ctx** out) {
+    return create_impl(X, nullptr, lambda, cuda_stream, ws, ws_bytes, out);
+}
+ml_status ml_create_lasso(const ml_data* X, const double* b, double lambda, void* cuda_stream, void* ws, size_t ws_bytes,
+                          ml_ctx** out) {
+    if (!b) return ML_E_INVAL;
+    return create_impl(X, b, lambda, cuda_stream, ws, ws_bytes, out);
 }
 
 ml_status ml_destroy(ml_ctx* c) {

@@ -166,6 +166,19 @@ __device__ __forceinline__ double dloss(double t, double delta) {
     if (fabs(delta) <= 1.0) return log1p(tau_neg(t) * expm1(-delta));
     return logloss(t + delta) - logloss(t);
 }
+// The sample loss of either instance of Eq. 1: logistic with labels y, or squared with targets b (the
+// LASSO of Eq. 2 with H = X^T X, g = -X^T b: ell_i = (z_i - b_i)^2 / 2, r_i = z_i - b_i, D_i = 1); b = nullptr selects
+// the logistic loss.  Multiplying by y = +-1 is exact, so the logistic values are bitwise those of row_state / dloss
+// with t = y z and delta = y dz.
+__device__ __forceinline__ RowState row_state_i(const int8_t* y, const double* b, int i, double z) {
+    if (b) { const double r = z - b[i]; return RowState{r, 1.0, 0.5 * r * r}; }
+    return row_state(z, (double)y[i]);
+}
+__device__ __forceinline__ double dloss_i(const int8_t* y, const double* b, int i, double z, double dz) {   // ell_i(z + dz) - ell_i(z)
+    if (b) { const double r = z - b[i]; return dz * (r + 0.5 * dz); }
+    const double yy = (double)y[i];
+    return dloss(yy * z, yy * dz);
+}
 __device__ __forceinline__ double soft(double t, double a) {   // Eq. 6
     double s = fabs(t) - a;
     if (s <= 0.0) return 0.0;

@@ -288,11 +288,10 @@ __device__ __noinline__ void ir_outer_batch2(const Prm& P, const PosState& X, in
         for (int k = 0; k < IR_NLS; ++k) { v[k] += fabs(w + a * d) - aw; a *= P.beta_ls; }
     }
     for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-        const double y = (double)P.y[i];
-        const double ti = y * P.z[i], yx = y * xd_r[i - r0];
+        const double zi = P.z[i], xd = xd_r[i - r0];
         double a = a4;
 #pragma unroll
-        for (int k = 0; k < IR_NLS; ++k) { v[IR_NLS + k] += dloss(ti, a * yx); a *= P.beta_ls; }
+        for (int k = 0; k < IR_NLS; ++k) { v[IR_NLS + k] += dloss_i(P.y, P.b, i, zi, a * xd); a *= P.beta_ls; }
     }
     ir_block_partials<2 * IR_NLS>(v, 0u, 0u, sh_w, part, IR_SO2);
 }
@@ -1115,10 +1114,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             for (int k = 0; k < 4; ++k) v[2 + k] += fabs(w + at[k] * d) - aw;
         }
         for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            const double y = (double)P.y[i];
-            const double ti = y * P.z[i], yx = y * xd_r[i - r0];
+            const double zi = P.z[i], xd = xd_r[i - r0];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[6 + k] += dloss(ti, at[k] * yx);
+            for (int k = 0; k < 4; ++k) v[6 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
         }
         ir_block_partials<10>(v, 1u << 1, 0u, sh_w, part, IR_SO);
     }
@@ -1162,7 +1160,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
             const double z = P.z[i] + alpha * xd_r[i - r0];
             P.z[i] = z;
-            const RowState st = row_state(z, (double)P.y[i]);
+            const RowState st = row_state_i(P.y, P.b, i, z);
             P.rD[i] = make_double2(st.r, st.D);
             v[0] += st.ell;
         }
@@ -1562,7 +1560,7 @@ __global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* sli
             double z = 0.0;
             for (int g2 = 0; g2 < ng; ++g2) z += gsum[g2 * nr + rr2];
             const int i = r0 + rr2;
-            const RowState st = row_state(z, (double)P.y[i]);
+            const RowState st = row_state_i(P.y, P.b, i, z);
             P.z[i] = z;
             P.rD[i] = make_double2(st.r, st.D);
             lsum += st.ell;

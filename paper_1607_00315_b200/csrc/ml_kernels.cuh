@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
 struct Prm {
     int m, n;
     const int8_t* y;
+    const double* b;   // squared loss (LASSO) targets; nullptr = logistic loss with labels y
     double lam, eps_h, sigma_in, sigma_out, beta_ls, tol, eta;
     int max_ls, inner_cg, pcd_snap, pad_p;
     double* w; uint32_t* wbits; double* z; double2* rD;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
         const int i = tile * TILE + threadIdx.x;
         if (i < P.m) {
             const double z = res[threadIdx.x].x;
-            const RowState st = row_state(z, (double)P.y[i]);
+            const RowState st = row_state_i(P.y, P.b, i, z);
             P.z[i] = z;
             P.rD[i] = make_double2(st.r, st.D);
             lsum += st.ell;
@@ -904,12 +905,10 @@ __global__ void __launch_bounds__(ML_NT) k_outer_ls(Prm P, ASet AS, int t0, int 
     } else {
         const int nb = gridDim.x - nblkA;
         for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
-            const double xd = P.Xd[i];
-            const double y = (double)P.y[i];
-            const double ti = y * P.z[i], yx = y * xd;
+            const double xd = P.Xd[i], zi = P.z[i];
 #pragma unroll
             for (int k = 0; k < NT1; ++k)
-                if (t0 + k < T1) r.s[1 + NT1 + k] += dloss(ti, at[k] * yx);
+                if (t0 + k < T1) r.s[1 + NT1 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
         }
     }
     if (grid_reduce(r, P.part, &c->red_ctr[5], sm)) {
@@ -957,7 +956,7 @@ __global__ void __launch_bounds__(ML_NT) k_update(Prm P, ASet AS, int nblkA) {
         for (int i = (blockIdx.x - nblkA) * ML_NT + threadIdx.x; i < P.m; i += nb * ML_NT) {
             const double z = P.z[i] + a * P.Xd[i];
             P.z[i] = z;
-            const RowState st = row_state(z, (double)P.y[i]);
+            const RowState st = row_state_i(P.y, P.b, i, z);
             P.rD[i] = make_double2(st.r, st.D);
             r.s[0] += st.ell;
         }

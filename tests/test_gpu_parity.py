@@ -56,6 +56,12 @@ def dataset(name):
         ds = mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40)
     elif name == "onehot":
         ds = mlgen.onehot(3000, 3)[0]
+    elif name == "lasso2s":    # squared loss (Q29) on the small-m dense design
+        ds = mlgen.lasso(mlgen.make(2, m=300, n=3000), 1, k=40, noise=0.5, lam_factor=0.1)
+    elif name == "lasso4s":    # squared loss on the large-m (global m-vector) path
+        ds = mlgen.lasso(mlgen.make(4, m=20000, n=40000), 2, k=200, noise=0.05, lam_factor=0.05)
+    elif name == "lasso_mid6k":
+        ds = mlgen.lasso(mlgen.make(3, m=6000, n=12000), 3, k=100, noise=0.05, lam_factor=0.05)
     elif name == "m1":
         ds = mlgen.from_dense(np.array([[0.5, -1.0, 2.0, 0.0, 1.5]], np.float32), np.array([1], np.int8), 0.1)
     elif name == "n1":
@@ -197,7 +203,9 @@ def _support_check(ds, w_g, w_o, g_o):
                                        ("cfg3s", {"multilevel": 0, "K_fine": 10}),
                                        ("cfg1", {"inner_cg": 0, "K_mid": 2, "K_coarse": 5}),
                                        ("cfg2s", {"continuation": 1}), ("cfg3s", {"continuation": 1}),
-                                       ("mid6k", {"continuation": 1}), ("onehot", {"continuation": 1})])
+                                       ("mid6k", {"continuation": 1}), ("onehot", {"continuation": 1}),
+                                       ("lasso2s", {}), ("lasso4s", {}), ("lasso_mid6k", {}),
+                                       ("lasso2s", {"continuation": 1}), ("lasso4s", {"multilevel": 0, "K_fine": 10})])
 def test_solve_parity(name, opts):
     """A9: ml_solve vs the oracle's solve (Algorithm 1 P:155-173 per P:798), both to kappa <= 1e-6."""
     ds = dataset(name)
@@ -270,7 +278,8 @@ def test_solve_parity_inner_variants(name, opts):
 
 @pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("mid6k", {}), ("cfg2s", {"inner_cg": 0}),
                                        ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0}),
-                                       ("cfg2s", {"continuation": 1}), ("cfg4s", {"continuation": 1})])
+                                       ("cfg2s", {"continuation": 1}), ("cfg4s", {"continuation": 1}),
+                                       ("lasso2s", {}), ("lasso4s", {})])
 def test_trace_parity(name, opts):
     """Relaxation by relaxation (Algorithm 1, DESIGN S1-S18/R1-R18): level, |A|, outcome, inner iterations and
     F after each of the first relaxations agree with the oracle's trace (decisions identical while rounding
@@ -374,3 +383,21 @@ def test_create_rejects_malformed_index():
     a = np.zeros((5, 4), np.float32)
     a[0, 1], a[3, 1], a[3, 3] = 1.0, 2.0, 3.0
     ml.Context(mlgen.from_dense(a, np.array([1, -1, 1, -1, 1], np.int8), 0.1))
+
+
+def test_lasso_orthogonal_closed_form_gpu():
+    """Squared loss (Q29) on an orthogonal (one-hot) design, n = 20000, no oracle involved:
+    w*_j = soft(x_j^T b, lam) / ||x_j||^2."""
+    base = mlgen.onehot(20000, 11)[0]
+    ds = mlgen.lasso(base, 6, k=2000, noise=0.5, lam_factor=0.1)
+    cp, ri, rv = base.csc_colptr, base.csc_row, base.csc_val.astype(np.float64)
+    xtb = np.add.reduceat(rv * ds.b[ri], cp[:-1])
+    nrm = np.add.reduceat(rv * rv, cp[:-1])
+    wref = np.sign(xtb) * np.maximum(np.abs(xtb) - ds.lam, 0.0) / nrm
+    ctx = ml.Context(ds)
+    r = ctx.ml_solve(ml.default_opts(tol_kkt=1e-12))
+    w = ctx.ml_get_w().cpu().numpy()
+    assert r["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    nz = wref != 0
+    assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-10

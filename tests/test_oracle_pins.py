@@ -516,3 +516,80 @@ def test_continuation_onehot_closed_form(multilevel):
     # the continuation stages use lambda_k > lambda: each stage's free set is no larger than the next stage's
     assert tr[0]["nA"] <= tr[1]["nA"] <= tr[2]["nA"] <= tr[3]["nA"]
     assert rep["relax_per_level"][0] >= 4
+
+
+# ----------------------------------------------------------------------------- squared loss (LASSO, Eq. 2; Q29)
+def _lasso_brute_force(X, b, lam):
+    """Enumerate supports S and signs s (3^n); on S the minimiser solves X_S^T X_S w_S = X_S^T b - lam s exactly;
+    accept iff the signs agree and |x_j^T (b - X_S w_S)| <= lam off S.  Returns (w*, F*)."""
+    m, n = X.shape
+    for k in range(n + 1):
+        for S in itertools.combinations(range(n), k):
+            S = list(S)
+            for sg in itertools.product((-1.0, 1.0), repeat=k):
+                sg = np.array(sg)
+                XS = X[:, S]
+                wS = np.linalg.solve(XS.T @ XS, XS.T @ b - lam * sg) if k else np.zeros(0)
+                if k and np.any(np.sign(wS) != sg):
+                    continue
+                res = b - XS @ wS
+                off = [j for j in range(n) if j not in S]
+                if off and np.max(np.abs(X[:, off].T @ res)) > lam * (1 + 1e-12):
+                    continue
+                w = np.zeros(n)
+                w[S] = wS
+                return w, 0.5 * res @ res + lam * np.abs(w).sum()
+    raise AssertionError("no KKT point found")
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("variant", [dict(), dict(multilevel=0), dict(continuation=1), dict(inner_cg=1, pcd_snap=0)])
+def test_lasso_brute_force_small(seed, variant):
+    """The squared-loss instance against exact support/sign enumeration on tiny data (every inner solver reaches
+    the unique minimiser; H = X^T X is positive definite for m > n)."""
+    rng = np.random.default_rng(300 + seed)
+    m, n = 30, 6
+    X = rng.standard_normal((m, n)).astype(np.float32)
+    base = mlgen.from_dense(X, np.ones(m, np.int8), 1.0)
+    ds = mlgen.lasso(base, seed, k=3, noise=0.3, lam_factor=0.2)
+    wref, Fref = _lasso_brute_force(X.astype(np.float64), ds.b, ds.lam)
+    o = oracle.Oracle(ds)
+    rep = o.solve(oracle.default_opts(**{"tol_kkt": 1e-12, "max_cycles": 2000, **variant}))
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    assert abs(rep["F"] - Fref) <= 1e-12 * Fref
+    assert np.max(np.abs(w - wref)) <= 1e-9 * max(1.0, np.max(np.abs(wref)))
+
+
+def test_lasso_orthogonal_design_closed_form():
+    """Orthogonal columns (one-hot design): the LASSO separates and w*_j = soft(x_j^T b, lam) / ||x_j||^2."""
+    base, a, p, q = mlgen.onehot(500, 9)
+    ds = mlgen.lasso(base, 4, k=60, noise=0.5, lam_factor=0.15)
+    cp, rv = base.csc_colptr, base.csc_val.astype(np.float64)
+    ri = base.csc_row
+    xtb = np.array([rv[cp[j]:cp[j + 1]] @ ds.b[ri[cp[j]:cp[j + 1]]] for j in range(base.n)])
+    nrm = np.array([rv[cp[j]:cp[j + 1]] @ rv[cp[j]:cp[j + 1]] for j in range(base.n)])
+    wref = np.sign(xtb) * np.maximum(np.abs(xtb) - ds.lam, 0.0) / nrm
+    o = oracle.Oracle(ds)
+    rep = o.solve(oracle.default_opts(tol_kkt=1e-12))
+    w = o.get_w()
+    assert rep["status"] == 0
+    assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
+    nz = wref != 0
+    assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-10
+
+
+def test_lasso_lambda_max_zero_solution():
+    """w = 0 is optimal iff lam >= lambda_max = ||X^T b||_inf (the squared loss's gradient at 0 is -X^T b)."""
+    base = mlgen.random_sparse(60, 40, 0.3, seed=3)
+    ds = mlgen.lasso(base, 2, k=5)
+    o = oracle.Oracle(ds.with_lambda(ds.lambda_max * (1 + 1e-9)))
+    rep = o.solve()
+    assert rep["status"] == 0 and rep["cycles"] == 0 and rep["nnz_w"] == 0
+    o2 = oracle.Oracle(ds.with_lambda(ds.lambda_max * (1 - 1e-3)))
+    rep2 = o2.solve()
+    assert rep2["status"] == 0 and rep2["nnz_w"] >= 1
+    F, g, h = o2.eval_f_grad()
+    assert np.allclose(h, np.array([np.sum(base.csc_val[base.csc_colptr[j]:base.csc_colptr[j + 1]].astype(np.float64) ** 2)
+                                    for j in range(base.n)]), rtol=1e-12)   # D = 1: h_j = ||x_j||^2
