@@ -41,6 +41,8 @@ typedef enum {
 
 typedef struct {                  /* X is m x n, rows = samples; 0 <= nnz < 2^31 */
     int64_t m, n, nnz;
+    /* CSR: may be all NULL when m <= 8192.  Up to that size every pass reads X by columns, including the margins
+       from the support's columns; ml_create returns ML_E_INVAL for a NULL CSR above it. */
     const int32_t *csr_rowptr;    /* [m+1] */
     const int32_t *csr_col;       /* [nnz], ascending inside each row */
     const float *csr_val;         /* [nnz] */

@@ -160,7 +160,8 @@ class Context:
     region).  All methods take / return torch CUDA tensors.
     """
 
-    def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None, host_tensors=None):
+    def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None, host_tensors=None,
+                 csr: bool = True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libml needs a CUDA device (no CPU fallback)")
@@ -173,14 +174,15 @@ class Context:
 
         if host_tensors is not None:   # pinned host tensors (rowptr, col, val, colptr, row, val, y): H2D copies
             (self.csr_rowptr, self.csr_col, self.csr_val, self.csc_colptr, self.csc_row, self.csc_val,
-             self.y) = (t.to(dev, non_blocking=True) for t in host_tensors)
+             self.y) = (None if t is None else t.to(dev, non_blocking=True) for t in host_tensors)
         else:
             def up(a, dt):
                 return torch.from_numpy(a).to(dev, dt)
 
-            self.csr_rowptr = up(ds.csr_rowptr, torch.int32)
-            self.csr_col = up(ds.csr_col, torch.int32)
-            self.csr_val = up(ds.csr_val, torch.float32)
+            # csr=False: columns only (accepted by ml_create for m <= 8192, include/ml.h)
+            self.csr_rowptr = up(ds.csr_rowptr, torch.int32) if csr else None
+            self.csr_col = up(ds.csr_col, torch.int32) if csr else None
+            self.csr_val = up(ds.csr_val, torch.float32) if csr else None
             self.csc_colptr = up(ds.csc_colptr, torch.int32)
             self.csc_row = up(ds.csc_row, torch.int32)
             self.csc_val = up(ds.csc_val, torch.float32)
@@ -188,7 +190,7 @@ class Context:
         self.stream = stream or torch.cuda.current_stream(dev)
         wsb = int(L.ml_workspace_bytes(self.m, self.n, self.nnz))
         self.ws = torch.empty(wsb + 512, dtype=torch.uint8, device=dev)
-        self.data = MLData(self.m, self.n, self.nnz, *[t.data_ptr() for t in (
+        self.data = MLData(self.m, self.n, self.nnz, *[0 if t is None else t.data_ptr() for t in (
             self.csr_rowptr, self.csr_col, self.csr_val, self.csc_colptr, self.csc_row, self.csc_val, self.y)])
         h = ctypes.c_void_p()
         self.b = None if getattr(ds, "b", None) is None else torch.from_numpy(np.asarray(ds.b, np.float64)).to(dev)
@@ -205,7 +207,8 @@ class Context:
 
     @classmethod
     def from_host(cls, ds, pinned, device="cuda:0"):
-        """Public entry with host buffers: H2D of X (CSR + CSC) and y from pinned memory, then ml_create."""
+        """Public entry with host buffers: H2D of X and y from pinned memory, then ml_create.  `pinned` lists
+        (csr_rowptr, csr_col, csr_val, csc_colptr, csc_row, csc_val, y); the CSR entries may be None for m <= 8192."""
         return cls(ds, device=device, host_tensors=pinned)
 
     # ------------------------------------------------------------------ helpers

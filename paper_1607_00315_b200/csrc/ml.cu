@@ -550,7 +550,9 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (X->m < 1 || X->n < 1 || X->nnz < 0 || X->nnz >= 2147483647LL || X->m >= 2147483647LL || X->n >= 2147483647LL)
         return ML_E_INVAL;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return ML_E_INVAL;
-    if (!X->csr_rowptr || !X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csr_col || !X->csr_val || !X->csc_row || !X->csc_val)))
+    const bool has_csr = X->csr_rowptr != nullptr;   // (optional when m <= SMALL_M: checked once the solver path is known)
+    if (!X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csc_row || !X->csc_val)) ||
+        (has_csr && X->nnz > 0 && (!X->csr_col || !X->csr_val)))
         return ML_E_INVAL;
     const size_t need = ml_workspace_bytes(X->m, X->n, X->nnz);
     if (!ws || ws_bytes < need) return ML_E_WORKSPACE;
@@ -658,6 +660,10 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
             c->inner_P = std::min(c->sms, IR_GMAX);
         }
     }
+    if (!has_csr && !c->sm_inner) {   // the large-m margins and heavy-row schedule read X by rows
+        delete c;
+        return ML_E_INVAL;
+    }
     // zero the control block, trace, bitmap, iterate and the heavy-unit counters
     cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st);
     cudaMemsetAsync(P.w, 0, sizeof(double) * X->n, c->st);
@@ -673,14 +679,15 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     if (!b) ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);   // (squared loss: no labels)
     ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
-    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
+    if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
         Units U = units_of(c, 0);
         ML_LAUNCH(c, k_units_build, c->gSeg, X->csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U, 8 * c->Gc);
         Units R = units_of(c, 3);
-        ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R, 8 * c->Gr);
+        if (has_csr)
+            ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R, 8 * c->Gr);
     }
     ml_status s = sync_ctl(c);
     if (s != ML_OK) { *out = c; return s; }

@@ -401,3 +401,21 @@ def test_lasso_orthogonal_closed_form_gpu():
     assert set(np.nonzero(w)[0]) == set(np.nonzero(wref)[0])
     nz = wref != 0
     assert np.max(np.abs(w[nz] - wref[nz]) / np.abs(wref[nz])) <= 1e-10
+
+
+def test_columns_only_context():
+    """include/ml.h: the CSR may be NULL for m <= 8192 (every pass reads X by columns there); the solve is bitwise
+    the one with both layouts.  Above that size ml_create rejects a missing CSR with ML_E_INVAL."""
+    ds = dataset("cfg2s")
+    a = ml.Context(ds)
+    ra = a.ml_solve()
+    b = ml.Context(ds, csr=False)
+    rb = b.ml_solve()
+    assert ra["F"] == rb["F"] and ra["cycles"] == rb["cycles"]
+    assert np.array_equal(a.ml_get_w().cpu().numpy(), b.ml_get_w().cpu().numpy())
+    F1, g1, h1 = a.ml_eval_f_grad()
+    F2, g2, h2 = b.ml_eval_f_grad()
+    assert F1 == F2 and torch.equal(g1, g2) and torch.equal(h1, h2)
+    with pytest.raises(ml.MLError) as e:
+        ml.Context(dataset("cfg4s"), csr=False)
+    assert "status 1" in str(e.value)
