@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     __shared__ int2 col_ext[IR_QC];
     __shared__ double pos_sh[7][IR_QS];   // wA gA hA d Hd s u of my positions (q <= IR_QS)
     __shared__ double row_sh[4][IR_RS];   // D, X s, X z, X d of my rows
+    __shared__ int s_res;                 // small m: all my column chunks stay in the S ring for the whole launch
     constexpr int SST = ir_sst(GSCH);
     cg::grid_group grid = cg::this_grid();
     Ctl* c = P.ctl;
@@ -489,7 +490,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         const bool need_hs = it < K - 1;
         ph_its += 1;
         const bool producer = threadIdx.x == blockDim.x - 32;   // lane 0 of the last warp (idle in D for small q)
-        if (!BIG && producer) pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
+        // small m: the first S-ring prefetch decides residency -- if it holds all my column chunks, S and G read
+        // them from shared memory for the whole relaxation (no TMA, no ring refills, G block-cooperative)
+        if (!BIG && producer && (it == 0 || !s_res)) {
+            pr.prefetch(S, SST, s_desc, s_idx, s_val, s_bar);   // overlaps the direction
+            if (it == 0) s_res = pr.p >= p1;
+        }
         PH_SUB(0);
         // ------------------------------------------------ D: direction on my positions
         int my_z = 0;
@@ -535,6 +541,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             ir_block_partials<12>(v, IR_DMAX, 0u, sh_w, part, IR_SD);
             my_z = pcd && sh_w[IR_W * 12 + 5] > 0.0;
         }
+        const bool resident = !BIG && s_res;   // (block-uniform; s_res is visible after the partials' barriers)
         PH_MARK(0);
         if (BIG) grid.sync();   // the units of my stream may belong to other blocks' positions
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
@@ -611,7 +618,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             __syncthreads();
             PH_SUB(2);
             uint32_t s_phase = 0u;
-            for (int st = 0;; st = (st + 1) % SST) {
+            for (int st = 0, used = 0;; st = (st + 1) % SST, ++used) {
+                if (resident && used == SST) break;   // (a resident ring is read once per pass, never refilled)
                 const SChunk d = s_desc[st];
                 if (!d.ok) break;
                 PH_SUB(3);
@@ -662,7 +670,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 PH_SUB(4);
                 __syncthreads();   // stage st consumed by every warp
                 PH_SUB(5);
-                if (producer) {
+                if (producer && !resident) {
                     SChunk nd;
                     if (pr.next(S, coef, nd)) { s_desc[st] = nd; pr.issue(S, nd, st, s_idx, s_val, s_bar); }
                     else s_desc[st].ok = 0;
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             __syncthreads();
             PH_SUB(3);
-            if (producer)
+            if (producer && !resident)
                 for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
             // my block partials (a block without zeroing columns writes zeros for X_A z)
             const int zpart = pcd && P.pcd_snap;
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if constexpr (BIG) grid.sync();   // B1
         else {   // B1, split: the G rings (aliasing the consumed S ring) are set up and issued while it completes
             const unsigned bar_old = gbar_arrive(&c->gbar);
-            if (need_hs) {
+            if (need_hs && !resident) {
                 if (lane == 0) {
                     for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
                     fence_mbar_init();
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (stop) {
             if (BIG)   // the scatter of this iteration is complete (B1): clear my rows for the next relaxation
                 for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) { P.Xu[r0 + k] = 0.0; P.Xzu[r0 + k] = 0.0; }
-            else if (need_hs) {   // drain the prefetched G rings
+            else if (need_hs && !resident) {   // drain the prefetched G rings
                 for (int stg2 = 0; stg2 < GST; ++stg2)
                     if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (g_phase >> stg2) & 1u); g_phase ^= 1u << stg2; }
                 __syncwarp();
@@ -881,7 +889,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         PH_MARK(4);
         if (stop) {
-            if (need_hs) {   // drain the prefetched rings
+            if (need_hs && !resident) {   // drain the prefetched rings
                 for (int stg2 = 0; stg2 < GST; ++stg2)
                     if (csG.desc[stg2].cf != 0.0) { mbar_wait(csG.bar + stg2, (g_phase >> stg2) & 1u); g_phase ^= 1u << stg2; }
                 __syncwarp();
@@ -1003,6 +1011,73 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;
             }
             PH_MARK(6);
+        } else if (need_hs && resident) {   // G from the resident chunks: each column's dot over the whole block
+            double* sv_sh = xs_sh;
+            for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 rows in flight per thread
+                double xs[8], xz[8], dd[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    xs[u] = i < m ? ld_cg(P.Xs + i) : 0.0;
+                    xz[u] = (zs && i < m) ? ld_cg(P.Xz + i) : 0.0;
+                    dd[u] = i < m ? P.rD[i].y : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < m) sv_sh[i] = dd[u] * (beta * xs[u] + (zs ? (1.0 - beta) * xz[u] : 0.0));
+                }
+            }
+            __syncthreads();
+            PH_MARK(5);
+            double acc[SST];
+#pragma unroll
+            for (int st = 0; st < SST; ++st) {   // chunk st: my elements k = vb + t + 256 u, in order
+                acc[st] = 0.0;
+                const SChunk d = s_desc[st];
+                if (d.ok) {
+                    const int* ci = s_idx + st * IR_SCH - d.a;
+                    const float* cv = s_val + st * IR_SCH - d.a;
+                    const int kend = min(d.ve, d.ce);
+                    double a = 0.0;
+#pragma unroll
+                    for (int u = 0; u < IR_SCH / 256; ++u) {
+                        const int k = d.vb + threadIdx.x + 256 * u;
+                        const bool in = k < kend;
+                        const double x = in ? (double)cv[k] : 0.0;
+                        const double sv = in ? sv_sh[ci[k]] : 0.0;
+                        a = fma(x, sv, a);
+                    }
+                    if (kend + (int)threadIdx.x < d.ve)   // the global tail past X's last 16-byte boundary
+                        a = fma((double)__ldg(S.val + kend + threadIdx.x), sv_sh[__ldg(S.idx + kend + threadIdx.x)], a);
+                    acc[st] = a;
+                    if (threadIdx.x == 0) nhs += d.ve - d.vb;
+                }
+            }
+            warp_reduce_slots<SST>(acc, 0u, 0u);
+            constexpr int SH = SlotPad<SST>::SH;
+            if ((lane & ((1 << SH) - 1)) == 0) sh_w[wid * SST + (lane >> SH)] = acc[0];
+            __syncthreads();
+            double* ctot = sh_w + IR_W * SST;
+            if (threadIdx.x < SST) {   // chunk totals, warps in order
+                double t = sh_w[threadIdx.x];
+#pragma unroll
+                for (int w = 1; w < IR_W; ++w) t += sh_w[w * SST + threadIdx.x];
+                ctot[threadIdx.x] = t;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my positions: their chunks in order, the step
+                double t = 0.0;
+#pragma unroll
+                for (int st = 0; st < SST; ++st)
+                    if (s_desc[st].ok && s_desc[st].p == p0 + k) t += ctot[st];
+                const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
+                const double x = X.wA[k] + X.d[k];
+                const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
+                X.Hd[k] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
+                X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;   // snapped coordinates become 0
+            }
+            PH_MARK(6);
         } else if (need_hs) {   // G: H sigma on my positions, then d += sigma, Hd += H sigma
             double* sv_sh = xs_sh;
             for (int i0 = threadIdx.x; i0 < m; i0 += 8 * blockDim.x) {   // 8 rows in flight per thread
@@ -1081,6 +1156,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         __syncthreads();   // my positions' d, Hd and the shared rings before the next direction
     }
+    if (!BIG && s_res && threadIdx.x == blockDim.x - 32)   // the resident ring's barriers
+        for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
     // accounting: X_A s scatters, Hs gathers
     {
         const long long s1 = warp_sum_ll(lane == 0 ? nsc : 0), s2 = warp_sum_ll(lane == 0 ? nhs : 0);
