@@ -1579,21 +1579,27 @@ __global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* sli
         const float* cv = s_val + st * IR_SCH - d.a;
         const int kend = min(d.ve, d.ce);
         constexpr int UB = IR_SCH / 256;
-        for (int k0 = d.vb + threadIdx.x; k0 < d.ve; k0 += UB * (int)blockDim.x) {   // rows distinct within a column
+        // rows distinct within a column; the staged part has branch-free (predicated) loads, the global tail past
+        // X's last 16-byte boundary (at most 3 nonzeros) its own loop (as in k_inner's S phase)
+        for (int k0 = d.vb + threadIdx.x; k0 < kend; k0 += UB * (int)blockDim.x) {
             int r[UB];
             double xv[UB], a[UB];
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
                 const int k = k0 + u * blockDim.x;
                 r[u] = -1;
+                xv[u] = 0.0;
                 if (k < kend) { r[u] = ci[k]; xv[u] = (double)cv[k]; }
-                else if (k < d.ve) { r[u] = __ldg(S.idx + k); xv[u] = (double)__ldg(S.val + k); }
             }
 #pragma unroll
             for (int u = 0; u < UB; ++u) a[u] = r[u] >= 0 ? xs_sh[r[u]] : 0.0;
 #pragma unroll
             for (int u = 0; u < UB; ++u)
                 if (r[u] >= 0) xs_sh[r[u]] = fma(xv[u], cf, a[u]);
+        }
+        for (int k = kend + threadIdx.x; k < d.ve; k += blockDim.x) {
+            const int r = __ldg(S.idx + k);
+            xs_sh[r] = fma((double)__ldg(S.val + k), cf, xs_sh[r]);
         }
         if (threadIdx.x == 0) nsc += d.ve - d.vb;
         __syncthreads();
