@@ -141,6 +141,11 @@ ml_status ml_profile_read(ml_ctx *c, double *ms_host, int64_t *passes_host, int6
    0-6 for relaxations with |A| < 2048, 8-14 for larger ones: direction, X_A s scatter, barrier + totals, row sums,
    barrier + totals + step decision, D o X sigma to shared memory, Hs stream + step; 7 and 15 unused. */
 ml_status ml_inner_phases(ml_ctx *c, uint64_t *ns_host, int reset);
+/* Batched replicas: the context's cooperative (persistent) kernels use at most `blocks` CTAs
+   (one per SM; <= 0 or more than the SM count restores the whole GPU).  Several contexts on their own streams, each
+   driven by its own host thread, then solve side by side: small problems are latency-bound on the whole GPU.
+   ML_E_INVAL if the small-m solver would own more than 64 rows per block (m > 64 blocks). */
+ml_status ml_set_sm_share(ml_ctx *c, int blocks);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */
 int64_t ml_trace(ml_ctx *c, void *rows_host, int64_t cap);

@@ -74,7 +74,7 @@ class TraceRow(ctypes.Structure):
 EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_create_lasso", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
            "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
-           "ml_profile_read", "ml_inner_phases"]
+           "ml_profile_read", "ml_inner_phases", "ml_set_sm_share"]
 
 _lib = None
 
@@ -129,6 +129,8 @@ def load(path: str | None = None):
     L.ml_profile_read.argtypes = [P, P, P, P, P]
     L.ml_inner_phases.restype = i32
     L.ml_inner_phases.argtypes = [P, P, i32]
+    L.ml_set_sm_share.restype = i32
+    L.ml_set_sm_share.argtypes = [P, i32]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
     _lib = L
@@ -308,6 +310,9 @@ class Context:
         self._check(load().ml_profile_read(self.h, ms, ps, nz, sg))
         return {name: {"ms": ms[k], "passes": ps[k], "nnz": nz[k], "segs": sg[k]}
                 for k, name in enumerate(self.CLASSES)}
+
+    def ml_set_sm_share(self, blocks):
+        return self._check(load().ml_set_sm_share(self.h, int(blocks)))
 
     def ml_inner_phases(self, reset=True):
         ns = (ctypes.c_uint64 * 16)()

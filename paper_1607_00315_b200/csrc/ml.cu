@@ -76,6 +76,7 @@ struct ml_ctx {
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // the k_inner instantiation in use
     int sms = SM_COUNT;               // the device's SM count (cooperative grids: one CTA per SM)
+    int coop_cap = SM_COUNT;          // cooperative grids use at most this many CTAs (ml_set_sm_share)
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
     size_t gsmall_bytes = 0;
     const void* msmall_fn = nullptr;   // k_margins_small<GSCH>
@@ -486,7 +487,7 @@ void launch_select(ml_ctx* c, SelIn in, int nin_host, int L, const std::vector<i
     // targets / offsets travel as kernel arguments (no host->device copies); one cooperative launch, a block per
     // 256 candidates (at most one per SM)
     PassScope ps(c, CLS_SELECT);
-    int G = std::max(1, std::min(c->sms, (nin_host + ML_NT - 1) / ML_NT));
+    int G = std::max(1, std::min(c->coop_cap, (nin_host + ML_NT - 1) / ML_NT));
     SelState* stp = c->sel;
     int Lv = L;
     void* args[] = {(void*)&in, (void*)&stp, (void*)&Lv, (void*)&T, (void*)&out, (void*)&O};
@@ -564,6 +565,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
         int dev = 0, sms = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
             c->sms = std::min(sms, SM_COUNT);   // (the partial buffers are sized for at most SM_COUNT blocks)
+        c->coop_cap = c->sms;
     }
     c->ws = (char*)align_up((size_t)ws);
     c->ws_bytes = ws_bytes;
@@ -1010,6 +1012,21 @@ ml_status ml_profile_read(ml_ctx* c, double* ms, int64_t* passes, int64_t* nnz, 
 }
 
 // diagnostics: ns per phase of the persistent inner solver (block 0), accumulated since the last reset
+// Batched replicas: cap the cooperative grids (k_inner, k_gather_small, k_margins_small,
+// k_select_coop) at `blocks` CTAs, so that several contexts on their own streams run side by side on one GPU.
+ml_status ml_set_sm_share(ml_ctx* c, int blocks) {
+    if (!c) return ML_E_INVAL;
+    const int full = std::min(c->sms, IR_GMAX);
+    if (blocks <= 0 || blocks > c->sms) blocks = c->sms;
+    if (c->sm_inner && c->X.m > (int64_t)IR_RS * std::min(blocks, IR_GMAX)) {   // k_inner: at most IR_RS rows per block
+        c->err = "ml_set_sm_share: too few blocks for m (at most 64 rows per block on the small-m path)";
+        return ML_E_INVAL;
+    }
+    c->coop_cap = blocks;
+    if (c->sm_inner || c->big_inner) c->inner_P = std::min(blocks, full);
+    return ML_OK;
+}
+
 ml_status ml_inner_phases(ml_ctx* c, uint64_t* ns_host, int reset) {
     if (!c) return ML_E_INVAL;
     ml_status s = sync_ctl(c);

@@ -419,3 +419,34 @@ def test_columns_only_context():
     with pytest.raises(ml.MLError) as e:
         ml.Context(dataset("cfg4s"), csr=False)
     assert "status 1" in str(e.value)
+
+
+def test_replicas_side_by_side():
+    """ml_set_sm_share (batched replicas): two contexts on their own streams and host threads, each
+    with half of the SMs, solve concurrently and both match the oracle; a share too small for m is rejected."""
+    import threading
+    ds = dataset("cfg2s")
+    r_o = oracle.Oracle(ds).solve()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    ctxs = [ml.Context(ds, stream=s) for s in streams]
+    for c in ctxs:
+        c.ml_set_sm_share(sms // 2)
+    out = [None, None]
+
+    def work(k):
+        out[k] = [ctxs[k].ml_solve() for _ in range(3)]
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for rs in out:
+        for r in rs:
+            assert r["status"] == 0 and r["kappa"] <= 1e-6
+            assert abs(r["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+    big = ml.Context(dataset("mid6k"))   # m = 6000 on the small-m path: needs >= 94 blocks (64 rows each)
+    with pytest.raises(ml.MLError):
+        big.ml_set_sm_share(16)
+    big.ml_set_sm_share(0)   # the whole GPU again
