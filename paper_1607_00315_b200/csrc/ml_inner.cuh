@@ -1030,7 +1030,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             __syncthreads();
             PH_MARK(5);
-            double acc[SST];
+            constexpr int NPG = SlotPad<SST>::NP;   // (the butterfly takes a power of two of slots)
+            double acc[NPG];
+#pragma unroll
+            for (int st = SST; st < NPG; ++st) acc[st] = 0.0;
 #pragma unroll
             for (int st = 0; st < SST; ++st) {   // chunk st: my elements k = vb + t + 256 u, in order
                 acc[st] = 0.0;
@@ -1054,15 +1057,15 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     if (threadIdx.x == 0) nhs += d.ve - d.vb;
                 }
             }
-            warp_reduce_slots<SST>(acc, 0u, 0u);
-            constexpr int SH = SlotPad<SST>::SH;
-            if ((lane & ((1 << SH) - 1)) == 0) sh_w[wid * SST + (lane >> SH)] = acc[0];
+            warp_reduce_slots<NPG>(acc, 0u, 0u);
+            constexpr int SH = SlotPad<NPG>::SH;
+            if ((lane & ((1 << SH) - 1)) == 0) sh_w[wid * NPG + (lane >> SH)] = acc[0];
             __syncthreads();
-            double* ctot = sh_w + IR_W * SST;
+            double* ctot = sh_w + IR_W * NPG;
             if (threadIdx.x < SST) {   // chunk totals, warps in order
                 double t = sh_w[threadIdx.x];
 #pragma unroll
-                for (int w = 1; w < IR_W; ++w) t += sh_w[w * SST + threadIdx.x];
+                for (int w = 1; w < IR_W; ++w) t += sh_w[w * NPG + threadIdx.x];
                 ctot[threadIdx.x] = t;
             }
             __syncthreads();
