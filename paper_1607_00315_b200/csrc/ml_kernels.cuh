@@ -324,7 +324,9 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
 // The last block to finish: nA, vmax, the convergence decision (R2), counters reset, epoch advance.
 template <int G, bool FINEST>
 __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, long long* acc) {
-    constexpr int SUP = 4;   // tiles per claim: one look-back per SUP tiles
+    // tiles per claim: one look-back per SUP tiles.  Coarse sets are small (tens of tiles): one tile per claim keeps
+    // every tile's block busy (4 per claim left a 13 k-column coarse set on 13 blocks)
+    constexpr int SUP = FINEST ? 4 : 1;
     __shared__ double2 res[TILE];
     __shared__ int s_tile, s_excl;
     __shared__ int s_wcnt[SUP][ML_NW];
