@@ -120,7 +120,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* Xzu = cv.take<double>(mm);
     double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
     double2* tilepart = cv.take<double2>(ntile_n + 1);
-    unsigned long long* status = cv.take<unsigned long long>(std::max(ntile_n, ntile_m) + 1);
+    unsigned long long* status = cv.take<unsigned long long>(std::max((nn + 63) / 64, ntile_m) + 1);   // (64-column coarse tiles)
     double2* hres = cv.take<double2>(std::max(nn, mm));
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
@@ -396,7 +396,8 @@ void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* lis
     }
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
               (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
-    const int grid = std::max(1, std::min(GRID_CAP, (nC_host + TILE - 1) / TILE));
+    const int ts = finest ? TILE : 64;   // (k_gather_free's tile size)
+    const int grid = std::max(1, std::min(GRID_CAP, (nC_host + ts - 1) / ts));
     if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, acc_of(c, cls))); }
     else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, acc_of(c, cls))); }
 }

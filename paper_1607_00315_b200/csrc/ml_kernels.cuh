@@ -124,15 +124,18 @@ __device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int
 // One tile of TILE consecutive segment positions; results (a0, a1) land in res[slot] (shared memory).
 // The tile's segment bounds are loaded once, in parallel (one thread per segment), so the G rounds only stream.
 // Heavy segments (> S.split) are not streamed here: their results come from S.hres, written by k_heavy.
-template <int G, class Op>
+// TS (segments per tile, a multiple of ML_NT / G, at most TILE): smaller tiles spread a short segment list over more
+// blocks (the coarse free-set gathers of the large-m path)
+template <int G, class Op, int TS = TILE>
 __device__ __forceinline__ void seg_tile(const Seg& S, const Op& op, int nseg, int tile, double2* res, long long& streamed,
                                          long long& segs) {
     constexpr int NG = ML_NT / G;
+    static_assert(TS % NG == 0 && TS <= TILE, "tile size");
     __shared__ int sb[TILE], se[TILE];
     {
-        const int p = tile * TILE + threadIdx.x;
+        const int p = tile * TS + threadIdx.x;
         int b = 0, e = 0;
-        if (p < nseg) {
+        if (threadIdx.x < TS && p < nseg) {
             const int j = S.list ? __ldg(S.list + p) : p;
             b = __ldg(S.ptr + j);
             e = __ldg(S.ptr + j + 1);
@@ -146,7 +149,7 @@ __device__ __forceinline__ void seg_tile(const Seg& S, const Op& op, int nseg, i
     __syncthreads();
     const int grp = threadIdx.x / G, lane = threadIdx.x % G;
 #pragma unroll 1
-    for (int r = 0; r < G; ++r) {
+    for (int r = 0; r < TS / NG; ++r) {
         const int slot = r * NG + grp;
         const int b = sb[slot], e = se[slot];
         double a0 = 0.0, a1 = 0.0;
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
     // tiles per claim: one look-back per SUP tiles.  Coarse sets are small (tens of tiles): one tile per claim keeps
     // every tile's block busy (4 per claim left a 13 k-column coarse set on 13 blocks)
     constexpr int SUP = FINEST ? 4 : 1;
+    constexpr int TS = FINEST ? TILE : 64;   // columns per tile (coarse: 64, so a 3.5 k-column set spans 55 blocks)
     __shared__ double2 res[TILE];
     __shared__ int s_tile, s_excl;
     __shared__ int s_wcnt[SUP][ML_NW];
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
     Ctl* ctl = P.ctl;
     if (ctl->skip) return;   // (not used at the finest level; coarse relaxations of a converged level)
     const int nC = S.list ? ctl->nC : P.n;
-    const int ntiles = (nC + TILE - 1) / TILE;
+    const int ntiles = (nC + TS - 1) / TS;
     const int nsup = (ntiles + SUP - 1) / SUP;
     const unsigned epoch = ctl->epoch;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -355,10 +359,10 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
             const int tile = sup * SUP + t;
             jj[t] = 0; flag[t] = 0; gg[t] = 0.0; hh[t] = 0.0; ww[t] = 0.0;
             if (tile < ntiles) {   // (uniform over the block)
-                seg_tile<G>(S, op, nC, tile, res, streamed, segs);
+                seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
                 __syncthreads();
-                const int p = tile * TILE + threadIdx.x;
-                if (p < nC) {
+                const int p = tile * TS + threadIdx.x;
+                if (threadIdx.x < TS && p < nC) {
                     const int j = S.list ? S.list[p] : p;
                     jj[t] = j;
                     gg[t] = res[threadIdx.x].x;
