@@ -587,6 +587,13 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     c->gM = std::max(1, std::min(GRID_CAP, (int)((X->m + ML_NT - 1) / ML_NT)));
     c->gSeg = std::max(1, std::min(GRID_CAP, (int)((X->n + ML_NT - 1) / ML_NT)));
     c->gHeavy = std::max(1, std::min(GRID_CAP, (int)((X->nnz / CHUNK + std::min<int64_t>(std::max(X->m, X->n), X->nnz / SPLIT_MIN) + 8) / ML_NW + 1)));
+    {   // whole waves only: the unit loop is grid-strided, so a partial second wave (592 blocks at 3 per SM) only
+        // delays the blocks that start late
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_heavy<OpGH, false>, ML_NT, 0) == cudaSuccess && occ > 0)
+            c->gHeavy = std::max(1, std::min(c->gHeavy, occ * c->sms));
+        cudaGetLastError();
+    }
     if (X->m <= SMALL_M) {   // shared-memory passes: W warps per block, private m-vectors / shared sv + TMA rings
         int W = 16;
         while (W > 1 && scatter_smem_bytes(W, (int)X->m) > 200 * 1024) --W;
