@@ -251,9 +251,9 @@ def test_lambda_max_zero_solution_gpu():
     assert r["status"] == 0 and r["cycles"] == 0 and r["nnz_w"] == 0
 
 
-@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
 def test_solve_parity_full_configs(name):
-    """Solve parity at BASELINE configs 2 and 3 (full size)."""
+    """Solve parity at BASELINE configs 2, 3 and 4 (full size; cfg 4's oracle solve takes ~20-40 s on one core)."""
     ds = mlgen.make(int(name[-1]))
     o = oracle.Oracle(ds)
     r_o = o.solve()
