@@ -332,8 +332,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nA = c->nA;
     const int ph_off = nA < 2048 ? 0 : IR_PHN / 2;
-    const int q = (nA + G - 1) / G;
-    const int p0 = min(nA, (int)blockIdx.x * q), p1 = min(nA, p0 + q);
+    // balanced contiguous position ranges: nA / G each, one more for the first nA % G blocks (the coarse free sets
+    // are written interleaved by k_gather_small, so that a block's range holds every G-th column of the level)
+    const int qb = nA / G, rb = nA % G;
+    const int p0 = (int)blockIdx.x * qb + min((int)blockIdx.x, rb), p1 = p0 + qb + ((int)blockIdx.x < rb ? 1 : 0);
     const int R = (m + G - 1) / G;
     const int r0 = min(m, (int)blockIdx.x * R), r1 = min(m, r0 + R);
     double* part = P.irpart;
@@ -1460,7 +1462,12 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
         int woff = 0, tot = 0;
         for (int w = 0; w < IR_W; ++w) { if (w < wid) woff += sh_cnt[w]; tot += sh_cnt[w]; }
         if (flag) {
-            const int o = base + woff + __popc(bal & ((1u << lane) - 1u));
+            int o = base + woff + __popc(bal & ((1u << lane) - 1u));
+            if (!FINEST) {   // coarse: interleave, column o goes to k_inner's block o mod G (balanced ranges, see
+                             // k_inner): a PCD-CG step's active columns spread evenly over the blocks
+                const int qb = nA / G, rb = nA % G, bb = o % G;
+                o = bb * qb + min(bb, rb) + o / G;
+            }
             AS.A[o] = j;
             AS.gA[o] = g;
             AS.hA[o] = (one_pass ? h1 : AS.Hs[p]) + P.eps_h;
