@@ -105,7 +105,8 @@ ml_status ml_get_w(ml_ctx *c, double *w_dev);
 /* per-sample state after the last evaluation/update: z, r, D (each [m], device; NULL skips) */
 ml_status ml_get_rows(ml_ctx *c, double *z_dev, double *r_dev, double *D_dev);
 
-/* A1 + A2: margins z = Xw from scratch (CSR pass) with fused tau, D, r, loss; F = L + lambda||w||_1;
+/* A1 + A2: margins z = Xw from scratch (CSR pass; for m <= 8192 from the support's CSC columns) with
+   fused tau, D, r, loss; F = L + lambda||w||_1;
    then g_C = X_C^T r and h_C = sum_i X_ij^2 D_i over C (CSC gather).  F_host may be NULL; g_C / h_C may be NULL. */
 ml_status ml_eval_f_grad(ml_ctx *c, const int32_t *C, int64_t nC, double *F_host, double *g_C, double *h_C);
 /* h_C = sum_i X_ij^2 D_i with D from the current state. */
@@ -139,7 +140,8 @@ ml_status ml_profile(ml_ctx *c, uint32_t class_mask);
 ml_status ml_profile_read(ml_ctx *c, double *ms_host, int64_t *passes_host, int64_t *nnz_host, int64_t *segs_host);
 /* Diagnostics: nanoseconds spent per phase of the persistent small-m inner solver, 16 entries (block 0): entries
    0-6 for relaxations with |A| < 2048, 8-14 for larger ones: direction, X_A s scatter, barrier + totals, row sums,
-   barrier + totals + step decision, D o X sigma to shared memory, Hs stream + step; 7 and 15 unused. */
+   barrier + totals + step decision, D o X sigma to shared memory, Hs stream + step; 7 and 15: the outer line
+   search and update that end each relaxation (R14-R18). */
 ml_status ml_inner_phases(ml_ctx *c, uint64_t *ns_host, int reset);
 /* Batched replicas: the context's cooperative (persistent) kernels use at most `blocks` CTAs
    (one per SM; <= 0 or more than the SM count restores the whole GPU).  Several contexts on their own streams, each
