@@ -61,7 +61,10 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 // 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
 constexpr int IR_NLS = ML_MAXLS - 4;
 enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 };   // IR_SU, +1: unit counts, nnz (BIG)
-constexpr int IR_UNIT = 2048;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
+#ifndef IR_UNIT_V
+#define IR_UNIT_V 2048
+#endif
+constexpr int IR_UNIT = IR_UNIT_V;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
 constexpr int IR_UCOST = 1024;   // BIG: a unit's fixed cost in nonzeros (TMA issue, barrier wait) for the balance
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
