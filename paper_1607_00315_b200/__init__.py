@@ -94,8 +94,9 @@ def load(path: str | None = None):
     L.ml_workspace_bytes.argtypes = [i64, i64, i64]
     L.ml_create.restype = i32
     L.ml_create.argtypes = [ctypes.POINTER(MLData), d, P, P, ctypes.c_size_t, ctypes.POINTER(P)]
-    L.ml_create_lasso.restype = i32
-    L.ml_create_lasso.argtypes = [ctypes.POINTER(MLData), P, d, P, P, ctypes.c_size_t, ctypes.POINTER(P)]
+    if hasattr(L, "ml_create_lasso"):   # (older builds, e.g. ML_LIB bisection, predate these entry points)
+        L.ml_create_lasso.restype = i32
+        L.ml_create_lasso.argtypes = [ctypes.POINTER(MLData), P, d, P, P, ctypes.c_size_t, ctypes.POINTER(P)]
     for f in ("ml_destroy",):
         getattr(L, f).restype = i32
         getattr(L, f).argtypes = [P]
@@ -129,8 +130,9 @@ def load(path: str | None = None):
     L.ml_profile_read.argtypes = [P, P, P, P, P]
     L.ml_inner_phases.restype = i32
     L.ml_inner_phases.argtypes = [P, P, i32]
-    L.ml_set_sm_share.restype = i32
-    L.ml_set_sm_share.argtypes = [P, i32]
+    if hasattr(L, "ml_set_sm_share"):
+        L.ml_set_sm_share.restype = i32
+        L.ml_set_sm_share.argtypes = [P, i32]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
     _lib = L

@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                                 if (r[u] >= 0) xz_sh[r[u]] = fma(xv[u], cf, a[u]);
                         }
                     }
-                    for (int k = kend + threadIdx.x; k < d.ve; k += blockDim.x) {
+                    for (int k = max(kend, d.vb) + threadIdx.x; k < d.ve; k += blockDim.x) {   // (a chunk may start past kend)
                         const int r = __ldg(S.idx + k);
                         const double xv = (double)__ldg(S.val + k);
                         xs_sh[r] = fma(xv, cf, xs_sh[r]);
@@ -1056,8 +1056,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         const double sv = in ? sv_sh[ci[k]] : 0.0;
                         a = fma(x, sv, a);
                     }
-                    if (kend + (int)threadIdx.x < d.ve)   // the global tail past X's last 16-byte boundary
-                        a = fma((double)__ldg(S.val + kend + threadIdx.x), sv_sh[__ldg(S.idx + kend + threadIdx.x)], a);
+                    const int kt = max(kend, d.vb) + (int)threadIdx.x;   // the global tail past X's last 16-byte
+                    if (kt < d.ve)                                          // boundary (a chunk may start past kend)
+                        a = fma((double)__ldg(S.val + kt), sv_sh[__ldg(S.idx + kt)], a);
                     acc[st] = a;
                     if (threadIdx.x == 0) nhs += d.ve - d.vb;
                 }
@@ -1610,7 +1611,7 @@ __global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* sli
             for (int u = 0; u < UB; ++u)
                 if (r[u] >= 0) xs_sh[r[u]] = fma(xv[u], cf, a[u]);
         }
-        for (int k = kend + threadIdx.x; k < d.ve; k += blockDim.x) {
+        for (int k = max(kend, d.vb) + threadIdx.x; k < d.ve; k += blockDim.x) {   // (a chunk may start past kend)
             const int r = __ldg(S.idx + k);
             xs_sh[r] = fma((double)__ldg(S.val + k), cf, xs_sh[r]);
         }

@@ -62,6 +62,22 @@ def dataset(name):
         ds = mlgen.lasso(mlgen.make(4, m=20000, n=40000), 2, k=200, noise=0.05, lam_factor=0.05)
     elif name == "lasso_mid6k":
         ds = mlgen.lasso(mlgen.make(3, m=6000, n=12000), 3, k=100, noise=0.05, lam_factor=0.05)
+    elif name.startswith("tail"):   # X's last nonzeros past its last 16-byte boundary, in a short last column (the
+        # chunk of that column starts after the staged part ends: its elements come from the global tail)
+        r = int(name[4:])
+        rng = np.random.default_rng(40 + r)
+        X = rng.standard_normal((300, 40)).astype(np.float32)
+        X[rng.random(X.shape) > 0.15] = 0.0
+        X[:, -1] = 0.0
+        k = max(1, r - 1)                        # the last column's nonzeros: it starts past the 16-byte boundary
+        i = 0
+        while (int(np.count_nonzero(X)) + k) % 4 != r:   # nnz = r mod 4
+            X[i, 0] = 0.0 if X[i, 0] != 0.0 else 1.0
+            i += 1
+        X[:k, -1] = rng.uniform(0.5, 1.5, k)
+        y = np.where(X @ rng.standard_normal(40) + 0.3 * rng.standard_normal(300) > 0, 1, -1).astype(np.int8)
+        lmax = 0.5 * np.max(np.abs(X.astype(np.float64).T @ y))
+        ds = mlgen.from_dense(X, y, 0.05 * lmax, name=name)
     elif name == "m1":
         ds = mlgen.from_dense(np.array([[0.5, -1.0, 2.0, 0.0, 1.5]], np.float32), np.array([1], np.int8), 0.1)
     elif name == "n1":
@@ -205,7 +221,8 @@ def _support_check(ds, w_g, w_o, g_o):
                                        ("cfg2s", {"continuation": 1}), ("cfg3s", {"continuation": 1}),
                                        ("mid6k", {"continuation": 1}), ("onehot", {"continuation": 1}),
                                        ("lasso2s", {}), ("lasso4s", {}), ("lasso_mid6k", {}),
-                                       ("lasso2s", {"continuation": 1}), ("lasso4s", {"multilevel": 0, "K_fine": 10})])
+                                       ("lasso2s", {"continuation": 1}), ("lasso4s", {"multilevel": 0, "K_fine": 10}),
+                                       ("tail3", {"multilevel": 0}), ("tail2", {"continuation": 1})])
 def test_solve_parity(name, opts):
     """A9: ml_solve vs the oracle's solve (Algorithm 1 P:155-173 per P:798), both to kappa <= 1e-6."""
     ds = dataset(name)
@@ -279,7 +296,8 @@ def test_solve_parity_inner_variants(name, opts):
 @pytest.mark.parametrize("name,opts", [("cfg2s", {}), ("cfg4s", {}), ("onehot", {}), ("mid6k", {}), ("cfg2s", {"inner_cg": 0}),
                                        ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0}),
                                        ("cfg2s", {"continuation": 1}), ("cfg4s", {"continuation": 1}),
-                                       ("lasso2s", {}), ("lasso4s", {})])
+                                       ("lasso2s", {}), ("lasso4s", {}),
+                                       ("tail1", {}), ("tail2", {}), ("tail3", {}), ("tail3", {"inner_cg": 0})])
 def test_trace_parity(name, opts):
     """Relaxation by relaxation (Algorithm 1, DESIGN S1-S18/R1-R18): level, |A|, outcome, inner iterations and
     F after each of the first relaxations agree with the oracle's trace (decisions identical while rounding
