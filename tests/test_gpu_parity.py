@@ -468,3 +468,25 @@ def test_replicas_side_by_side():
     with pytest.raises(ml.MLError):
         big.ml_set_sm_share(16)
     big.ml_set_sm_share(0)   # the whole GPU again
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303])
+def test_random_designs_parity(seed):
+    """Randomised solve parity (tools/random_parity.py in small): random shapes on both solver paths, densities,
+    empty rows / columns, logistic or squared loss, option sets; GPU and oracle both converge to the same F."""
+    rng = np.random.default_rng(seed)
+    pool = [{}, {"inner_cg": 1, "pcd_snap": 0}, {"multilevel": 0}, {"continuation": 1}]
+    for _ in range(4):
+        m = int(rng.choice([37, 300, 777, 2000, 9000]))
+        n = int(rng.choice([13, 150, 1301]))
+        base = mlgen.random_sparse(m, n, float(rng.choice([0.01, 0.05, 0.3])), seed=int(rng.integers(1 << 30)),
+                                   lam_factor=float(rng.choice([0.05, 0.1, 0.3])),
+                                   empty_rows=int(rng.integers(0, min(5, m // 2) + 1)),
+                                   empty_cols=int(rng.integers(0, min(20, n // 2) + 1)))
+        ds = mlgen.lasso(base, int(rng.integers(1 << 30)), k=5) if rng.random() < 0.3 else base
+        opts = pool[int(rng.integers(len(pool)))]
+        r_o = oracle.Oracle(ds).solve(oracle.default_opts(**opts))
+        r_g = ml.Context(ds).ml_solve(ml.default_opts(**opts))
+        assert r_o["status"] == r_g["status"] == 0, (m, n, opts, r_o["status"], r_g["status"])
+        assert r_g["kappa"] <= 1e-6
+        assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"]), (m, n, opts, r_g["F"], r_o["F"])
