@@ -165,7 +165,7 @@ class Context:
     """
 
     def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None, host_tensors=None,
-                 csr: bool = True):
+                 csr: bool = True, ws_fill: int | None = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libml needs a CUDA device (no CPU fallback)")
@@ -194,6 +194,12 @@ class Context:
         self.stream = stream or torch.cuda.current_stream(dev)
         wsb = int(L.ml_workspace_bytes(self.m, self.n, self.nnz))
         self.ws = torch.empty(wsb + 512, dtype=torch.uint8, device=dev)
+        if ws_fill is not None:   # (tests: a workspace that held other data before; ml_create must not depend on it)
+            words = self.ws[: (wsb + 512) // 8 * 8].view(torch.int64)
+            if ws_fill == "epochs":   # look-back status words of epochs 0..63 (flag 1, count 5), cycling
+                words.copy_(((torch.arange(words.numel(), device=dev, dtype=torch.int64) % 64) << 34) | (1 << 32) | 5)
+            else:
+                words.fill_(int(ws_fill))
         self.data = MLData(self.m, self.n, self.nnz, *[0 if t is None else t.data_ptr() for t in (
             self.csr_rowptr, self.csr_col, self.csr_val, self.csc_colptr, self.csc_row, self.csc_val, self.y)])
         h = ctypes.c_void_p()

@@ -99,6 +99,11 @@ struct ml_ctx {
 
 namespace {
 
+// look-back status words of the compaction tiles: 64-column coarse tiles and 256-row / -column tiles (all zeroed at
+// create: the words are epoch-tagged, and a stale word from another use of the memory must not match epoch 0)
+inline size_t status_words(int64_t n, int64_t m) {
+    return std::max<size_t>(((size_t)n + 63) / 64, ((size_t)m + TILE - 1) / TILE) + 2;
+}
 void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     const size_t nn = (size_t)n, mm = (size_t)m;
     const size_t ntile_n = (nn + TILE - 1) / TILE, ntile_m = (mm + TILE - 1) / TILE;
@@ -120,7 +125,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* Xzu = cv.take<double>(mm);
     double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
     double2* tilepart = cv.take<double2>(ntile_n + 1);
-    unsigned long long* status = cv.take<unsigned long long>(std::max((nn + 63) / 64, ntile_m) + 1);   // (64-column coarse tiles)
+    unsigned long long* status = cv.take<unsigned long long>(status_words(n, m));   // (64-column coarse tiles)
     double2* hres = cv.take<double2>(std::max(nn, mm));
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
@@ -678,7 +683,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st);
     cudaMemsetAsync(P.w, 0, sizeof(double) * X->n, c->st);
     cudaMemsetAsync(P.wbits, 0, sizeof(uint32_t) * ((X->n + 31) / 32 + 1), c->st);
-    cudaMemsetAsync(P.status, 0, sizeof(unsigned long long) * (std::max(X->n, X->m) / TILE + 2), c->st);
+    cudaMemsetAsync(P.status, 0, sizeof(unsigned long long) * status_words(X->n, X->m), c->st);
     for (int k = 0; k < 4; ++k) cudaMemsetAsync(c->um[k].hcnt, 0, sizeof(int) * c->um[k].hcap, c->st);
     Ctl init;
     std::memset(&init, 0, sizeof(init));

@@ -490,3 +490,17 @@ def test_random_designs_parity(seed):
         assert r_o["status"] == r_g["status"] == 0, (m, n, opts, r_o["status"], r_g["status"])
         assert r_g["kappa"] <= 1e-6
         assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"]), (m, n, opts, r_g["F"], r_o["F"])
+
+
+def test_solve_with_stale_workspace():
+    """ml_create must not depend on the workspace's previous contents.  The workspace is pre-filled with words that
+    look like look-back statuses of epochs 0..63 (flag 1, count 5) before ml_create; the large-m solve (64-column
+    coarse tiles) must still match the oracle."""
+    # m > 8192 (large-m path) and coarse sets wider than m / 4 columns: their 64-column tiles reach past the status
+    # words of the 256-row tiles
+    ds = mlgen.random_sparse(9000, 6000, 0.1, seed=3, lam_factor=0.02)
+    r_o = oracle.Oracle(ds).solve()
+    ctx = ml.Context(ds, ws_fill="epochs")
+    r_g = ctx.ml_solve()
+    assert r_g["status"] == 0 and r_g["kappa"] <= 1e-6
+    assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])

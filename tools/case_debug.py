@@ -14,8 +14,10 @@ import paper_1607_00315_b200 as ml  # noqa: E402
 
 
 def case(idx, seed=7):
+    """The dataset and options of case `idx` of tools/random_parity.py --seed `seed`."""
     rng = np.random.default_rng(seed)
     opts_pool = [{}, {"inner_cg": 1, "pcd_snap": 0}, {"inner_cg": 0}, {"multilevel": 0}, {"continuation": 1}]
+    opts = {}
     for k in range(idx + 1):
         m = int(rng.choice([37, 200, 777, 2000, 5000, 9000, 12000]))
         n = int(rng.choice([13, 150, 1301, 4000, 9000]))
@@ -24,11 +26,14 @@ def case(idx, seed=7):
                                    empty_rows=int(rng.integers(0, min(5, m // 2) + 1)), empty_cols=int(rng.integers(0, min(20, n // 2) + 1)))
         ds = mlgen.lasso(base, int(rng.integers(1 << 30)), k=5) if rng.random() < 0.25 else base
         opts = opts_pool[int(rng.integers(len(opts_pool)))]
+        if opts.get("inner_cg") == 0:
+            opts = {**opts, "max_cycles": 3000}
     return ds, opts
 
 
 if __name__ == "__main__":
-    ds, opts = case(int(sys.argv[1]))
+    ds, opts = case(int(sys.argv[1]), int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+    print(json.dumps({"m": ds.m, "n": ds.n, "nnz": ds.nnz, "lasso": ds.b is not None, "opts": opts}), flush=True)
     o = oracle.Oracle(ds)
     r_o = o.solve(oracle.default_opts(**opts))
     ctx = ml.Context(ds)
