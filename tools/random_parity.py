@@ -17,14 +17,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=40)
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--big", action="store_true", help="large-m designs only (m > 8192)")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     opts_pool = [{}, {"inner_cg": 1, "pcd_snap": 0}, {"inner_cg": 0}, {"multilevel": 0}, {"continuation": 1}]
     fails = 0
     for k in range(a.cases):
-        m = int(rng.choice([37, 200, 777, 2000, 5000, 9000, 12000]))
-        n = int(rng.choice([13, 150, 1301, 4000, 9000]))
-        dens = float(rng.choice([0.005, 0.02, 0.1, 0.5]))
+        m = int(rng.choice([9000, 20000, 40000] if a.big else [37, 200, 777, 2000, 5000, 9000, 12000]))
+        n = int(rng.choice([500, 5000, 30000] if a.big else [13, 150, 1301, 4000, 9000]))
+        dens = float(rng.choice([0.001, 0.005, 0.02] if a.big else [0.005, 0.02, 0.1, 0.5]))
         base = mlgen.random_sparse(m, n, dens, seed=int(rng.integers(1 << 30)), lam_factor=float(rng.choice([0.05, 0.1, 0.3])),
                                    empty_rows=int(rng.integers(0, min(5, m // 2) + 1)), empty_cols=int(rng.integers(0, min(20, n // 2) + 1)))
         ds = mlgen.lasso(base, int(rng.integers(1 << 30)), k=5) if rng.random() < 0.25 else base
