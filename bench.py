@@ -2,14 +2,18 @@
 """bench.py — multilevel proximal-Newton l1-logistic regression on B200 (BASELINE.json metric).
 
 One STEP = one full `ml_solve` from w = 0 to KKT <= 1e-6 (Algorithm 1; every SURVEY §8a row runs
-inside it) on one BASELINE.json configuration (default: configs[1], the 2000 x 20000 dense correlated design).
+inside it) on one BASELINE.json configuration (default: configs[4], the largest single-GPU configuration, 2e6 x 2e7
+Zipf sparse with 2e8 nonzeros; `--config 2` selects the dense 2000 x 20000 design).
 
   value     data-pass GB/s over the whole timed region: 8 bytes (fp32 value + int32 index) for every nonzero of X
             streamed by the solve's X passes (device counters), summed over ranks, / max-over-ranks time
   e2e       the same metric through the public API with host buffers: pinned H2D of X (CSC only for m <= 8192)
             and y, ml_create, ml_solve, D2H of w inside the timed region, after one untimed end-to-end step
   roofline  the pass class with the largest device-time share (CUDA events around each of its passes, on the
-            library's stream, inside the timed region); algorithmic bytes per DESIGN.md section 9
+            library's stream, inside the timed region); algorithmic bytes per DESIGN.md section 9; `rooflines` has
+            the same for every X-pass class (each timed in its own extra step after the timed region)
+  hessvec   Hessian-vector products per second through ml_hessvec (median of 10) on the solution's support and on
+            all columns, with nnz(X_C)
   cpu_baseline  the CPU oracle (single thread) solving the same workload on this host (rank 0, N = 1)
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
@@ -189,6 +193,45 @@ def class_bytes(name, prof, ds):
     return 8 * nnz
 
 
+def roof_entry(name, prof, ds, peak, traffic=None):
+    p = prof[name]
+    if p["ms"] <= 0 or p["passes"] <= 0:
+        return None
+    b = class_bytes(name, prof, ds)
+    ach = b / (p["ms"] * 1e-3) / 1e9
+    return {"achieved": round(ach, 1), "frac": round(ach / peak, 4), "passes": p["passes"],
+            "bytes_per_pass": int(b / p["passes"]), "us_per_pass": round(1e3 * p["ms"] / p["passes"], 2),
+            "traffic": traffic}
+
+
+def hessvec_rate(ctx, ds, torch, device):
+    """HV/s through the public API: ml_hessvec on C = supp(w) of the last solve and on all columns,
+    median of 10 after 2 warm-ups, CUDA events on the library's stream."""
+    import numpy as np
+    w = ctx.ml_get_w()
+    out = {}
+    colnnz = np.diff(ds.csc_colptr)
+    for key, C in (("support", torch.nonzero(w).flatten().to(torch.int32)), ("all", None)):
+        nC = ds.n if C is None else int(C.numel())
+        if nC == 0:
+            continue
+        v = torch.ones(nC, dtype=torch.float64, device=device)
+        ts = []
+        for k in range(12):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.stream)
+            ctx.ml_hessvec(C, v)
+            e1.record(ctx.stream)
+            torch.cuda.synchronize(device)
+            if k >= 2:
+                ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        nnzC = int(colnnz.sum() if C is None else colnnz[C.cpu().numpy()].sum())
+        out[key] = {"nC": nC, "nnz": nnzC, "ms": round(ms, 4), "hv_per_s": round(1e3 / ms, 1),
+                    "x_gbs": round(2 * 8 * nnzC / (ms * 1e-3) / 1e9, 1)}
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -246,9 +289,11 @@ def run_ours(args):
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    tdict = {}
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            tdict = json.load(open(tpath))
+            traffic = tdict.get(dom)
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None, "peak": peak,
@@ -258,6 +303,20 @@ def run_ours(args):
             "ms_per_pass": dom_ms / max(prof[dom]["passes"], 1),
             "share_of_step": round(share_warm[dom] / tot_warm, 3),
             "shares": {n: round(v / tot_warm, 3) for n, v in share_warm.items() if v > 0}}
+
+    # every X-pass class: one extra (untimed for `value`) solve per class with events around that class only
+    rooflines = {}
+    for name in xpass:
+        if prof_w[name]["ms"] <= 0:
+            continue
+        ctx.ml_profile(1 << ml.Context.CLASSES.index(name))
+        ctx.ml_solve(opts)
+        pr = ctx.ml_profile_read()
+        ent = roof_entry(name, pr, ds, peak, tdict.get(name))
+        if ent:
+            rooflines[name] = ent
+    ctx.ml_profile(0)
+    hv = hessvec_rate(ctx, ds, torch, device)
 
     # end-to-end through the public API with host buffers
     e2e = None
@@ -315,7 +374,8 @@ def run_ours(args):
             "solve": {"ok": ok, "F": r0["F"], "kappa": r0["kappa"], "cycles": r0["cycles"],
                       "relaxations": r0["relaxations"], "nnz_w": r0["nnz_w"], "x_nnz_streamed": r0["nnz_touched"],
                       "x_passes": r0["x_passes"]},
-            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "rooflines": rooflines, "hessvec": hv,
+            "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -324,23 +384,57 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def host_cpu():
+    """CPU model (/proc/cpuinfo) and logical core count of this host."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+def pin_one_core():
+    """The oracle is single-threaded: run it pinned to one core (sched_setaffinity); returns the previous mask."""
+    try:
+        prev = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(prev)})
+        return prev
+    except Exception:
+        return None
+
+
 def cpu_baseline(ds, cfg):
-    """The oracle as it stands, single-threaded, on a bounded sample of the same workload."""
+    """The oracle as it stands, single-threaded and pinned to one core, on a bounded sample of the same workload."""
     import oracle
+    model, ncpu = host_cpu()
+    prev = pin_one_core()
+    try:
+        return _cpu_baseline(ds, cfg, oracle, model, ncpu)
+    finally:
+        if prev:
+            os.sched_setaffinity(0, prev)
+
+
+def _cpu_baseline(ds, cfg, oracle, model, ncpu):
     o = oracle.Oracle(ds)
+    host = {"cpu_model": model, "host_cores": ncpu, "pinned": "sched_setaffinity, 1 core"}
     if cfg <= 3:
         t0 = time.perf_counter()
         r = o.solve()
         t = time.perf_counter() - t0
         return {"value": round(8.0 * r["nnz_touched"] / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                 "sample": f"one full oracle solve to kappa<=1e-6 ({r['cycles']} cycles)", "seconds": round(t, 2),
-                "time_to_kkt_ms": t * 1e3, "F": r["F"]}
+                "time_to_kkt_ms": t * 1e3, "F": r["F"], **host}
     t0 = time.perf_counter()
-    n0 = 0
     o.eval_f_grad()   # margins + gradient/diag over all columns: one CSR and one CSC pass
     t = time.perf_counter() - t0
     return {"value": round(8.0 * 2 * ds.nnz / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": "one oracle eval_f_grad (full CSR margins pass + full CSC gather)", "seconds": round(t, 2)}
+            "sample": "one oracle eval_f_grad (full CSR margins pass + full CSC gather; the full oracle solve of this "
+                      "config takes minutes: tests/golden)", "seconds": round(t, 2), **host}
 
 
 def run_reference(args):
@@ -353,6 +447,8 @@ def run_reference(args):
     import oracle
     ds = mlgen.make(args.config)
     o = oracle.Oracle(ds)
+    model, ncpu = host_cpu()
+    pin_one_core()
 
     def step():
         if args.config <= 3:
@@ -375,7 +471,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CFG_NAMES[args.config], "m": ds.m, "n": ds.n, "nnz": ds.nnz},
-            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": model, "host_cores": ncpu, "pinned": "sched_setaffinity, 1 core"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -385,7 +482,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -13,11 +13,18 @@
  *     device memory: all scratch is carved from `ws` (size from ml_workspace_bytes).
  *   - All work is enqueued on the stream given to ml_create.  Calls that return host scalars synchronise that
  *     stream only.  One context per stream / host thread; no global mutable state.
- *   - Index lists C are int32, strictly ascending, in [0, n).  C == NULL with nC == n means all columns.
+ *   - Index lists C are int32, strictly ascending, in [0, n).  C == NULL with nC == n means all columns.  API calls
+ *     that take C check it with one device pass and synchronise the stream (ML_E_INVAL if it is malformed).
+ *   - Alignment: csr_col, csr_val, csc_row, csc_val 16-byte aligned (they are streamed with 16-byte vector loads and
+ *     TMA bulk copies); pointer arrays 4-byte, b 8-byte aligned.  ml_create returns ML_E_INVAL otherwise.
  * Errors
  *   - Every call returns ml_status; nothing throws or exits across the ABI; ml_last_error gives detail.
- *   - ML_E_INVAL: m, n < 1, nnz >= 2^31, lambda <= 0 or non-finite, y not in {-1,+1}, bad C, too small workspace,
- *     malformed X (pointers not from 0 to nnz, indices out of range or not strictly ascending inside a row/column).
+ *   - ML_E_INVAL: m, n < 1, nnz >= 2^31, lambda <= 0 or non-finite, y not in {-1,+1}, bad C (out of range or not
+ *     strictly ascending), misaligned X arrays, malformed X (pointers not from 0 to nnz, indices out of range or not
+ *     strictly ascending inside a row/column).
+ *   - ML_E_NONFINITE: a NaN or Inf among X's values or the LASSO targets b (ml_create), or in w (ml_set_w; w is left
+ *     unchanged).  "Finite entries only (no NaN/Inf accepted into solvers)".
+ *   - ML_E_WORKSPACE: ws smaller than ml_workspace_bytes.
  *   - ML_E_CUDA: a CUDA runtime error (message in ml_last_error).
  *   - ML_E_STAGNATION: no trial step passed the line search; the iterate is unchanged.
  *   - ML_E_NOT_CONVERGED: ml_solve hit max_cycles; w holds the last evaluated iterate.
@@ -36,7 +43,7 @@ typedef struct ml_ctx ml_ctx;
 
 typedef enum {
     ML_OK = 0, ML_E_INVAL = 1, ML_E_CUDA = 2, ML_E_WORKSPACE = 3, ML_E_STAGNATION = 4,
-    ML_E_NOT_CONVERGED = 5, ML_E_CONTRACT = 6
+    ML_E_NOT_CONVERGED = 5, ML_E_CONTRACT = 6, ML_E_NONFINITE = 7
 } ml_status;
 
 typedef struct {                  /* X is m x n, rows = samples; 0 <= nnz < 2^31 */
@@ -88,7 +95,8 @@ void ml_default_opts(ml_solve_opts *o);
 size_t ml_workspace_bytes(int64_t m, int64_t n, int64_t nnz);
 
 /* Bind X, y, lambda (> 0) to a context; w = 0.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
-   Validates sizes, lambda and y (one device pass).  Builds the static heavy-row schedule (one pass over rowptr). */
+   Validates sizes, alignment, lambda, y, X's index structure and the finiteness of X's values (device passes; one
+   stream synchronisation).  Builds the static heavy-row schedule (one pass over rowptr). */
 ml_status ml_create(const ml_data *X, double lambda, void *cuda_stream, void *ws, size_t ws_bytes, ml_ctx **out);
 /* The squared-loss instance of Eq. 1: the LASSO of Eq. 2 with H = X^T X and g = -X^T b, i.e.
    F(w) = sum_i (x_i^T w - b_i)^2 / 2 + lambda ||w||_1 (DESIGN Q29).  b: [m] targets (device, fp64, borrowed like X);
@@ -98,7 +106,8 @@ ml_status ml_create_lasso(const ml_data *X, const double *b, double lambda, void
                           ml_ctx **out);
 ml_status ml_destroy(ml_ctx *c);
 
-/* w <- w_dev[n] (device); margins are recomputed at the next evaluation. */
+/* w <- w_dev[n] (device); margins are recomputed at the next evaluation.  Checks w_dev for NaN / Inf first (one
+   device pass, synchronises the stream): ML_E_NONFINITE and w unchanged if it holds one. */
 ml_status ml_set_w(ml_ctx *c, const double *w_dev);
 /* w_dev[n] <- w */
 ml_status ml_get_w(ml_ctx *c, double *w_dev);

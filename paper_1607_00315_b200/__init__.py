@@ -21,7 +21,8 @@ _SRC = os.path.join(_HERE, "csrc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
-ML_OK, ML_E_INVAL, ML_E_CUDA, ML_E_WORKSPACE, ML_E_STAGNATION, ML_E_NOT_CONVERGED, ML_E_CONTRACT = range(7)
+(ML_OK, ML_E_INVAL, ML_E_CUDA, ML_E_WORKSPACE, ML_E_STAGNATION, ML_E_NOT_CONVERGED, ML_E_CONTRACT,
+ ML_E_NONFINITE) = range(8)
 
 
 def _sources():

@@ -21,8 +21,8 @@ using namespace ml;
 
 namespace {
 
-constexpr int SM_COUNT = 148;   // B200; cooperative grids use the device's own count (ml_ctx::sms)
-constexpr int GRID_CAP = SM_COUNT * 4;
+constexpr int SM_MAX = IR_GMAX;   // partial buffers are sized for this many SMs; grids use the device's own count
+constexpr int GRID_CAP = 148 * 4;   // grid-stride passes: 4 blocks per B200 SM (any count works, this sizes partials)
 constexpr int TRACE_CAP = 1 << 16;
 constexpr int NV_MAX = 96;   // widest reduction payload (doubles per block)
 constexpr int SMALL_M = 8192;   // m-vectors up to this size are accumulated in shared memory (k_scatter_smem)
@@ -75,8 +75,9 @@ struct ml_ctx {
     bool big_inner = false;  // k_inner<., true>: the same with the m-vectors in global memory (m > SMALL_M)
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // the k_inner instantiation in use
-    int sms = SM_COUNT;               // the device's SM count (cooperative grids: one CTA per SM)
-    int coop_cap = SM_COUNT;          // cooperative grids use at most this many CTAs (ml_set_sm_share)
+    int sms = 148;                    // the device's SM count, capped at SM_MAX (cooperative grids: one CTA per SM)
+    int coop_cap = 148;               // cooperative grids use at most this many CTAs (ml_set_sm_share)
+    int scat_bps = 0, gath_bps = 0;   // blocks per SM of the cooperative API scatter / gather
     const void* gsmall_fn[2] = {nullptr, nullptr};   // k_gather_small<GSCH, false / true>
     size_t gsmall_bytes = 0;
     const void* msmall_fn = nullptr;   // k_margins_small<GSCH>
@@ -127,7 +128,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double2* tilepart = cv.take<double2>(ntile_n + 1);
     unsigned long long* status = cv.take<unsigned long long>(status_words(n, m));   // (64-column coarse tiles)
     double2* hres = cv.take<double2>(std::max(nn, mm));
-    double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_COUNT * 4 + 1) * mm + SM_COUNT * 4 + 64 : 1);
+    double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_MAX * 4 + 1) * mm + SM_MAX * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
     int* slist = cv.take<int>(mm <= SMALL_M ? nn + 1 : 1);   // k_margins_small: supp(w) in column order
     const size_t ucap2 = mm > SMALL_M ? nn + (size_t)nnz / IR_UNIT + 64 : 1;   // k_inner<., true>: column units
@@ -272,7 +273,7 @@ __global__ void k_check_y(const int8_t* y, int m, Ctl* ctl, unsigned long long* 
 // Element-parallel (long rows of a dense X are not one warp's serial loop): a descent idx[k] <= idx[k-1] is legal only
 // at a segment start, so the descents counted over all k >= 1 minus those at the starts of non-empty segments
 // (each start counted once) must be 0; the difference is summed into ctl->idx_desc (>= 0 per array).
-__global__ void k_check_index(const int* ptr, const int* idx, int len, int bound, long long nnz, Ctl* ctl) {
+__global__ void k_check_index(const int* ptr, const int* idx, const float* val, int len, int bound, long long nnz, Ctl* ctl) {
     const int lane = threadIdx.x & 31;
     const long long T = (long long)gridDim.x * blockDim.x, t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int bad = 0;
@@ -285,15 +286,35 @@ __global__ void k_check_index(const int* ptr, const int* idx, int len, int bound
         }
         if (b < e && b > 0 && idx[b] <= idx[b - 1]) net -= 1;
     }
-    for (long long k = t0; k < nnz; k += T) {   // ranges; every descent (added)
+    int nonfin = 0;
+    for (long long k = t0; k < nnz; k += T) {   // ranges; every descent (added); values finite
         const int r = idx[k];
         bad |= (r < 0) || (r >= bound);
         if (k > 0 && r <= idx[k - 1]) net += 1;
+        nonfin |= !isfinite(val[k]);
     }
     if (bad) atomicOr(&ctl->bad_y, 2);
+    if (nonfin) atomicOr(&ctl->bad_y, 4);
     net = warp_sum_ll(net);
     if (lane == 0 && net != 0) atomicAdd((unsigned long long*)&ctl->idx_desc, (unsigned long long)net);
 }
+// finiteness of a caller's fp64 vector (LASSO targets b, ml_set_w): flags ctl->bad_y |= flag
+__global__ void k_check_finite(const double* v, long long len, Ctl* ctl, int flag) {
+    int nonfin = 0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len; k += (long long)gridDim.x * blockDim.x)
+        nonfin |= !isfinite(v[k]);
+    if (__any_sync(0xffffffffu, nonfin) && (threadIdx.x & 31) == 0) atomicOr(&ctl->bad_y, flag);
+}
+// an index list C: in [0, n) and strictly ascending (include/ml.h); flags ctl->bad_y |= 16
+__global__ void k_check_list(const int* C, long long nC, int n, Ctl* ctl) {
+    int bad = 0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nC; k += (long long)gridDim.x * blockDim.x) {
+        const int j = C[k];
+        bad |= (j < 0) || (j >= n) || (k > 0 && j <= C[k - 1]);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&ctl->bad_y, 16);
+}
+__global__ void k_clear_flag(Ctl* ctl, int flag) { ctl->bad_y &= ~flag; }
 // support bitmap, |supp| and ||w||_1 from w (deterministic: per-block partials + last block)
 __global__ void __launch_bounds__(ML_NT) k_w_stats(Prm P, int n) {
     __shared__ double sm[3 * ML_NW + 3];
@@ -543,6 +564,7 @@ const char* ml_status_str(ml_status s) {
         case ML_E_STAGNATION: return "line search stagnation";
         case ML_E_NOT_CONVERGED: return "not converged";
         case ML_E_CONTRACT: return "objective increased (contract violation)";
+        case ML_E_NONFINITE: return "non-finite input";
     }
     return "unknown";
 }
@@ -561,6 +583,11 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (!X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csc_row || !X->csc_val)) ||
         (has_csr && X->nnz > 0 && (!X->csr_col || !X->csr_val)))
         return ML_E_INVAL;
+    // the index / value arrays are streamed with 16-byte vector loads and TMA bulk copies: 16-byte alignment
+    auto mis16 = [](const void* p) { return ((uintptr_t)p & 15u) != 0; };
+    if (mis16(X->csc_row) || mis16(X->csc_val) || (has_csr && (mis16(X->csr_col) || mis16(X->csr_val))) ||
+        ((uintptr_t)X->csc_colptr & 3u) || (has_csr && ((uintptr_t)X->csr_rowptr & 3u)) || ((uintptr_t)b & 7u))
+        return ML_E_INVAL;
     const size_t need = ml_workspace_bytes(X->m, X->n, X->nnz);
     if (!ws || ws_bytes < need) return ML_E_WORKSPACE;
     ml_ctx* c = new ml_ctx();
@@ -570,7 +597,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     {
         int dev = 0, sms = 0;
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
-            c->sms = std::min(sms, SM_COUNT);   // (the partial buffers are sized for at most SM_COUNT blocks)
+            c->sms = std::min(sms, SM_MAX);   // (the partial buffers are sized for at most SM_MAX blocks)
         c->coop_cap = c->sms;
     }
     c->ws = (char*)align_up((size_t)ws);
@@ -611,6 +638,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
             c->sm_scatter = bps >= 1;
             c->scat_W = W;
             c->scat_bytes = bytes;
+            c->scat_bps = bps;
             c->scat_P = c->sms * bps;
             c->gMP = std::max(1, std::min(GRID_CAP, (int)((X->m + 15) / 16)));
             c->gMP = std::max(c->gMP, (int)((X->m + ML_NT - 1) / ML_NT));
@@ -624,6 +652,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
             c->sm_gather = true;
             c->gath_W = W;
             c->gath_bytes = bytes;
+            c->gath_bps = bps;
             c->gath_P = c->sms * bps;
         }
         // persistent inner solver: 1024-element G chunks when the two m-vectors leave room, else 512
@@ -693,8 +722,9 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     if (!b) ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);   // (squared loss: no labels)
-    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, (int)X->n, (int)X->m, X->nnz, c->ctl);
-    if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, (int)X->m, (int)X->n, X->nnz, c->ctl);
+    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, X->csc_val, (int)X->n, (int)X->m, X->nnz, c->ctl);
+    if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, X->csr_val, (int)X->m, (int)X->n, X->nnz, c->ctl);
+    if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
@@ -706,12 +736,11 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     }
     ml_status s = sync_ctl(c);
     if (s != ML_OK) { *out = c; return s; }
-    if (c->h.bad_y || c->h.idx_desc != 0) {   // bit 0: labels not +-1; bit 1 / descents: malformed CSR / CSC
-        c->err = ((c->h.bad_y & 2) || c->h.idx_desc != 0)
-                     ? "X: pointers or indices malformed (indices must be in range and strictly ascending per segment)"
-                                  : "y: labels must be -1 or +1";
+    if (c->h.bad_y || c->h.idx_desc != 0) {   // bit 0: labels not +-1; bit 1 / descents: malformed CSR / CSC;
+        // bit 2: non-finite X values; bit 3: non-finite LASSO targets
+        const bool index = (c->h.bad_y & 3) || c->h.idx_desc != 0;
         delete c;
-        return ML_E_INVAL;
+        return index ? ML_E_INVAL : ML_E_NONFINITE;
     }
     c->npos = (long long)c->h.dsupp;
     long long zero = 0;
@@ -741,6 +770,13 @@ ml_status ml_destroy(ml_ctx* c) {
 
 ml_status ml_set_w(ml_ctx* c, const double* w_dev) {
     if (!c || !w_dev) return ML_E_INVAL;
+    ML_LAUNCH(c, k_check_finite, c->gA, w_dev, (long long)c->X.n, c->ctl, 32);
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    if (c->h.bad_y & 32) {   // w is left unchanged
+        ML_LAUNCH(c, k_clear_flag, 1, c->ctl, 32);
+        return ML_E_NONFINITE;
+    }
     cudaMemcpyAsync(c->P.w, w_dev, sizeof(double) * c->X.n, cudaMemcpyDeviceToDevice, c->st);
     ML_LAUNCH(c, k_w_stats, c->gA, c->P, (int)c->X.n);
     return cuda_fail(c, "ml_set_w");
@@ -758,9 +794,20 @@ ml_status ml_get_rows(ml_ctx* c, double* z, double* r, double* D) {
     return cuda_fail(c, "ml_get_rows");
 }
 
+// C == NULL with nC == n, or nC entries strictly ascending in [0, n): one device pass and a stream synchronisation
 static ml_status check_list(ml_ctx* c, const int32_t* C, int64_t nC) {
     if (!C) return nC == c->X.n ? ML_OK : ML_E_INVAL;
     if (nC < 0 || nC > c->X.n) return ML_E_INVAL;
+    if (nC == 0) return ML_OK;
+    ML_LAUNCH(c, k_check_list, std::max(1, std::min(GRID_CAP, (int)((nC + ML_NT - 1) / ML_NT))), C, (long long)nC,
+              (int)c->X.n, c->ctl);
+    ml_status s = sync_ctl(c);
+    if (s != ML_OK) return s;
+    if (c->h.bad_y & 16) {
+        ML_LAUNCH(c, k_clear_flag, 1, c->ctl, 16);
+        c->err = "C: indices must be strictly ascending in [0, n)";
+        return ML_E_INVAL;
+    }
     return ML_OK;
 }
 
@@ -781,7 +828,8 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
 }
 
 ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host, double* g_C, double* h_C) {
-    if (!c || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (!c) return ML_E_INVAL;
+    if (ml_status s = check_list(c, C, nC)) return s;
     launch_margins(c);
     if ((g_C || h_C) && nC > 0) api_gather(c, C, (int)nC, g_C, h_C);
     if (F_host) {
@@ -793,13 +841,15 @@ ml_status ml_eval_f_grad(ml_ctx* c, const int32_t* C, int64_t nC, double* F_host
 }
 
 ml_status ml_diag_hess(ml_ctx* c, const int32_t* C, int64_t nC, double* h_C) {
-    if (!c || !h_C || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (!c || !h_C) return ML_E_INVAL;
+    if (ml_status s = check_list(c, C, nC)) return s;
     if (nC > 0) api_gather(c, C, (int)nC, nullptr, h_C);
     return cuda_fail(c, "ml_diag_hess");
 }
 
 ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C, double* Hv_C) {
-    if (!c || !v_C || !Hv_C || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (!c || !v_C || !Hv_C) return ML_E_INVAL;
+    if (ml_status s = check_list(c, C, nC)) return s;
     if (nC == 0) return ML_OK;
     const int slot = C ? 1 : 0;
     if (C) {
@@ -817,7 +867,8 @@ ml_status ml_hessvec(ml_ctx* c, const int32_t* C, int64_t nC, const double* v_C,
 ml_status ml_shrink_linesearch(ml_ctx* c, const int32_t* C, int64_t nC, const double* g_C, const double* h_C,
                                const double* d_C, const double* Xd, const ml_solve_opts* o, double* alpha_host,
                                double* F_new_host) {
-    if (!c || !g_C || (!d_C && !h_C) || check_list(c, C, nC) != ML_OK) return ML_E_INVAL;
+    if (!c || !g_C || (!d_C && !h_C)) return ML_E_INVAL;
+    if (ml_status s = check_list(c, C, nC)) return s;
     ml_solve_opts def;
     ml_default_opts(&def);
     set_params(c, o ? o : &def);
@@ -981,7 +1032,10 @@ ml_status ml_solve(ml_ctx* c, const ml_solve_opts* o_in, ml_solve_report* rep) {
     // relaxations per level from the device trace
     const int nt = std::min(h.ntrace, TRACE_CAP);
     std::vector<TraceRow> tr(nt);
-    if (nt) cudaMemcpy(tr.data(), c->trace, sizeof(TraceRow) * nt, cudaMemcpyDeviceToHost);
+    if (nt) {   // on the context's stream (include/ml.h: all work is enqueued there)
+        cudaMemcpyAsync(tr.data(), c->trace, sizeof(TraceRow) * nt, cudaMemcpyDeviceToHost, c->st);
+        cudaStreamSynchronize(c->st);
+    }
     for (const TraceRow& r : tr) {
         rep->relax_per_level[std::min(std::max(r.level, 0), 31)]++;
         if (r.F_after > r.F_before + 1e-12 * std::fabs(r.F_before)) rep->status = ML_E_CONTRACT;
@@ -1037,6 +1091,8 @@ ml_status ml_set_sm_share(ml_ctx* c, int blocks) {
     }
     c->coop_cap = blocks;
     if (c->sm_inner || c->big_inner) c->inner_P = std::min(blocks, full);
+    if (c->sm_scatter) c->scat_P = blocks * c->scat_bps;   // the API's cooperative scatter / gather
+    if (c->sm_gather) c->gath_P = blocks * c->gath_bps;
     return ML_OK;
 }
 
@@ -1055,7 +1111,10 @@ int64_t ml_trace(ml_ctx* c, void* rows_host, int64_t cap) {
     if (sync_ctl(c) != ML_OK) return -1;
     const int nt = std::min(c->h.ntrace, TRACE_CAP);
     const int k = (int)std::min<int64_t>(nt, cap);
-    if (rows_host && k) cudaMemcpy(rows_host, c->trace, sizeof(TraceRow) * k, cudaMemcpyDeviceToHost);
+    if (rows_host && k) {
+        cudaMemcpyAsync(rows_host, c->trace, sizeof(TraceRow) * k, cudaMemcpyDeviceToHost, c->st);
+        cudaStreamSynchronize(c->st);
+    }
     return nt;
 }
 

@@ -745,6 +745,13 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         for (int g = 0; g < ng; ++g) xu += red[g * R + threadIdx.x];
         out[row0 + threadIdx.x] = xu;
     }
+    // more rows per block than threads (a small grid, e.g. ml_set_sm_share): the remaining rows one thread each,
+    // partials in block order
+    for (int r = (int)blockDim.x + threadIdx.x; r < R && row0 + r < m; r += blockDim.x) {
+        double xu = 0.0;
+        for (int k = 0; k < (int)gridDim.x; ++k) xu += ld_cg(parts + (size_t)k * m + row0 + r);
+        out[row0 + r] = xu;
+    }
     (void)P;
 }
 

@@ -43,10 +43,17 @@ def test_workspace_and_validation_host_only():
     d = ml.MLData(0, 5, 0, None, None, None, None, None, None, None)
     h = ctypes.c_void_p()
     assert L.ml_create(ctypes.byref(d), 1.0, None, None, 0, ctypes.byref(h)) == ml.ML_E_INVAL
-    d = ml.MLData(3, 5, 4, 1, 1, 1, 1, 1, 1, 1)
+    d = ml.MLData(3, 5, 4, 16, 16, 16, 16, 16, 16, 16)   # (fake, never dereferenced: checks come first)
     assert L.ml_create(ctypes.byref(d), -1.0, None, None, 0, ctypes.byref(h)) == ml.ML_E_INVAL
     assert L.ml_create(ctypes.byref(d), float("nan"), None, None, 0, ctypes.byref(h)) == ml.ML_E_INVAL
     assert L.ml_create(ctypes.byref(d), 1.0, None, None, 10, ctypes.byref(h)) == ml.ML_E_WORKSPACE
+    # include/ml.h alignment: a value / index array not 16-byte aligned is rejected before any device work
+    for k in range(4):
+        p = [16] * 7
+        p[[1, 2, 4, 5][k]] = 20
+        d2 = ml.MLData(3, 5, 4, *p)
+        assert L.ml_create(ctypes.byref(d2), 1.0, None, None, 10, ctypes.byref(h)) == ml.ML_E_INVAL
+    assert L.ml_status_str(ml.ML_E_NONFINITE) == b"non-finite input"
     assert L.ml_status_str(ml.ML_E_STAGNATION) == b"line search stagnation"
     o = ml.default_opts()
     assert o.tol_kkt == 1e-6 and o.K_fine == 2 and o.K_mid == 3 and o.K_coarse == 5 and o.inner_cg == 2 and o.pcd_snap == 1

@@ -28,11 +28,33 @@ def rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
+def absX(ds):
+    """|X| as a scipy CSC (for the elementwise tolerances: each output's sum of absolute terms)."""
+    import scipy.sparse as sp
+    return sp.csc_matrix((np.abs(ds.csc_val.astype(np.float64)), ds.csc_row, ds.csc_colptr), shape=(ds.m, ds.n))
+
+
+def elem(a, b, scale, tol=1e-9, what=""):
+    """Elementwise: |a_k - b_k| <= tol * scale_k, scale_k = the sum of the absolute values of the terms of output k
+    (a relative-L2 check alone lets a wrong light column hide under a few heavy ones)."""
+    a, b, scale = (np.asarray(x, np.float64) for x in (a, b, scale))
+    bad = np.abs(a - b) > tol * scale + 1e-300
+    assert not bad.any(), (what, int(bad.sum()), np.flatnonzero(bad)[:5])
+
+
 def dt(a, dtype=torch.float64):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0", dtype)
 
 
 _CACHE = {}
+
+
+def _full(cfg):
+    """A full-size BASELINE config, generated once per test session (cfg 5: 23 s, 3.3 GB of host memory)."""
+    key = f"full{cfg}"
+    if key not in _CACHE:
+        _CACHE[key] = mlgen.make(cfg)
+    return _CACHE[key]
 
 
 def dataset(name):
@@ -120,6 +142,13 @@ def test_eval_f_grad_parity(name, wkind):
     assert rel(g_g.cpu().numpy(), g_o) <= 1e-9
     assert rel(h_g.cpu().numpy(), h_o) <= 1e-9
     assert rel(z_g, z_o) <= 1e-9 and rel(r_g, r_o) <= 1e-9 and rel(D_g, D_o) <= 1e-9
+    A = absX(ds)
+    zs = A @ np.abs(w)
+    elem(z_g, z_o, zs, what="z")
+    elem(r_g, r_o, np.abs(r_o) + 0.25 * zs, what="r")     # |dr/dz| = D <= 1/4
+    elem(D_g, D_o, np.abs(D_o) + 0.1 * zs, what="D")      # |dD/dz| <= 0.1
+    elem(g_g.cpu().numpy(), g_o, A.T @ np.abs(r_o) + A.T @ (0.25 * zs), what="g")
+    elem(h_g.cpu().numpy(), h_o, h_o + A.multiply(A).T @ (0.1 * zs), what="h")
 
 
 def _lists(ds, seed):
@@ -145,6 +174,11 @@ def test_restricted_gather_hessvec(name):
     ctx.ml_set_w(dt(w))
     ctx.ml_eval_f_grad(want_g=False, want_h=False)
     rng = np.random.default_rng(8)
+    A = absX(ds)
+    _, r_o, D_o, _ = o.rows()
+    zs = A @ np.abs(w)
+    gs_all = A.T @ (np.abs(r_o) + 0.25 * zs)
+    hs_all = A.multiply(A).T @ (D_o + 0.1 * zs)
     for key, C in _lists(ds, 4).items():
         if len(C) == 0:
             continue
@@ -152,12 +186,19 @@ def test_restricted_gather_hessvec(name):
         Fg, g_g, h_g = ctx.ml_eval_f_grad(dt(C, torch.int32))
         assert rel(g_g.cpu().numpy(), g_o) <= 1e-9, key
         assert rel(h_g.cpu().numpy(), h_o) <= 1e-9, key
+        elem(g_g.cpu().numpy(), g_o, gs_all[C], what=("g", key))
+        elem(h_g.cpu().numpy(), h_o, hs_all[C], what=("h", key))
         hd = ctx.ml_diag_hess(dt(C, torch.int32))
         assert rel(hd.cpu().numpy(), h_o) <= 1e-9, key
+        elem(hd.cpu().numpy(), h_o, hs_all[C], what=("diag", key))
         v = rng.standard_normal(len(C))
         Hv_o = o.hessvec(C, v)
         Hv_g = ctx.ml_hessvec(dt(C, torch.int32), dt(v))
         assert rel(Hv_g.cpu().numpy(), Hv_o) <= 1e-9, key
+        vfull = np.zeros(ds.n)
+        vfull[C] = np.abs(v)
+        AC = A[:, C]
+        elem(Hv_g.cpu().numpy(), Hv_o, AC.T @ ((D_o + 0.1 * zs) * (A @ vfull)), what=("Hv", key))
     v = rng.standard_normal(ds.n)
     assert rel(ctx.ml_hessvec(None, dt(v)).cpu().numpy(), o.hessvec(None, v)) <= 1e-9
 
@@ -271,7 +312,7 @@ def test_lambda_max_zero_solution_gpu():
 @pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
 def test_solve_parity_full_configs(name):
     """Solve parity at BASELINE configs 2, 3 and 4 (full size; cfg 4's oracle solve takes ~20-40 s on one core)."""
-    ds = mlgen.make(int(name[-1]))
+    ds = _full(int(name[-1]))
     o = oracle.Oracle(ds)
     r_o = o.solve()
     ctx = ml.Context(ds)
@@ -321,7 +362,7 @@ def test_trace_parity(name, opts):
 def test_full_size_sampled_eval_parity(cfg):
     """BASELINE configs 4 and 5 at full size: F, g_C, h_C on a sampled column list (random + the 20 heaviest
     columns), in the launch configuration the bench uses, against the oracle's one-by-one evaluation."""
-    ds = mlgen.make(cfg)
+    ds = _full(cfg)
     rng = np.random.default_rng(cfg)
     lens = np.diff(ds.csc_colptr)
     C = np.unique(np.r_[rng.choice(ds.n, 2000, replace=False), np.argsort(lens)[-20:]]).astype(np.int32)
@@ -339,14 +380,25 @@ def test_full_size_sampled_eval_parity(cfg):
     assert rel(g_g.cpu().numpy(), g_o) <= 1e-9
     assert rel(h_g.cpu().numpy(), h_o) <= 1e-9
     v = rng.standard_normal(len(C))
-    assert rel(ctx.ml_hessvec(dt(C, torch.int32), dt(v)).cpu().numpy(), o.hessvec(C, v)) <= 1e-9
+    Hv_g, Hv_o = ctx.ml_hessvec(dt(C, torch.int32), dt(v)).cpu().numpy(), o.hessvec(C, v)
+    assert rel(Hv_g, Hv_o) <= 1e-9
+    # elementwise, each sampled column against the sum of its absolute terms
+    A = absX(ds)
+    _, r_o, D_o, _ = o.rows()
+    zs = A @ np.abs(w)
+    AC = A[:, C]
+    elem(g_g.cpu().numpy(), g_o, AC.T @ (np.abs(r_o) + 0.25 * zs), what="g")
+    elem(h_g.cpu().numpy(), h_o, AC.multiply(AC).T @ (D_o + 0.1 * zs), what="h")
+    vfull = np.zeros(ds.n)
+    vfull[C] = np.abs(v)
+    elem(Hv_g, Hv_o, AC.T @ ((D_o + 0.1 * zs) * (A @ vfull)), what="Hv")
 
 
 @pytest.mark.parametrize("cfg", [4, 5])
 def test_full_size_solve_kkt_by_oracle(cfg):
     """Full-size GPU solve; the oracle re-evaluates the gradient at the GPU's w and checks the KKT conditions
     (|g_j| <= lam(1+1e-6) off the support, |g_j + lam sign w_j| <= 1e-6 lam on it) and F."""
-    ds = mlgen.make(cfg)
+    ds = _full(cfg)
     ctx = ml.Context(ds)
     r = ctx.ml_solve()
     assert r["status"] == 0 and r["kappa"] <= 1e-6, r
@@ -504,3 +556,180 @@ def test_solve_with_stale_workspace():
     r_g = ctx.ml_solve()
     assert r_g["status"] == 0 and r_g["kappa"] <= 1e-6
     assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+
+
+def _ls_pair(ds, w, mode, seed=2):
+    """One ml_shrink_linesearch on both sides from the same w: PCD step (d = NULL), a given long step, or an ascent
+    direction (every Armijo trial fails: ML_E_STAGNATION, iterate unchanged)."""
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    _, g, h = o.eval_f_grad()
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    ctx.ml_eval_f_grad(want_g=False, want_h=False)
+    C = np.arange(ds.n, dtype=np.int32)
+    rng = np.random.default_rng(seed)
+    if mode == "pcd":
+        res_o = o.shrink_linesearch(C, g, h=h)
+        res_g = ctx.ml_shrink_linesearch(dt(C, torch.int32), dt(g), h=dt(h))
+    else:
+        d = np.abs(rng.normal(0, 2.0, ds.n))
+        if mode == "ascent":   # uphill on both the smooth part and the l1 term: Delta > 0, no alpha passes
+            d = d * np.sign(g)
+            d[w != 0] = np.abs(d[w != 0]) * np.sign(w[w != 0])
+            d[(w == 0) & (g == 0)] = 0.0
+        else:                  # a long step along minus the min-norm subgradient (P:248-256): a descent direction
+            v = np.where(w != 0, g + ds.lam * np.sign(w), np.sign(g) * np.maximum(np.abs(g) - ds.lam, 0.0))
+            d = -d * v
+        res_o = o.shrink_linesearch(C, g, d=d)
+        res_g = ctx.ml_shrink_linesearch(dt(C, torch.int32), dt(g), d=dt(d))
+    return o, ctx, res_o, res_g
+
+
+@pytest.mark.parametrize("name", ["cfg4s", "cfg4"])
+@pytest.mark.parametrize("mode", ["pcd", "given", "ascent"])
+def test_shrink_linesearch_parity_large_m(name, mode):
+    """A7 on the large-m API path (m > 8192: the fp64 X_C d scatter and k_outer_ls over all rows), including a forced
+    stagnation (Eq. 4; include/ml.h: alpha = 0, ML_E_STAGNATION, iterate unchanged)."""
+    ds = _full(4) if name == "cfg4" else dataset(name)
+    w = random_w(ds.n, "pct", 9)
+    o, ctx, (a_o, F_o, st_o), (a_g, F_g, st_g) = _ls_pair(ds, w, mode)
+    assert st_o == st_g
+    if mode == "ascent":
+        assert st_g == ml.ML_E_STAGNATION and a_g == 0.0 and a_o == 0.0
+        assert np.array_equal(ctx.ml_get_w().cpu().numpy(), w)
+    else:
+        assert st_g == 0 and a_o == a_g, (a_o, a_g)
+    assert abs(F_g - F_o) <= 1e-9 * abs(F_o)
+    assert rel(ctx.ml_get_w().cpu().numpy(), o.get_w()) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_select_coarse_exact_full_size(cfg):
+    """A8 at BASELINE configs 4 and 5 (n = 1e6 / 2e7 candidates): exact set equality with the oracle given the
+    oracle's gradient bits (ties by ascending index, DESIGN Q14), at the level sizes a solve uses."""
+    ds = _full(cfg)
+    rng = np.random.default_rng(cfg)
+    w = np.zeros(ds.n)
+    idx = rng.choice(ds.n, 3000, replace=False)
+    w[idx] = rng.normal(0, 0.2, len(idx))
+    o = oracle.Oracle(ds)
+    o.set_w(w)
+    _, g, _ = o.eval_f_grad()
+    g = g.copy()
+    g[::5] = np.round(g[::5], 3)   # exact ties
+    ctx = ml.Context(ds)
+    ctx.ml_set_w(dt(w))
+    nS = int(np.count_nonzero(w))
+    gd = dt(g)
+    for k in (nS, nS + 1, nS + 4321, 2 * nS + 100000, (ds.n + nS) // 2):
+        C_o = o.select_coarse(g, k)
+        C_g = ctx.ml_select_coarse(gd, k).cpu().numpy()
+        assert np.array_equal(C_g, C_o), (k, len(C_g), len(C_o))
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_solve_vs_oracle_golden(cfg):
+    """Full-size solve at BASELINE configs 4 and 5 against the oracle's own solution, committed under tests/golden/
+    by tools/make_golden.py (which calls only oracle/): F within 1e-6 relative, both kappa <= 1e-6, supports equal
+    outside the band ||g_j| - lambda| < 1e-4 (BASELINE.json north_star), and w on the common support close."""
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", f"cfg{cfg}_solution.npz"))
+    meta = json.loads(str(z["meta"]))
+    ds = _full(cfg)
+    assert (meta["m"], meta["n"], meta["nnz"]) == (ds.m, ds.n, ds.nnz) and meta["lam"] == ds.lam
+    ctx = ml.Context(ds)
+    r = ctx.ml_solve()
+    assert r["status"] == 0 and r["kappa"] <= 1e-6 and meta["kappa"] <= 1e-6
+    assert abs(r["F"] - meta["F"]) <= 1e-6 * abs(meta["F"]), (r["F"], meta["F"])
+    w = ctx.ml_get_w().cpu().numpy()
+    sg = np.flatnonzero(w)
+    so = z["supp"].astype(np.int64)
+    band = set(z["band"].tolist())
+    diff = set(sg.tolist()) ^ set(so.tolist())
+    outside = [j for j in diff if j not in band]
+    assert not outside, outside[:10]
+    common = np.intersect1d(sg, so)
+    wo = np.zeros(ds.n)
+    wo[so] = z["w_supp"]
+    assert np.linalg.norm(w[common] - wo[common]) <= 1e-6 * np.linalg.norm(wo[common])   # (oracle variants: 2e-10)
+
+
+# ----------------------------------------------------------------------------- boundary error behaviour
+def test_nonfinite_inputs_rejected():
+    """include/ml.h ML_E_NONFINITE (SPEC S:24 'finite entries only'): NaN / Inf among X's values (CSC or CSR) or the
+    LASSO targets -> ml_create fails; a NaN in ml_set_w's vector -> ML_E_NONFINITE with w unchanged."""
+    import dataclasses
+    good = mlgen.from_dense(np.eye(4, 3, dtype=np.float32) + 1.0, np.array([1, -1, 1, -1], np.int8), 0.1)
+    for field, val in (("csc_val", np.nan), ("csc_val", np.inf), ("csr_val", -np.inf)):
+        a = getattr(good, field).copy()
+        a[2] = val
+        with pytest.raises(ml.MLError) as e:
+            ml.Context(dataclasses.replace(good, **{field: a}))
+        assert e.value.status == ml.ML_E_NONFINITE, str(e.value)
+    las = mlgen.lasso(mlgen.make(1), 1, k=5)
+    b = las.b.copy()
+    b[7] = np.nan
+    with pytest.raises(ml.MLError) as e:
+        ml.Context(dataclasses.replace(las, b=b))
+    assert e.value.status == ml.ML_E_NONFINITE
+    ctx = ml.Context(dataset("cfg1"))
+    w0 = random_w(ctx.n, "ten", 1)
+    ctx.ml_set_w(dt(w0))
+    bad = w0.copy()
+    bad[3] = np.nan
+    with pytest.raises(ml.MLError) as e:
+        ctx.ml_set_w(dt(bad))
+    assert e.value.status == ml.ML_E_NONFINITE
+    assert np.array_equal(ctx.ml_get_w().cpu().numpy(), w0)
+    ctx.ml_set_w(dt(w0))   # the context stays usable
+    F, _, _ = ctx.ml_eval_f_grad(want_g=False, want_h=False)
+    assert np.isfinite(F)
+
+
+def test_bad_index_list_rejected():
+    """include/ml.h: C must be strictly ascending in [0, n); every API entry taking C checks it on the device and
+    returns ML_E_INVAL (unsorted, duplicate, out of range, negative), then keeps working on a good list."""
+    ds = dataset("cfg3s")
+    ctx = ml.Context(ds)
+    good = np.array([3, 17, 400, ds.n - 1], np.int32)
+    bads = [np.array([17, 3, 400], np.int32), np.array([3, 3, 400], np.int32), np.array([3, ds.n], np.int32),
+            np.array([-1, 3], np.int32)]
+    for C in bads:
+        Ct = dt(C, torch.int32)
+        v = dt(np.ones(len(C)))
+        for call in (lambda: ctx.ml_eval_f_grad(Ct), lambda: ctx.ml_diag_hess(Ct), lambda: ctx.ml_hessvec(Ct, v),
+                     lambda: ctx.ml_shrink_linesearch(Ct, v, h=v)):
+            with pytest.raises(ml.MLError) as e:
+                call()
+            assert e.value.status == ml.ML_E_INVAL, (C, str(e.value))
+    o = oracle.Oracle(ds)
+    o.eval_f_grad()
+    _, g_o, h_o = o.eval_f_grad(good)
+    _, g_g, h_g = ctx.ml_eval_f_grad(dt(good, torch.int32))
+    assert rel(g_g.cpu().numpy(), g_o) <= 1e-9 and rel(h_g.cpu().numpy(), h_o) <= 1e-9
+
+
+def test_misaligned_arrays_rejected():
+    """include/ml.h alignment: X's index / value arrays 16-byte aligned (16-byte vector loads, TMA bulk copies);
+    an array starting 4 bytes into an allocation is rejected with ML_E_INVAL instead of faulting the context."""
+    import ctypes
+    ds = dataset("cfg1")
+    L = ml.load()
+    dev = "cuda:0"
+    arrs = {k: torch.from_numpy(getattr(ds, k)).to(dev) for k in ("csr_rowptr", "csr_col", "csr_val", "csc_colptr",
+                                                                    "csc_row", "csc_val", "y")}
+    shifted = torch.zeros(ds.nnz + 4, dtype=torch.float32, device=dev)
+    shifted[1:1 + ds.nnz] = arrs["csc_val"]
+    ws = torch.empty(int(L.ml_workspace_bytes(ds.m, ds.n, ds.nnz)) + 512, dtype=torch.uint8, device=dev)
+    for bad in ("csc_val",):
+        ptrs = {k: v.data_ptr() for k, v in arrs.items()}
+        ptrs[bad] = shifted.data_ptr() + 4
+        data = ml.MLData(ds.m, ds.n, ds.nnz, ptrs["csr_rowptr"], ptrs["csr_col"], ptrs["csr_val"], ptrs["csc_colptr"],
+                         ptrs["csc_row"], ptrs["csc_val"], ptrs["y"])
+        h = ctypes.c_void_p()
+        st = L.ml_create(ctypes.byref(data), ds.lam, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.byref(h))
+        assert st == ml.ML_E_INVAL
+    torch.cuda.synchronize()
+    ml.Context(ds).ml_solve()   # the process's CUDA context is intact

@@ -593,3 +593,85 @@ def test_lasso_lambda_max_zero_solution():
     F, g, h = o2.eval_f_grad()
     assert np.allclose(h, np.array([np.sum(base.csc_val[base.csc_colptr[j]:base.csc_colptr[j + 1]].astype(np.float64) ** 2)
                                     for j in range(base.n)]), rtol=1e-12)   # D = 1: h_j = ||x_j||^2
+
+
+# ----------------------------------------------------------------------------- the PCD branch of shrink_linesearch
+def test_pcd_direction_spec_example():
+    """Eq. 5 with D = diag(h): SPEC S:222 'H=I, x=0, g=(-3,0.5), lambda=1, PCD -> z=(2,0)'.  The oracle's
+    d_C == NULL branch builds d from the given g and h; a design on which F falls steeply along e_0 (x_i0 = y_i) makes
+    Armijo accept alpha = 1, so the new iterate IS the PCD direction."""
+    m = 10
+    y = np.where(np.arange(m) % 3 == 0, -1, 1).astype(np.int8)
+    X = np.stack([y.astype(np.float32), np.where(np.arange(m) % 2 == 0, 1.0, -1.0).astype(np.float32)], 1)
+    ds = mlgen.from_dense(X, y, lam=1.0)
+    o = oracle.Oracle(ds)
+    C = np.arange(2, dtype=np.int32)
+    a, Fn, st = o.shrink_linesearch(C, np.array([-3.0, 0.5]), h=np.array([1.0, 1.0]),
+                                    opts=oracle.default_opts(eps_h=0.0))
+    assert st == 0 and a == 1.0
+    assert np.array_equal(o.get_w(), np.array([2.0, 0.0]))
+    # F at the new iterate from the definition P:786
+    assert abs(Fn - (np.sum(np.logaddexp(0, -y * (X.astype(np.float64) @ [2.0, 0.0]))) + 2.0)) <= 1e-13 * Fn
+    # S:220-221: x = 0, g = 0 -> z = 0 (no step: alpha reported as 0 or the iterate unchanged)
+    o2 = oracle.Oracle(ds)
+    o2.shrink_linesearch(C, np.zeros(2), h=np.ones(2), opts=oracle.default_opts(eps_h=0.0))
+    assert np.array_equal(o2.get_w(), np.zeros(2))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_pcd_direction_numpy(seed):
+    """The d_C == NULL branch at a random iterate: d = Sh_{lam/hh}(w - g/hh) - w with hh = h + eps_h (Eq. 5-6,
+    P:92-98, D = diag H per P:99), re-derived in numpy from the closed form; the accepted step is alpha d with
+    alpha the first of 1, 1/2, ... passing Armijo on F re-evaluated from P:786."""
+    ds, X, y = _dense_problem(m=60, n=12, seed=40 + seed)
+    o = oracle.Oracle(ds)
+    rng = np.random.default_rng(seed)
+    w = rng.normal(0, 0.4, ds.n) * (rng.random(ds.n) < 0.6)
+    o.set_w(w)
+    _, g, h = o.eval_f_grad()
+    C = np.arange(ds.n, dtype=np.int32)
+    eps = 1e-12
+    hh = h + eps
+    t = w - g / hh
+    d = np.sign(t) * np.maximum(np.abs(t) - ds.lam / hh, 0.0) - w
+
+    def F(wv):
+        return np.sum(np.logaddexp(0, -y * (X @ wv))) + ds.lam * np.abs(wv).sum()
+
+    Delta = g @ d + ds.lam * (np.abs(w + d).sum() - np.abs(w).sum())
+    assert Delta < 0
+    alpha, Fn, st = o.shrink_linesearch(C, g, h=h)
+    assert st == 0
+    a_ref = 1.0
+    while F(w + a_ref * d) - F(w) > 1e-2 * a_ref * Delta:
+        a_ref *= 0.5
+    assert alpha == a_ref
+    assert np.max(np.abs(o.get_w() - (w + alpha * d))) <= 1e-13 * (1 + np.max(np.abs(w)))
+
+
+def test_report_fields_pinned():
+    """Report fields of the solve (Q19): at lambda >= lambda_max the solve is S2 + S3 + the final
+    evaluation, so exactly two EVAL_ALLs stream X: x_passes = 4 (CSR margins + CSC gather, twice), nnz_touched =
+    4 nnz.  paper_ratio = ||v(w)||_1 / (||v(0)||_1 min(#pos,#neg)/m) recomputed in numpy from the gradient of
+    P:792 at the returned w and at 0."""
+    ds = mlgen.make(1)
+    o = oracle.Oracle(ds)
+    o_big = oracle.Oracle(mlgen.Dataset(**{**ds.__dict__, "lam": ds.lambda_max * (1 + 1e-9)}))
+    rb = o_big.solve()
+    assert rb["cycles"] == 0 and rb["x_passes"] == 4 and rb["nnz_touched"] == 4 * ds.nnz
+    r = o.solve()
+    X = np.zeros((ds.m, ds.n))
+    for i in range(ds.m):
+        X[i, ds.csr_col[ds.csr_rowptr[i]:ds.csr_rowptr[i + 1]]] = ds.csr_val[ds.csr_rowptr[i]:ds.csr_rowptr[i + 1]]
+    y = ds.y.astype(np.float64)
+
+    def v_of(wv):
+        t = y * (X @ wv)
+        gr = X.T @ (-y / (1.0 + np.exp(t)))            # (tau(t) - 1) y, P:792
+        return np.where(wv != 0, gr + ds.lam * np.sign(wv), np.sign(gr) * np.maximum(np.abs(gr) - ds.lam, 0.0))
+
+    w = o.get_w()
+    npos = int(np.sum(ds.y > 0))
+    ref = np.abs(v_of(w)).sum() / (np.abs(v_of(np.zeros(ds.n))).sum() * min(npos, ds.m - npos) / ds.m)
+    assert r["status"] == 0 and r["paper_ratio"] > 0
+    assert abs(r["paper_ratio"] - ref) <= 1e-6 * ref + 1e-15
