@@ -75,7 +75,7 @@ class TraceRow(ctypes.Structure):
 EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_create_lasso", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
            "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
-           "ml_profile_read", "ml_inner_phases", "ml_set_sm_share"]
+           "ml_profile_read", "ml_inner_phases", "ml_set_sm_share", "ml_set_engine"]
 
 _lib = None
 
@@ -134,6 +134,9 @@ def load(path: str | None = None):
     if hasattr(L, "ml_set_sm_share"):
         L.ml_set_sm_share.restype = i32
         L.ml_set_sm_share.argtypes = [P, i32]
+    if hasattr(L, "ml_set_engine"):
+        L.ml_set_engine.restype = i32
+        L.ml_set_engine.argtypes = [P, ctypes.c_uint32]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
     _lib = L
@@ -319,6 +322,9 @@ class Context:
         self._check(load().ml_profile_read(self.h, ms, ps, nz, sg))
         return {name: {"ms": ms[k], "passes": ps[k], "nnz": nz[k], "segs": sg[k]}
                 for k, name in enumerate(self.CLASSES)}
+
+    def ml_set_engine(self, flags):
+        return self._check(load().ml_set_engine(self.h, int(flags)))
 
     def ml_set_sm_share(self, blocks):
         return self._check(load().ml_set_sm_share(self.h, int(blocks)))

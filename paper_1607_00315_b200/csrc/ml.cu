@@ -15,6 +15,7 @@
 
 #include "../../include/ml.h"
 #include "ml_kernels.cuh"
+#include "ml_merge.cuh"
 #include "ml_select.cuh"
 
 using namespace ml;
@@ -96,6 +97,13 @@ struct ml_ctx {
     long long prof_passes[16] = {0};
     std::string err;
     Ctl h;             // host mirror of the control block
+    // merge-path column passes (ml_merge.cuh), large m: the static plan over all columns and one for lists
+    bool mp = false;
+    MPList mp_all, mp_l;
+    int mp_tiles_cap = 0, mp_grid_all = 0, mp_grid_l = 0;
+    int* mp_vptr = nullptr;
+    int* mp_bsum = nullptr;
+    double2* mp_out = nullptr;
 };
 
 namespace {
@@ -149,6 +157,19 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     size_t lvl_cap = 2 * nn + 2 * SEL_LMAX + 64;
     int* lvl = cv.take<int>(lvl_cap);
     unsigned char* lev = cv.take<unsigned char>(nn);
+    // merge-path plans (large m): tile starts and carries for all columns and for a list, list offsets, outputs
+    const bool big = mm > SMALL_M;
+    const size_t mtiles = big ? (nn + (size_t)nnz) / MP_TILE + 2 : 1;
+    int2* mp_ts_all = cv.take<int2>(mtiles + 1);
+    double2* mp_cv_all = cv.take<double2>(mtiles);
+    int* mp_cx_all = cv.take<int>(mtiles);
+    int2* mp_ts_l = cv.take<int2>(mtiles + 1);
+    double2* mp_cv_l = cv.take<double2>(mtiles);
+    int* mp_cx_l = cv.take<int>(mtiles);
+    int* mp_vptr = cv.take<int>(big ? nn + 1 : 1);
+    int* mp_bsum = cv.take<int>(big ? nn / MP_SCAN + 2 : 1);
+    double2* mp_out = cv.take<double2>(big ? nn : 1);
+
     UnitsMem um[4];
     for (int k = 0; k < 4; ++k) {
         um[k].u = cv.take<int4>(ucap);
@@ -168,6 +189,12 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.irpart = irpart;
     P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.unz = unz;
     c->slist = slist;
+    c->mp_tiles_cap = (int)std::min<size_t>(mtiles - 1, 0x7fffffff);
+    c->mp_all = MPList{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, mp_ts_all, mp_cv_all, mp_cx_all};
+    c->mp_l = MPList{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, mp_ts_l, mp_cv_l, mp_cx_l};
+    c->mp_vptr = mp_vptr;
+    c->mp_bsum = mp_bsum;
+    c->mp_out = mp_out;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
 }
 
@@ -400,6 +427,42 @@ void launch_margins(ml_ctx* c) {
     ML_DISPATCH_G(c->Gr, ML_LAUNCH(c, k_margins<GG>, grid, c->P, S, acc_of(c, CLS_MARGINS)));
 }
 
+// merge-path plan of a list (virtual offsets by a three-launch scan, then the tile starts); list == nullptr: the
+// static all-columns plan built at create
+MPList mp_plan(ml_ctx* c, const int* list, const int* nC_dev, int nC_host) {
+    if (!list) return c->mp_all;
+    MPList L = c->mp_l;
+    L.colptr = c->X.csc_colptr; L.idx = c->X.csc_row; L.val = c->X.csc_val;
+    L.list = list; L.vptr = c->mp_vptr; L.nC_dev = nC_dev; L.nC_host = nC_host;
+    const int nb = std::max(1, (nC_host + MP_SCAN - 1) / MP_SCAN);
+    ML_LAUNCH(c, k_vscan_sums, nb, c->X.csc_colptr, list, nC_dev, nC_host, c->mp_bsum);
+    k_vscan_top<<<1, 1024, 0, c->st>>>(c->mp_bsum, nC_dev, nC_host);
+    c->launches++;
+    ML_LAUNCH(c, k_vscan_apply, nb, c->X.csc_colptr, list, nC_dev, nC_host, c->mp_bsum, c->mp_vptr);
+    const long long tiles = ((long long)nC_host + c->X.nnz) / MP_TILE + 2;
+    ML_LAUNCH(c, k_mp_search, (int)std::max<long long>(1, (tiles + ML_NT) / ML_NT), L, c->mp_tiles_cap);
+    return L;
+}
+template <class Term>
+void mp_pass(ml_ctx* c, const MPList& L, Term term, double2* out, const int* skip, long long* acc) {
+    const bool lst = L.list != nullptr;
+    k_mp_pass<Term><<<lst ? c->mp_grid_l : c->mp_grid_all, MP_NT, mp_smem_bytes(lst), c->st>>>(L, term, out, skip, acc);
+    ML_LAUNCH(c, k_mp_fixup, std::max(1, std::min(GRID_CAP, (c->mp_tiles_cap + ML_NT - 1) / ML_NT)), L, out, skip);
+    c->launches++;
+}
+template <class Term>
+bool mp_setup_kernel(ml_ctx* c) {
+    int occ_l = 0, occ_a = 0;
+    if (cudaFuncSetAttribute(k_mp_pass<Term>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mp_smem_bytes(true)) != cudaSuccess)
+        return false;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_l, k_mp_pass<Term>, MP_NT, mp_smem_bytes(true));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, k_mp_pass<Term>, MP_NT, mp_smem_bytes(false));
+    if (occ_l < 1 || occ_a < 1) return false;
+    c->mp_grid_l = occ_l * c->sms;
+    c->mp_grid_all = occ_a * c->sms;
+    return true;
+}
+
 // A2 + A3 over C (list == nullptr: all columns, finest) into the ASet
 // RELAX(C) start + A2/A3 over C.  Small m: one cooperative launch (k_gather_small also does k_relax_begin's work);
 // large m: k_relax_begin, then the segment-engine gather.
@@ -418,6 +481,17 @@ void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* lis
         cudaLaunchCooperativeKernel(finest ? c->gsmall_fn[1] : c->gsmall_fn[0], dim3(c->inner_P), dim3(32 * IR_W), args,
                                     c->gsmall_bytes, c->st);
         c->launches++;
+        return;
+    }
+    if (c->mp) {   // merge-path column sums into mp_out, then the free-set compaction from them
+        MPList L = mp_plan(c, list, nullptr, nC_host);
+        mp_pass(c, L, TermGH{c->P.rD}, c->mp_out, &c->ctl->skip, acc_of(c, cls));
+        Seg So = S;
+        So.hres = c->mp_out;
+        const int ts = finest ? TILE : 64;
+        const int grid = std::max(1, std::min(GRID_CAP, (nC_host + ts - 1) / ts));
+        if (finest) ML_LAUNCH(c, (k_gather_free<32, true, true>), grid, c->P, So, AS, (long long*)nullptr);
+        else ML_LAUNCH(c, (k_gather_free<32, false, true>), grid, c->P, So, AS, (long long*)nullptr);
         return;
     }
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
@@ -704,6 +778,12 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
             c->inner_P = std::min(c->sms, IR_GMAX);
         }
     }
+    if (!c->sm_inner && mp_setup_kernel<TermGH>(c) && mp_setup_kernel<TermV2>(c) && mp_setup_kernel<TermV1>(c)) {
+        c->mp = false;   // large m: merge-path column passes (ml_merge.cuh) on request (ml_set_engine bit 0)
+        c->mp_all.colptr = X->csc_colptr; c->mp_all.idx = X->csc_row; c->mp_all.val = X->csc_val;
+        c->mp_all.list = nullptr; c->mp_all.vptr = X->csc_colptr; c->mp_all.nC_dev = nullptr; c->mp_all.nC_host = (int)X->n;
+    }
+    cudaGetLastError();
     if (!has_csr && !c->sm_inner) {   // the large-m margins and heavy-row schedule read X by rows
         delete c;
         return ML_E_INVAL;
@@ -726,6 +806,8 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, X->csr_val, (int)X->m, (int)X->n, X->nnz, c->ctl);
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
+    if (c->mp_grid_all)   // the static merge-path plan over all columns (X is fixed for the context's life)
+        ML_LAUNCH(c, k_mp_search, std::max(1, (c->mp_tiles_cap + ML_NT) / ML_NT), c->mp_all, c->mp_tiles_cap);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
         Units U = units_of(c, 0);
@@ -1081,6 +1163,14 @@ ml_status ml_profile_read(ml_ctx* c, double* ms, int64_t* passes, int64_t* nnz, 
 // diagnostics: ns per phase of the persistent inner solver (block 0), accumulated since the last reset
 // Batched replicas: cap the cooperative grids (k_inner, k_gather_small, k_margins_small,
 // k_select_coop) at `blocks` CTAs, so that several contexts on their own streams run side by side on one GPU.
+ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
+    if (!c) return ML_E_INVAL;
+    const bool want = (flags & 1u) != 0;
+    if (want && c->mp_grid_all == 0) return ML_E_INVAL;   // (small m: the shared-memory passes; no merge-path plan)
+    c->mp = want;
+    return ML_OK;
+}
+
 ml_status ml_set_sm_share(ml_ctx* c, int blocks) {
     if (!c) return ML_E_INVAL;
     const int full = std::min(c->sms, IR_GMAX);

@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
 // the ASet (A, gA, hA + eps_h, wA) with a decoupled look-back scan over dynamically claimed groups of SUP tiles
 // (one look-back per group).  FINEST additionally computes ||w||_1 and sum |v| exactly.
 // The last block to finish: nA, vmax, the convergence decision (R2), counters reset, epoch advance.
-template <int G, bool FINEST>
+// MPOUT: the column sums were computed by the merge-path pass (ml_merge.cuh) into S.hres[p] (every position)
+template <int G, bool FINEST, bool MPOUT = false>
 __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, long long* acc) {
     // tiles per claim: one look-back per SUP tiles.  Coarse sets are small (tens of tiles): one tile per claim keeps
     // every tile's block busy (4 per claim left a 13 k-column coarse set on 13 blocks)
@@ -359,7 +360,12 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
             const int tile = sup * SUP + t;
             jj[t] = 0; flag[t] = 0; gg[t] = 0.0; hh[t] = 0.0; ww[t] = 0.0;
             if (tile < ntiles) {   // (uniform over the block)
-                seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
+                if (MPOUT) {
+                    const int p = tile * TS + threadIdx.x;
+                    if (threadIdx.x < TS && p < nC) res[threadIdx.x] = S.hres[p];
+                } else {
+                    seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
+                }
                 __syncthreads();
                 const int p = tile * TS + threadIdx.x;
                 if (threadIdx.x < TS && p < nC) {
