@@ -316,6 +316,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     const unsigned long long ph_k0 = ph_t;
     int ph_its = 0;
     (void)ph_k0;
+#ifdef IR_BLKDBG
+    unsigned long long bd_t0 = 0, bd_s = 0, bd_g = 0;   // this block's S and G work (BIG), before the barriers
+#endif
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ double sh_w[IR_W * 2 * IR_NLS + 2 * IR_NLS];   // >= IR_W * N + N for every ir_block_partials<N>
     __shared__ double sh_t[12], sh_r[4], sh_l1[2 * IR_NLS];
@@ -549,6 +552,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         const bool resident = !BIG && s_res;   // (block-uniform; s_res is visible after the partials' barriers)
         PH_MARK(0);
         if (BIG) grid.sync();   // the units of my stream may belong to other blocks' positions
+#ifdef IR_BLKDBG
+        __syncthreads();
+        bd_t0 = gtimer();
+#endif
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         if constexpr (BIG) {   // per-warp rings, fp64 reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
@@ -693,6 +700,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (zpart) zparts[(size_t)blockIdx.x * m + i] = my_z ? xz_sh[i] : 0.0;
             }
         }
+#ifdef IR_BLKDBG
+        if (BIG) { __syncthreads(); bd_s += gtimer() - bd_t0; }
+#endif
         PH_MARK(1);
         if constexpr (BIG) grid.sync();   // B1
         else {   // B1, split: the G rings (aliasing the consumed S ring) are set up and issued while it completes
@@ -910,6 +920,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (BIG && need_hs) {   // G from L2: Hsigma = beta X^T (D o Xs) (+ (1 - beta) X^T (D o Xz)) + eps sigma
             __syncthreads();
             PH_MARK(5);
+#ifdef IR_BLKDBG
+            bd_t0 = gtimer();
+#endif
             ColStream<GSCH, GST>& cs = csG;
             int stg = 0;
             double a = 0.0, az = 0.0;
@@ -1003,6 +1016,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             __syncwarp();
             if (lane == 0)
                 for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
+#ifdef IR_BLKDBG
+            __syncthreads();
+            bd_g += gtimer() - bd_t0;
+#endif
             grid.sync();   // every unit's partial
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
                 const int p = p0 + k;
@@ -1165,6 +1182,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         __syncthreads();   // my positions' d, Hd and the shared rings before the next direction
     }
+#ifdef IR_BLKDBG
+    if (BIG && threadIdx.x == 0) {   // tph[0..2]: sum / max / (2^62 - min) of S work over blocks; [3..5] the same for G
+        atomicAdd(&c->tph[0], bd_s); atomicMax(&c->tph[1], bd_s); atomicMax(&c->tph[2], (1ull << 62) - bd_s);
+        atomicAdd(&c->tph[3], bd_g); atomicMax(&c->tph[4], bd_g); atomicMax(&c->tph[5], (1ull << 62) - bd_g);
+    }
+#endif
     if (!BIG && s_res && threadIdx.x == blockDim.x - 32)   // the resident ring's barriers
         for (int k = 0; k < SST; ++k) mbar_inval(s_bar + k);
     // accounting: X_A s scatters, Hs gathers
