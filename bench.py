@@ -173,24 +173,27 @@ def parse_opts(text):
     return out
 
 
+BPN = 8   # algorithmic bytes per nonzero of X streamed: fp32 value + int32 index (4 for the index-free dense X)
+
+
 def class_bytes(name, prof, ds):
-    """Algorithmic bytes of a pass class: X stream 8 B/nnz, pointer pairs 8 B/segment,
+    """Algorithmic bytes of a pass class: X stream BPN B/nnz, pointer pairs 8 B/segment,
     list 4 B/segment, each m-vector once per pass, outputs once."""
     p = prof[name]
     nnz, segs, passes = p["nnz"], p["segs"], max(p["passes"], 1)
     m = ds.m
     if name == "margins":      # X (CSR) + rowptr + y + z, r, D written + w gathers of the support (upper: 8/seg)
-        return 8 * nnz + 4 * segs + passes * (m * 1 + 24 * m)
+        return BPN * nnz + 4 * segs + passes * (m * 1 + 24 * m)
     if name in ("gather_fine", "gather_coarse"):   # X (CSC) + colptr pairs + (r, D) once + outputs 28 B/col
-        return 8 * nnz + 8 * segs + passes * 16 * m + 12 * segs
+        return BPN * nnz + 8 * segs + passes * 16 * m + 12 * segs
     if name == "scatter_XAs":  # X_A (nonzero-coefficient columns) + colptr + coef + Xs read-modify-write once
-        return 8 * nnz + 12 * segs + passes * 16 * m
+        return BPN * nnz + 12 * segs + passes * 16 * m
     if name == "gather_Hs":    # X_A + colptr + sv once + Hs out
-        return 8 * nnz + 16 * segs + passes * 8 * m
+        return BPN * nnz + 16 * segs + passes * 8 * m
     if name == "inner_fused":  # persistent small-m inner solver: its scatter and Hs passes (counted in those classes)
         sc, hs = prof["scatter_XAs"], prof["gather_Hs"]
-        return 8 * (sc["nnz"] + hs["nnz"]) + 12 * sc["segs"] + 16 * hs["segs"]
-    return 8 * nnz
+        return BPN * (sc["nnz"] + hs["nnz"]) + 12 * sc["segs"] + 16 * hs["segs"]
+    return BPN * nnz
 
 
 def roof_entry(name, prof, ds, peak, traffic=None):
@@ -228,7 +231,7 @@ def hessvec_rate(ctx, ds, torch, device):
         ms = statistics.median(ts)
         nnzC = int(colnnz.sum() if C is None else colnnz[C.cpu().numpy()].sum())
         out[key] = {"nC": nC, "nnz": nnzC, "ms": round(ms, 4), "hv_per_s": round(1e3 / ms, 1),
-                    "x_gbs": round(2 * 8 * nnzC / (ms * 1e-3) / 1e9, 1)}
+                    "x_gbs": round(2 * BPN * nnzC / (ms * 1e-3) / 1e9, 1)}
     return out
 
 
@@ -244,7 +247,9 @@ def run_ours(args):
     torch.cuda.set_device(device)
     ml.build()
     ds = mlgen.make(args.config)
-    ctx = ml.Context(ds, device=str(device))
+    if args.dense and ds.nnz != ds.m * ds.n:
+        raise SystemExit("--dense needs a dense configuration (1 or 2)")
+    ctx = ml.Context(ds, device=str(device), dense=args.dense)
     opts = ml.default_opts(**parse_opts(args.opts))
 
     # warm-up; the last warm-up step times every pass class to find the dominant one
@@ -279,7 +284,7 @@ def run_ours(args):
     prof = ctx.ml_profile_read()
     ok = all(r["status"] == 0 and r["kappa"] <= 1e-6 for r in reps)
     nnz_total = sum(r["nnz_touched"] for r in reps)
-    bytes_total = 8.0 * nnz_total
+    bytes_total = float(BPN) * nnz_total
     value, t_max = aggregate(bytes_total, t_ms, ws, device)
 
     # roofline of the dominant pass class, measured in the timed region
@@ -321,11 +326,13 @@ def run_ours(args):
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        # the library reads X only by columns when m <= 8192 (include/ml.h): the CSR is not copied there
+        # the library reads X only by columns when m <= 8192 (include/ml.h): the CSR is not copied there; an index-free
+        # dense X (--dense) copies the column-major values only
         cols_only = ds.m <= 8192
         keep = [np.ascontiguousarray(a) for a in (ds.csr_rowptr, ds.csr_col, ds.csr_val, ds.csc_colptr, ds.csc_row,
                                                   ds.csc_val, ds.y)]
-        pinned = [None if (cols_only and k < 3) else torch.from_numpy(a).pin_memory() for k, a in enumerate(keep)]
+        skip = {0, 1, 2, 3, 4} if args.dense else ({0, 1, 2} if cols_only else set())
+        pinned = [None if k in skip else torch.from_numpy(a).pin_memory() for k, a in enumerate(keep)]
         h2d = sum(t.numel() * t.element_size() for t in pinned if t is not None)
         d2h = 8 * ds.n
         e2e_steps = max(1, min(args.steps, 3))
@@ -350,7 +357,7 @@ def run_ours(args):
         torch.cuda.synchronize(device)
         te = (time.perf_counter() - t0) * 1e3
         te_max, = allreduce([te], "max", ws, device)
-        be, = allreduce([8.0 * nnz_e], "sum", ws, device)
+        be, = allreduce([float(BPN) * nnz_e], "sum", ws, device)
         e2e = {"value": round(be / (te_max * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": te_max / e2e_steps, "steps": e2e_steps}
 
@@ -369,6 +376,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (X CSR+CSC %.0f MB > 126 MB); no flush" % (16 * ds.nnz / 1e6)
                        if 16 * ds.nnz > 126e6 else "small config: L2-resident",
                        "step": "one ml_solve from w=0 to kappa<=1e-6",
+                       "x_storage": "dense column-major values, index-free" if args.dense else
+                       ("CSC (CSR unused for m <= 8192)" if ds.m <= 8192 else "CSR + CSC"),
                        **({"opts": parse_opts(args.opts)} if args.opts else {})},
             "time_to_kkt_ms": t_max / args.steps,
             "solve": {"ok": ok, "F": r0["F"], "kappa": r0["kappa"], "cycles": r0["cycles"],
@@ -488,8 +497,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--opts", default="", help="ml_solve_opts overrides, e.g. multilevel=0,K_fine=10")
     ap.add_argument("--single", action="store_true", help="one untimed solve (for ncu launch lists / captures)")
+    ap.add_argument("--dense", action="store_true", help="index-free dense X (configs 1-2; include/ml.h)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    global BPN
+    BPN = 4 if args.dense else 8
     if args.single:
         import mlgen
         import paper_1607_00315_b200 as ml

@@ -53,6 +53,9 @@ typedef struct {                  /* X is m x n, rows = samples; 0 <= nnz < 2^31
     const int32_t *csr_rowptr;    /* [m+1] */
     const int32_t *csr_col;       /* [nnz], ascending inside each row */
     const float *csr_val;         /* [nnz] */
+    /* Index-free dense X (Eq. 2's dense H): csc_colptr == csc_row == NULL with nnz = m n,
+       m <= 8192 and the CSR NULL.  csc_val then holds X column-major (element (i, j) at j m + i); the row of element
+       k of column j is k - j m, so no index is stored, copied or read. */
     const int32_t *csc_colptr;    /* [n+1] */
     const int32_t *csc_row;       /* [nnz], ascending inside each column */
     const float *csc_val;         /* [nnz] */

@@ -169,7 +169,7 @@ class Context:
     """
 
     def __init__(self, ds, lam: float | None = None, device: str = "cuda:0", stream=None, host_tensors=None,
-                 csr: bool = True, ws_fill: int | None = None):
+                 csr: bool = True, ws_fill: int | None = None, dense: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libml needs a CUDA device (no CPU fallback)")
@@ -187,12 +187,15 @@ class Context:
             def up(a, dt):
                 return torch.from_numpy(a).to(dev, dt)
 
-            # csr=False: columns only (accepted by ml_create for m <= 8192, include/ml.h)
+            # csr=False: columns only (accepted by ml_create for m <= 8192, include/ml.h); dense=True: the index-free
+            # dense X (column-major values only: no CSR, no CSC pointers or row indices; nnz = m n, m <= 8192)
+            if dense:
+                csr = False
             self.csr_rowptr = up(ds.csr_rowptr, torch.int32) if csr else None
             self.csr_col = up(ds.csr_col, torch.int32) if csr else None
             self.csr_val = up(ds.csr_val, torch.float32) if csr else None
-            self.csc_colptr = up(ds.csc_colptr, torch.int32)
-            self.csc_row = up(ds.csc_row, torch.int32)
+            self.csc_colptr = None if dense else up(ds.csc_colptr, torch.int32)
+            self.csc_row = None if dense else up(ds.csc_row, torch.int32)
             self.csc_val = up(ds.csc_val, torch.float32)
             self.y = up(ds.y, torch.int8)
         self.stream = stream or torch.cuda.current_stream(dev)

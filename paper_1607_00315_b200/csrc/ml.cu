@@ -104,6 +104,11 @@ struct ml_ctx {
     int* mp_vptr = nullptr;
     int* mp_bsum = nullptr;
     double2* mp_out = nullptr;
+    // index-free dense X (m <= SMALL_M, csc_row == csc_colptr == NULL, nnz == m n): the library's own column pointers
+    // (j m) and the row table rowtab[t] = t that stands in for the staged row indices (Seg::rowtab)
+    bool dense = false;
+    int* dense_colptr = nullptr;
+    int* rowtab = nullptr;
 };
 
 namespace {
@@ -139,6 +144,8 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* parts = cv.take<double>(mm <= SMALL_M ? (size_t)(SM_MAX * 4 + 1) * mm + SM_MAX * 4 + 64 : 1);
     double* irpart = cv.take<double>((size_t)IR_NSLOT * IR_GMAX);
     int* slist = cv.take<int>(mm <= SMALL_M ? nn + 1 : 1);   // k_margins_small: supp(w) in column order
+    int* dense_colptr = cv.take<int>(mm <= SMALL_M ? nn + 1 : 1);   // index-free dense X (small m)
+    int* rowtab = cv.take<int>(mm <= SMALL_M ? mm : 1);
     const size_t ucap2 = mm > SMALL_M ? nn + (size_t)nnz / IR_UNIT + 64 : 1;   // k_inner<., true>: column units
     int2* uext = cv.take<int2>(ucap2);
     int* upos = cv.take<int>(ucap2);
@@ -189,6 +196,8 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.irpart = irpart;
     P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.unz = unz;
     c->slist = slist;
+    c->dense_colptr = dense_colptr;
+    c->rowtab = rowtab;
     c->mp_tiles_cap = (int)std::min<size_t>(mtiles - 1, 0x7fffffff);
     c->mp_all = MPList{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, mp_ts_all, mp_cv_all, mp_cx_all};
     c->mp_l = MPList{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, mp_ts_l, mp_cv_l, mp_cx_l};
@@ -218,7 +227,8 @@ Units units_of(ml_ctx* c, int slot) {
 
 Seg seg_rows(ml_ctx* c) { return Seg{c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, c->X.nnz, nullptr, c->hres, 8 * c->Gr}; }
 Seg seg_cols(ml_ctx* c, const int* list) {
-    return Seg{c->X.csc_colptr, c->X.csc_row, c->X.csc_val, c->X.nnz, list, c->hres, 8 * c->Gc};
+    return Seg{c->X.csc_colptr, c->X.csc_row, c->X.csc_val, c->X.nnz, list, c->hres, 8 * c->Gc,
+               c->dense ? c->rowtab : nullptr};
 }
 
 #define ML_LAUNCH(c, kernel, grid, ...)                                                        \
@@ -311,14 +321,15 @@ __global__ void k_check_index(const int* ptr, const int* idx, const float* val, 
             bad = 1;
             continue;
         }
-        if (b < e && b > 0 && idx[b] <= idx[b - 1]) net -= 1;
+        if (idx && b < e && b > 0 && idx[b] <= idx[b - 1]) net -= 1;
     }
     int nonfin = 0;
     for (long long k = t0; k < nnz; k += T) {   // ranges; every descent (added); values finite
+        nonfin |= !isfinite(val[k]);
+        if (!idx) continue;   // (index-free dense X: values only)
         const int r = idx[k];
         bad |= (r < 0) || (r >= bound);
         if (k > 0 && r <= idx[k - 1]) net += 1;
-        nonfin |= !isfinite(val[k]);
     }
     if (bad) atomicOr(&ctl->bad_y, 2);
     if (nonfin) atomicOr(&ctl->bad_y, 4);
@@ -342,6 +353,13 @@ __global__ void k_check_list(const int* C, long long nC, int n, Ctl* ctl) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&ctl->bad_y, 16);
 }
 __global__ void k_clear_flag(Ctl* ctl, int flag) { ctl->bad_y &= ~flag; }
+// index-free dense X: column pointers j m and the row table t
+__global__ void k_dense_init(int* colptr, int* rowtab, int m, int n) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= n || k < m; k += gridDim.x * blockDim.x) {
+        if (k <= n) colptr[k] = k * m;
+        if (k < m) rowtab[k] = k;
+    }
+}
 // support bitmap, |supp| and ||w||_1 from w (deterministic: per-block partials + last block)
 __global__ void __launch_bounds__(ML_NT) k_w_stats(Prm P, int n) {
     __shared__ double sm[3 * ML_NW + 3];
@@ -654,8 +672,11 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
         return ML_E_INVAL;
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return ML_E_INVAL;
     const bool has_csr = X->csr_rowptr != nullptr;   // (optional when m <= SMALL_M: checked once the solver path is known)
-    if (!X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csc_row || !X->csc_val)) ||
-        (has_csr && X->nnz > 0 && (!X->csr_col || !X->csr_val)))
+    // index-free dense X: no CSC pointers or row indices, every column full (nnz = m n), read by columns (small m)
+    const bool dense = !X->csc_colptr && !X->csc_row && X->nnz == X->m * X->n;
+    if (dense && (X->m > SMALL_M || has_csr || !X->csc_val || (!X->y && !b))) return ML_E_INVAL;
+    if (!dense && (!X->csc_colptr || (!X->y && !b) || (X->nnz > 0 && (!X->csc_row || !X->csc_val)) ||
+                   (has_csr && X->nnz > 0 && (!X->csr_col || !X->csr_val))))
         return ML_E_INVAL;
     // the index / value arrays are streamed with 16-byte vector loads and TMA bulk copies: 16-byte alignment
     auto mis16 = [](const void* p) { return ((uintptr_t)p & 15u) != 0; };
@@ -678,6 +699,10 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     c->ws_bytes = ws_bytes;
     Carve cv{c->ws};
     carve_all(cv, c, X->m, X->n, X->nnz);
+    if (dense) {
+        c->dense = true;
+        c->X.csc_colptr = c->dense_colptr;   // (filled below; csc_row stays NULL: Seg::idx == nullptr selects the
+    }                                         //  index-free reads)
     Prm& P = c->P;
     P.m = (int)X->m;
     P.n = (int)X->n;
@@ -802,7 +827,8 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     cudaMemcpyAsync(c->ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, c->st);
     unsigned long long* npos_dev = reinterpret_cast<unsigned long long*>(&c->ctl->dsupp);
     if (!b) ML_LAUNCH(c, k_check_y, c->gM, X->y, (int)X->m, c->ctl, npos_dev);   // (squared loss: no labels)
-    ML_LAUNCH(c, k_check_index, GRID_CAP, X->csc_colptr, X->csc_row, X->csc_val, (int)X->n, (int)X->m, X->nnz, c->ctl);
+    if (dense) ML_LAUNCH(c, k_dense_init, GRID_CAP, c->dense_colptr, c->rowtab, (int)X->m, (int)X->n);
+    ML_LAUNCH(c, k_check_index, GRID_CAP, c->X.csc_colptr, X->csc_row, X->csc_val, (int)X->n, (int)X->m, X->nnz, c->ctl);
     if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, X->csr_val, (int)X->m, (int)X->n, X->nnz, c->ctl);
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
@@ -811,7 +837,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
     {
         Units U = units_of(c, 0);
-        ML_LAUNCH(c, k_units_build, c->gSeg, X->csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U, 8 * c->Gc);
+        ML_LAUNCH(c, k_units_build, c->gSeg, c->X.csc_colptr, (const int*)nullptr, (const int*)nullptr, (int)X->n, U, 8 * c->Gc);
         Units R = units_of(c, 3);
         if (has_csr)
             ML_LAUNCH(c, k_units_build, c->gM, X->csr_rowptr, (const int*)nullptr, (const int*)nullptr, (int)X->m, R, 8 * c->Gr);

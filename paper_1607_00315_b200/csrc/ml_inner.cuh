@@ -65,13 +65,17 @@ enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 }; 
 #define IR_UNIT_V 2048
 #endif
 constexpr int IR_UNIT = IR_UNIT_V;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
-constexpr int IR_UCOST = 1024;   // BIG: a unit's fixed cost in nonzeros (TMA issue, barrier wait) for the balance
+#ifndef IR_UCOST_V
+#define IR_UCOST_V 1024
+#endif
+constexpr int IR_UCOST = IR_UCOST_V;   // BIG: a unit's fixed cost in nonzeros (TMA issue, barrier wait) for the balance
 constexpr unsigned IR_DMAX = (1u << 10) | (1u << 11);
 
 // my positions' state, indexed by p - p0: shared memory when q <= IR_QS, else the ASet arrays (offset by p0)
 constexpr int IR_QS = 160, IR_RS = 64;   // cached positions / rows per block (rows: m <= IR_RS * G)
 struct PosState { const double* wA; const double* gA; const double* hA; double* d; double* Hd; double* s; double* u; };
-struct SChunk { int p, a, vb, ve, ce, ok; };   // copy [a, ce) of column p, valid [vb, ve); ok = 0: no chunk
+struct SChunk { int p, a, vb, ve, ce, ok, cb, pad; };   // copy [a, ce) of column p (starting at cb), valid [vb, ve);
+                                                       // ok = 0: no chunk
 
 __host__ __device__ constexpr int ir_sst(int gsch) { return gsch >= 1024 ? 8 : 4; }   // the S ring fits the G rings
 __host__ __device__ inline size_t ir_sring_bytes(int sst) {
@@ -82,7 +86,7 @@ __host__ __device__ inline size_t ir_ring_bytes() {
     const size_t g = (size_t)IR_W * stream_warp_bytes<GSCH, GST>(0), s = ir_sring_bytes(ir_sst(GSCH));
     return ((g > s ? g : s) + 15) / 16 * 16;
 }
-static_assert(sizeof(SChunk) == 24, "SChunk layout");
+static_assert(sizeof(SChunk) == 32, "SChunk layout");
 // dynamic shared memory: the rings (S ring and G rings alias), then two m-vectors (X_A s | sv, X_A z); BIG: rings only
 template <int GSCH>
 __host__ __device__ inline size_t inner_smem_bytes(int m) { return ir_ring_bytes<GSCH>() + (size_t)16 * m; }
@@ -228,6 +232,7 @@ struct SProducer {
             d.p = p;
             d.a = start & ~3;
             d.vb = start;
+            d.cb = b;
             d.ve = min(e, d.a + IR_SCH);
             d.ce = max(d.a, min((d.ve + 3) & ~3, nnz4));
             d.ok = 1;
@@ -238,9 +243,9 @@ struct SProducer {
     }
     __device__ void issue(const Seg& S, const SChunk& d, int st, int* s_idx, float* s_val, uint64_t* s_bar) const {
         fence_proxy_async();
-        mbar_arrive_expect_tx(s_bar + st, 8u * (uint32_t)(d.ce - d.a));
+        mbar_arrive_expect_tx(s_bar + st, (S.idx ? 8u : 4u) * (uint32_t)(d.ce - d.a));   // (dense X: values only)
         if (d.ce > d.a) {
-            bulk_g2s(s_idx + st * IR_SCH, S.idx + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
+            if (S.idx) bulk_g2s(s_idx + st * IR_SCH, S.idx + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
             bulk_g2s(s_val + st * IR_SCH, S.val + d.a, 4u * (uint32_t)(d.ce - d.a), s_bar + st);
         }
     }
@@ -579,7 +584,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 const double cf = ld_cg(coef + pu);
                 if (cf != 0.0) {
                     const int zf = pcd && P.pcd_snap && ld_cg(AS.u + pu) != 0.0;   // z_p = s_p on a zeroing column
-                    const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                    const int* ci = S.idx ? cs.sidx + stg * GSCH - dsc.a : S.rowtab - dsc.cb;
                     const float* cv = cs.sval + stg * GSCH - dsc.a;
                     const int kend = min(dsc.ve, dsc.ce);
                     int k = dsc.vb + lane;
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         if (zf) red_add_global(P.Xzu + r, xv);
                     }
                     for (; k < dsc.ve; k += 32) {
-                        const int r = __ldg(S.idx + k);
+                        const int r = seg_idx(S, k, dsc.cb);
                         const double xv = (double)__ldg(S.val + k) * cf;
                         red_add_global(P.Xu + r, xv);
                         if (zf) red_add_global(P.Xzu + r, xv);
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 const double cf = coef[d.p - p0];
                 if (cf != 0.0) {
                     const int zf = my_z && X.u[d.p - p0] != 0.0;   // z_p = s_p on a zeroing column
-                    const int* ci = s_idx + st * IR_SCH - d.a;
+                    const int* ci = S.idx ? s_idx + st * IR_SCH - d.a : S.rowtab - d.cb;
                     const float* cv = s_val + st * IR_SCH - d.a;
                     const int kend = min(d.ve, d.ce);
                     // rows are distinct within a column: all loads of a batch are issued before its stores.  The
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         }
                     }
                     for (int k = max(kend, d.vb) + threadIdx.x; k < d.ve; k += blockDim.x) {   // (a chunk may start past kend)
-                        const int r = __ldg(S.idx + k);
+                        const int r = seg_idx(S, k, d.cb);
                         const double xv = (double)__ldg(S.val + k);
                         xs_sh[r] = fma(xv, cf, xs_sh[r]);
                         if (zf) xz_sh[r] = fma(xv, cf, xz_sh[r]);
@@ -931,7 +936,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (dsc.cf == 0.0) break;
                 mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
                 g_phase ^= 1u << stg;
-                const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                const int* ci = S.idx ? cs.sidx + stg * GSCH - dsc.a : S.rowtab - dsc.cb;
                 const float* cv = cs.sval + stg * GSCH - dsc.a;
                 const int kend = min(dsc.ve, dsc.ce);
                 int k = dsc.vb + lane;
@@ -991,7 +996,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     for (; k < kend; k += 32) a = fma((double)cv[k], ld_cg(P.sv + ci[k]), a);
                 }
                 for (; k < dsc.ve; k += 32) {
-                    const int r = __ldg(S.idx + k);
+                    const int r = seg_idx(S, k, dsc.cb);
                     const double xv = (double)__ldg(S.val + k);
                     a = fma(xv, ld_cg(P.sv + r), a);
                     if (zs) az = fma(xv, ld_cg(P.svz + r), az);
@@ -1061,7 +1066,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 acc[st] = 0.0;
                 const SChunk d = s_desc[st];
                 if (d.ok) {
-                    const int* ci = s_idx + st * IR_SCH - d.a;
+                    const int* ci = S.idx ? s_idx + st * IR_SCH - d.a : S.rowtab - d.cb;
                     const float* cv = s_val + st * IR_SCH - d.a;
                     const int kend = min(d.ve, d.ce);
                     double a = 0.0;
@@ -1075,7 +1080,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     }
                     const int kt = max(kend, d.vb) + (int)threadIdx.x;   // the global tail past X's last 16-byte
                     if (kt < d.ve)                                          // boundary (a chunk may start past kend)
-                        a = fma((double)__ldg(S.val + kt), sv_sh[__ldg(S.idx + kt)], a);
+                        a = fma((double)__ldg(S.val + kt), sv_sh[seg_idx(S, kt, d.cb)], a);
                     acc[st] = a;
                     if (threadIdx.x == 0) nhs += d.ve - d.vb;
                 }
@@ -1131,7 +1136,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (dsc.cf == 0.0) break;
                 mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
                 g_phase ^= 1u << stg;
-                const int* ci = cs.sidx + stg * GSCH - dsc.a;
+                const int* ci = S.idx ? cs.sidx + stg * GSCH - dsc.a : S.rowtab - dsc.cb;
                 const float* cv = cs.sval + stg * GSCH - dsc.a;
                 const int kend = min(dsc.ve, dsc.ce);
                 int k = dsc.vb + lane;
@@ -1144,7 +1149,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 }
                 a += (a1 + a2) + a3;
                 for (; k < kend; k += 32) a = fma((double)cv[k], sv_sh[ci[k]], a);
-                for (; k < dsc.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[__ldg(S.idx + k)], a);
+                for (; k < dsc.ve; k += 32) a = fma((double)__ldg(S.val + k), sv_sh[seg_idx(S, k, dsc.cb)], a);
                 if (dsc.last) {
                     const double t = warp_sum(a);
                     if (lane == 0) {
@@ -1376,7 +1381,7 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
             mbar_wait(cs.bar + stg, (phase >> stg) & 1u);
             GS_MARK(6);
             phase ^= 1u << stg;
-            const int* ci = cs.sidx + stg * GSCH - dsc.a;
+            const int* ci = S.idx ? cs.sidx + stg * GSCH - dsc.a : S.rowtab - dsc.cb;
             const float* cv = cs.sval + stg * GSCH - dsc.a;
             const int kend = min(dsc.ve, dsc.ce);
             int k = dsc.vb + lane;
@@ -1398,7 +1403,7 @@ __global__ void __launch_bounds__(256, 1) k_gather_small(Prm P, Seg S, ASet AS, 
                 b = fma(x0 * x0, q0.y, b);
             }
             for (; k < dsc.ve; k += 32) {
-                const double2 q0 = rd_sh[__ldg(S.idx + k)];
+                const double2 q0 = rd_sh[seg_idx(S, k, dsc.cb)];
                 const double x0 = (double)__ldg(S.val + k);
                 a = fma(x0, q0.x, a);
                 b = fma(x0 * x0, q0.y, b);
@@ -1612,7 +1617,7 @@ __global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* sli
         mbar_wait(s_bar + st, (s_phase >> st) & 1u);
         s_phase ^= 1u << st;
         const double cf = P.w[__ldg(slist + d.p)];
-        const int* ci = s_idx + st * IR_SCH - d.a;
+        const int* ci = S.idx ? s_idx + st * IR_SCH - d.a : S.rowtab - d.cb;
         const float* cv = s_val + st * IR_SCH - d.a;
         const int kend = min(d.ve, d.ce);
         constexpr int UB = IR_SCH / 256;
@@ -1635,7 +1640,7 @@ __global__ void __launch_bounds__(256, 1) k_margins_small(Prm P, Seg S, int* sli
                 if (r[u] >= 0) xs_sh[r[u]] = fma(xv[u], cf, a[u]);
         }
         for (int k = max(kend, d.vb) + threadIdx.x; k < d.ve; k += blockDim.x) {   // (a chunk may start past kend)
-            const int r = __ldg(S.idx + k);
+            const int r = seg_idx(S, k, d.cb);
             xs_sh[r] = fma((double)__ldg(S.val + k), cf, xs_sh[r]);
         }
         if (threadIdx.x == 0) nsc += d.ve - d.vb;

@@ -56,13 +56,17 @@ struct Units {
 // a segment source: rows of CSR or columns of CSC restricted to a list
 struct Seg {
     const int* ptr;   // rowptr / colptr
-    const int* idx;   // col / row indices
+    const int* idx;   // col / row indices; nullptr: a dense X read by columns (index-free, ml.h), where the row of
+                      // element k of a column starting at cb is k - cb
     const float* val;
     long long nnz;
     const int* list;  // positions -> segment ids (nullptr = identity)
     double2* hres;    // heavy results per position
     int split;        // segments longer than this take the heavy (split) path
+    const int* rowtab;   // dense X: rowtab[t] = t (t < m), so that rowtab - cb stands in for a staged index chunk
 };
+// the index of element k of a segment starting at cb (dense X: computed, no load)
+__device__ __forceinline__ int seg_idx(const Seg& S, long long k, int cb) { return S.idx ? __ldg(S.idx + k) : (int)(k - cb); }
 
 // ------------------------------------------------------------------ per-element operations
 struct OpMargin {     // z_i = sum_k X_ik w_k, gathers gated by the support bitmap
@@ -89,15 +93,27 @@ struct OpDot {        // acc = sum_i X_ij v_i
 };
 // Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).  Each lane streams U 16-byte vectors of
 // indices and U of values per iteration (all loads issued before use), peeling the unaligned ends.
+// cb: the start of the segment's column / row (dense X: the index of element k is k - cb)
 template <int G, int U = 2, class Op>
-__device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int e, int lane, double& a0, double& a1) {
+__device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int e, int lane, double& a0, double& a1,
+                                          int cb) {
     for (int k = (b & ~3) + 4 * lane; k < e; k += 4 * U * G) {
         int4 iv[U];
         float4 vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int ku = k + 4 * G * u;
-            if (ku < e && ku + 4 <= S.nnz) { iv[u] = ld_stream_i4(S.idx + ku); vv[u] = ld_stream_f4(S.val + ku); }
+            if (!S.idx) {   // dense X: values only
+                iv[u] = make_int4(ku - cb, ku + 1 - cb, ku + 2 - cb, ku + 3 - cb);
+                if (ku < e && ku + 4 <= S.nnz) vv[u] = ld_stream_f4(S.val + ku);
+                else if (ku < e) {
+                    vv[u].x = S.val[ku];
+                    vv[u].y = (ku + 1 < S.nnz) ? S.val[ku + 1] : 0.f;
+                    vv[u].z = (ku + 2 < S.nnz) ? S.val[ku + 2] : 0.f;
+                    vv[u].w = 0.f;
+                } else vv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!(ku < e)) iv[u] = make_int4(0, 0, 0, 0);
+            } else if (ku < e && ku + 4 <= S.nnz) { iv[u] = ld_stream_i4(S.idx + ku); vv[u] = ld_stream_f4(S.val + ku); }
             else if (ku < e) {
                 iv[u].x = S.idx[ku]; vv[u].x = S.val[ku];
                 iv[u].y = (ku + 1 < S.nnz) ? S.idx[ku + 1] : 0; vv[u].y = (ku + 1 < S.nnz) ? S.val[ku + 1] : 0.f;
@@ -153,7 +169,7 @@ __device__ __forceinline__ void seg_tile(const Seg& S, const Op& op, int nseg, i
         const int slot = r * NG + grp;
         const int b = sb[slot], e = se[slot];
         double a0 = 0.0, a1 = 0.0;
-        seg_accum<G>(S, op, b, e, lane, a0, a1);
+        seg_accum<G>(S, op, b, e, lane, a0, a1, b);
         a0 = group_sum<G>(a0);
         a1 = group_sum<G>(a1);
         if (lane == 0 && e >= 0) res[slot] = make_double2(a0, a1);
@@ -233,15 +249,15 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
                 int r[4];
                 float v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) { r[u] = __ldg(S.idx + k + 32 * u); v[u] = __ldg(S.val + k + 32 * u); }
+                for (int u = 0; u < 4; ++u) { r[u] = seg_idx(S, k + 32 * u, b0); v[u] = __ldg(S.val + k + 32 * u); }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) atomicAdd(out + r[u], (double)v[u] * cf);
             }
-            for (; k < e; k += 32) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
+            for (; k < e; k += 32) atomicAdd(out + seg_idx(S, k, b0), (double)__ldg(S.val + k) * cf);
         } else {
             if (lane == 0) streamed += e - b;
             double a0 = 0.0, a1 = 0.0;
-            seg_accum<32, 4>(S, op, b, e, lane, a0, a1);
+            seg_accum<32, 4>(S, op, b, e, lane, a0, a1, b0);
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
             int last = 0;
@@ -525,7 +541,7 @@ __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, i
         if (lane == 0) segs += 1;
         if (e - b > S.split) continue;   // heavy columns: k_heavy<SCATTER>
         if (lane == 0) streamed += e - b;
-        for (int k = b + lane; k < e; k += G) atomicAdd(out + __ldg(S.idx + k), (double)__ldg(S.val + k) * cf);
+        for (int k = b + lane; k < e; k += G) atomicAdd(out + seg_idx(S, k, b), (double)__ldg(S.val + k) * cf);
     }
     acc_add(nnz_acc, streamed, segs);
 }
@@ -537,7 +553,8 @@ __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, i
 // load chain per chunk.  Block b owns positions [b*q, (b+1)*q); warp w takes every W-th position of that range.
 // SCH: elements per staged chunk (4*SCH bytes of indices + 4*SCH of values); NSTG: chunks in flight per warp.
 
-struct ChunkDesc { int a, vb, ve, ce; int p, last; double cf; };   // copy start, valid [vb, ve), copied to ce
+// copy start, valid [vb, ve), copied to ce; cb: the start of the chunk's column (dense X: its row indices)
+struct ChunkDesc { int a, vb, ve, ce; int p, last, cb, pad; double cf; };
 
 template <int SCH, int NSTG>
 struct ColStream {
@@ -582,7 +599,7 @@ struct ColStream {
             const int start = b + noff;
             if (cf == 0.0 || start >= e) {
                 if (!coef && noff == 0 && cf != 0.0) {   // gather mode: an empty column still gets its (zero) output
-                    d.a = b & ~3; d.vb = b; d.ve = b; d.ce = d.a; d.cf = 1.0; d.p = p; d.last = 1;
+                    d.a = b & ~3; d.vb = b; d.ve = b; d.ce = d.a; d.cf = 1.0; d.p = p; d.last = 1; d.cb = b;
                     ++kk;
                     return true;
                 }
@@ -591,6 +608,7 @@ struct ColStream {
             if (noff == 0 && lane == 0) { streamed += e - b; segs += 1; }
             d.a = start & ~3;
             d.vb = start;
+            d.cb = b;
             d.ve = min(e, d.a + SCH);
             d.ce = min((d.ve + 3) & ~3, nnz4);
             if (d.ce < d.a) d.ce = d.a;
@@ -605,8 +623,8 @@ struct ColStream {
         const uint32_t bytes = 4u * (uint32_t)(d.ce - d.a);
         if (bytes) {
             fence_proxy_async();
-            mbar_arrive_expect_tx(bar + st, 2 * bytes);
-            bulk_g2s(sidx + st * SCH, S->idx + d.a, bytes, bar + st);
+            mbar_arrive_expect_tx(bar + st, S->idx ? 2 * bytes : bytes);   // (dense X: values only)
+            if (S->idx) bulk_g2s(sidx + st * SCH, S->idx + d.a, bytes, bar + st);
             bulk_g2s(sval + st * SCH, S->val + d.a, bytes, bar + st);
         } else {
             mbar_arrive(bar + st);
@@ -696,7 +714,7 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         if (d.cf == 0.0) break;
         mbar_wait(cs.bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
-        const int* ci = cs.sidx + st * SCH - d.a;
+        const int* ci = S.idx ? cs.sidx + st * SCH - d.a : S.rowtab - d.cb;
         const float* cv = cs.sval + st * SCH - d.a;
         const int kend = min(d.ve, d.ce);
         int k = d.vb + cs.lane;
@@ -710,7 +728,7 @@ __global__ void k_scatter_smem(Seg S, const int* nseg_dev, int nseg_host, const 
         }
         for (; k < kend; k += 32) { const int r = ci[k]; mine[r] = fma((double)cv[k], d.cf, mine[r]); }
         for (; k < d.ve; k += 32) {   // array tail not covered by 16-byte copies
-            const int r = __ldg(S.idx + k);
+            const int r = seg_idx(S, k, d.cb);
             mine[r] = fma((double)__ldg(S.val + k), d.cf, mine[r]);
         }
         __syncwarp();
@@ -783,7 +801,7 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         if (d.cf == 0.0) break;
         mbar_wait(cs.bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
-        const int* ci = cs.sidx + st * SCH - d.a;
+        const int* ci = S.idx ? cs.sidx + st * SCH - d.a : S.rowtab - d.cb;
         const float* cv = cs.sval + st * SCH - d.a;
         const int kend = min(d.ve, d.ce);
         int k = d.vb + cs.lane;
@@ -796,7 +814,7 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
         }
         a += (a1 + a2) + a3;
         for (; k < kend; k += 32) a = fma((double)cv[k], sv[ci[k]], a);
-        for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv[__ldg(S.idx + k)], a);
+        for (; k < d.ve; k += 32) a = fma((double)__ldg(S.val + k), sv[seg_idx(S, k, d.cb)], a);
         if (d.last) {
             const double t = warp_sum(a);
             if (cs.lane == 0) out[d.p] = t;

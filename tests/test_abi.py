@@ -54,6 +54,10 @@ def test_workspace_and_validation_host_only():
         d2 = ml.MLData(3, 5, 4, *p)
         assert L.ml_create(ctypes.byref(d2), 1.0, None, None, 10, ctypes.byref(h)) == ml.ML_E_INVAL
     assert L.ml_status_str(ml.ML_E_NONFINITE) == b"non-finite input"
+    # index-free dense X (include/ml.h): NULL CSC pointers / rows are accepted only with nnz = m n, m <= 8192, no CSR
+    for (mm, nn, nz, csr) in ((3, 5, 14, 0), (9000, 2, 18000, 0), (3, 5, 15, 16)):
+        d3 = ml.MLData(mm, nn, nz, csr, csr, csr, None, None, 16, 16)
+        assert L.ml_create(ctypes.byref(d3), 1.0, None, None, 10, ctypes.byref(h)) == ml.ML_E_INVAL
     assert L.ml_status_str(ml.ML_E_STAGNATION) == b"line search stagnation"
     o = ml.default_opts()
     assert o.tol_kkt == 1e-6 and o.K_fine == 2 and o.K_mid == 3 and o.K_coarse == 5 and o.inner_cg == 2 and o.pcd_snap == 1

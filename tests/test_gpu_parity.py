@@ -764,3 +764,46 @@ def test_merge_path_gather_bitwise_reproducible():
     ctx2 = ml.Context(ds)
     r2 = ctx2.ml_solve()
     assert r1["cycles"] == r2["cycles"] and r1["nnz_w"] == r2["nnz_w"]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg2m", "n1"])
+def test_dense_index_free_bitwise(name):
+    """Index-free dense X (include/ml.h): values only, no CSR / CSC pointers / row indices on the
+    device.  The arithmetic is the indexed path's, so every output is bitwise equal to it: F, g, h, Hv, the line search,
+    the coarse selection and the whole solve (and therefore the oracle parity of the indexed path carries over)."""
+    ds = dataset(name)
+    assert ds.nnz == ds.m * ds.n
+    a, b = ml.Context(ds), ml.Context(ds, dense=True)
+    assert b.csc_row is None and b.csc_colptr is None and b.csr_col is None
+    rng = np.random.default_rng(3)
+    w = random_w(ds.n, "ten", 5)
+    for c in (a, b):
+        c.ml_set_w(dt(w))
+    Fa, ga, ha = a.ml_eval_f_grad()
+    Fb, gb, hb = b.ml_eval_f_grad()
+    assert Fa == Fb and torch.equal(ga, gb) and torch.equal(ha, hb)
+    C = np.sort(rng.choice(ds.n, max(1, ds.n // 3), replace=False)).astype(np.int32)
+    v = dt(rng.standard_normal(len(C)))
+    assert torch.equal(a.ml_hessvec(dt(C, torch.int32), v), b.ml_hessvec(dt(C, torch.int32), v))
+    assert torch.equal(a.ml_diag_hess(dt(C, torch.int32)), b.ml_diag_hess(dt(C, torch.int32)))
+    g = ga.clone()
+    assert torch.equal(a.ml_select_coarse(g, ds.n // 2 + 3), b.ml_select_coarse(g, ds.n // 2 + 3))
+    la = a.ml_shrink_linesearch(None, g, h=ha)
+    lb = b.ml_shrink_linesearch(None, g, h=hb)
+    assert la == lb and torch.equal(a.ml_get_w(), b.ml_get_w())
+    ra = ml.Context(ds).ml_solve()
+    cb = ml.Context(ds, dense=True)
+    rb = cb.ml_solve()
+    assert ra["F"] == rb["F"] and ra["cycles"] == rb["cycles"] and ra["relaxations"] == rb["relaxations"]
+    r_o = oracle.Oracle(ds).solve()
+    assert rb["status"] == 0 and abs(rb["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+
+
+def test_dense_full_cfg2_solve():
+    """BASELINE config 2 (2000 x 20000 dense) solved index-free: bitwise the indexed solve, and the oracle's F."""
+    ds = _full(2)
+    ra = ml.Context(ds).ml_solve()
+    rb = ml.Context(ds, dense=True).ml_solve()
+    assert ra["F"] == rb["F"] and ra["cycles"] == rb["cycles"]
+    r_o = oracle.Oracle(ds).solve()
+    assert abs(rb["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
