@@ -160,10 +160,13 @@ ml_status ml_inner_phases(ml_ctx *c, uint64_t *ns_host, int reset);
    driven by its own host thread, then solve side by side: small problems are latency-bound on the whole GPU.
    ML_E_INVAL if the small-m solver would own more than 64 rows per block (m > 64 blocks). */
 ml_status ml_set_sm_share(ml_ctx *c, int blocks);
-/* Engine selection for A/B measurement and parity tests.  flags bit 0: the large-m (m > 8192) column gathers of A2
-   use the merge-path column pass (every thread gets the same number of nonzeros + column ends whatever the column
-   lengths; default on for large m); 0 selects the per-column segment engine.  ML_E_INVAL when bit 0 is asked for on
-   a small-m context (which reads X through shared-memory passes). */
+/* Engine selection for A/B measurement and parity tests (defaults need no call).
+   bit 0: the large-m (m > 8192) column gathers of A2 use the merge-path column pass (every thread gets the same number
+          of nonzeros + column ends whatever the column lengths; off by default: measured slower than the segment
+          engine on configs 4-5); ML_E_INVAL on a small-m context (which reads X through shared-memory passes).
+   bit 3: the large-m inner solver's X_A s and H sigma streams claim their column units dynamically from a grid-wide
+          counter whatever the unit count (by default only with >= 32 units per warp, where static shares left blocks
+          waiting on the slowest). */
 ml_status ml_set_engine(ml_ctx *c, uint32_t flags);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */

@@ -1194,6 +1194,7 @@ ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
     const bool want = (flags & 1u) != 0;
     if (want && c->mp_grid_all == 0) return ML_E_INVAL;   // (small m: the shared-memory passes; no merge-path plan)
     c->mp = want;
+    c->P.dyn = (flags & 8u) ? 1 : 0;   // bit 3: dynamic unit claims in the large-m inner solver whatever the unit count
     return ML_OK;
 }
 

@@ -64,7 +64,11 @@ enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 }; 
 #ifndef IR_UNIT_V
 #define IR_UNIT_V 2048
 #endif
-constexpr int IR_UNIT = IR_UNIT_V;   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
+constexpr int IR_UNIT = IR_UNIT_V;
+#ifndef IR_DYN_V
+#define IR_DYN_V 32
+#endif
+constexpr int IR_DYN = IR_DYN_V;   // BIG: the S and G streams claim units dynamically when there are >= IR_DYN per warp   // BIG: columns are streamed in units of at most IR_UNIT nonzeros
 #ifndef IR_UCOST_V
 #define IR_UCOST_V 1024
 #endif
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     __syncthreads();
     SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
     int u0 = 0, u1 = 0;   // BIG: my range of column units (balanced by nonzeros across blocks)
+    int nU = 0;           // BIG: all units (the S and G streams claim them dynamically, Ctl::s_ctr / g_ctr)
     if constexpr (BIG) {
         int nu_loc = 0, nz_loc = 0;
         for (int k = threadIdx.x; k < q0; k += blockDim.x) {
@@ -479,8 +484,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             zbase += zwtot;
             __syncthreads();
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) { P.ustart[nA] = NU; P.unz[NU] = NZ; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { P.ustart[nA] = NU; P.unz[NU] = NZ; c->s_ctr = 0u; c->g_ctr = 0u; }
         grid.sync();
+        nU = NU;
         if (threadIdx.x == 0) {   // my units: those starting in my share [b T, (b+1) T) of the nonzeros
             const long long T = (NZ + G - 1) / G;
             for (int h = 0; h < 2; ++h) {
@@ -573,7 +579,13 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             ColStream<GSCH, GST> cs;
             cs.streamed = 0;
             cs.segs = 0;
-            stream_begin(cs, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            if (nU >= IR_DYN * G * IR_W || P.dyn) {   // many units per warp: dynamic claims (no block waits on another
+                                                       // at B1)
+                cs.claim = &c->s_ctr;
+                stream_begin(cs, S, nullptr, 0, nU, gbase, P.uext, nU);
+            } else {
+                stream_begin(cs, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            }
             int stg = 0;
             while (true) {
                 const ChunkDesc dsc = cs.desc[stg];
@@ -709,7 +721,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (BIG) { __syncthreads(); bd_s += gtimer() - bd_t0; }
 #endif
         PH_MARK(1);
-        if constexpr (BIG) grid.sync();   // B1
+        if constexpr (BIG) {
+            grid.sync();   // B1
+            if (blockIdx.x == 0 && threadIdx.x == 0) c->s_ctr = 0u;   // (every warp's S claims are done)
+        }
         else {   // B1, split: the G rings (aliasing the consumed S ring) are set up and issued while it completes
             const unsigned bar_old = gbar_arrive(&c->gbar);
             if (need_hs && !resident) {
@@ -850,7 +865,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             g_phase = 0u;
             csG.streamed = 0;
             csG.segs = 0;
-            stream_begin(csG, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            if (nU >= IR_DYN * G * IR_W || P.dyn) {
+                csG.claim = &c->g_ctr;
+                stream_begin(csG, S, nullptr, 0, nU, gbase, P.uext, nU);
+            } else {
+                stream_begin(csG, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+            }
         }
         PH_MARK(3);
         grid.sync();   // B2
@@ -1026,6 +1046,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             bd_g += gtimer() - bd_t0;
 #endif
             grid.sync();   // every unit's partial
+            if (blockIdx.x == 0 && threadIdx.x == 0) c->g_ctr = 0u;
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
                 const int p = p0 + k;
                 const int ua = ld_cg(P.ustart + p), ub = ld_cg(P.ustart + p + 1);

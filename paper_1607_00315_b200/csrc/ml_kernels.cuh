@@ -41,6 +41,7 @@ struct Ctl {
     int units_n[4], units_h[4];   // per unit slot: #units, #heavy segments
     int ntrace, trace_cap, bad_y, pad2;
     unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics
+    unsigned s_ctr, g_ctr;       // large-m inner solver: unit claim counters of the S and G streams
 };
 
 // heavy-segment schedule for one segment list
@@ -287,7 +288,7 @@ struct Prm {
     const int8_t* y;
     const double* b;   // squared loss (LASSO) targets; nullptr = logistic loss with labels y
     double lam, eps_h, sigma_in, sigma_out, beta_ls, tol, eta;
-    int max_ls, inner_cg, pcd_snap, pad_p;
+    int max_ls, inner_cg, pcd_snap, dyn;   // dyn: large-m streams claim units dynamically whatever their count
     double* w; uint32_t* wbits; double* z; double2* rD;
     double* Xd; double* Xs; double* sv; double* Xu;   // Xu: scatter target of the atomic path (kept zero between uses)
     double* Xz; double* svz; double* Xzu;             // snap path: X_A z, D o Xz; Xzu: atomic scatter target of z (kept zero)
@@ -568,9 +569,22 @@ struct ColStream {
     const double* coef;
     int* sidx; float* sval; uint64_t* bar; ChunkDesc* desc;
     const int2* ext; int ext_p0, ext_n;   // optional cached segment extents of positions [ext_p0, ext_p0 + ext_n)
+    // dynamic schedule (claim != nullptr): the warp claims CLAIM_B positions of [p0, p1) at a time from a grid-wide
+    // counter, so that no warp idles while another still holds a static share; its ring keeps streaming across claims
+    static constexpr int CLAIM_B = 8;
+    unsigned* claim = nullptr;
+    int cb0 = 0, cbn = 0;
 
+    __device__ void claim_next() {
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd(claim, (unsigned)CLAIM_B);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        cb0 = base;
+        cbn = max(0, min(CLAIM_B, p1 - base));
+        load_batch();
+    }
     __device__ void load_batch() {
-        const int p = p0 + wid + W * (batch * 32 + lane);
+        const int p = claim ? (lane < cbn ? cb0 + lane : p1) : p0 + wid + W * (batch * 32 + lane);
         mb = 0; me = 0; mcf = 0.0;
         if (p < p1) {
             mcf = coef ? coef[p] : 1.0;
@@ -591,9 +605,18 @@ struct ColStream {
     // next chunk descriptor (all lanes, uniform); false when the warp's range is exhausted
     __device__ bool next(ChunkDesc& d) {
         while (true) {
-            if (kk == 32) { ++batch; load_batch(); }
-            const int p = p0 + wid + W * (batch * 32 + kk);
-            if (p >= p1) return false;
+            int p;
+            if (claim) {
+                if (kk == cbn) {
+                    claim_next();
+                    if (cbn == 0) return false;
+                }
+                p = cb0 + kk;
+            } else {
+                if (kk == 32) { ++batch; load_batch(); }
+                p = p0 + wid + W * (batch * 32 + kk);
+                if (p >= p1) return false;
+            }
             const int b = __shfl_sync(0xffffffffu, mb, kk), e = __shfl_sync(0xffffffffu, me, kk);
             const double cf = __shfl_sync(0xffffffffu, mcf, kk);
             const int start = b + noff;
@@ -853,7 +876,8 @@ __device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG>& cs, const Seg
     cs.sval = reinterpret_cast<float*>(base + 4 * NSTG * SCH);
     cs.bar = reinterpret_cast<uint64_t*>(base + 8 * NSTG * SCH);
     cs.desc = reinterpret_cast<ChunkDesc*>(cs.bar + NSTG);
-    cs.load_batch();
+    if (cs.claim) { cs.cbn = 0; cs.kk = 0; }   // (the first next() claims)
+    else cs.load_batch();
     for (int st = 0; st < NSTG; ++st) {
         ChunkDesc d;
         const bool ok = cs.next(d);

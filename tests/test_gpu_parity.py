@@ -737,13 +737,14 @@ def test_misaligned_arrays_rejected():
 
 @pytest.mark.parametrize("name", ["cfg4s", "lasso4s", "sparse_big"])
 def test_column_engines_agree(name):
-    """The large-m column engines (ml_set_engine: merge-path pass, or per-column segments) give the same gradients
-    inside the solve: both solves match the oracle, with identical relaxation traces (levels, |A|, outcomes)."""
+    """The large-m engines (ml_set_engine: merge-path or per-column gathers; static or dynamic unit schedules in the
+    inner solver) agree inside the solve: every combination matches the oracle, with identical relaxation traces
+    (levels, |A|, outcomes)."""
     ds = mlgen.random_sparse(12000, 9000, 0.01, seed=7, lam_factor=0.05, empty_rows=20, empty_cols=300) \
         if name == "sparse_big" else dataset(name)
     r_o = oracle.Oracle(ds).solve()
     res = []
-    for eng in (1, 0):   # bit 0: merge-path gathers (ml_set_engine)
+    for eng in (1, 0, 8):   # bit 0: merge-path gathers; bit 3: dynamic unit claims (ml_set_engine)
         ctx = ml.Context(ds)
         ctx.ml_set_engine(eng)
         r = ctx.ml_solve()
