@@ -60,7 +60,9 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 // outer line search + update (R14-R18): 0 g.d, 1 max|d|, 2..5 l1 trials 0..3, 6..9 loss trials 0..3; the rest:
 // 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
 constexpr int IR_NLS = ML_MAXLS - 4;
-enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_NSLOT = IR_SU + 2 };   // IR_SU, +1: unit counts, nnz (BIG)
+enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_SO3 = IR_SU + 2, IR_NSLOT = IR_SO3 + 6 };
+// IR_SU, +1: unit counts, nnz (BIG); IR_SO3: trials 1/2, 1/4, 1/8 of a large-m outer line search (l1, loss) when
+// alpha = 1 failed
 #ifndef IR_UNIT_V
 #define IR_UNIT_V 2048
 #endif
@@ -940,8 +942,27 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         acc_steps += 1;
         // R12, m side: Xd += X sigma on my rows (sigma = beta s, or beta s + (1 - beta) z on the snap path)
-        for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x)
-            xd_r[k] += beta * xs_r[k] + (zs ? (1.0 - beta) * xz_r[k] : 0.0);
+        if (BIG) {   // (thousands of rows per block in global memory: 8 rows in flight per thread)
+            for (int k0 = threadIdx.x; k0 < r1 - r0; k0 += 8 * blockDim.x) {
+                double xd[8], xs[8], xz[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u * blockDim.x;
+                    const bool in = k < r1 - r0;
+                    xd[u] = in ? xd_r[k] : 0.0;
+                    xs[u] = in ? xs_r[k] : 0.0;
+                    xz[u] = (in && zs) ? xz_r[k] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u * blockDim.x;
+                    if (k < r1 - r0) xd_r[k] = xd[u] + (beta * xs[u] + (zs ? (1.0 - beta) * xz[u] : 0.0));
+                }
+            }
+        } else {
+            for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x)
+                xd_r[k] += beta * xs_r[k] + (zs ? (1.0 - beta) * xz_r[k] : 0.0);
+        }
         if (BIG && need_hs) {   // G from L2: Hsigma = beta X^T (D o Xs) (+ (1 - beta) X^T (D o Xz)) + eps sigma
             __syncthreads();
             PH_MARK(5);
@@ -1237,7 +1258,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     at[0] = 1.0;
 #pragma unroll
     for (int k = 1; k < 4; ++k) at[k] = at[k - 1] * P.beta_ls;
-    {   // first batch {1, 1/2, 1/4, 1/8} (Eq. 4; Armijo Q7; term-by-term differences Q26)
+    // first batch {1, 1/2, 1/4, 1/8} (Eq. 4; Armijo Q7; term-by-term differences Q26).  Large m: alpha = 1
+    // alone first -- it is the common outcome, and each trial costs an exp / expm1 / log1p per row (thousands of rows
+    // per block) -- then {1/2, 1/4, 1/8} only if it fails
+    constexpr int NT1 = BIG ? 1 : 4;
+    {
         double v[10];
 #pragma unroll
         for (int k = 0; k < 10; ++k) v[k] = 0.0;
@@ -1246,17 +1271,39 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             v[0] += X.gA[k0] * d;
             v[1] = fmax(v[1], fabs(d));
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[2 + k] += fabs(w + at[k] * d) - aw;
+            for (int k = 0; k < NT1; ++k) v[2 + k] += fabs(w + at[k] * d) - aw;
         }
         for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
             const double zi = P.z[i], xd = xd_r[i - r0];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) v[6 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
+            for (int k = 0; k < NT1; ++k) v[6 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
         }
         ir_block_partials<10>(v, 1u << 1, 0u, sh_w, part, IR_SO);
     }
     grid.sync();
     ir_totals(part, IR_SO, 10, 1u << 1, 0u, sh_t);
+    if (BIG && sh_t[1] != 0.0 && P.max_ls > 1 &&
+        !(sh_t[6] + P.lam * sh_t[2] <= P.sigma_out * (sh_t[0] + P.lam * sh_t[2]))) {   // alpha = 1 failed
+        double v[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = 0.0;
+        for (int k0 = threadIdx.x; k0 < q0; k0 += blockDim.x) {
+            const double d = X.d[k0], w = X.wA[k0], aw = fabs(w);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) v[k - 1] += fabs(w + at[k] * d) - aw;
+        }
+        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            const double zi = P.z[i], xd = xd_r[i - r0];
+#pragma unroll
+            for (int k = 1; k < 4; ++k) v[2 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
+        }
+        ir_block_partials<6>(v, 0u, 0u, sh_w, part, IR_SO3);
+        grid.sync();
+        __shared__ double sh_t3[6];
+        ir_totals(part, IR_SO3, 6, 0u, 0u, sh_t3);
+        if (threadIdx.x < 3) { sh_t[3 + threadIdx.x] = sh_t3[threadIdx.x]; sh_t[7 + threadIdx.x] = sh_t3[3 + threadIdx.x]; }
+        __syncthreads();
+    }
     const double Delta = sh_t[0] + P.lam * sh_t[2];
     if (sh_t[1] == 0.0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { c->skip = 1; c->outcome = OUT_NOSTEP; ir_trace(P, c, OUT_NOSTEP, acc_steps, IR_FB(F0), F0, IR_AL(0.0)); }
