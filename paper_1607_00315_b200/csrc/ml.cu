@@ -26,7 +26,8 @@ constexpr int SM_MAX = IR_GMAX;   // partial buffers are sized for this many SMs
 constexpr int GRID_CAP = 148 * 4;   // grid-stride passes: 4 blocks per B200 SM (any count works, this sizes partials)
 constexpr int TRACE_CAP = 1 << 16;
 constexpr int NV_MAX = 96;   // widest reduction payload (doubles per block)
-constexpr int SMALL_M = 8192;   // m-vectors up to this size are accumulated in shared memory (k_scatter_smem)
+constexpr int SMALL_M = 8192;
+constexpr int64_t CLAIM_NNZ = 16 << 20;   // k_heavy claims its units dynamically from this many nonzeros of X   // m-vectors up to this size are accumulated in shared memory (k_scatter_smem)
 
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -222,6 +223,16 @@ Units units_of(ml_ctx* c, int slot) {
     U.cap = c->um[slot].cap;
     U.n = c->ctl ? &c->ctl->units_n[slot] : nullptr;
     U.h = c->ctl ? &c->ctl->units_h[slot] : nullptr;
+    U.claim = nullptr;
+    return U;
+}
+// the same for a k_heavy launch that claims its units dynamically (the claim counter zeroed on the stream first);
+// only where there are many units (nnz >= 16 M): on small X the memset and the claims cost more than the balance gains
+Units units_claim(ml_ctx* c, int slot) {
+    Units U = units_of(c, slot);
+    if (c->X.nnz < CLAIM_NNZ) return U;
+    cudaMemsetAsync(&c->ctl->hclaim, 0, sizeof(unsigned), c->st);
+    U.claim = &c->ctl->hclaim;
     return U;
 }
 
@@ -439,7 +450,7 @@ void launch_margins(ml_ctx* c) {
         return;
     }
     Seg S = seg_rows(c);
-    ML_LAUNCH(c, (k_heavy<OpMargin, false>), c->gHeavy, S, units_of(c, 3), OpMargin{c->P.w, c->P.wbits},
+    ML_LAUNCH(c, (k_heavy<OpMargin, false>), c->gHeavy, S, units_claim(c, 3), OpMargin{c->P.w, c->P.wbits},
               (const double*)nullptr, (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_MARGINS));
     const int grid = std::max(1, std::min(GRID_CAP, (int)((c->X.m + TILE - 1) / TILE)));
     ML_DISPATCH_G(c->Gr, ML_LAUNCH(c, k_margins<GG>, grid, c->P, S, acc_of(c, CLS_MARGINS)));
@@ -512,7 +523,7 @@ void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* lis
         else ML_LAUNCH(c, (k_gather_free<32, false, true>), grid, c->P, So, AS, (long long*)nullptr);
         return;
     }
-    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, list ? 1 : 0), OpGH{c->P.rD},
+    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_claim(c, list ? 1 : 0), OpGH{c->P.rD},
               (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
     const int ts = finest ? TILE : 64;   // (k_gather_free's tile size)
     const int grid = std::max(1, std::min(GRID_CAP, (nC_host + ts - 1) / ts));
@@ -538,7 +549,7 @@ void launch_scatter(ml_ctx* c, int cls, const int* list, int slot, const int* ns
         c->launches++;
         return;
     }
-    ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_of(c, slot), OpDot{nullptr}, coef, out,
+    ML_LAUNCH(c, (k_heavy<OpDot, true>), c->gHeavy, S, units_claim(c, slot), OpDot{nullptr}, coef, out,
               (const int*)nullptr, (const int*)nullptr, acc_of(c, cls));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, k_scatter<GG>, c->gSeg, S, nseg_dev, nseg_host, coef, out, acc_of(c, cls)));
 }
@@ -554,7 +565,7 @@ void launch_gather_dot(ml_ctx* c, int cls, const int* list, int slot, const int*
         c->launches++;
         return;
     }
-    ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_of(c, slot), OpDot{v}, (const double*)nullptr,
+    ML_LAUNCH(c, (k_heavy<OpDot, false>), c->gHeavy, S, units_claim(c, slot), OpDot{v}, (const double*)nullptr,
               (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, cls));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 1, OpDot>), c->gSeg, S, OpDot{v}, nseg_dev, nseg_host, out,
                                    (double*)nullptr, acc_of(c, cls)));
@@ -928,7 +939,7 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
     }
     PassScope ps(c, CLS_API);
     Seg S = seg_cols(c, C);
-    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_of(c, slot), OpGH{c->P.rD}, (const double*)nullptr,
+    ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_claim(c, slot), OpGH{c->P.rD}, (const double*)nullptr,
               (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_API));
     const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,

@@ -42,6 +42,7 @@ struct Ctl {
     int ntrace, trace_cap, bad_y, pad2;
     unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics
     unsigned s_ctr, g_ctr;       // large-m inner solver: unit claim counters of the S and G streams
+    unsigned hclaim, pad4;       // k_heavy: unit claim counter (zeroed before each launch)
 };
 
 // heavy-segment schedule for one segment list
@@ -52,6 +53,7 @@ struct Units {
     double2* part;    // per-unit partials
     int* hcnt;        // per-heavy-segment arrival counters (kept at 0 between launches)
     int cap;
+    unsigned* claim;  // k_heavy: warps claim units four at a time from this counter (zeroed before the launch)
 };
 
 // a segment source: rows of CSR or columns of CSC restricted to a list
@@ -233,7 +235,15 @@ __global__ void __launch_bounds__(ML_NT) k_heavy(Seg S, Units U, Op op, const do
     const int nunits = min(*U.n, U.cap);
     const int gw = (blockIdx.x * ML_NT + threadIdx.x) >> 5, nw = (gridDim.x * ML_NT) >> 5;
     long long streamed = 0;
-    for (int u = gw; u < nunits; u += nw) {
+    int uend = 0;
+    for (int u = U.claim ? 0 : gw;; u = U.claim ? u + 1 : u + nw) {
+        if (U.claim && u >= uend) {   // dynamic: the next four units
+            int ub = 0;
+            if (lane == 0) ub = (int)atomicAdd(U.claim, 4u);
+            u = __shfl_sync(0xffffffffu, ub, 0);
+            uend = u + 4;
+        }
+        if (u >= nunits) break;
         const int4 un = U.u[u];
         const int p = un.x;
         if (SCATTER && coef[p] == 0.0) continue;   // (z pass: most units have a zero coefficient)
