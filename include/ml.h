@@ -28,8 +28,11 @@
  *   - ML_E_CUDA: a CUDA runtime error (message in ml_last_error).
  *   - ML_E_STAGNATION: no trial step passed the line search; the iterate is unchanged.
  *   - ML_E_NOT_CONVERGED: ml_solve hit max_cycles; w holds the last evaluated iterate.
- * Determinism: for m <= 8192 every reduction has a fixed order (ml_solve is bitwise reproducible); for larger m the
- *   Hessian-vector scatter X_A s (and the API's ml_hessvec) add with fp64 atomics: reproducible to rounding only.
+ * Determinism: ml_solve is bitwise reproducible at every m: every reduction has a fixed order, except the large-m
+ *   (m > 8192) solver's X_A s scatter, which adds 64-bit fixed-point integers (order-independent; the scale, a power
+ *   of 2, bounds each row's sum by 2^62: max |X| x max |coef| x the longest row, so a term is rounded to at most
+ *   2^-53 of that bound).  For m > 8192 the API's ml_hessvec and ml_shrink_linesearch (d given without Xd) scatter
+ *   X_C v with fp64 atomics: reproducible to rounding only.
  */
 #ifndef ML_H
 #define ML_H

@@ -364,6 +364,20 @@ __global__ void k_check_list(const int* C, long long nC, int n, Ctl* ctl) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&ctl->bad_y, 16);
 }
 __global__ void k_clear_flag(Ctl* ctl, int flag) { ctl->bad_y &= ~flag; }
+// max |X_ij| and the longest row (the large-m solver's fixed-point scale of X_A s)
+__global__ void k_xstats(const float* val, long long nnz, const int* rowptr, int m, Ctl* ctl) {
+    double mx = 0.0;
+    int mr = 0;
+    const long long T = (long long)gridDim.x * blockDim.x, t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (long long k = t0; k < nnz; k += T) mx = fmax(mx, fabs((double)val[k]));
+    for (long long i = t0; i < m; i += T) mr = max(mr, rowptr[i + 1] - rowptr[i]);
+    mx = warp_max(mx);
+    mr = __reduce_max_sync(0xffffffffu, (unsigned)mr);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(&ctl->xmax, mx);
+        atomicMax(&ctl->maxrow, mr);
+    }
+}
 // index-free dense X: column pointers j m and the row table t
 __global__ void k_dense_init(int* colptr, int* rowtab, int m, int n) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= n || k < m; k += gridDim.x * blockDim.x) {
@@ -843,6 +857,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (has_csr) ML_LAUNCH(c, k_check_index, GRID_CAP, X->csr_rowptr, X->csr_col, X->csr_val, (int)X->m, (int)X->n, X->nnz, c->ctl);
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
+    if (c->big_inner) ML_LAUNCH(c, k_xstats, GRID_CAP, X->csc_val, X->nnz, X->csr_rowptr, (int)X->m, c->ctl);
     if (c->mp_grid_all)   // the static merge-path plan over all columns (X is fixed for the context's life)
         ML_LAUNCH(c, k_mp_search, std::max(1, (c->mp_tiles_cap + ML_NT) / ML_NT), c->mp_all, c->mp_tiles_cap);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)

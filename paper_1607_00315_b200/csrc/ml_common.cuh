@@ -208,6 +208,15 @@ __device__ __forceinline__ void mbar_inval(uint64_t* bar) {
 __device__ __forceinline__ void red_add_global(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "d"(v) : "memory");
 }
+// fixed-point reduction: v rounded to the nearest multiple of 1 / q, added as a 64-bit integer.  Integer addition is
+// associative, so the sum does not depend on the order of the reductions (bitwise reproducible)
+__device__ __forceinline__ void red_add_fixed(double* p, double v, double q) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"((unsigned long long)__double2ll_rn(v * q))
+                 : "memory");
+}
+__device__ __forceinline__ double ld_fixed(const double* p, double qi) {
+    return (double)(long long)__ldcg(reinterpret_cast<const unsigned long long*>(p)) * qi;
+}
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");

@@ -317,7 +317,8 @@ __device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int 
     c->ntrace += 1;
 }
 
-// BIG (m > SMALL_M): the m-vectors live in global memory: S scatters with fp64 reductions into Xu (Xzu) through
+// BIG (m > SMALL_M): the m-vectors live in global memory: S scatters with 64-bit fixed-point reductions (integer
+// addition: order-independent, so bitwise reproducible; scale from max |X| x max |coef| x the longest row) into Xu (Xzu) through
 // per-warp TMA column rings, R takes my rows of Xu directly (and clears them), G gathers D o Xs (D o Xz) from L2 and
 // applies beta at each column end.  The iteration structure, barriers, decisions and the tail are the same.
 template <int GSCH, int GST, bool BIG>
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     }
 
     int next_pcd = 1, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;   // R6: PCD first
+    double fq = 1.0, fqi = 1.0;   // BIG: this iteration's fixed-point scale of X_A s (and its inverse)
     double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = 0.0, slope = 0.0, ss = 0.0, ps = 0.0;
     double sHs = 0.0, vq = 0.0;
     const double vmax_C = c->vmax;
@@ -555,6 +557,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     v[3] += u * u;
                     v[4] += u * sp;
                     v[5] += sp * sp;
+                    v[10] = fmax(v[10], fabs(u));   // (max |coef| of the X_A u pass: its fixed-point scale)
                     v[11] = fmax(v[11], fabs(vv));
                 }
             }
@@ -565,12 +568,31 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         const bool resident = !BIG && s_res;   // (block-uniform; s_res is visible after the partials' barriers)
         PH_MARK(0);
         if (BIG) grid.sync();   // the units of my stream may belong to other blocks' positions
+        if (BIG) {   // X_A s in fixed point: |(X_A coef)_i| <= maxrow * max|X| * max|coef| < 2^62 q (every block alike)
+            __shared__ double s_q[2];
+            if (wid == 0) {
+                double cm = 0.0;
+                for (int b = lane; b < G; b += 32) cm = fmax(cm, ld_cg(part + (size_t)(IR_SD + 10) * G + b));
+                cm = warp_max(cm);
+                if (lane == 0) {
+                    const double bound = (double)c->maxrow * c->xmax * cm;
+                    int ex = 0;
+                    frexp(bound, &ex);
+                    const bool ok = bound > 0.0 && isfinite(bound);
+                    s_q[0] = ok ? ldexp(1.0, 62 - ex) : 1.0;
+                    s_q[1] = ok ? ldexp(1.0, ex - 62) : 1.0;
+                }
+            }
+            __syncthreads();
+            fq = s_q[0];
+            fqi = s_q[1];
+        }
 #ifdef IR_BLKDBG
         __syncthreads();
         bd_t0 = gtimer();
 #endif
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
-        if constexpr (BIG) {   // per-warp rings, fp64 reductions into Xu / Xzu (kept zero between uses)
+        if constexpr (BIG) {   // per-warp rings, fixed-point reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
             if (lane == 0) {
                 for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
@@ -609,21 +631,21 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         for (int u = 0; u < 4; ++u) { r[u] = ci[k + 32 * u]; xv[u] = (double)cv[k + 32 * u] * cf; }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            red_add_global(P.Xu + r[u], xv[u]);
-                            if (zf) red_add_global(P.Xzu + r[u], xv[u]);
+                            red_add_fixed(P.Xu + r[u], xv[u], fq);
+                            if (zf) red_add_fixed(P.Xzu + r[u], xv[u], fq);
                         }
                     }
                     for (; k < kend; k += 32) {
                         const int r = ci[k];
                         const double xv = (double)cv[k] * cf;
-                        red_add_global(P.Xu + r, xv);
-                        if (zf) red_add_global(P.Xzu + r, xv);
+                        red_add_fixed(P.Xu + r, xv, fq);
+                        if (zf) red_add_fixed(P.Xzu + r, xv, fq);
                     }
                     for (; k < dsc.ve; k += 32) {
                         const int r = seg_idx(S, k, dsc.cb);
                         const double xv = (double)__ldg(S.val + k) * cf;
-                        red_add_global(P.Xu + r, xv);
-                        if (zf) red_add_global(P.Xzu + r, xv);
+                        red_add_fixed(P.Xu + r, xv, fq);
+                        if (zf) red_add_fixed(P.Xzu + r, xv, fq);
                     }
                 }
                 __syncwarp();
@@ -783,8 +805,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     for (int u = 0; u < 4; ++u) {
                         const int k = k0 + u * blockDim.x;
                         const bool in = k < nr;
-                        xu[u] = in ? ld_cg(P.Xu + r0 + k) : 0.0;
-                        xzu[u] = (in && dual) ? ld_cg(P.Xzu + r0 + k) : 0.0;
+                        xu[u] = in ? ld_fixed(P.Xu + r0 + k, fqi) : 0.0;
+                        xzu[u] = (in && dual) ? ld_fixed(P.Xzu + r0 + k, fqi) : 0.0;
                         xo[u] = (in && !pcd) ? xs_r[k] : 0.0;
                         dd[u] = in ? P.rD[r0 + k].y : 0.0;
                     }

@@ -43,6 +43,8 @@ struct Ctl {
     unsigned long long tph[16];  // persistent inner solver: ns spent per phase (block 0), diagnostics
     unsigned s_ctr, g_ctr;       // large-m inner solver: unit claim counters of the S and G streams
     unsigned hclaim, pad4;       // k_heavy: unit claim counter (zeroed before each launch)
+    double xmax;                 // max |X_ij| (large m: the fixed-point scale of X_A s)
+    int maxrow, pad5;            // longest row of X
 };
 
 // heavy-segment schedule for one segment list

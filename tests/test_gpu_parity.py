@@ -808,3 +808,22 @@ def test_dense_full_cfg2_solve():
     assert ra["F"] == rb["F"] and ra["cycles"] == rb["cycles"]
     r_o = oracle.Oracle(ds).solve()
     assert abs(rb["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
+
+
+@pytest.mark.parametrize("name,flags", [("cfg4s", 0), ("cfg4s", 8), ("lasso4s", 0), ("cfg4s_cg", 8)])
+def test_large_m_solve_bitwise_reproducible(name, flags):
+    """The large-m path is bitwise reproducible: X_A s is reduced in 64-bit fixed point (integer
+    addition does not depend on the order of the reductions), every other sum has a fixed order, and dynamic unit
+    claims (flags 8) change only which warp sums a unit.  Two solves from w = 0 return identical w, F and traces."""
+    ds = dataset("cfg4s" if name == "cfg4s_cg" else name)
+    opts = {"inner_cg": 1, "pcd_snap": 0} if name == "cfg4s_cg" else {}
+    out = []
+    for rep in range(2):
+        ctx = ml.Context(ds)
+        ctx.ml_set_engine(flags)
+        r = ctx.ml_solve(ml.default_opts(**opts))
+        out.append((r["F"], r["cycles"], ctx.ml_get_w().cpu().numpy(), [(t["nA"], t["inner_iters"], t["F_after"])
+                                                                       for t in ctx.trace()]))
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])
+    assert out[0][3] == out[1][3]
