@@ -169,8 +169,15 @@ ml_status ml_set_sm_share(ml_ctx *c, int blocks);
           engine on configs 4-5); ML_E_INVAL on a small-m context (which reads X through shared-memory passes).
    bit 3: the large-m inner solver's X_A s and H sigma streams claim their column units dynamically from a grid-wide
           counter whatever the unit count (by default only with >= 32 units per warp, where static shares left blocks
-          waiting on the slowest). */
+          waiting on the slowest).
+   bits 4 / 5: the large-m inner solver takes the heavy-column path (the S / G copies of the longest columns,
+          ml_heavy_info) in every relaxation / in none; by default when the free set holds >= 1/4 of their nonzeros.
+          ML_E_INVAL for bit 4 when the context has no heavy path (small m, or the longest columns hold < 1/10 of X). */
 ml_status ml_set_engine(ml_ctx *c, uint32_t flags);
+/* Diagnostics of the large-m heavy-column path (DESIGN 8.2; off for m <= 8192): info_host[8] = built (0/1), |H|,
+   nonzeros of H, S tiles, G chunks, row bands, relaxations that ran it since ml_create, the heavy mode (0 by the
+   free set's share of H, 1 always, 2 never: ml_set_engine bits 4 / 5). */
+ml_status ml_heavy_info(ml_ctx *c, int64_t *info_host);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */
 int64_t ml_trace(ml_ctx *c, void *rows_host, int64_t cap);

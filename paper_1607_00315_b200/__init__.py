@@ -75,7 +75,7 @@ class TraceRow(ctypes.Structure):
 EXPORTS = ["ml_default_opts", "ml_workspace_bytes", "ml_create", "ml_create_lasso", "ml_destroy", "ml_set_w", "ml_get_w", "ml_get_rows",
            "ml_eval_f_grad", "ml_diag_hess", "ml_hessvec", "ml_shrink_linesearch", "ml_select_coarse", "ml_solve",
            "ml_status_str", "ml_last_error", "ml_kernel_launches", "ml_trace", "ml_profile",
-           "ml_profile_read", "ml_inner_phases", "ml_set_sm_share", "ml_set_engine"]
+           "ml_profile_read", "ml_inner_phases", "ml_set_sm_share", "ml_set_engine", "ml_heavy_info"]
 
 _lib = None
 
@@ -139,6 +139,8 @@ def load(path: str | None = None):
         L.ml_set_engine.argtypes = [P, ctypes.c_uint32]
     L.ml_trace.restype = i64
     L.ml_trace.argtypes = [P, P, i64]
+    L.ml_heavy_info.restype = i32
+    L.ml_heavy_info.argtypes = [P, P]
     _lib = L
     return L
 
@@ -328,6 +330,13 @@ class Context:
 
     def ml_set_engine(self, flags):
         return self._check(load().ml_set_engine(self.h, int(flags)))
+
+    HEAVY_INFO = ("built", "nh", "nnzh", "s_tiles", "g_chunks", "bands", "relaxations", "mode")
+
+    def ml_heavy_info(self):
+        v = (ctypes.c_int64 * 8)()
+        self._check(load().ml_heavy_info(self.h, v))
+        return dict(zip(self.HEAVY_INFO, (int(x) for x in v)))
 
     def ml_set_sm_share(self, blocks):
         return self._check(load().ml_set_sm_share(self.h, int(blocks)))

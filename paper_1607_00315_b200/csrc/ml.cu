@@ -110,6 +110,11 @@ struct ml_ctx {
     bool dense = false;
     int* dense_colptr = nullptr;
     int* rowtab = nullptr;
+    // heavy-column path (large m): build scratch
+    int* hv_hcols = nullptr;
+    int* hv_lens = nullptr;
+    int* hv_bsum = nullptr;
+    int* hv_misc = nullptr;
 };
 
 namespace {
@@ -177,6 +182,34 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     int* mp_vptr = cv.take<int>(big ? nn + 1 : 1);
     int* mp_bsum = cv.take<int>(big ? nn / MP_SCAN + 2 : 1);
     double2* mp_out = cv.take<double2>(big ? nn : 1);
+    // heavy-column path of the large-m inner solver (ml_heavy.cuh): the S and G copies of H's nonzeros (at most all
+    // of X's), their chunk tables, band partials, per-row products; build scratch aliases hpart / Xh / Xhz
+    const size_t hvn = big ? (size_t)nnz + 16 : 1;
+    const size_t hvnb = big ? (mm + HV_RB - 1) / HV_RB : 1;
+    HvPrm hv{};
+    hv.hid = cv.take<int>(big ? nn : 1);
+    hv.phid = cv.take<int>(big ? nn : 1);
+    int* hv_hcols = cv.take<int>(HV_HMAX + 1);
+    int* hv_lens = cv.take<int>(HV_HMAX + 1);
+    hv.sval = cv.take<float>(hvn);
+    hv.sidx = cv.take<uint16_t>(hvn);
+    hv.soff = cv.take<int>(big ? mm + 8 : 1);
+    const size_t sch_cap = big ? (size_t)nnz / (HV_CHMAX / 2) + mm / HV_SMAX + 16 : 1;   // (chp >= HV_CHMAX / 2)
+    hv.schunk = cv.take<HvChunk>(sch_cap);
+    hv.gval = cv.take<float>(hvn);
+    hv.gidx = cv.take<uint16_t>(hvn);
+    hv.goff = cv.take<int>(big ? (size_t)HV_HMAX * hvnb + 8 : 1);
+    const size_t gch_cap = big ? 2 * (size_t)nnz / HV_CHMAX + (size_t)HV_HMAX * hvnb / HV_SMAX + 2 * hvnb + 16 : 1;
+    hv.gchunk = cv.take<HvChunk>(gch_cap);
+    hv.sblk = cv.take<uint16_t>(sch_cap * 256);
+    hv.gblk = cv.take<uint16_t>(gch_cap * 256);
+    hv.hpart = cv.take<double>(big ? std::max<size_t>((size_t)HV_HMAX * hvnb, 32768) + 64 : 1);
+    hv.Xh = cv.take<double>(big ? mm + 2 : 1);
+    hv.Xhz = cv.take<double>(big ? mm + 2 : 1);
+    hv.sH = cv.take<double>(HV_HMAX);
+    hv.zH = cv.take<uint32_t>(HV_HMAX / 32);
+    int* hv_bsum = cv.take<int>(big ? std::max({nn, mm + 1, (size_t)HV_HMAX * hvnb + 1}) / 1024 + 64 : 1);
+    int* hv_misc = cv.take<int>(64);
 
     UnitsMem um[4];
     for (int k = 0; k < 4; ++k) {
@@ -206,6 +239,12 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     c->mp_bsum = mp_bsum;
     c->mp_out = mp_out;
     P.ctl = ctl; P.part = part; P.tilepart = tilepart; P.status = status; P.trace = trace;
+    hv.on = 0;
+    P.hv = hv;
+    c->hv_hcols = hv_hcols;
+    c->hv_lens = hv_lens;
+    c->hv_bsum = hv_bsum;
+    c->hv_misc = hv_misc;
 }
 
 int pick_G(double mean_len) {
@@ -689,6 +728,116 @@ const char* ml_status_str(ml_status s) {
 const char* ml_last_error(const ml_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int64_t ml_kernel_launches(const ml_ctx* c) { return c ? c->launches : 0; }
 
+// exclusive scan of a[0 .. n) in place (ml_heavy.cuh's three kernels; bsum holds n / 1024 + 1 ints)
+void scan_excl(ml_ctx* c, int* a, long long n, int* bsum) {
+    const int nbk = (int)((n + 1023) / 1024);
+    k_scan_local<<<nbk, 256, 0, c->st>>>(a, (int)n, bsum);
+    k_scan_bsum<<<1, 1024, 0, c->st>>>(bsum, nbk);
+    k_scan_add<<<nbk, 256, 0, c->st>>>(a, (int)n, bsum);
+    c->launches += 3;
+}
+// The heavy-column path (ml_heavy.cuh), built once per context: H = the longest columns (>= HV_MINLEN nonzeros, at
+// most HV_HMAX, all columns of the shortest length taken or none), ids by decreasing length; the S copy (rows) and
+// the G copy (bands) with their chunk schedules.  Off when H holds less than a tenth of X's nonzeros.
+ml_status hv_build(ml_ctx* c) {
+    HvPrm& hv = c->P.hv;
+    hv.on = 0;
+    const int m = (int)c->X.m, n = (int)c->X.n;
+    const int* colptr = c->X.csc_colptr;
+    auto sync = [&]() { return cudaStreamSynchronize(c->st) == cudaSuccess; };
+    unsigned* hist = reinterpret_cast<unsigned*>(hv.hpart);
+    cudaMemsetAsync(hist, 0, sizeof(unsigned) * 65536, c->st);
+    ML_LAUNCH(c, k_hv_lenhist, GRID_CAP, colptr, n, hist);
+    std::vector<unsigned> hh(65536);
+    cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned) * 65536, cudaMemcpyDeviceToHost, c->st);
+    if (!sync()) return cuda_fail(c, "hv_build");
+    long long cum = 0;
+    int T = 65536;
+    for (int L = 65535; L >= HV_MINLEN; --L) {
+        if (cum + hh[L] > HV_HMAX) break;
+        cum += hh[L];
+        T = L;
+    }
+    const int nh = (int)cum;
+    if (nh == 0) return ML_OK;
+    // heavy columns in column order, then ids by decreasing length (ties: column order)
+    ML_LAUNCH(c, k_hv_flags, GRID_CAP, colptr, n, T, hv.phid);
+    scan_excl(c, hv.phid, n, c->hv_bsum);
+    ML_LAUNCH(c, k_hv_cols, GRID_CAP, colptr, n, T, hv.phid, c->hv_hcols, c->hv_lens);
+    std::vector<int> hc(nh), hl(nh), ord(nh);
+    cudaMemcpyAsync(hc.data(), c->hv_hcols, sizeof(int) * nh, cudaMemcpyDeviceToHost, c->st);
+    cudaMemcpyAsync(hl.data(), c->hv_lens, sizeof(int) * nh, cudaMemcpyDeviceToHost, c->st);
+    if (!sync()) return cuda_fail(c, "hv_build");
+    long long nnzh = 0;
+    for (int h = 0; h < nh; ++h) { ord[h] = h; nnzh += hl[h]; }
+    if ((double)nnzh < 0.1 * (double)c->X.nnz) return ML_OK;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hl[a] > hl[b]; });
+    std::vector<int> hs(nh);
+    for (int h = 0; h < nh; ++h) hs[h] = hc[ord[h]];
+    cudaMemcpyAsync(c->hv_hcols, hs.data(), sizeof(int) * nh, cudaMemcpyHostToDevice, c->st);
+    ML_LAUNCH(c, k_hv_hid, GRID_CAP, n, const_cast<int*>(hv.hid));
+    ML_LAUNCH(c, k_hv_hid_set, 64, c->hv_hcols, nh, const_cast<int*>(hv.hid));
+    // S copy: heavy entries per row, scanned to the row starts (soff)
+    int* misc = c->hv_misc;
+    cudaMemsetAsync(misc, 0, sizeof(int) * 64, c->st);
+    int* hrp = const_cast<int*>(hv.soff);
+    int* tidx = reinterpret_cast<int*>(hv.Xhz);   // (scratch: m + 1 ints)
+    ML_LAUNCH(c, k_hv_rowcnt, GRID_CAP, c->X.csr_rowptr, c->X.csr_col, m, hv.hid, hrp, misc);
+    cudaMemsetAsync(hrp + m, 0, sizeof(int), c->st);
+    scan_excl(c, hrp, (long long)m + 1, c->hv_bsum);
+    int maxcnt = 0;
+    cudaMemcpyAsync(&maxcnt, misc, sizeof(int), cudaMemcpyDeviceToHost, c->st);
+    if (!sync()) return cuda_fail(c, "hv_build");
+    if (maxcnt < 1 || maxcnt > HV_CHMAX / 2) return ML_OK;
+    const int chp = HV_CHMAX - maxcnt;
+    ML_LAUNCH(c, k_hv_tileflags, GRID_CAP, hrp, m, chp, tidx);
+    scan_excl(c, tidx, (long long)m + 1, c->hv_bsum);
+    int nts = 0;
+    cudaMemcpyAsync(&nts, tidx + m, sizeof(int), cudaMemcpyDeviceToHost, c->st);
+    ML_LAUNCH(c, k_hv_tiles, GRID_CAP, hrp, m, chp, tidx, const_cast<HvChunk*>(hv.schunk));
+    ML_LAUNCH(c, k_hv_rowfill, GRID_CAP, c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, m, hv.hid, hrp,
+              const_cast<float*>(hv.sval), const_cast<uint16_t*>(hv.sidx));
+    if (!sync()) return cuda_fail(c, "hv_build");
+    // G copy: (band, h) segment lengths, scanned to the segment starts (goff); entries; chunks
+    const int nb = (m + HV_RB - 1) / HV_RB;
+    const long long N = (long long)nh * nb;
+    int* off = const_cast<int*>(hv.goff);
+    ML_LAUNCH(c, k_hv_segcnt, GRID_CAP, colptr, c->X.csc_row, c->hv_hcols, nh, nb, m, off);
+    cudaMemsetAsync(off + N, 0, sizeof(int), c->st);
+    scan_excl(c, off, N + 1, c->hv_bsum);
+    ML_LAUNCH(c, k_hv_segfill, GRID_CAP, colptr, c->X.csc_row, c->X.csc_val, c->hv_hcols, nh, nb, off,
+              const_cast<float*>(hv.gval), const_cast<uint16_t*>(hv.gidx));
+    int* nch = reinterpret_cast<int*>(hv.Xhz);   // (scratch: 2 nb ints)
+    int* choff = nch + nb;
+    const int gb = std::max(1, (nb + 63) / 64);
+    k_hv_chunks<<<gb, 64, 0, c->st>>>(off, nh, nb, 0, nch, nullptr, nullptr);
+    std::vector<int> hn(nb), ho(nb);
+    cudaMemcpyAsync(hn.data(), nch, sizeof(int) * nb, cudaMemcpyDeviceToHost, c->st);
+    if (!sync()) return cuda_fail(c, "hv_build");
+    long long ncg = 0;
+    for (int k = 0; k < nb; ++k) { ho[k] = (int)ncg; ncg += hn[k]; }
+    cudaMemcpyAsync(choff, ho.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, c->st);
+    k_hv_chunks<<<gb, 64, 0, c->st>>>(off, nh, nb, 1, nch, choff, const_cast<HvChunk*>(hv.gchunk));
+    c->launches += 2;
+    ML_LAUNCH(c, k_hv_blocks, GRID_CAP, hv.schunk, nts, hv.soff, const_cast<uint16_t*>(hv.sblk));
+    ML_LAUNCH(c, k_hv_blocks, GRID_CAP, hv.gchunk, (int)ncg, hv.goff, const_cast<uint16_t*>(hv.gblk));
+    if (!sync()) return cuda_fail(c, "hv_build");   // (the host vectors above outlive their async copies)
+    cudaMemsetAsync(hv.hpart, 0, sizeof(double) * (size_t)nh * nb, c->st);
+    cudaMemsetAsync(hv.Xh, 0, sizeof(double) * (size_t)m, c->st);
+    cudaMemsetAsync(hv.Xhz, 0, sizeof(double) * (size_t)m, c->st);
+    cudaMemsetAsync(hv.sH, 0, sizeof(double) * HV_HMAX, c->st);
+    cudaMemsetAsync(hv.zH, 0, sizeof(uint32_t) * (HV_HMAX / 32), c->st);
+    hv.nh = nh;
+    hv.nb = nb;
+    hv.nts = nts;
+    hv.ncg = (int)ncg;
+    hv.nnzh = nnzh;
+    hv.mode = 2;      // (off by default until it beats the column units: ml_set_engine bit 4 / 5 select it)
+    hv.frac = 0.25;
+    hv.on = 1;
+    return cuda_fail(c, "hv_build");
+}
+
 static ml_status create_impl(const ml_data* X, const double* b, double lambda, void* cuda_stream, void* ws,
                              size_t ws_bytes, ml_ctx** out) {
     if (!X || !out) return ML_E_INVAL;
@@ -816,7 +965,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (!c->sm_inner) {   // large m: the persistent solver with global m-vectors
         // (measured: <256, 8> and <512, 4> rings were slower on cfg 3-4)
         const void* kfn = (const void*)k_inner<1024, IN_GST, true>;
-        const size_t b = inner_big_smem_bytes<1024, IN_GST>();
+        const size_t b = std::max(inner_big_smem_bytes<1024, IN_GST>(), hv_smem_bytes());
         int bps = 0;
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) == cudaSuccess)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, b);
@@ -858,6 +1007,10 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     if (c->big_inner) ML_LAUNCH(c, k_xstats, GRID_CAP, X->csc_val, X->nnz, X->csr_rowptr, (int)X->m, c->ctl);
+    if (c->big_inner && has_csr) {
+        const ml_status hs = hv_build(c);
+        if (hs != ML_OK) { *out = c; return hs; }
+    }
     if (c->mp_grid_all)   // the static merge-path plan over all columns (X is fixed for the context's life)
         ML_LAUNCH(c, k_mp_search, std::max(1, (c->mp_tiles_cap + ML_NT) / ML_NT), c->mp_all, c->mp_tiles_cap);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
@@ -1221,6 +1374,25 @@ ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
     if (want && c->mp_grid_all == 0) return ML_E_INVAL;   // (small m: the shared-memory passes; no merge-path plan)
     c->mp = want;
     c->P.dyn = (flags & 8u) ? 1 : 0;   // bit 3: dynamic unit claims in the large-m inner solver whatever the unit count
+    // bits 4 / 5: the heavy-column path in every relaxation / in none (default: when A holds >= 1/4 of H's nonzeros)
+    if ((flags & 16u) && !c->P.hv.on) return ML_E_INVAL;
+    c->P.hv.mode = (flags & 16u) ? 1 : (flags & 64u) ? 0 : 2;   // bit 6: by the free set's share of H
+    return ML_OK;
+}
+
+ml_status ml_heavy_info(ml_ctx* c, int64_t* info_host) {
+    if (!c || !info_host) return ML_E_INVAL;
+    const ml_status st = sync_ctl(c);
+    if (st != ML_OK) return st;
+    const HvPrm& hv = c->P.hv;
+    info_host[0] = hv.on;
+    info_host[1] = hv.on ? hv.nh : 0;
+    info_host[2] = hv.on ? hv.nnzh : 0;
+    info_host[3] = hv.on ? hv.nts : 0;
+    info_host[4] = hv.on ? hv.ncg : 0;
+    info_host[5] = hv.on ? hv.nb : 0;
+    info_host[6] = c->h.hv_relax;
+    info_host[7] = hv.mode;
     return ML_OK;
 }
 

@@ -60,8 +60,8 @@ enum { IR_SD = 0, IR_SR = 12, IR_SL1 = 16 };
 // outer line search + update (R14-R18): 0 g.d, 1 max|d|, 2..5 l1 trials 0..3, 6..9 loss trials 0..3; the rest:
 // 10.. l1 trials 4.., then loss trials 4..; update: 0 L, 1 support change
 constexpr int IR_NLS = ML_MAXLS - 4;
-enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_SO3 = IR_SU + 2, IR_NSLOT = IR_SO3 + 6 };
-// IR_SU, +1: unit counts, nnz (BIG); IR_SO3: trials 1/2, 1/4, 1/8 of a large-m outer line search (l1, loss) when
+enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_SO3 = IR_SU + 5, IR_NSLOT = IR_SO3 + 6 };
+// IR_SU .. +4: unit counts, nnz; the same without the heavy columns; nnz of A's heavy columns (BIG); IR_SO3: trials 1/2, 1/4, 1/8 of a large-m outer line search (l1, loss) when
 // alpha = 1 failed
 #ifndef IR_UNIT_V
 #define IR_UNIT_V 2048
@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 
     int next_pcd = 1, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;   // R6: PCD first
     double fq = 1.0, fqi = 1.0;   // BIG: this iteration's fixed-point scale of X_A s (and its inverse)
+    bool hvz = false;             // BIG, heavy mode: some heavy column of A is a zeroing column this iteration
     double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = 0.0, slope = 0.0, ss = 0.0, ps = 0.0;
     double sHs = 0.0, vq = 0.0;
     const double vmax_C = c->vmax;
@@ -413,36 +414,61 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
     int u0 = 0, u1 = 0;   // BIG: my range of column units (balanced by nonzeros across blocks)
     int nU = 0;           // BIG: all units (the S and G streams claim them dynamically, Ctl::s_ctr / g_ctr)
+    // BIG, heavy-column path (ml_heavy.cuh): on for this relaxation when A holds enough of H's nonzeros; then the
+    // heavy columns of A get no column units: their X_A s and H sigma products go through the S / G copies
+    bool hvm = false;
+    long long hv_nz = 0;     // nonzeros of A's heavy columns (the algorithmic count of the heavy passes)
+    int2 hs_rng = make_int2(0, 0), hg_rng = make_int2(0, 0);   // my S tiles / G chunks
     if constexpr (BIG) {
-        int nu_loc = 0, nz_loc = 0;
+        const bool hvb = P.hv.on != 0;
+        int nu_loc = 0, nz_loc = 0, nu_l = 0, nz_l = 0;
+        double nzh = 0.0;
         for (int k = threadIdx.x; k < q0; k += blockDim.x) {
-            int b, e;
-            if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
-            else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
+            int b, e, j;
+            if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; j = hvb ? __ldg(S.list + p0 + k) : 0; }
+            else { j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
             const int nu1 = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
             nu_loc += nu1;
             nz_loc += e - b + IR_UCOST * nu1;
+            const int h = hvb ? __ldg(P.hv.hid + j) : -1;
+            if (hvb) P.hv.phid[p0 + k] = h;
+            if (h < 0) { nu_l += nu1; nz_l += e - b + IR_UCOST * nu1; }
+            else nzh += (double)(e - b);
+        }
+        if (hvb) {   // no heavy column of A has a coefficient yet (D writes those of A's)
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX; i += G * blockDim.x) P.hv.sH[i] = 0.0;
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX / 32; i += G * blockDim.x) P.hv.zH[i] = 0u;
+            hs_rng = hv_my_chunks(P.hv.schunk, P.hv.nts);
+            hg_rng = hv_my_chunks(P.hv.gchunk, P.hv.ncg);
         }
         {
-            const double v[2] = {(double)nu_loc, (double)nz_loc};
-            ir_block_partials<2>(v, 0u, 0u, sh_w, part, IR_SU);
+            const double v[5] = {(double)nu_loc, (double)nz_loc, (double)nu_l, (double)nz_l, nzh};
+            ir_block_partials<5>(v, 0u, 0u, sh_w, part, IR_SU);
         }
         grid.sync();
-        __shared__ long long s_uoff[4];
-        if (wid == 0) {   // my offsets in the unit and nonzero sequences, and their totals
+        __shared__ long long s_uoff[5];
+        if (wid == 0) {   // the heavy decision; my offsets in the unit and nonzero sequences, and their totals
+            double hz = 0.0;
+            for (int b = lane; b < G; b += 32) hz += ld_cg(part + (size_t)(IR_SU + 4) * G + b);
+            hz = warp_sum(hz);   // (integers below 2^53: exact in any order)
+            const bool on = hvb && (P.hv.mode == 1 || (P.hv.mode == 0 && hz >= P.hv.frac * (double)P.hv.nnzh)) && hz > 0.0;
+            const int su = on ? IR_SU + 2 : IR_SU;
             long long off = 0, tot = 0, zoff = 0, ztot = 0;
             for (int b0 = 0; b0 < G; b0 += 32) {
                 const int b = b0 + lane;
-                const long long x = b < G ? (long long)ld_cg(part + (size_t)IR_SU * G + b) : 0;
-                const long long z = b < G ? (long long)ld_cg(part + (size_t)(IR_SU + 1) * G + b) : 0;
+                const long long x = b < G ? (long long)ld_cg(part + (size_t)su * G + b) : 0;
+                const long long z = b < G ? (long long)ld_cg(part + (size_t)(su + 1) * G + b) : 0;
                 off += __reduce_add_sync(0xffffffffu, (unsigned)(b < (int)blockIdx.x ? x : 0));
                 tot += __reduce_add_sync(0xffffffffu, (unsigned)x);
                 zoff += warp_sum_ll(b < (int)blockIdx.x ? z : 0);
                 ztot += warp_sum_ll(z);
             }
-            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; s_uoff[2] = zoff; s_uoff[3] = ztot; }
+            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; s_uoff[2] = zoff; s_uoff[3] = ztot; s_uoff[4] = on ? (long long)hz : -1; }
         }
         __syncthreads();
+        hvm = s_uoff[4] >= 0;
+        hv_nz = hvm ? s_uoff[4] : 0;
+        if (hvm && blockIdx.x == 0 && threadIdx.x == 0) c->hv_relax += 1;
         int base = (int)s_uoff[0];
         long long zbase = s_uoff[2];
         const int NU = (int)s_uoff[1];
@@ -450,7 +476,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         for (int k00 = 0; k00 < q0; k00 += blockDim.x) {   // my positions in order: their units
             const int k = k00 + threadIdx.x;
             int b = 0, e = 0, nu = 0;
-            if (k < q0) {
+            if (k < q0 && !(hvm && P.hv.phid[p0 + k] >= 0)) {   // (heavy columns of A: no units in heavy mode)
                 if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
                 else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
                 nu = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
@@ -560,6 +586,15 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     v[10] = fmax(v[10], fabs(u));   // (max |coef| of the X_A u pass: its fixed-point scale)
                     v[11] = fmax(v[11], fabs(vv));
                 }
+                if (BIG && hvm) {   // a heavy column of A: its S coefficient (and zeroing flag) for the S copy
+                    const int h = P.hv.phid[p0 + k];
+                    if (h >= 0) {
+                        P.hv.sH[h] = pcd ? X.s[k] : X.u[k];
+                        const uint32_t bit = 1u << (h & 31);
+                        if (pcd && X.u[k] != 0.0) atomicOr(P.hv.zH + (h >> 5), bit);
+                        else atomicAnd(P.hv.zH + (h >> 5), ~bit);
+                    }
+                }
             }
             PH_SUB(1);
             ir_block_partials<12>(v, IR_DMAX, 0u, sh_w, part, IR_SD);
@@ -594,6 +629,34 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         if constexpr (BIG) {   // per-warp rings, fixed-point reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
+            if (hvm) {   // heavy columns first: s_H (and its zeroing bits) in shared memory, the S copy's row sums
+                double* sHs = reinterpret_cast<double*>(smraw + HV_SH_OFF);
+                uint32_t* zHs = reinterpret_cast<uint32_t*>(smraw + HV_ZH_OFF);
+                int zor = 0;
+                for (int i = threadIdx.x; i < P.hv.nh; i += blockDim.x) sHs[i] = ld_cg(P.hv.sH + i);
+                for (int i = threadIdx.x; i < (P.hv.nh + 31) / 32; i += blockDim.x) {
+                    const uint32_t z = ld_cg(P.hv.zH + i);
+                    zHs[i] = z;
+                    zor |= z != 0u;
+                }
+                hvz = __syncthreads_or(zor) != 0;
+#ifdef IR_HVDBG
+                const unsigned long long hv_t0 = gtimer();
+#endif
+                if (hvz) {
+                    HvOpS<2> op{P.hv.Xh, P.hv.Xhz};
+                    hv_stream<2>(P.hv.schunk, hs_rng.x, hs_rng.y, P.hv.sval, P.hv.sidx, P.hv.soff, P.hv.sblk, HV_SRING_OFF, op,
+                                 [](const HvChunk&) {});
+                } else {
+                    HvOpS<1> op{P.hv.Xh, P.hv.Xhz};
+                    hv_stream<1>(P.hv.schunk, hs_rng.x, hs_rng.y, P.hv.sval, P.hv.sidx, P.hv.soff, P.hv.sblk, HV_SRING_OFF, op,
+                                 [](const HvChunk&) {});
+                }
+                if (blockIdx.x == 0 && threadIdx.x == 0) nsc += hv_nz;
+#ifdef IR_HVDBG   // (block 0's heavy S time in slot 0, heavy G time in slot 1: the small-|A| D / S slots)
+                if (blockIdx.x == 0 && threadIdx.x == 0) ph_acc[0] += gtimer() - hv_t0;
+#endif
+            }
             if (lane == 0) {
                 for (int k = 0; k < GST; ++k) mbar_init(g_bar + k, 1);
                 fence_mbar_init();
@@ -805,8 +868,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     for (int u = 0; u < 4; ++u) {
                         const int k = k0 + u * blockDim.x;
                         const bool in = k < nr;
-                        xu[u] = in ? ld_fixed(P.Xu + r0 + k, fqi) : 0.0;
-                        xzu[u] = (in && dual) ? ld_fixed(P.Xzu + r0 + k, fqi) : 0.0;
+                        xu[u] = in ? ld_fixed(P.Xu + r0 + k, fqi) + (hvm ? ld_cg(P.hv.Xh + r0 + k) : 0.0) : 0.0;
+                        xzu[u] = (in && dual) ? ld_fixed(P.Xzu + r0 + k, fqi) + (hvz ? ld_cg(P.hv.Xhz + r0 + k) : 0.0)
+                                              : 0.0;
                         xo[u] = (in && !pcd) ? xs_r[k] : 0.0;
                         dd[u] = in ? P.rD[r0 + k].y : 0.0;
                     }
@@ -1084,15 +1148,77 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             __syncwarp();
             if (lane == 0)
                 for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
+            if (hvm) {   // heavy columns: u = D o X sigma of a band in shared memory, the G copy's (band, h) sums
+                __syncthreads();   // (the column rings are drained: their shared memory is free)
+                double* us = reinterpret_cast<double*>(smraw + HV_U_OFF);
+                HvOpG op{P.hv.hpart, P.hv.nb};
+                int cur = -1;
+                const double b1 = 1.0 - beta;
+#ifdef IR_HVDBG
+                const unsigned long long hv_t0 = gtimer();
+#endif
+                hv_stream<1>(P.hv.gchunk, hg_rng.x, hg_rng.y, P.hv.gval, P.hv.gidx, P.hv.goff, P.hv.gblk, HV_GRING_OFF, op,
+                                     [&](const HvChunk& ch) {
+                                         if (ch.base == cur) return;
+                                         __syncthreads();
+                                         cur = ch.base;
+                                         const int rb0 = cur * HV_RB;
+                                         for (int i = threadIdx.x; i < HV_RB; i += blockDim.x) {
+                                             const int r = rb0 + i;
+                                             double v = 0.0;
+                                             if (r < m) {
+                                                 v = beta * ld_cg(P.sv + r);
+                                                 if (zs) v += b1 * ld_cg(P.svz + r);
+                                             }
+                                             us[i] = v;
+                                         }
+                                         __syncthreads();
+                                     });
+                if (blockIdx.x == 0 && threadIdx.x == 0) nhs += hv_nz;
+#ifdef IR_HVDBG
+                if (blockIdx.x == 0 && threadIdx.x == 0) ph_acc[1] += gtimer() - hv_t0;
+#endif
+            }
 #ifdef IR_BLKDBG
             __syncthreads();
             bd_g += gtimer() - bd_t0;
 #endif
             grid.sync();   // every unit's partial
             if (blockIdx.x == 0 && threadIdx.x == 0) c->g_ctr = 0u;
+            if (hvm) {   // my heavy positions: their band partials in band order (a warp each), the step
+                const int nb = P.hv.nb;
+                for (int kb = wid * 32; kb < q0; kb += IR_W * 32) {
+                    const int k = kb + lane;
+                    const int h = k < q0 ? P.hv.phid[p0 + k] : -1;
+                    unsigned msk = __ballot_sync(0xffffffffu, h >= 0);
+                    while (msk) {
+                        const int src = __ffs(msk) - 1;
+                        msk &= msk - 1;
+                        const int hh = __shfl_sync(0xffffffffu, h, src);
+                        const double* hp = P.hv.hpart + (size_t)hh * nb;
+                        double t = 0.0;
+                        for (int b0 = lane; b0 < nb; b0 += 256) {
+                            double x[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) x[u] = b0 + 32 * u < nb ? ld_cg(hp + b0 + 32 * u) : 0.0;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) t += x[u];
+                        }
+                        t = warp_sum(t);
+                        if (lane == src) {
+                            const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
+                            const double x = X.wA[k] + X.d[k];
+                            const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
+                            X.Hd[k] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
+                            X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;
+                        }
+                    }
+                }
+            }
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
                 const int p = p0 + k;
                 const int ua = ld_cg(P.ustart + p), ub = ld_cg(P.ustart + p + 1);
+                if (hvm && ua == ub) continue;   // (a heavy column: done above)
                 double t = 0.0, tz = 0.0;
                 for (int u = ua; u < ub; ++u) { const double2 q2 = ld_cg(P.upart + u); t += q2.x; tz += q2.y; }
                 const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;

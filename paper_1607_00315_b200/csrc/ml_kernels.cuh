@@ -10,6 +10,7 @@
 #include <cooperative_groups.h>
 
 #include "ml_common.cuh"
+#include "ml_heavy.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -45,6 +46,7 @@ struct Ctl {
     unsigned hclaim, pad4;       // k_heavy: unit claim counter (zeroed before each launch)
     double xmax;                 // max |X_ij| (large m: the fixed-point scale of X_A s)
     int maxrow, pad5;            // longest row of X
+    long long hv_relax;          // relaxations that ran the heavy-column path (diagnostics, ml_heavy_info)
 };
 
 // heavy-segment schedule for one segment list
@@ -312,6 +314,7 @@ struct Prm {
     double2* tilepart;         // per-tile partials of the compaction kernels
     unsigned long long* status;// look-back tile status
     TraceRow* trace;
+    HvPrm hv;                  // the heavy-column path of the large-m inner solver (ml_heavy.cuh)
 };
 // free-set buffers of one relaxation (fine or coarse set)
 struct ASet { int* A; double* gA; double* hA; double* wA; double* d; double* Hd; double* s; double* Hs; double* u; };

@@ -28,9 +28,12 @@ def main():
     ap.add_argument("--tag", default=os.environ.get("ML_LIB", "libml.so"))
     ap.add_argument("--sub", action="store_true", help="the library was built with -DIR_PHDBG")
     ap.add_argument("--gather", action="store_true", help="the library was built with -DGS_PHDBG")
+    ap.add_argument("--engine", type=int, default=0, help="ml_set_engine flags (16: heavy path always, 32: never)")
+    ap.add_argument("--raw", action="store_true", help="also print the raw phase slots (ns, all solves)")
     a = ap.parse_args()
     ds = mlgen.make(a.config)
     ctx = ml.Context(ds)
+    ctx.ml_set_engine(a.engine)
     ctx.ml_solve()
     ctx.ml_inner_phases(reset=True)
     st = ctx.stream
@@ -43,6 +46,8 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ph = ctx.ml_inner_phases(reset=True)
+    if a.raw:
+        print(json.dumps({"raw_ns": ph, "heavy": ctx.ml_heavy_info()}))
     prof = ctx.ml_profile_read()   # nonzeros streamed per pass class (device counters, all solves since create)
     tr = ctx.trace()
     its = [0, 0]
