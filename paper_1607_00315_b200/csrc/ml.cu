@@ -77,6 +77,8 @@ struct ml_ctx {
     bool big_inner = false;  // k_inner<., true>: the same with the m-vectors in global memory (m > SMALL_M)
     int inner_W = 0, inner_P = 0;
     const void* inner_fn = nullptr;   // the k_inner instantiation in use
+    const void* inner_fn_hv = nullptr;   // large m: the instantiation with the heavy-column path
+    size_t inner_bytes_hv = 0;
     int sms = 148;                    // the device's SM count, capped at SM_MAX (cooperative grids: one CTA per SM)
     int coop_cap = 148;               // cooperative grids use at most this many CTAs (ml_set_sm_share)
     int scat_bps = 0, gath_bps = 0;   // blocks per SM of the cooperative API scatter / gather
@@ -635,7 +637,9 @@ void launch_relax_body(ml_ctx* c, ASet& AS, int K, int inner_cg) {
     long long* a1 = acc_of(c, CLS_SCATTER);
     long long* a2 = acc_of(c, CLS_HS);
     void* args[] = {(void*)&Pc, (void*)&A2, (void*)&S, (void*)&Kk, (void*)&icg, (void*)&a1, (void*)&a2};
-    cudaLaunchCooperativeKernel(c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args, c->inner_bytes, c->st);
+    const bool hv = c->inner_fn_hv && c->P.hv.on && c->P.hv.mode != 2;
+    cudaLaunchCooperativeKernel(hv ? c->inner_fn_hv : c->inner_fn, dim3(c->inner_P), dim3(32 * IR_W), args,
+                                hv ? c->inner_bytes_hv : c->inner_bytes, c->st);
     c->launches++;
 }
 
@@ -963,18 +967,24 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
         cudaGetLastError();
     }
     if (!c->sm_inner) {   // large m: the persistent solver with global m-vectors
-        // (measured: <256, 8> and <512, 4> rings were slower on cfg 3-4)
+        // (measured: <256, 8> and <512, 4> rings were slower on cfg 3-4); a second instantiation carries the
+        // heavy-column path (its shared memory would shrink L1 for the default one)
         const void* kfn = (const void*)k_inner<1024, IN_GST, true>;
-        const size_t b = std::max(inner_big_smem_bytes<1024, IN_GST>(), hv_smem_bytes());
-        int bps = 0;
+        const size_t b = inner_big_smem_bytes<1024, IN_GST>();
+        const void* kfh = (const void*)k_inner<1024, IN_GST, true, true>;
+        const size_t bh = std::max(inner_big_smem_bytes<1024, IN_GST>(), hv_smem_bytes());
+        int bps = 0, bph = 0;
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) == cudaSuccess)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, b);
+        if (cudaFuncSetAttribute(kfh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bh) == cudaSuccess)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bph, kfh, 32 * IR_W, bh);
         cudaGetLastError();
         if (bps >= 1) {
             c->big_inner = true;
             c->inner_fn = kfn;
             c->inner_bytes = b;
             c->inner_P = std::min(c->sms, IR_GMAX);
+            if (bph >= 1) { c->inner_fn_hv = kfh; c->inner_bytes_hv = bh; }
         }
     }
     if (!c->sm_inner && mp_setup_kernel<TermGH>(c) && mp_setup_kernel<TermV2>(c) && mp_setup_kernel<TermV1>(c)) {
@@ -1007,7 +1017,7 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     if (c->big_inner) ML_LAUNCH(c, k_xstats, GRID_CAP, X->csc_val, X->nnz, X->csr_rowptr, (int)X->m, c->ctl);
-    if (c->big_inner && has_csr) {
+    if (c->big_inner && c->inner_fn_hv && has_csr) {
         const ml_status hs = hv_build(c);
         if (hs != ML_OK) { *out = c; return hs; }
     }

@@ -291,6 +291,7 @@ __device__ __forceinline__ int2 hv_my_chunks(const HvChunk* chunks, int nch) {
 template <int NV> struct HvOpS {
     double* Xh; double* Xhz;
     __device__ __forceinline__ void prod(uint32_t h, float x, double (&p)[NV]) const {
+        h &= HV_HMAX - 1;   // (entries outside the chunk hold stale indices; their products are discarded)
         const double v = (double)x * reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF)[h];
         p[0] = v;
         if constexpr (NV == 2)
@@ -314,7 +315,7 @@ struct HvOpG {
     double* hpart;
     int nb;
     __device__ __forceinline__ void prod(uint32_t r, float x, double (&p)[1]) const {
-        p[0] = (double)x * reinterpret_cast<const double*>(hv_dyn + HV_U_OFF)[r];
+        p[0] = (double)x * reinterpret_cast<const double*>(hv_dyn + HV_U_OFF)[r & 4095u];   // (as above)
     }
     __device__ __forceinline__ void fma(uint32_t r, float x, double (&a)[1]) const {
         a[0] = ::fma((double)x, reinterpret_cast<const double*>(hv_dyn + HV_U_OFF)[r], a[0]);

@@ -321,7 +321,7 @@ __device__ __forceinline__ void ir_trace(const Prm& P, Ctl* c, int outcome, int 
 // addition: order-independent, so bitwise reproducible; scale from max |X| x max |coef| x the longest row) into Xu (Xzu) through
 // per-warp TMA column rings, R takes my rows of Xu directly (and clears them), G gathers D o Xs (D o Xz) from L2 and
 // applies beta at each column end.  The iteration structure, barriers, decisions and the tail are the same.
-template <int GSCH, int GST, bool BIG>
+template <int GSCH, int GST, bool BIG, bool HVP = false>   // HVP: with the heavy-column path (ml_heavy.cuh)
 __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, int inner_cg, long long* acc_sc,
                                                   long long* acc_hs) {
     unsigned long long ph_t = gtimer(), ph_acc[IR_PHN] = {};
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     long long hv_nz = 0;     // nonzeros of A's heavy columns (the algorithmic count of the heavy passes)
     int2 hs_rng = make_int2(0, 0), hg_rng = make_int2(0, 0);   // my S tiles / G chunks
     if constexpr (BIG) {
-        const bool hvb = P.hv.on != 0;
+        const bool hvb = HVP && P.hv.on != 0;
         int nu_loc = 0, nz_loc = 0, nu_l = 0, nz_l = 0;
         double nzh = 0.0;
         for (int k = threadIdx.x; k < q0; k += blockDim.x) {
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         if constexpr (BIG) {   // per-warp rings, fixed-point reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
-            if (hvm) {   // heavy columns first: s_H (and its zeroing bits) in shared memory, the S copy's row sums
+            if constexpr (HVP) if (hvm) {   // heavy columns first: s_H (and its zeroing bits) in shared memory, the S copy's row sums
                 double* sHs = reinterpret_cast<double*>(smraw + HV_SH_OFF);
                 uint32_t* zHs = reinterpret_cast<uint32_t*>(smraw + HV_ZH_OFF);
                 int zor = 0;
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             __syncwarp();
             if (lane == 0)
                 for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
-            if (hvm) {   // heavy columns: u = D o X sigma of a band in shared memory, the G copy's (band, h) sums
+            if constexpr (HVP) if (hvm) {   // heavy columns: u = D o X sigma of a band in shared memory, the G copy's (band, h) sums
                 __syncthreads();   // (the column rings are drained: their shared memory is free)
                 double* us = reinterpret_cast<double*>(smraw + HV_U_OFF);
                 HvOpG op{P.hv.hpart, P.hv.nb};

@@ -894,3 +894,18 @@ def test_heavy_path_not_built_small_m():
     assert ctx.ml_heavy_info()["built"] == 0
     with pytest.raises(Exception):
         ctx.ml_set_engine(16)
+
+
+@pytest.mark.parametrize("fill", [-1, 0x7FF8000000000000])
+def test_heavy_path_stale_workspace(fill):
+    """The heavy path must not depend on the workspace's previous contents either: with every word of the workspace
+    set to all-ones (or a NaN pattern) before ml_create, the forced heavy-path solve of cfg4s matches the oracle (the
+    copies' padding entries past a chunk hold stale indices; their products are discarded)."""
+    ds = dataset("cfg4s")
+    r_o = oracle.Oracle(ds).solve()
+    ctx = ml.Context(ds, ws_fill=fill)
+    ctx.ml_set_engine(16)
+    r_g = ctx.ml_solve()
+    assert ctx.ml_heavy_info()["relaxations"] > 0
+    assert r_g["status"] == 0 and r_g["kappa"] <= 1e-6
+    assert abs(r_g["F"] - r_o["F"]) <= 1e-6 * abs(r_o["F"])
