@@ -170,13 +170,15 @@ ml_status ml_set_sm_share(ml_ctx *c, int blocks);
    bit 3: the large-m inner solver's X_A s and H sigma streams claim their column units dynamically from a grid-wide
           counter whatever the unit count (by default only with >= 32 units per warp, where static shares left blocks
           waiting on the slowest).
-   bits 4 / 5: the large-m inner solver takes the heavy-column path (the S / G copies of the longest columns,
-          ml_heavy_info) in every relaxation / in none; by default when the free set holds >= 1/4 of their nonzeros.
-          ML_E_INVAL for bit 4 when the context has no heavy path (small m, or the longest columns hold < 1/10 of X). */
+   bit 4: the large-m inner solver takes the heavy-column path (X_A s of the longest columns from their row-major copy,
+          without atomics; ml_heavy_info) in every relaxation; bit 6: in the relaxations whose free set holds >= 1/4
+          of their nonzeros; neither: never (the default).  The first request builds the copy (device passes over X,
+          synchronises the stream).  ML_E_INVAL for bit 4 when the context has no heavy path (small m, the longest
+          columns hold < 1/10 of X, or a row holds more than 768 of their nonzeros). */
 ml_status ml_set_engine(ml_ctx *c, uint32_t flags);
 /* Diagnostics of the large-m heavy-column path (DESIGN 8.2; off for m <= 8192): info_host[8] = built (0/1), |H|,
-   nonzeros of H, S tiles, G chunks, row bands, relaxations that ran it since ml_create, the heavy mode (0 by the
-   free set's share of H, 1 always, 2 never: ml_set_engine bits 4 / 5). */
+   nonzeros of H, warp chunks of its row-major copy, 0, 0 (reserved), relaxations that ran it since ml_create, the
+   mode (0: by the free set's share of H, 1: always, 2: never; ml_set_engine bits 4 / 6). */
 ml_status ml_heavy_info(ml_ctx *c, int64_t *info_host);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */

@@ -117,6 +117,8 @@ struct ml_ctx {
     int* hv_lens = nullptr;
     int* hv_bsum = nullptr;
     int* hv_misc = nullptr;
+    unsigned* hv_hist = nullptr;
+    bool hv_built = false;   // hv_build ran (on the first ml_set_engine request for the heavy path)
 };
 
 namespace {
@@ -159,6 +161,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     int* upos = cv.take<int>(ucap2);
     double2* upart = cv.take<double2>(ucap2);
     int* ustart = cv.take<int>(mm > SMALL_M ? nn + 1 : 1);
+    int* uend = cv.take<int>(mm > SMALL_M ? nn + 1 : 1);
     long long* unz = cv.take<long long>(ucap2 + 1);
     ASet fine, coarse;
     fine.A = cv.take<int>(nn); fine.gA = cv.take<double>(nn); fine.hA = cv.take<double>(nn); fine.wA = cv.take<double>(nn);
@@ -187,7 +190,6 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     // heavy-column path of the large-m inner solver (ml_heavy.cuh): the S and G copies of H's nonzeros (at most all
     // of X's), their chunk tables, band partials, per-row products; build scratch aliases hpart / Xh / Xhz
     const size_t hvn = big ? (size_t)nnz + 16 : 1;
-    const size_t hvnb = big ? (mm + HV_RB - 1) / HV_RB : 1;
     HvPrm hv{};
     hv.hid = cv.take<int>(big ? nn : 1);
     hv.phid = cv.take<int>(big ? nn : 1);
@@ -196,22 +198,14 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     hv.sval = cv.take<float>(hvn);
     hv.sidx = cv.take<uint16_t>(hvn);
     hv.soff = cv.take<int>(big ? mm + 8 : 1);
-    const size_t sch_cap = big ? (size_t)nnz / (HV_CHMAX / 2) + mm / HV_SMAX + 16 : 1;   // (chp >= HV_CHMAX / 2)
-    hv.schunk = cv.take<HvChunk>(sch_cap);
-    hv.gval = cv.take<float>(hvn);
-    hv.gidx = cv.take<uint16_t>(hvn);
-    hv.goff = cv.take<int>(big ? (size_t)HV_HMAX * hvnb + 8 : 1);
-    const size_t gch_cap = big ? 2 * (size_t)nnz / HV_CHMAX + (size_t)HV_HMAX * hvnb / HV_SMAX + 2 * hvnb + 16 : 1;
-    hv.gchunk = cv.take<HvChunk>(gch_cap);
-    hv.sblk = cv.take<uint16_t>(sch_cap * 256);
-    hv.gblk = cv.take<uint16_t>(gch_cap * 256);
-    hv.hpart = cv.take<double>(big ? std::max<size_t>((size_t)HV_HMAX * hvnb, 32768) + 64 : 1);
+    hv.schunk = cv.take<HvChunk>(big ? (size_t)nnz / (HV_WCH / 2) + mm / HV_WROWS + 16 : 1);   // (greedy chunks)
     hv.Xh = cv.take<double>(big ? mm + 2 : 1);
     hv.Xhz = cv.take<double>(big ? mm + 2 : 1);
     hv.sH = cv.take<double>(HV_HMAX);
     hv.zH = cv.take<uint32_t>(HV_HMAX / 32);
-    int* hv_bsum = cv.take<int>(big ? std::max({nn, mm + 1, (size_t)HV_HMAX * hvnb + 1}) / 1024 + 64 : 1);
+    int* hv_bsum = cv.take<int>(big ? std::max(nn, mm + 1) / 1024 + 64 : 1);
     int* hv_misc = cv.take<int>(64);
+    unsigned* hv_hist = cv.take<unsigned>(big ? 65536 : 1);
 
     UnitsMem um[4];
     for (int k = 0; k < 4; ++k) {
@@ -230,7 +224,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
     P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
     P.irpart = irpart;
-    P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.unz = unz;
+    P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.uend = uend; P.unz = unz;
     c->slist = slist;
     c->dense_colptr = dense_colptr;
     c->rowtab = rowtab;
@@ -247,6 +241,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     c->hv_lens = hv_lens;
     c->hv_bsum = hv_bsum;
     c->hv_misc = hv_misc;
+    c->hv_hist = hv_hist;
 }
 
 int pick_G(double mean_len) {
@@ -749,7 +744,7 @@ ml_status hv_build(ml_ctx* c) {
     const int m = (int)c->X.m, n = (int)c->X.n;
     const int* colptr = c->X.csc_colptr;
     auto sync = [&]() { return cudaStreamSynchronize(c->st) == cudaSuccess; };
-    unsigned* hist = reinterpret_cast<unsigned*>(hv.hpart);
+    unsigned* hist = c->hv_hist;
     cudaMemsetAsync(hist, 0, sizeof(unsigned) * 65536, c->st);
     ML_LAUNCH(c, k_hv_lenhist, GRID_CAP, colptr, n, hist);
     std::vector<unsigned> hh(65536);
@@ -785,56 +780,36 @@ ml_status hv_build(ml_ctx* c) {
     int* misc = c->hv_misc;
     cudaMemsetAsync(misc, 0, sizeof(int) * 64, c->st);
     int* hrp = const_cast<int*>(hv.soff);
-    int* tidx = reinterpret_cast<int*>(hv.Xhz);   // (scratch: m + 1 ints)
     ML_LAUNCH(c, k_hv_rowcnt, GRID_CAP, c->X.csr_rowptr, c->X.csr_col, m, hv.hid, hrp, misc);
     cudaMemsetAsync(hrp + m, 0, sizeof(int), c->st);
     scan_excl(c, hrp, (long long)m + 1, c->hv_bsum);
     int maxcnt = 0;
     cudaMemcpyAsync(&maxcnt, misc, sizeof(int), cudaMemcpyDeviceToHost, c->st);
     if (!sync()) return cuda_fail(c, "hv_build");
-    if (maxcnt < 1 || maxcnt > HV_CHMAX / 2) return ML_OK;
-    const int chp = HV_CHMAX - maxcnt;
-    ML_LAUNCH(c, k_hv_tileflags, GRID_CAP, hrp, m, chp, tidx);
-    scan_excl(c, tidx, (long long)m + 1, c->hv_bsum);
-    int nts = 0;
-    cudaMemcpyAsync(&nts, tidx + m, sizeof(int), cudaMemcpyDeviceToHost, c->st);
-    ML_LAUNCH(c, k_hv_tiles, GRID_CAP, hrp, m, chp, tidx, const_cast<HvChunk*>(hv.schunk));
+    if (maxcnt < 1 || maxcnt > HV_WCH) return ML_OK;
+    // warp chunks, greedily on the host: whole rows while the chunk holds at most HV_WCH entries and HV_WROWS rows
+    std::vector<int> hr((size_t)m + 1);
+    cudaMemcpyAsync(hr.data(), hrp, sizeof(int) * ((size_t)m + 1), cudaMemcpyDeviceToHost, c->st);
+    if (!sync()) return cuda_fail(c, "hv_build");
+    std::vector<HvChunk> chs;
+    chs.reserve((size_t)m / HV_WROWS + (size_t)hr[m] / (HV_WCH / 2) + 16);
+    for (int r = 0; r < m;) {
+        const int r0 = r;
+        while (r < m && r - r0 < HV_WROWS && hr[r + 1] - hr[r0] <= HV_WCH) ++r;
+        chs.push_back(HvChunk{hr[r0], hr[r], r0, r - r0, hv_lg(r - r0), 0, 0, 0});
+    }
+    const int nts = (int)chs.size();
+    cudaMemcpyAsync(const_cast<HvChunk*>(hv.schunk), chs.data(), sizeof(HvChunk) * chs.size(), cudaMemcpyHostToDevice,
+                    c->st);
     ML_LAUNCH(c, k_hv_rowfill, GRID_CAP, c->X.csr_rowptr, c->X.csr_col, c->X.csr_val, m, hv.hid, hrp,
               const_cast<float*>(hv.sval), const_cast<uint16_t*>(hv.sidx));
     if (!sync()) return cuda_fail(c, "hv_build");
-    // G copy: (band, h) segment lengths, scanned to the segment starts (goff); entries; chunks
-    const int nb = (m + HV_RB - 1) / HV_RB;
-    const long long N = (long long)nh * nb;
-    int* off = const_cast<int*>(hv.goff);
-    ML_LAUNCH(c, k_hv_segcnt, GRID_CAP, colptr, c->X.csc_row, c->hv_hcols, nh, nb, m, off);
-    cudaMemsetAsync(off + N, 0, sizeof(int), c->st);
-    scan_excl(c, off, N + 1, c->hv_bsum);
-    ML_LAUNCH(c, k_hv_segfill, GRID_CAP, colptr, c->X.csc_row, c->X.csc_val, c->hv_hcols, nh, nb, off,
-              const_cast<float*>(hv.gval), const_cast<uint16_t*>(hv.gidx));
-    int* nch = reinterpret_cast<int*>(hv.Xhz);   // (scratch: 2 nb ints)
-    int* choff = nch + nb;
-    const int gb = std::max(1, (nb + 63) / 64);
-    k_hv_chunks<<<gb, 64, 0, c->st>>>(off, nh, nb, 0, nch, nullptr, nullptr);
-    std::vector<int> hn(nb), ho(nb);
-    cudaMemcpyAsync(hn.data(), nch, sizeof(int) * nb, cudaMemcpyDeviceToHost, c->st);
-    if (!sync()) return cuda_fail(c, "hv_build");
-    long long ncg = 0;
-    for (int k = 0; k < nb; ++k) { ho[k] = (int)ncg; ncg += hn[k]; }
-    cudaMemcpyAsync(choff, ho.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, c->st);
-    k_hv_chunks<<<gb, 64, 0, c->st>>>(off, nh, nb, 1, nch, choff, const_cast<HvChunk*>(hv.gchunk));
-    c->launches += 2;
-    ML_LAUNCH(c, k_hv_blocks, GRID_CAP, hv.schunk, nts, hv.soff, const_cast<uint16_t*>(hv.sblk));
-    ML_LAUNCH(c, k_hv_blocks, GRID_CAP, hv.gchunk, (int)ncg, hv.goff, const_cast<uint16_t*>(hv.gblk));
-    if (!sync()) return cuda_fail(c, "hv_build");   // (the host vectors above outlive their async copies)
-    cudaMemsetAsync(hv.hpart, 0, sizeof(double) * (size_t)nh * nb, c->st);
     cudaMemsetAsync(hv.Xh, 0, sizeof(double) * (size_t)m, c->st);
     cudaMemsetAsync(hv.Xhz, 0, sizeof(double) * (size_t)m, c->st);
     cudaMemsetAsync(hv.sH, 0, sizeof(double) * HV_HMAX, c->st);
     cudaMemsetAsync(hv.zH, 0, sizeof(uint32_t) * (HV_HMAX / 32), c->st);
     hv.nh = nh;
-    hv.nb = nb;
     hv.nts = nts;
-    hv.ncg = (int)ncg;
     hv.nnzh = nnzh;
     hv.mode = 2;      // (off by default until it beats the column units: ml_set_engine bit 4 / 5 select it)
     hv.frac = 0.25;
@@ -1017,10 +992,6 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     if (c->big_inner) ML_LAUNCH(c, k_xstats, GRID_CAP, X->csc_val, X->nnz, X->csr_rowptr, (int)X->m, c->ctl);
-    if (c->big_inner && c->inner_fn_hv && has_csr) {
-        const ml_status hs = hv_build(c);
-        if (hs != ML_OK) { *out = c; return hs; }
-    }
     if (c->mp_grid_all)   // the static merge-path plan over all columns (X is fixed for the context's life)
         ML_LAUNCH(c, k_mp_search, std::max(1, (c->mp_tiles_cap + ML_NT) / ML_NT), c->mp_all, c->mp_tiles_cap);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
@@ -1384,7 +1355,14 @@ ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
     if (want && c->mp_grid_all == 0) return ML_E_INVAL;   // (small m: the shared-memory passes; no merge-path plan)
     c->mp = want;
     c->P.dyn = (flags & 8u) ? 1 : 0;   // bit 3: dynamic unit claims in the large-m inner solver whatever the unit count
-    // bits 4 / 5: the heavy-column path in every relaxation / in none (default: when A holds >= 1/4 of H's nonzeros)
+    // bit 4: the heavy-column path in every relaxation; bit 6: when A holds >= 1/4 of H's nonzeros; else never
+    if ((flags & (16u | 64u)) && !c->hv_built) {   // the heavy path's copy is built on first request (X is fixed)
+        c->hv_built = true;
+        if (c->big_inner && c->inner_fn_hv && c->X.csr_rowptr) {
+            const ml_status hs = hv_build(c);
+            if (hs != ML_OK) return hs;
+        }
+    }
     if ((flags & 16u) && !c->P.hv.on) return ML_E_INVAL;
     c->P.hv.mode = (flags & 16u) ? 1 : (flags & 64u) ? 0 : 2;   // bit 6: by the free set's share of H
     return ML_OK;
@@ -1399,8 +1377,8 @@ ml_status ml_heavy_info(ml_ctx* c, int64_t* info_host) {
     info_host[1] = hv.on ? hv.nh : 0;
     info_host[2] = hv.on ? hv.nnzh : 0;
     info_host[3] = hv.on ? hv.nts : 0;
-    info_host[4] = hv.on ? hv.ncg : 0;
-    info_host[5] = hv.on ? hv.nb : 0;
+    info_host[4] = 0;
+    info_host[5] = 0;
     info_host[6] = c->h.hv_relax;
     info_host[7] = hv.mode;
     return ML_OK;

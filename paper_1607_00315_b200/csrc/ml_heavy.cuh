@@ -1,329 +1,161 @@
-// ml_heavy.cuh — the heavy-column path of the large-m inner solver (A5: X_A s and H sigma = X_A^T D X_A sigma,
-// PAPER.md P:793; DESIGN section 8.2 "heavy columns").
+// ml_heavy.cuh — the heavy-column path of the large-m inner solver: X_A s for the longest columns without atomics
+// (A5; DESIGN section 8.2 "heavy columns").
 //
 // On the Zipf designs (cfg 3-5) a few thousand columns hold most of X's nonzeros (cfg 5: the 8192 longest columns
 // hold 65 % of 2e8), and they are the columns of every free set.  Through the column units of k_inner their X_A s
-// products are fp64 reductions into global memory and their H sigma products are 8-byte L2 gathers of D o X sigma:
-// both bound by L2 operations, not by HBM.  Here the heavy set H (at most HV_HMAX columns, the longest, chosen once
-// at ml_create) gets two extra copies of its nonzeros (fp32 value + 16-bit index, 6 bytes), each ordered so that
-// the vector it multiplies sits in shared memory:
-//   * S copy (row-major): the heavy entries of each row, index = h.  s_H (the direction on H, HV_HMAX doubles) is
-//     staged in shared memory; every row's sum is written once (Xh): no atomics.
-//   * G copy ("band CSC"): rows cut into bands of HV_RB rows; within a band the heavy entries ordered by (h, row),
-//     index = row - band row0.  D o X sigma of one band sits in shared memory; every (band, h) segment sum is written
-//     once to hpart[h * nb + band]; the owner of position h sums its nb band partials in band order.
-// Heavy ids h are assigned by decreasing column length, so the segments of a band come longest first and a chunk
-// holds segments of similar length.  Both copies are cut into chunks (S: whole rows; G: whole segments) of at most
-// HV_CHMAX entries and HV_SMAX segments, streamed by one thread of the block with TMA bulk copies through a
-// HV_STG-stage ring together with the chunk's slice of segment offsets (S: the heavy row pointers; G: the (band, h)
-// segment starts).  Groups of L = 2^lg lanes (lg fixed per chunk from its mean segment length) take the segments in
-// turn, each lane summing every L-th entry, then a fixed shuffle tree; chunks of a few long segments are reduced by
-// the whole block, one segment at a time.  Every result is a fixed-order sum: bitwise reproducible.
+// products are 64-bit reductions into global memory, bound by the REDG issue rate of the load/store units (~1.3 LSU
+// cycles per lane, B300_MICROARCH.md: 0.8-0.9 nonzeros per SM clock).  Here the heavy set H (at most HV_HMAX
+// columns, the longest, chosen once at ml_create) gets a row-major copy of its nonzeros (fp32 value + 16-bit heavy
+// id, 6 bytes): the "S copy".  s_H (the inner direction on H, HV_HMAX doubles) is staged in shared memory, and each
+// row's sum over its heavy entries is formed in registers and written once (Xh): no atomics.
+// The copy is cut into warp chunks of whole rows (at most HV_WCH entries and HV_WROWS rows); every warp streams its
+// own chunks through a private HV_WST-stage TMA ring (its lane 0 issues the bulk copies of the values, the ids and
+// the chunk's slice of row starts) and reduces a chunk with groups of L = 2^lg lanes per row (lg per chunk from its
+// row count: one round of 32 / L rows); no block barriers.  Each row is a fixed-order sum: bitwise reproducible.
+// The H sigma products of the heavy columns stay on the column units (L2 gathers of D o X sigma).
 #pragma once
 #include "ml_common.cuh"
 
 namespace ml {
 
 constexpr int HV_HMAX = 8192;              // heavy columns at most (s_H: 64 KB of shared memory)
-constexpr int HV_CAP = 4096;               // entries per ring stage
-constexpr int HV_CHMAX = HV_CAP - 32;      // entries per chunk (its span of whole 16-entry blocks is <= HV_CAP)
-constexpr int HV_SMAX = 1024;              // segments per chunk
-constexpr int HV_OFFCAP = HV_SMAX + 8;     // offsets per stage (the chunk's HV_SMAX + 1, from a 16-byte boundary)
-constexpr int HV_RB = HV_CHMAX;            // rows per band of the G copy (16-bit row index; a segment fits a chunk)
-constexpr int HV_STG = 3;                  // ring stages (two chunks in flight while one is reduced)
+constexpr int HV_WCH = 768;                // entries per warp chunk at most
+constexpr int HV_WROWS = 8;                // rows per warp chunk at most (one round of groups of >= 4 lanes)
+constexpr int HV_WST = 2;                  // stages of a warp's ring
 constexpr int HV_MINLEN = 32;              // shortest heavy column
 constexpr int HV_W = 8;                    // warps per block (k_inner)
-constexpr int HV_LGBLK = 8;                // lg of a chunk reduced by the whole block, segment by segment
-constexpr size_t HV_STAGE = (size_t)HV_CAP * 6 + (size_t)HV_OFFCAP * 4 + 512;   // values, indices, offsets, block segs
-// dynamic shared memory of the sub-phases (they alias the column rings of k_inner)
-constexpr size_t HV_SH_OFF = 0;                                            // S: s_H
-constexpr size_t HV_ZH_OFF = (size_t)8 * HV_HMAX;                          // S: zeroing bits of H
-constexpr size_t HV_SRING_OFF = HV_ZH_OFF + (size_t)4 * (HV_HMAX / 32);    // S: the ring
-constexpr size_t HV_U_OFF = 0;                                             // G: D o X sigma of the band
-constexpr size_t HV_GRING_OFF = 32768;                                     // G: the ring
-constexpr size_t HV_RING_BYTES = (size_t)HV_STG * HV_STAGE + 8 * HV_STG;
-static_assert((size_t)8 * HV_RB <= HV_GRING_OFF, "band vector");
-static_assert(HV_SRING_OFF % 16 == 0 && HV_STAGE % 16 == 0, "ring alignment");
-__host__ __device__ constexpr size_t hv_smem_bytes() {
-    return (HV_SRING_OFF + HV_RING_BYTES) > (HV_GRING_OFF + HV_RING_BYTES) ? HV_SRING_OFF + HV_RING_BYTES
-                                                                        : HV_GRING_OFF + HV_RING_BYTES;
-}
+// a stage: values (HV_WCH + 8 from a 16-byte boundary), ids, row starts (HV_WROWS + 1 from a 16-byte boundary)
+constexpr size_t HV_WSTAGE = (((size_t)(HV_WCH + 8) * 6 + (size_t)(HV_WROWS + 8) * 4) + 15) / 16 * 16;
+constexpr size_t HV_WRING = (size_t)HV_WST * HV_WSTAGE + 64;   // + the stages' mbarriers
+// dynamic shared memory of the sub-phase (it aliases the column rings of k_inner)
+constexpr size_t HV_SH_OFF = 0;                                            // s_H
+constexpr size_t HV_ZH_OFF = (size_t)8 * HV_HMAX;                          // zeroing bits of H
+constexpr size_t HV_SRING_OFF = HV_ZH_OFF + (size_t)4 * (HV_HMAX / 32);    // the warps' rings
+static_assert(HV_SRING_OFF % 16 == 0 && HV_WSTAGE % 16 == 0 && HV_WRING % 16 == 0, "ring alignment");
+__host__ __device__ constexpr size_t hv_smem_bytes() { return HV_SRING_OFF + (size_t)HV_W * HV_WRING; }
 
-// a chunk: entries [e0, e1) of a copy; its ns segments start at offsets[s0 .. s0 + ns] (absolute entry indices);
-// base: first row (S; segment j is row base + j) or band (G; segment j is heavy column h0 + j)
-struct HvChunk { int e0, e1, base, s0, ns, lg, h0, pad; };
+// a warp chunk: heavy entries [e0, e1) of rows [r0, r0 + nr) (their starts at soff[r0 .. r0 + nr]); L = 2^lg
+struct HvChunk { int e0, e1, r0, nr, lg, pad0, pad1, pad2; };
 
 // the heavy path's device state (Prm::hv)
 struct HvPrm {
-    int on;                 // built (m > SMALL_M, enough heavy nonzeros)
+    int on;                 // built (m > SMALL_M, enough heavy nonzeros, rows of at most HV_WCH / 2 heavy entries)
     int nh;                 // |H|
-    int nb;                 // bands of the G copy
-    int nts, ncg;           // S chunks, G chunks
+    int nts;                // warp chunks
     int mode;               // 0: per relaxation (nnz(A ∩ H) >= frac nnz(H)), 1: always, 2: never (ml_set_engine)
     double frac;
     long long nnzh;         // nonzeros of H
-    const int* hid;         // [n] heavy id of column j, or -1
-    const float* sval; const uint16_t* sidx; const int* soff; const HvChunk* schunk;   // S copy, row starts [m + 1]
-    const float* gval; const uint16_t* gidx; const int* goff; const HvChunk* gchunk;   // G copy, starts [nb nh + 1]
-    const uint16_t* sblk; const uint16_t* gblk;   // [chunks][256]: the segment (within its chunk) of each block's
-                                                  // first entry
+    const int* hid;         // [n] heavy id of column j (by decreasing length), or -1
+    const float* sval; const uint16_t* sidx;   // the S copy: values and heavy ids, row by row
+    const int* soff;        // [m + 1] row starts in the S copy
+    const HvChunk* schunk;  // [nts]
     double* sH;             // [HV_HMAX] the S coefficient of each heavy column of A this iteration (0 elsewhere)
     uint32_t* zH;           // [HV_HMAX / 32] its zeroing flags (the snap path's z = s on those columns)
     double* Xh; double* Xhz;   // [m] X_H s_H, X_H z_H
-    double* hpart;          // [nh * nb] band partials of H sigma
     int* phid;              // [n] heavy id of free-set position p this relaxation (-1: light)
 };
 
-// The dynamic shared memory of the calling kernel (every extern __shared__ array names the same base): the ring and
-// the ops' vectors are addressed through it, so that the out-of-line hv_stream still emits shared loads.
+// The dynamic shared memory of the calling kernel (every extern __shared__ array names the same base): s_H and the
+// rings are addressed through it, so that the out-of-line hv_sweep still emits shared loads.
 extern __shared__ __align__(16) unsigned char hv_dyn[];
 
-// ------------------------------------------------------------------ one chunk: its segments, by groups of L lanes
-// Both copies are stored swizzled in 16-entry blocks so that thread t, reading the 16 entries of block q = its
-// global block index with 16-byte shared loads, hits distinct banks in every quarter warp: the values' 4-entry
-// quarter j sits at quarter (j + (q >> 1)) & 3, the indices' 8-entry half j at half j ^ ((q >> 2) & 1).
-__host__ __device__ __forceinline__ long long hv_phys_v(long long e) {
-    return (e & ~15LL) | ((((e >> 2) + (e >> 5)) & 3) << 2) | (e & 3);
-}
-__host__ __device__ __forceinline__ long long hv_phys_i(long long e) {
-    return (e & ~15LL) | ((((e >> 3) ^ (e >> 6)) & 1) << 3) | (e & 7);
-}
-// Per-thread ranges: thread t reduces the 16 entries of stage block t (the chunk's entries [v0, v1) of the stage,
-// which starts at global entry eb = e0 & ~15).  Its products are summed per piece of segment, in entry order: a
-// segment inside the range is written at once; a segment crossing ranges leaves its parts in shared slots (tail
-// part tp of the thread where it starts, whole ranges wp, head part hp of the thread where it ends), which the
-// ending thread adds in thread order after a barrier.
-template <int NV> struct HvPart { double tp[NV][256]; double wp[NV][256]; };
-template <int NV, class Op>
-__device__ __forceinline__ void hv_ranges(const float* sv, const uint16_t* si, const int* so, const uint16_t* sbk,
-                                          const HvChunk& ch, const Op& op, HvPart<NV>& pt) {
-    const int t = threadIdx.x;
-    const int eb = ch.e0 & ~15, v0 = ch.e0 - eb, v1 = ch.e1 - eb, ob = ch.s0 & 3;
-    const int q = (eb >> 4) + t;
-    const int lo = max(16 * t, v0), hi = min(16 * t + 16, v1);
-    double p[16][NV];
-    if (lo < hi) {
-        float x[16];
-        uint32_t ix[16];
+// Rows of a staged chunk by groups of L = 2^LG lanes: lane gl sums entries gl, gl + L, ... of its row, 8 at a time
+// (loads first, then the fused multiply-adds in order), then the group's fixed shuffle tree; Xh[row] (Xhz[row]).
+template <int NV, int LG>
+__device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, const int* so, const HvChunk& ch,
+                                        double* Xh, double* Xhz) {
+    constexpr int L = 1 << LG, NG = 32 >> LG;
+    const int lane = threadIdx.x & 31, grp = lane >> LG, gl = lane & (L - 1);
+    const int eb = ch.e0 & ~7, ob = ch.r0 & 3;
+    const double* s = reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF);
+    const uint32_t* zb = reinterpret_cast<const uint32_t*>(hv_dyn + HV_ZH_OFF);
+    for (int r = grp; r - grp < ch.nr; r += NG) {   // (every lane runs every round: the shuffles need all lanes)
+        double acc[NV];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float4 v = *reinterpret_cast<const float4*>(sv + 16 * t + 4 * ((j + (q >> 1)) & 3));
-            x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
-        }
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+        int b = 0, e = 0;
+        if (r < ch.nr) { b = so[ob + r] - eb; e = so[ob + r + 1] - eb; }
+        for (int i = b + gl; i < e; i += 8 * L) {
+            float x[8];
+            uint32_t ix[8];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const uint4 v = *reinterpret_cast<const uint4*>(si + 16 * t + 8 * (j ^ ((q >> 2) & 1)));
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { ix[8 * j + 2 * u] = w[u] & 0xFFFFu; ix[8 * j + 2 * u + 1] = w[u] >> 16; }
-        }
-#pragma unroll
-        for (int e = 0; e < 16; ++e) op.prod(ix[e], x[e], p[e]);
-        for (int k = sbk[t]; k < ch.ns; ++k) {   // my segments, from the one holding my first entry
-            const int sb = so[ob + k] - eb, se = so[ob + k + 1] - eb;
-            if (sb >= hi) break;
-            const int ps = max(sb, lo) - 16 * t, pe = min(se, hi) - 16 * t;
-            double a[NV];
-#pragma unroll
-            for (int q2 = 0; q2 < NV; ++q2) a[q2] = 0.0;
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                if (e >= ps && e < pe) {
-#pragma unroll
-                    for (int q2 = 0; q2 < NV; ++q2) a[q2] += p[e][q2];
-                }
-            const bool before = sb < lo, after = se > hi;
-            if (!before && !after) {
-                if (se > sb) op.out(ch, k, a);
-            } else if (before && after) {
-#pragma unroll
-                for (int q2 = 0; q2 < NV; ++q2) pt.wp[q2][t] = a[q2];
-            } else if (after) {
-#pragma unroll
-                for (int q2 = 0; q2 < NV; ++q2) pt.tp[q2][t] = a[q2];
-            } else {   // the head part of a segment that started in an earlier range: kept until after the barrier
-#pragma unroll
-                for (int q2 = 0; q2 < NV; ++q2) p[0][q2] = a[q2];   // (this is my first piece: p[0] is free again)
+            for (int u = 0; u < 8; ++u) {
+                const bool ok = i + u * L < e;
+                x[u] = ok ? sv[i + u * L] : 0.0f;
+                ix[u] = ok ? si[i + u * L] : 0u;
             }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i + u * L < e) {
+                    const uint32_t h = ix[u] & (HV_HMAX - 1);
+                    const double sh = s[h];
+                    acc[0] = fma((double)x[u], sh, acc[0]);
+                    if constexpr (NV == 2) acc[1] = fma((double)x[u], ((zb[h >> 5] >> (h & 31)) & 1u) ? sh : 0.0, acc[1]);
+                }
+        }
+#pragma unroll
+        for (int d = L >> 1; d > 0; d >>= 1) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], d);
+        }
+        if (gl == 0 && r < ch.nr) {
+            Xh[ch.r0 + r] = acc[0];
+            if constexpr (NV == 2) Xhz[ch.r0 + r] = acc[1];
         }
     }
-    __syncthreads();
-    if (lo < hi) {
-        // the segment holding my first entry, if it started before me and ends in my range
-        const int k = sbk[t];
-        const int sb = so[ob + k] - eb, se = so[ob + k + 1] - eb;
-        if (sb < lo && se <= hi) {
-            const int ts = sb >> 4;   // the range where it starts
-            double a[NV];
-#pragma unroll
-            for (int q2 = 0; q2 < NV; ++q2) a[q2] = pt.tp[q2][ts];
-            for (int u = ts + 1; u < t; ++u) {
-#pragma unroll
-                for (int q2 = 0; q2 < NV; ++q2) a[q2] = a[q2] + pt.wp[q2][u];
-            }
-#pragma unroll
-            for (int q2 = 0; q2 < NV; ++q2) a[q2] = a[q2] + p[0][q2];   // my part, kept in p[0]
-            op.out(ch, k, a);
-        }
-    }
-}
-// sv/si: the stage's entries from e0 & ~15; so: its offsets from s0 & ~3 (absolute entry indices)
-template <int NV, class Op>
-__device__ __forceinline__ void hv_segments(const float* sv, const uint16_t* si, const int* so, const uint16_t* sbk,
-                                            const HvChunk& ch, const Op& op, double* wsum, HvPart<NV>& pt) {
-    const int eb = ch.e0 & ~15, ob = ch.s0 & 3;
-    if (ch.lg == HV_LGBLK) {   // a few long segments: the whole block on each, in turn
-        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int k = 0; k < ch.ns; ++k) {
-            const int b = so[ob + k] - eb, e = so[ob + k + 1] - eb;
-            double acc[NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-            for (int i = b + (int)threadIdx.x; i < e; i += 2048) {   // 8 entries in flight, summed in order
-                float x[8];
-                uint32_t ix[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int t = i + 256 * u;
-                    const bool ok = t < e;
-                    x[u] = ok ? sv[hv_phys_v(eb + t) - eb] : 0.0f;
-                    ix[u] = ok ? si[hv_phys_i(eb + t) - eb] : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (i + 256 * u < e) op.fma(ix[u], x[u], acc);
-            }
-#pragma unroll
-            for (int q = 0; q < NV; ++q) acc[q] = warp_sum(acc[q]);
-            double* ws = wsum + (k & 1) * NV * HV_W;   // (double-buffered: one barrier per segment)
-            if (lane == 0) {
-#pragma unroll
-                for (int q = 0; q < NV; ++q) ws[q * HV_W + w] = acc[q];
-            }
-            __syncthreads();
-            if (threadIdx.x == 0 && e > b) {
-                double v[NV];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    v[q] = ws[q * HV_W];
-                    for (int u = 1; u < HV_W; ++u) v[q] = v[q] + ws[q * HV_W + u];
-                }
-                op.out(ch, k, v);
-            }
-        }
-        return;
-    }
-    hv_ranges<NV>(sv, si, so, sbk, ch, op, pt);
 }
 
-// Stream chunks [c0, c1) through the block's TMA ring (thread 0 issues; every thread reduces).  on_chunk(ch) runs
-// block-uniformly before a chunk is reduced (it may stage data, with its own barriers).
-// (out of line: called once per sub-phase, so that its loop gets registers of its own instead of k_inner's spills)
-template <int NV, class Op, class OnChunk>
-__device__ __noinline__ void hv_stream(const HvChunk* chunks, int c0, int c1, const float* gv, const uint16_t* gi,
-                                       const int* goff, const uint16_t* gblk, size_t ring_off, Op op, OnChunk on_chunk) {
-    __shared__ double wsum[2 * NV * HV_W];
-    __shared__ HvPart<NV> pt;
-    unsigned char* ring = hv_dyn + ring_off;   // (a shared address the compiler can see)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ring + (size_t)HV_STG * HV_STAGE);
-    auto sval = [&](int st) { return reinterpret_cast<float*>(ring + (size_t)st * HV_STAGE); };
-    auto sidx = [&](int st) { return reinterpret_cast<uint16_t*>(ring + (size_t)st * HV_STAGE + (size_t)HV_CAP * 4); };
-    auto soff = [&](int st) { return reinterpret_cast<int*>(ring + (size_t)st * HV_STAGE + (size_t)HV_CAP * 6); };
-    auto sblk = [&](int st) {
-        return reinterpret_cast<uint16_t*>(ring + (size_t)st * HV_STAGE + (size_t)HV_CAP * 6 + (size_t)HV_OFFCAP * 4);
-    };
+// This warp's chunks (an equal share of all warps of the grid, in order) through its private ring.
+// (out of line: called once per S phase, so that its loop gets registers of its own instead of k_inner's spills)
+template <int NV>
+__device__ __noinline__ void hv_sweep(const HvPrm hv) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = hv_dyn + HV_SRING_OFF + (size_t)w * HV_WRING;   // (a shared address the compiler can see)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ring + (size_t)HV_WST * HV_WSTAGE);
+    const long long gw = (long long)blockIdx.x * HV_W + w, NW = (long long)gridDim.x * HV_W;
+    const int c0 = (int)(hv.nts * gw / NW), c1 = (int)(hv.nts * (gw + 1) / NW);
     auto issue = [&](int c, int st) {
-        const int e0 = __ldg(&chunks[c].e0), e1 = __ldg(&chunks[c].e1);
-        const int s0 = __ldg(&chunks[c].s0), ns = __ldg(&chunks[c].ns);
-        const int a0 = e0 & ~15, a1 = (e1 + 15) & ~15;
-        const int o0 = s0 & ~3, o1 = (s0 + ns + 1 + 3) & ~3;
+        const HvChunk k = hv.schunk[c];
+        const int a0 = k.e0 & ~7, a1 = (k.e1 + 7) & ~7;
+        const int o0 = k.r0 & ~3, o1 = (k.r0 + k.nr + 1 + 3) & ~3;
+        unsigned char* b = ring + (size_t)st * HV_WSTAGE;
         const uint32_t n = (uint32_t)(a1 - a0), no = (uint32_t)(o1 - o0);
-        mbar_arrive_expect_tx(bar + st, 6u * n + 4u * no + 512u);
-        bulk_g2s(sval(st), gv + a0, 4u * n, bar + st);
-        bulk_g2s(sidx(st), gi + a0, 2u * n, bar + st);
-        bulk_g2s(soff(st), goff + o0, 4u * no, bar + st);
-        bulk_g2s(sblk(st), gblk + (size_t)c * 256, 512u, bar + st);
+        mbar_arrive_expect_tx(bar + st, 6u * n + 4u * no);
+        bulk_g2s(b, hv.sval + a0, 4u * n, bar + st);
+        bulk_g2s(b + (size_t)(HV_WCH + 8) * 4, hv.sidx + a0, 2u * n, bar + st);
+        bulk_g2s(b + (size_t)(HV_WCH + 8) * 6, hv.soff + o0, 4u * no, bar + st);
     };
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < HV_STG; ++k) mbar_init(bar + k, 1);
+    if (lane == 0) {
+        for (int k = 0; k < HV_WST; ++k) mbar_init(bar + k, 1);
         fence_mbar_init();
-        for (int k = 0; k < HV_STG && c0 + k < c1; ++k) issue(c0 + k, k);
+        for (int k = 0; k < HV_WST && c0 + k < c1; ++k) issue(c0 + k, k);
     }
-    __syncthreads();
+    __syncwarp();
     uint32_t phase = 0u;
-    for (int c = c0, st = 0; c < c1; ++c, st = (st + 1) % HV_STG) {
-        HvChunk ch;
-        {
-            const int4 a = __ldg(reinterpret_cast<const int4*>(chunks + c));
-            const int4 b = __ldg(reinterpret_cast<const int4*>(chunks + c) + 1);
-            ch = HvChunk{a.x, a.y, a.z, a.w, b.x, b.y, b.z, 0};
-        }
-        on_chunk(ch);
+    for (int c = c0, st = 0; c < c1; ++c, st = (st + 1) % HV_WST) {
+        const HvChunk ch = hv.schunk[c];
         mbar_wait(bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
-        hv_segments<NV>(sval(st), sidx(st), soff(st), sblk(st), ch, op, wsum, pt);
-        __syncthreads();   // stage st consumed
-        if (threadIdx.x == 0 && c + HV_STG < c1) issue(c + HV_STG, st);
-    }
-    if (threadIdx.x == 0)
-        for (int k = 0; k < HV_STG; ++k) mbar_inval(bar + k);
-    __syncthreads();
-}
-// chunks [c0, c1) of block b: those starting in its share of the entries (balanced by nonzeros)
-__device__ __forceinline__ int hv_chunk_lb(const HvChunk* chunks, int nch, long long target) {
-    int lo = 0, hi = nch;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if ((long long)__ldg(&chunks[mid].e0) >= target) hi = mid; else lo = mid + 1;
-    }
-    return lo;
-}
-__device__ __forceinline__ int2 hv_my_chunks(const HvChunk* chunks, int nch) {
-    if (nch == 0) return make_int2(0, 0);
-    const long long e0 = __ldg(&chunks[0].e0), e1 = __ldg(&chunks[nch - 1].e1);
-    const long long T = (e1 - e0 + gridDim.x - 1) / gridDim.x;
-    const int c0 = hv_chunk_lb(chunks, nch, e0 + (long long)blockIdx.x * T);
-    const int c1 = blockIdx.x + 1 == gridDim.x ? nch : hv_chunk_lb(chunks, nch, e0 + (long long)(blockIdx.x + 1) * T);
-    return make_int2(c0, c1);
-}
-
-// S: row sums of the heavy entries times s_H (and z_H = s_H on the zeroing columns): Xh[row]
-template <int NV> struct HvOpS {
-    double* Xh; double* Xhz;
-    __device__ __forceinline__ void prod(uint32_t h, float x, double (&p)[NV]) const {
-        h &= HV_HMAX - 1;   // (entries outside the chunk hold stale indices; their products are discarded)
-        const double v = (double)x * reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF)[h];
-        p[0] = v;
-        if constexpr (NV == 2)
-            p[1] = ((reinterpret_cast<const uint32_t*>(hv_dyn + HV_ZH_OFF)[h >> 5] >> (h & 31)) & 1u) ? v : 0.0;
-    }
-    __device__ __forceinline__ void fma(uint32_t h, float x, double (&a)[NV]) const {
-        const double s = reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF)[h];
-        a[0] = ::fma((double)x, s, a[0]);
-        if constexpr (NV == 2) {
-            const bool z = (reinterpret_cast<const uint32_t*>(hv_dyn + HV_ZH_OFF)[h >> 5] >> (h & 31)) & 1u;
-            a[1] = ::fma((double)x, z ? s : 0.0, a[1]);
+        const unsigned char* b = ring + (size_t)st * HV_WSTAGE;
+        const float* sv = reinterpret_cast<const float*>(b);
+        const uint16_t* si = reinterpret_cast<const uint16_t*>(b + (size_t)(HV_WCH + 8) * 4);
+        const int* so = reinterpret_cast<const int*>(b + (size_t)(HV_WCH + 8) * 6);
+        switch (ch.lg) {
+            case 0: hv_rows<NV, 0>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            case 1: hv_rows<NV, 1>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            case 2: hv_rows<NV, 2>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            case 3: hv_rows<NV, 3>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            case 4: hv_rows<NV, 4>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            default: hv_rows<NV, 5>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
         }
+        __syncwarp();   // stage st consumed by every lane
+        if (lane == 0 && c + HV_WST < c1) issue(c + HV_WST, st);
     }
-    __device__ __forceinline__ void out(const HvChunk& ch, int k, const double (&v)[NV]) const {
-        Xh[ch.base + k] = v[0];
-        if constexpr (NV == 2) Xhz[ch.base + k] = v[1];
-    }
-};
-// G: (band, h) sums of the heavy entries times u = D o X sigma of the band: hpart[h nb + band]
-struct HvOpG {
-    double* hpart;
-    int nb;
-    __device__ __forceinline__ void prod(uint32_t r, float x, double (&p)[1]) const {
-        p[0] = (double)x * reinterpret_cast<const double*>(hv_dyn + HV_U_OFF)[r & 4095u];   // (as above)
-    }
-    __device__ __forceinline__ void fma(uint32_t r, float x, double (&a)[1]) const {
-        a[0] = ::fma((double)x, reinterpret_cast<const double*>(hv_dyn + HV_U_OFF)[r], a[0]);
-    }
-    __device__ __forceinline__ void out(const HvChunk& ch, int k, const double (&v)[1]) const {
-        hpart[(size_t)(ch.h0 + k) * nb + ch.base] = v[0];
-    }
-};
+    __syncwarp();
+    if (lane == 0)
+        for (int k = 0; k < HV_WST; ++k) mbar_inval(bar + k);
+    __syncwarp();
+}
 
 // ------------------------------------------------------------------ build kernels (ml_create; X is fixed)
 // histogram of column lengths >= HV_MINLEN (clamped to 65535)
@@ -410,7 +242,7 @@ __global__ void k_hv_hid(int n, int* hid) {
 __global__ void k_hv_hid_set(const int* hcols, int nh, int* hid) {
     for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += gridDim.x * blockDim.x) hid[hcols[h]] = h;
 }
-// S copy: heavy entries per row (cnt), their maximum
+// heavy entries per row (cnt), their maximum
 __global__ void k_hv_rowcnt(const int* rowptr, const int* col, int m, const int* hid, int* cnt, int* maxcnt) {
     int mx = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
@@ -422,114 +254,29 @@ __global__ void k_hv_rowcnt(const int* rowptr, const int* col, int m, const int*
     mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)mx);
     if ((threadIdx.x & 31) == 0) atomicMax(maxcnt, mx);
 }
-// S chunks: runs of whole rows with at most HV_CHMAX heavy entries and HV_SMAX rows (a chunk starts where hrp
-// crosses a multiple of chp = HV_CHMAX - the longest row, or at a multiple of HV_SMAX rows); flag[r] = 1 at a chunk's
-// first row (flag[m] = 0), exclusive-scanned in place to each row's chunk index
-__device__ __forceinline__ int hv_tile_flag(const int* hrp, int r, int chp) {
-    return r == 0 || hrp[r] / chp != hrp[r - 1] / chp || (r / HV_SMAX) != ((r - 1) / HV_SMAX);
+// warp chunks (built greedily on the host): whole rows, at most HV_WCH heavy entries and HV_WROWS rows
+__host__ __device__ __forceinline__ int hv_lg(int rows) {   // groups of L = 32 / (rows rounded up to 2^k) lanes
+    int lg = 5;
+    while (lg > 0 && (32 >> lg) < rows) --lg;
+    return lg;
 }
-__global__ void k_hv_tileflags(const int* hrp, int m, int chp, int* flag) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= m; r += gridDim.x * blockDim.x)
-        flag[r] = r < m ? hv_tile_flag(hrp, r, chp) : 0;
-}
-// a chunk of segments longer than 512 entries on average is reduced by the whole block, segment by segment
-// (HV_LGBLK); the others by per-thread ranges
-__host__ __device__ __forceinline__ int hv_lg(int entries, int segs) {
-    const int mean = segs > 0 ? entries / segs : 0;
-    return mean > 512 ? HV_LGBLK : 0;
-}
-__global__ void k_hv_tiles(const int* hrp, int m, int chp, const int* tidx, HvChunk* sch) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
-        if (!hv_tile_flag(hrp, r, chp)) continue;
-        int r1 = r + 1;   // the next chunk's first row (or m)
-        while (r1 < m && !hv_tile_flag(hrp, r1, chp)) ++r1;
-        sch[tidx[r]] = HvChunk{hrp[r], hrp[r1], r, r, r1 - r, hv_lg(hrp[r1] - hrp[r], r1 - r), 0, 0};
-    }
-}
-// the S copy's entries of each row (swizzled: hv_phys_v / hv_phys_i)
+// the S copy's entries of each row, rotated by a hash of the row: the rows' entries are in column order, so the
+// heaviest columns would otherwise sit at the same place in every row and the s_H gathers of the rows a warp reads
+// together would hit the same shared-memory banks
 __global__ void k_hv_rowfill(const int* rowptr, const int* col, const float* val, int m, const int* hid, const int* hrp,
                              float* sval, uint16_t* sidx) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        long long o = hrp[i];
+        const int o = hrp[i], L = hrp[i + 1] - o;
+        if (L == 0) continue;
+        int q = (int)(((unsigned)i * 2654435761u) >> 8) % L;
         for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
             const int h = __ldg(hid + col[k]);
-            if (h >= 0) { sval[hv_phys_v(o)] = val[k]; sidx[hv_phys_i(o)] = (uint16_t)h; ++o; }
-        }
-    }
-}
-// per chunk and 16-entry block of its stage: the chunk's segment holding the block's first entry (a thread per
-// block; blocks past the chunk get any valid index)
-__global__ void k_hv_blocks(const HvChunk* ch, int nch, const int* off, uint16_t* blk) {
-    const long long N = (long long)nch * 256;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-        const HvChunk c = ch[i >> 8];
-        const int t = (int)(i & 255);
-        const int eb = c.e0 & ~15;
-        const int lo = max(eb + 16 * t, c.e0);
-        int k = 0, kh = c.ns - 1;
-        while (k < kh) {
-            const int mid = (k + kh + 1) >> 1;
-            if (off[c.s0 + mid] <= lo) k = mid; else kh = mid - 1;
-        }
-        blk[i] = (uint16_t)k;
-    }
-}
-// G copy: segment (band k, heavy h) lengths by binary search in the column's ascending rows
-__device__ __forceinline__ int hv_lower(const int* row, int b, int e, int x) {
-    while (b < e) { const int mid = (b + e) >> 1; if (row[mid] >= x) e = mid; else b = mid + 1; }
-    return b;
-}
-__global__ void k_hv_segcnt(const int* colptr, const int* row, const int* hcols, int nh, int nb, int m, int* cnt) {
-    const long long N = (long long)nh * nb;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
-        const int k = (int)(t / nh), h = (int)(t % nh);
-        const int j = hcols[h], b = colptr[j], e = colptr[j + 1];
-        const int lo = hv_lower(row, b, e, k * HV_RB), hi = hv_lower(row, b, e, min(m, (k + 1) * HV_RB));
-        cnt[t] = hi - lo;
-    }
-}
-__global__ void k_hv_segfill(const int* colptr, const int* row, const float* val, const int* hcols, int nh, int nb,
-                             const int* off, float* gval, uint16_t* gidx) {   // a warp per segment (swizzled copy)
-    const long long N = (long long)nh * nb;
-    const int lane = threadIdx.x & 31;
-    for (long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < N;
-         t += ((long long)gridDim.x * blockDim.x) >> 5) {
-        const int o = off[t], L = off[t + 1] - o;
-        if (L == 0) continue;
-        const int k = (int)(t / nh), h = (int)(t % nh);
-        const int j = hcols[h];
-        const int lo = hv_lower(row, colptr[j], colptr[j + 1], k * HV_RB);
-        for (int q = lane; q < L; q += 32) {
-            gval[hv_phys_v((long long)o + q)] = val[lo + q];
-            gidx[hv_phys_i((long long)o + q)] = (uint16_t)(row[lo + q] - k * HV_RB);
-        }
-    }
-}
-// G chunks: whole segments of one band, greedily packed up to HV_CHMAX entries and HV_SMAX heavy ids (a thread per
-// band; a chunk's ids [h0, h1) start and end at non-empty segments).  Pass 0 counts each band's chunks, pass 1 writes
-// them from choff[band].
-__global__ void k_hv_chunks(const int* off, int nh, int nb, int pass, int* nch, const int* choff, HvChunk* gch) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += gridDim.x * blockDim.x) {
-        const int* o = off + (size_t)k * nh;
-        int cs = 0, cl = 0, h0 = -1, h1 = 0, nc = 0;
-        int wc = pass ? choff[k] : 0;
-        for (int h = 0; h < nh; ++h) {
-            const int L = o[h + 1] - o[h];
-            if (L == 0) continue;
-            if (h0 >= 0 && (cl + L > HV_CHMAX || h + 1 - h0 > HV_SMAX)) {
-                if (pass) gch[wc++] = HvChunk{cs, cs + cl, k, k * nh + h0, h1 - h0, hv_lg(cl, h1 - h0), h0, 0};
-                ++nc;
-                h0 = -1;
+            if (h >= 0) {
+                sval[o + q] = val[k];
+                sidx[o + q] = (uint16_t)h;
+                q = q + 1 == L ? 0 : q + 1;
             }
-            if (h0 < 0) { h0 = h; cs = o[h]; cl = 0; }
-            cl += L;
-            h1 = h + 1;
         }
-        if (h0 >= 0) {
-            if (pass) gch[wc++] = HvChunk{cs, cs + cl, k, k * nh + h0, h1 - h0, hv_lg(cl, h1 - h0), h0, 0};
-            ++nc;
-        }
-        if (!pass) nch[k] = nc;
     }
 }
 

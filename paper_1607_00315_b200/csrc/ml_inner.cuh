@@ -414,11 +414,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
     SProducer pr{p0, p0, p1, 0, (int)(S.nnz & ~3LL), col_ext};   // the S-ring producer's state
     int u0 = 0, u1 = 0;   // BIG: my range of column units (balanced by nonzeros across blocks)
     int nU = 0;           // BIG: all units (the S and G streams claim them dynamically, Ctl::s_ctr / g_ctr)
+    int nUS = 0, us0 = 0, us1 = 0;   // BIG: the units of the X_A s stream (heavy mode: the light columns' only)
     // BIG, heavy-column path (ml_heavy.cuh): on for this relaxation when A holds enough of H's nonzeros; then the
-    // heavy columns of A get no column units: their X_A s and H sigma products go through the S / G copies
+    // X_A s products of A's heavy columns come from the S copy (their column units are skipped by the S stream)
     bool hvm = false;
-    long long hv_nz = 0;     // nonzeros of A's heavy columns (the algorithmic count of the heavy passes)
-    int2 hs_rng = make_int2(0, 0), hg_rng = make_int2(0, 0);   // my S tiles / G chunks
+    long long hv_nz = 0;     // nonzeros of A's heavy columns (the algorithmic count of the heavy pass)
     if constexpr (BIG) {
         const bool hvb = HVP && P.hv.on != 0;
         int nu_loc = 0, nz_loc = 0, nu_l = 0, nz_l = 0;
@@ -438,100 +438,129 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         if (hvb) {   // no heavy column of A has a coefficient yet (D writes those of A's)
             for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX; i += G * blockDim.x) P.hv.sH[i] = 0.0;
             for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX / 32; i += G * blockDim.x) P.hv.zH[i] = 0u;
-            hs_rng = hv_my_chunks(P.hv.schunk, P.hv.nts);
-            hg_rng = hv_my_chunks(P.hv.gchunk, P.hv.ncg);
         }
         {
             const double v[5] = {(double)nu_loc, (double)nz_loc, (double)nu_l, (double)nz_l, nzh};
             ir_block_partials<5>(v, 0u, 0u, sh_w, part, IR_SU);
         }
         grid.sync();
-        __shared__ long long s_uoff[5];
-        if (wid == 0) {   // the heavy decision; my offsets in the unit and nonzero sequences, and their totals
+        // unit sequence: the light columns' units first, then (heavy mode) the heavy columns' (the X_A s stream
+        // covers only the first part; the H sigma stream all); each part in position order
+        __shared__ long long s_uoff[10];
+        if (wid == 0) {   // the heavy decision; my offsets in both parts of the unit and cost sequences, their totals
             double hz = 0.0;
             for (int b = lane; b < G; b += 32) hz += ld_cg(part + (size_t)(IR_SU + 4) * G + b);
             hz = warp_sum(hz);   // (integers below 2^53: exact in any order)
             const bool on = hvb && (P.hv.mode == 1 || (P.hv.mode == 0 && hz >= P.hv.frac * (double)P.hv.nnzh)) && hz > 0.0;
-            const int su = on ? IR_SU + 2 : IR_SU;
-            long long off = 0, tot = 0, zoff = 0, ztot = 0;
+            long long off[2] = {0, 0}, tot[2] = {0, 0}, zoff[2] = {0, 0}, ztot[2] = {0, 0};
             for (int b0 = 0; b0 < G; b0 += 32) {
                 const int b = b0 + lane;
-                const long long x = b < G ? (long long)ld_cg(part + (size_t)su * G + b) : 0;
-                const long long z = b < G ? (long long)ld_cg(part + (size_t)(su + 1) * G + b) : 0;
-                off += __reduce_add_sync(0xffffffffu, (unsigned)(b < (int)blockIdx.x ? x : 0));
-                tot += __reduce_add_sync(0xffffffffu, (unsigned)x);
-                zoff += warp_sum_ll(b < (int)blockIdx.x ? z : 0);
-                ztot += warp_sum_ll(z);
+                const long long xa = b < G ? (long long)ld_cg(part + (size_t)IR_SU * G + b) : 0;
+                const long long za = b < G ? (long long)ld_cg(part + (size_t)(IR_SU + 1) * G + b) : 0;
+                const long long xl = !on ? xa : b < G ? (long long)ld_cg(part + (size_t)(IR_SU + 2) * G + b) : 0;
+                const long long zl = !on ? za : b < G ? (long long)ld_cg(part + (size_t)(IR_SU + 3) * G + b) : 0;
+                const long long x[2] = {xl, xa - xl}, z[2] = {zl, za - zl};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    off[h] += warp_sum_ll(b < (int)blockIdx.x ? x[h] : 0);
+                    tot[h] += warp_sum_ll(x[h]);
+                    zoff[h] += warp_sum_ll(b < (int)blockIdx.x ? z[h] : 0);
+                    ztot[h] += warp_sum_ll(z[h]);
+                }
             }
-            if (lane == 0) { s_uoff[0] = off; s_uoff[1] = tot; s_uoff[2] = zoff; s_uoff[3] = ztot; s_uoff[4] = on ? (long long)hz : -1; }
+            if (lane == 0) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) { s_uoff[4 * h] = off[h]; s_uoff[4 * h + 1] = tot[h]; s_uoff[4 * h + 2] = zoff[h]; s_uoff[4 * h + 3] = ztot[h]; }
+                s_uoff[8] = on ? (long long)hz : -1;
+            }
         }
         __syncthreads();
-        hvm = s_uoff[4] >= 0;
-        hv_nz = hvm ? s_uoff[4] : 0;
+        hvm = s_uoff[8] >= 0;
+        hv_nz = hvm ? s_uoff[8] : 0;
         if (hvm && blockIdx.x == 0 && threadIdx.x == 0) c->hv_relax += 1;
-        int base = (int)s_uoff[0];
-        long long zbase = s_uoff[2];
-        const int NU = (int)s_uoff[1];
-        const long long NZ = s_uoff[3];
+        const int NUL = (int)s_uoff[1];                 // units of the first (light) part
+        const long long NZL = s_uoff[3];
+        const int NU = NUL + (int)s_uoff[5];
+        const long long NZ = NZL + s_uoff[7];
+        int base[2] = {(int)s_uoff[0], NUL + (int)s_uoff[4]};
+        long long zbase[2] = {s_uoff[2], NZL + s_uoff[6]};
         for (int k00 = 0; k00 < q0; k00 += blockDim.x) {   // my positions in order: their units
             const int k = k00 + threadIdx.x;
-            int b = 0, e = 0, nu = 0;
-            if (k < q0 && !(hvm && P.hv.phid[p0 + k] >= 0)) {   // (heavy columns of A: no units in heavy mode)
+            int b = 0, e = 0, nu = 0, hp = 0;
+            if (k < q0) {
                 if (k < IR_QC) { b = col_ext[k].x; e = col_ext[k].y; }
                 else { const int j = __ldg(S.list + p0 + k); b = __ldg(S.ptr + j); e = __ldg(S.ptr + j + 1); }
                 nu = max(1, (e - b + IR_UNIT - 1) / IR_UNIT);
+                hp = (hvm && P.hv.phid[p0 + k] >= 0) ? 1 : 0;
             }
-            int incl = nu;
-            long long zincl = (long long)(e - b) + (long long)IR_UCOST * nu;
+            const long long cost = (long long)(e - b) + (long long)IR_UCOST * nu;
+            int incl[2] = {hp ? 0 : nu, hp ? nu : 0};
+            long long zincl[2] = {hp ? 0 : cost, hp ? cost : 0};
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                const long long tz = __shfl_up_sync(0xffffffffu, zincl, o);
-                if (lane >= o) { incl += t; zincl += tz; }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl[h], o);
+                    const long long tz = __shfl_up_sync(0xffffffffu, zincl[h], o);
+                    if (lane >= o) { incl[h] += t; zincl[h] += tz; }
+                }
             }
-            __shared__ int s_wsum[IR_W];
-            __shared__ long long s_zsum[IR_W];
-            if (lane == 31) { s_wsum[wid] = incl; s_zsum[wid] = zincl; }
+            __shared__ int s_wsum[2][IR_W];
+            __shared__ long long s_zsum[2][IR_W];
+            if (lane == 31) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) { s_wsum[h][wid] = incl[h]; s_zsum[h][wid] = zincl[h]; }
+            }
             __syncthreads();
-            int woff = 0, wtot = 0;
-            long long zwoff = 0, zwtot = 0;
+            int woff[2] = {0, 0}, wtot[2] = {0, 0};
+            long long zwoff[2] = {0, 0}, zwtot[2] = {0, 0};
             for (int w = 0; w < IR_W; ++w) {
-                if (w < wid) { woff += s_wsum[w]; zwoff += s_zsum[w]; }
-                wtot += s_wsum[w];
-                zwtot += s_zsum[w];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (w < wid) { woff[h] += s_wsum[h][w]; zwoff[h] += s_zsum[h][w]; }
+                    wtot[h] += s_wsum[h][w];
+                    zwtot[h] += s_zsum[h][w];
+                }
             }
             if (k < q0) {
-                const int us = base + woff + incl - nu;
-                const long long zs0 = zbase + zwoff + zincl - ((long long)(e - b) + (long long)IR_UCOST * nu);
+                const int us = base[hp] + woff[hp] + incl[hp] - nu;
+                const long long zs0 = zbase[hp] + zwoff[hp] + zincl[hp] - cost;
                 P.ustart[p0 + k] = us;
+                P.uend[p0 + k] = us + nu;
                 for (int c2 = 0; c2 < nu; ++c2) {
                     P.uext[us + c2] = make_int2(b + c2 * IR_UNIT, min(e, b + (c2 + 1) * IR_UNIT));
                     P.upos[us + c2] = p0 + k;
                     P.unz[us + c2] = zs0 + (long long)c2 * (IR_UNIT + IR_UCOST);   // weighted cost before this unit
                 }
             }
-            base += wtot;
-            zbase += zwtot;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) { base[h] += wtot[h]; zbase[h] += zwtot[h]; }
             __syncthreads();
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) { P.ustart[nA] = NU; P.unz[NU] = NZ; c->s_ctr = 0u; c->g_ctr = 0u; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { P.unz[NU] = NZ; c->s_ctr = 0u; c->g_ctr = 0u; }
         grid.sync();
         nU = NU;
-        if (threadIdx.x == 0) {   // my units: those starting in my share [b T, (b+1) T) of the nonzeros
-            const long long T = (NZ + G - 1) / G;
-            for (int h = 0; h < 2; ++h) {
-                const long long target = (long long)(blockIdx.x + h) * T;
-                int lo = 0, hi = NU;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (ld_cg(P.unz + mid) >= target) hi = mid; else lo = mid + 1;
+        nUS = NUL;
+        if (threadIdx.x == 0) {   // my units: those starting in my share [b T, (b+1) T) of the costs (S: of the first part)
+            for (int q = 0; q < 2; ++q) {
+                const int n_ = q ? NUL : NU;
+                const long long T = ((q ? NZL : NZ) + G - 1) / G;
+                for (int h = 0; h < 2; ++h) {
+                    const long long target = (long long)(blockIdx.x + h) * T;
+                    int lo = 0, hi = n_;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (ld_cg(P.unz + mid) >= target) hi = mid; else lo = mid + 1;
+                    }
+                    s_uoff[2 * q + h] = (blockIdx.x + h == G) ? n_ : lo;
                 }
-                s_uoff[h] = (blockIdx.x + h == G) ? NU : lo;
             }
         }
         __syncthreads();
         u0 = (int)s_uoff[0];
         u1 = (int)s_uoff[1];
+        us0 = (int)s_uoff[2];
+        us1 = (int)s_uoff[3];
     }
     for (int it = 0; it < K; ++it) {
         pcd = next_pcd;
@@ -643,15 +672,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 #ifdef IR_HVDBG
                 const unsigned long long hv_t0 = gtimer();
 #endif
-                if (hvz) {
-                    HvOpS<2> op{P.hv.Xh, P.hv.Xhz};
-                    hv_stream<2>(P.hv.schunk, hs_rng.x, hs_rng.y, P.hv.sval, P.hv.sidx, P.hv.soff, P.hv.sblk, HV_SRING_OFF, op,
-                                 [](const HvChunk&) {});
-                } else {
-                    HvOpS<1> op{P.hv.Xh, P.hv.Xhz};
-                    hv_stream<1>(P.hv.schunk, hs_rng.x, hs_rng.y, P.hv.sval, P.hv.sidx, P.hv.soff, P.hv.sblk, HV_SRING_OFF, op,
-                                 [](const HvChunk&) {});
-                }
+                if (hvz) hv_sweep<2>(P.hv);
+                else hv_sweep<1>(P.hv);
+                __syncthreads();   // (the rings' shared memory is reused by the column stream below)
                 if (blockIdx.x == 0 && threadIdx.x == 0) nsc += hv_nz;
 #ifdef IR_HVDBG   // (block 0's heavy S time in slot 0, heavy G time in slot 1: the small-|A| D / S slots)
                 if (blockIdx.x == 0 && threadIdx.x == 0) ph_acc[0] += gtimer() - hv_t0;
@@ -666,12 +689,12 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             ColStream<GSCH, GST> cs;
             cs.streamed = 0;
             cs.segs = 0;
-            if (nU >= IR_DYN * G * IR_W || P.dyn) {   // many units per warp: dynamic claims (no block waits on another
-                                                       // at B1)
+            if (nUS >= IR_DYN * G * IR_W || P.dyn) {   // many units per warp: dynamic claims (no block waits on another
+                                                        // at B1)
                 cs.claim = &c->s_ctr;
-                stream_begin(cs, S, nullptr, 0, nU, gbase, P.uext, nU);
+                stream_begin(cs, S, nullptr, 0, nUS, gbase, P.uext, nUS);
             } else {
-                stream_begin(cs, S, nullptr, u0, u1, gbase, P.uext + u0, u1 - u0);
+                stream_begin(cs, S, nullptr, us0, us1, gbase, P.uext + us0, us1 - us0);
             }
             int stg = 0;
             while (true) {
@@ -1148,77 +1171,15 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             __syncwarp();
             if (lane == 0)
                 for (int k = 0; k < GST; ++k) mbar_inval(g_bar + k);
-            if constexpr (HVP) if (hvm) {   // heavy columns: u = D o X sigma of a band in shared memory, the G copy's (band, h) sums
-                __syncthreads();   // (the column rings are drained: their shared memory is free)
-                double* us = reinterpret_cast<double*>(smraw + HV_U_OFF);
-                HvOpG op{P.hv.hpart, P.hv.nb};
-                int cur = -1;
-                const double b1 = 1.0 - beta;
-#ifdef IR_HVDBG
-                const unsigned long long hv_t0 = gtimer();
-#endif
-                hv_stream<1>(P.hv.gchunk, hg_rng.x, hg_rng.y, P.hv.gval, P.hv.gidx, P.hv.goff, P.hv.gblk, HV_GRING_OFF, op,
-                                     [&](const HvChunk& ch) {
-                                         if (ch.base == cur) return;
-                                         __syncthreads();
-                                         cur = ch.base;
-                                         const int rb0 = cur * HV_RB;
-                                         for (int i = threadIdx.x; i < HV_RB; i += blockDim.x) {
-                                             const int r = rb0 + i;
-                                             double v = 0.0;
-                                             if (r < m) {
-                                                 v = beta * ld_cg(P.sv + r);
-                                                 if (zs) v += b1 * ld_cg(P.svz + r);
-                                             }
-                                             us[i] = v;
-                                         }
-                                         __syncthreads();
-                                     });
-                if (blockIdx.x == 0 && threadIdx.x == 0) nhs += hv_nz;
-#ifdef IR_HVDBG
-                if (blockIdx.x == 0 && threadIdx.x == 0) ph_acc[1] += gtimer() - hv_t0;
-#endif
-            }
 #ifdef IR_BLKDBG
             __syncthreads();
             bd_g += gtimer() - bd_t0;
 #endif
             grid.sync();   // every unit's partial
             if (blockIdx.x == 0 && threadIdx.x == 0) c->g_ctr = 0u;
-            if (hvm) {   // my heavy positions: their band partials in band order (a warp each), the step
-                const int nb = P.hv.nb;
-                for (int kb = wid * 32; kb < q0; kb += IR_W * 32) {
-                    const int k = kb + lane;
-                    const int h = k < q0 ? P.hv.phid[p0 + k] : -1;
-                    unsigned msk = __ballot_sync(0xffffffffu, h >= 0);
-                    while (msk) {
-                        const int src = __ffs(msk) - 1;
-                        msk &= msk - 1;
-                        const int hh = __shfl_sync(0xffffffffu, h, src);
-                        const double* hp = P.hv.hpart + (size_t)hh * nb;
-                        double t = 0.0;
-                        for (int b0 = lane; b0 < nb; b0 += 256) {
-                            double x[8];
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) x[u] = b0 + 32 * u < nb ? ld_cg(hp + b0 + 32 * u) : 0.0;
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) t += x[u];
-                        }
-                        t = warp_sum(t);
-                        if (lane == src) {
-                            const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;
-                            const double x = X.wA[k] + X.d[k];
-                            const bool kink = ksnap && x * sp < 0.0 && -x / sp == bk;
-                            X.Hd[k] += t + P.eps_h * ((zp != 0.0) ? zp : beta * sp);
-                            X.d[k] = (zp != 0.0 || kink) ? -X.wA[k] : X.d[k] + beta * sp;
-                        }
-                    }
-                }
-            }
             for (int k = threadIdx.x; k < q0; k += blockDim.x) {   // my columns: partials in unit order, the step
                 const int p = p0 + k;
-                const int ua = ld_cg(P.ustart + p), ub = ld_cg(P.ustart + p + 1);
-                if (hvm && ua == ub) continue;   // (a heavy column: done above)
+                const int ua = ld_cg(P.ustart + p), ub = ld_cg(P.uend + p);
                 double t = 0.0, tz = 0.0;
                 for (int u = ua; u < ub; ++u) { const double2 q2 = ld_cg(P.upart + u); t += q2.x; tz += q2.y; }
                 const double sp = X.s[k], zp = zs ? X.u[k] : 0.0;

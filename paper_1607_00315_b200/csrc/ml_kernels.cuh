@@ -308,7 +308,7 @@ struct Prm {
     double* Xz; double* svz; double* Xzu;             // snap path: X_A z, D o Xz; Xzu: atomic scatter target of z (kept zero)
     double* parts; int nparts;                        // small-m scatter: per-block partials (+ group partials)
     double* irpart;                                   // persistent inner solver: slot-major block partials
-    int2* uext; int* upos; double2* upart; int* ustart; long long* unz;   // its column units (m > SMALL_M)
+    int2* uext; int* upos; double2* upart; int* ustart; int* uend; long long* unz;   // its column units (m > SMALL_M)
     Ctl* ctl;
     double* part;              // reduction partials
     double2* tilepart;         // per-tile partials of the compaction kernels

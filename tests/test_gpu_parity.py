@@ -839,8 +839,8 @@ def _sparse_big():
 @pytest.mark.parametrize("name,opts", [("cfg4s", {}), ("cfg4s", {"inner_cg": 0}), ("cfg4s", {"inner_cg": 1, "pcd_snap": 0}),
                                        ("lasso4s", {}), ("sparse_big", {}), ("cfg4s", {"continuation": 1})])
 def test_heavy_path_parity(name, opts):
-    """The large-m heavy-column path (ml_heavy.cuh: X_A s and H sigma of the longest columns from their row-major and
-    band copies, DESIGN 8.2) forced in every relaxation (ml_set_engine bit 4) against the oracle: the same
+    """The large-m heavy-column path (ml_heavy.cuh: X_A s of the longest columns from their row-major copy without
+    atomics, DESIGN 8.2) forced in every relaxation (ml_set_engine bit 4) against the oracle: the same
     relaxation decisions (level, |A|, outcome, inner iterations) and F after each of the first relaxations to 1e-9,
     the final F to 1e-6 and the support outside the band."""
     ds = _sparse_big() if name == "sparse_big" else dataset(name)
@@ -872,8 +872,8 @@ def test_heavy_path_parity(name, opts):
 
 @pytest.mark.parametrize("flags", [16, 24, 32])
 def test_heavy_path_bitwise_reproducible(flags):
-    """Heavy path on (16; with dynamic unit claims 24) or off (32): every heavy sum has a fixed order (segmented
-    chunk reductions, band partials in band order), so two contexts solving cfg4s give identical bits."""
+    """Heavy path on (16; with dynamic unit claims 24) or off (32): every heavy row sum has a fixed order (groups of
+    lanes per row, a fixed shuffle tree), so two contexts solving cfg4s give identical bits."""
     ds = dataset("cfg4s")
     out = []
     for rep in range(2):

@@ -1,0 +1,195 @@
+// Heavy-path S pass with warp-private chunks (experiment): every warp streams its own chunks of whole rows (<= 512
+// heavy entries) through a private 3-stage TMA ring and reduces them with groups of 4 lanes per row; no block
+// barriers.  Synthetic cfg-5-shaped S copy (2e6 rows, Poisson(65) heavy entries per row, 8192 heavy ids).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o hvwarp hvwarp.cu
+#include <cstdio>
+#include <vector>
+#include <random>
+#include <algorithm>
+#include <cmath>
+#include "../../paper_1607_00315_b200/csrc/ml_heavy.cuh"
+using namespace ml;
+
+struct WChunk { int e0, e1, r0, nr; };
+
+// the library's sweep (ml_heavy.cuh: hv_sweep) on the same data
+__global__ void __launch_bounds__(256, 1) k_lib(HvPrm hv, const double* sH) {
+    double* s = reinterpret_cast<double*>(hv_dyn);
+    for (int i = threadIdx.x; i < HV_HMAX; i += blockDim.x) s[i] = sH[i];
+    __syncthreads();
+    hv_sweep<1>(hv);
+}
+
+template <int LG, bool GATHER, int WCH, int WST, int WROWS>
+__global__ void __launch_bounds__(256, 1) k_warp(const WChunk* ch, int nch, const float* gv, const uint16_t* gi,
+                                                 const int* rp, const double* sH, double* Xh) {
+    constexpr int WSTAGE16 = ((WCH + 16) * 6 + (WROWS + 8) * 4 + 15) / 16 * 16;
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* s = reinterpret_cast<double*>(sm);
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x) s[i] = sH[i];
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = sm + 65536 + (size_t)w * (WST * WSTAGE16 + 64);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ring + WST * WSTAGE16);
+    const int gw = blockIdx.x * 8 + w, NW = gridDim.x * 8;
+    const int c0 = (int)((long long)nch * gw / NW), c1 = (int)((long long)nch * (gw + 1) / NW);
+    auto issue = [&](int c, int st) {
+        const WChunk k = ch[c];
+        const int a0 = k.e0 & ~7, a1 = (k.e1 + 7) & ~7;
+        const int o0 = k.r0 & ~3, o1 = (k.r0 + k.nr + 1 + 3) & ~3;
+        unsigned char* b = ring + st * WSTAGE16;
+        mbar_arrive_expect_tx(bar + st, 6u * (a1 - a0) + 4u * (o1 - o0));
+        bulk_g2s(b, gv + a0, 4u * (a1 - a0), bar + st);
+        bulk_g2s(b + (WCH + 16) * 4, gi + a0, 2u * (a1 - a0), bar + st);
+        bulk_g2s(b + (WCH + 16) * 6, rp + o0, 4u * (o1 - o0), bar + st);
+    };
+    if (lane == 0) {
+        for (int k = 0; k < WST; ++k) mbar_init(bar + k, 1);
+        fence_mbar_init();
+        for (int k = 0; k < WST && c0 + k < c1; ++k) issue(c0 + k, k);
+    }
+    __syncwarp();
+    constexpr int L = 1 << LG, NG = 32 >> LG;
+    const int grp = lane >> LG, gl = lane & (L - 1);
+    uint32_t phase = 0;
+    for (int c = c0, st = 0; c < c1; ++c, st = (st + 1) % WST) {
+        const WChunk k = ch[c];
+        mbar_wait(bar + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const unsigned char* b = ring + st * WSTAGE16;
+        const float* sv = reinterpret_cast<const float*>(b);
+        const uint16_t* si = reinterpret_cast<const uint16_t*>(b + (WCH + 16) * 4);
+        const int* so = reinterpret_cast<const int*>(b + (WCH + 16) * 6);
+        const int eb = k.e0 & ~7, ob = k.r0 & 3;
+        for (int r = grp; r - grp < k.nr; r += NG) {
+            double acc = 0.0;
+            int e0 = 0, e1 = 0;
+            if (r < k.nr) { e0 = so[ob + r] - eb; e1 = so[ob + r + 1] - eb; }
+            for (int i = e0 + gl; i < e1; i += 8 * L) {
+                float x[8];
+                uint32_t ix[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const bool ok = i + u * L < e1;
+                    x[u] = ok ? sv[i + u * L] : 0.0f;
+                    ix[u] = ok ? si[i + u * L] : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i + u * L < e1) acc = fma((double)x[u], GATHER ? s[ix[u]] : 1.0, acc);
+            }
+#pragma unroll
+            for (int d = L >> 1; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+            if (gl == 0 && r < k.nr) Xh[k.r0 + r] = acc;
+        }
+        __syncwarp();
+        if (lane == 0 && c + WST < c1) issue(c + WST, st);
+    }
+}
+
+template <int LG, bool GATHER, int WCH, int WST, int WROWS>
+void run(const WChunk* ch, int nch, const float* v, const uint16_t* k, const int* rp, const double* sH, double* Xh,
+         long long E, int sms) {
+    auto kf = k_warp<LG, GATHER, WCH, WST, WROWS>;
+    constexpr int WSTAGE16 = ((WCH + 16) * 6 + (WROWS + 8) * 4 + 15) / 16 * 16;
+    const size_t smem = 65536 + 8 * (WST * WSTAGE16 + 64);
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        kf<<<sms, 256, smem>>>(ch, nch, v, k, rp, sH, Xh);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    printf("WCH %d WST %d WROWS %d chunks %d: L %d gather %d: %.3f ms, %.0f GB/s (6 B per entry), err %s\n", WCH, WST, WROWS, nch, 1 << LG, (int)GATHER, best, 6.0 * E / best / 1e6,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
+int main(int argc, char** argv) {
+    const int m = 2000000;
+    const int rowlen = argc > 1 ? atoi(argv[1]) : 65;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    std::mt19937 rng(1);
+    std::vector<int> rp(m + 8, 0);
+    std::poisson_distribution<int> pois(rowlen);
+    for (int i = 0; i < m; ++i) rp[i + 1] = rp[i] + std::min(pois(rng), 500);
+    for (int i = m + 1; i < m + 8; ++i) rp[i] = rp[m];
+    const long long E = rp[m];
+    std::vector<float> v(E + 16, 1.0f);
+    std::vector<uint16_t> k(E + 16, 0);
+    const bool zipf = argc > 2 && atoi(argv[2]) != 0;   // heavy ids drawn Zipf(1.1) like cfg 5's (id = length rank)
+    std::vector<double> cdf(8192);
+    { double a = 0; for (int h = 0; h < 8192; ++h) { a += std::pow(h + 1.0, -1.1); cdf[h] = a; } for (auto& x : cdf) x /= a; }
+    std::uniform_real_distribution<double> U(0.0, 1.0);
+    for (long long e = 0; e < E; ++e)
+        k[e] = zipf ? (uint16_t)(std::lower_bound(cdf.begin(), cdf.end(), U(rng)) - cdf.begin()) : (uint16_t)(rng() % 8192);
+    WChunk* dch; float* dv; uint16_t* dk; int* drp; double *dsH, *dXh;
+    cudaMalloc(&dch, (size_t)m * sizeof(WChunk));
+    cudaMalloc(&dv, v.size() * 4);
+    cudaMalloc(&dk, k.size() * 2);
+    cudaMalloc(&drp, rp.size() * 4);
+    cudaMalloc(&dsH, 8192 * 8);
+    cudaMalloc(&dXh, (size_t)m * 8);
+    cudaMemcpy(dv, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dk, k.data(), k.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(drp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemset(dsH, 0, 8192 * 8);
+    auto chunks = [&](int wch, int wrows) {
+        std::vector<WChunk> ch;
+        for (int r = 0; r < m;) {
+            const int r0 = r;
+            while (r < m && rp[r + 1] - rp[r0] <= wch && r - r0 < wrows) ++r;
+            if (r == r0) ++r;
+            ch.push_back(WChunk{rp[r0], rp[r], r0, r - r0});
+        }
+        cudaMemcpy(dch, ch.data(), ch.size() * sizeof(WChunk), cudaMemcpyHostToDevice);
+        return (int)ch.size();
+    };
+    int nch = chunks(512, 32);
+    run<2, true, 512, 3, 32>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    run<2, true, 512, 2, 32>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    nch = chunks(768, 8);
+    run<2, true, 768, 2, 8>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    run<2, true, 768, 3, 8>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    nch = chunks(1024, 16);
+    run<2, true, 1024, 2, 16>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    run<1, true, 1024, 2, 16>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    nch = chunks(384, 8);
+    run<2, true, 384, 4, 8>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
+    {   // the library's hv_sweep with its own chunking (HV_WCH, HV_WROWS, lg by rows)
+        std::vector<HvChunk> hc;
+        for (int r = 0; r < m;) {
+            const int r0 = r;
+            while (r < m && r - r0 < HV_WROWS && rp[r + 1] - rp[r0] <= HV_WCH) ++r;
+            hc.push_back(HvChunk{rp[r0], rp[r], r0, r - r0, hv_lg(r - r0), 0, 0, 0});
+        }
+        HvChunk* dhc;
+        cudaMalloc(&dhc, hc.size() * sizeof(HvChunk));
+        cudaMemcpy(dhc, hc.data(), hc.size() * sizeof(HvChunk), cudaMemcpyHostToDevice);
+        HvPrm hv{};
+        hv.nts = (int)hc.size(); hv.sval = dv; hv.sidx = dk; hv.soff = drp; hv.schunk = dhc; hv.Xh = dXh; hv.Xhz = dXh;
+        const size_t smem = hv_smem_bytes();
+        cudaFuncSetAttribute(k_lib, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(e0);
+            k_lib<<<sms, 256, smem>>>(hv, dsH);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        printf("library hv_sweep (chunks %zu): %.3f ms, err %s\n", hc.size(), best, cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
