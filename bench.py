@@ -429,6 +429,7 @@ def cpu_baseline(ds, cfg):
 
 
 def _cpu_baseline(ds, cfg, oracle, model, ncpu):
+    import numpy as np
     o = oracle.Oracle(ds)
     host = {"cpu_model": model, "host_cores": ncpu, "pinned": "sched_setaffinity, 1 core"}
     if cfg <= 3:
@@ -441,9 +442,21 @@ def _cpu_baseline(ds, cfg, oracle, model, ncpu):
     t0 = time.perf_counter()
     o.eval_f_grad()   # margins + gradient/diag over all columns: one CSR and one CSC pass
     t = time.perf_counter() - t0
+    # the same oracle's other passes over all of X, once each (per-kernel CPU timings next to the GPU's)
+    kern = {"eval_f_grad (CSR + CSC pass)": {"s": round(t, 3), "GBs": round(8.0 * 2 * ds.nnz / t / 1e9, 4)}}
+    t1 = time.perf_counter()
+    o.diag_hess()
+    t1 = time.perf_counter() - t1
+    kern["diag_hess (CSC pass)"] = {"s": round(t1, 3), "GBs": round(8.0 * ds.nnz / t1 / 1e9, 4)}
+    v = np.random.default_rng(0).standard_normal(ds.n)
+    t2 = time.perf_counter()
+    o.hessvec(None, v)
+    t2 = time.perf_counter() - t2
+    kern["hessvec (two CSC passes)"] = {"s": round(t2, 3), "GBs": round(8.0 * 2 * ds.nnz / t2 / 1e9, 4),
+                                        "hv_per_s": round(1.0 / t2, 4)}
     return {"value": round(8.0 * 2 * ds.nnz / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": "one oracle eval_f_grad (full CSR margins pass + full CSC gather; the full oracle solve of this "
-                      "config takes minutes: tests/golden)", "seconds": round(t, 2), **host}
+                      "config takes minutes: tests/golden)", "seconds": round(t, 2), "kernels": kern, **host}
 
 
 def run_reference(args):
