@@ -29,6 +29,9 @@ constexpr int IR_SCH = 2048;               // S phase: block-shared ring of IR_S
 #ifndef IR_GU
 #define IR_GU 8   // BIG G phase: L2 gathers in flight per lane (multiple of 4)
 #endif
+#ifndef IR_RB
+#define IR_RB 4   // BIG R phase: rows in flight per thread
+#endif
 constexpr int IR_QC = 1024;               // column extents of up to IR_QC own positions cached in shared memory
 // phase timers (block 0, thread 0): 8 phases for small |A| and 8 for large |A|.  Debug builds: IR_PHDBG puts
 // sub-phases of the small-|A| iteration in slots 8..15 (large |A| relaxations are then not timed) and the kernel time
@@ -885,10 +888,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             double a_ss = 0.0, a_sz = 0.0, a_zz = 0.0;
             const int nr = r1 - r0;
             if (BIG) {   // my rows of Xu (Xzu), cleared for the next scatter; sv = D o Xs, svz = D o Xz for the G phase
-                for (int k0 = threadIdx.x; k0 < nr; k0 += 4 * blockDim.x) {
-                    double xu[4], xzu[4], xo[4], dd[4];
+                for (int k0 = threadIdx.x; k0 < nr; k0 += IR_RB * blockDim.x) {
+                    double xu[IR_RB], xzu[IR_RB], xo[IR_RB], dd[IR_RB];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < IR_RB; ++u) {
                         const int k = k0 + u * blockDim.x;
                         const bool in = k < nr;
                         xu[u] = in ? ld_fixed(P.Xu + r0 + k, fqi) + (hvm ? ld_cg(P.hv.Xh + r0 + k) : 0.0) : 0.0;
@@ -898,7 +901,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         dd[u] = in ? P.rD[r0 + k].y : 0.0;
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < IR_RB; ++u) {
                         const int k = k0 + u * blockDim.x;
                         if (k >= nr) break;
                         const double xs = pcd ? xu[u] : xu[u] + bcg * xo[u];
