@@ -108,8 +108,11 @@ __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, con
 // This warp's chunks (an equal share of all warps of the grid, in order) through its private ring.
 // (out of line: called once per S phase, so that its loop gets registers of its own instead of k_inner's spills)
 template <int NV>
-__device__ __noinline__ void hv_sweep(const HvPrm hv) {
+__device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = nullptr) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef IR_HVDBG
+    const unsigned long long t_start = clock64();
+#endif
     unsigned char* ring = hv_dyn + HV_SRING_OFF + (size_t)w * HV_WRING;   // (a shared address the compiler can see)
     uint64_t* bar = reinterpret_cast<uint64_t*>(ring + (size_t)HV_WST * HV_WSTAGE);
     const long long gw = (long long)blockIdx.x * HV_W + w, NW = (long long)gridDim.x * HV_W;
@@ -154,6 +157,14 @@ __device__ __noinline__ void hv_sweep(const HvPrm hv) {
     __syncwarp();
     if (lane == 0)
         for (int k = 0; k < HV_WST; ++k) mbar_inval(bar + k);
+#ifdef IR_HVDBG   // (per-warp sweep cycles: sum, max, count; and the cycles from the first issue to the first stage)
+    if (dbg && lane == 0) {
+        const unsigned long long dt = clock64() - t_start;
+        atomicAdd(dbg, dt);
+        atomicMax(dbg + 1, dt);
+        atomicAdd(dbg + 2, 1ull);
+    }
+#endif
     __syncwarp();
 }
 

@@ -675,8 +675,8 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 #ifdef IR_HVDBG
                 const unsigned long long hv_t0 = gtimer();
 #endif
-                if (hvz) hv_sweep<2>(P.hv);
-                else hv_sweep<1>(P.hv);
+                if (hvz) hv_sweep<2>(P.hv, c->tph + 2);
+                else hv_sweep<1>(P.hv, c->tph + 2);
                 __syncthreads();   // (the rings' shared memory is reused by the column stream below)
                 if (blockIdx.x == 0 && threadIdx.x == 0) nsc += hv_nz;
 #ifdef IR_HVDBG   // (block 0's heavy S time in slot 0, heavy G time in slot 1: the small-|A| D / S slots)

@@ -141,6 +141,13 @@ int main(int argc, char** argv) {
     cudaMemcpy(dk, k.data(), k.size() * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(drp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemset(dsH, 0, 8192 * 8);
+    if (argc > 3 && atoi(argv[3]) != 0) {   // nonzero s_H and X values (the solve's data are not zeros)
+        std::vector<double> sh(8192);
+        for (auto& x : sh) x = U(rng) - 0.5;
+        cudaMemcpy(dsH, sh.data(), 8192 * 8, cudaMemcpyHostToDevice);
+        for (auto& x : v) x = (float)U(rng);
+        cudaMemcpy(dv, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+    }
     auto chunks = [&](int wch, int wrows) {
         std::vector<WChunk> ch;
         for (int r = 0; r < m;) {
