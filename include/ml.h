@@ -172,13 +172,15 @@ ml_status ml_set_sm_share(ml_ctx *c, int blocks);
           waiting on the slowest).
    bit 4: the large-m inner solver takes the heavy-column path (X_A s of the longest columns from their row-major copy,
           without atomics; ml_heavy_info) in every relaxation; bit 6: in the relaxations whose free set holds >= 1/4
-          of their nonzeros; neither: never (the default).  The first request builds the copy (device passes over X,
+          of their nonzeros; bit 5: never; none of them: the context's default, which is bit 6 when X has >= 2^26
+          nonzeros and those columns hold >= 2^26 (the copy is then built by ml_create; measured faster on cfg 5,
+          slower on cfg 3-4), else never.  A first request on a smaller X builds the copy (device passes over X,
           synchronises the stream).  ML_E_INVAL for bit 4 when the context has no heavy path (small m, the longest
           columns hold < 1/10 of X, or a row holds more than 768 of their nonzeros). */
 ml_status ml_set_engine(ml_ctx *c, uint32_t flags);
 /* Diagnostics of the large-m heavy-column path (DESIGN 8.2; off for m <= 8192): info_host[8] = built (0/1), |H|,
    nonzeros of H, warp chunks of its row-major copy, 0, 0 (reserved), relaxations that ran it since ml_create, the
-   mode (0: by the free set's share of H, 1: always, 2: never; ml_set_engine bits 4 / 6). */
+   mode (0: by the free set's share of H, 1: always, 2: never; ml_set_engine bits 4 / 5 / 6). */
 ml_status ml_heavy_info(ml_ctx *c, int64_t *info_host);
 /* Diagnostics: copy up to `cap` relaxation records of the last solve into rows_host (host memory, 48 bytes each:
    int32 level, outcome, inner_iters, nA; int64 nC; double F_before, F_after, alpha); returns the record count. */

@@ -118,7 +118,8 @@ struct ml_ctx {
     int* hv_bsum = nullptr;
     int* hv_misc = nullptr;
     unsigned* hv_hist = nullptr;
-    bool hv_built = false;   // hv_build ran (on the first ml_set_engine request for the heavy path)
+    bool hv_built = false;   // hv_build ran (at ml_create for large X, else on the first ml_set_engine request)
+    int hv_mode0 = 2;        // the heavy path's default mode (0 when built at ml_create for large X, else 2)
 };
 
 namespace {
@@ -188,7 +189,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     int* mp_bsum = cv.take<int>(big ? nn / MP_SCAN + 2 : 1);
     double2* mp_out = cv.take<double2>(big ? nn : 1);
     // heavy-column path of the large-m inner solver (ml_heavy.cuh): the S and G copies of H's nonzeros (at most all
-    // of X's), their chunk tables, band partials, per-row products; build scratch aliases hpart / Xh / Xhz
+    // of X's), its warp chunks, per-row products, the zeroing columns' unit list
     const size_t hvn = big ? (size_t)nnz + 16 : 1;
     HvPrm hv{};
     hv.hid = cv.take<int>(big ? nn : 1);
@@ -200,9 +201,8 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     hv.soff = cv.take<int>(big ? mm + 8 : 1);
     hv.schunk = cv.take<HvChunk>(big ? (size_t)nnz / (HV_WCH / 2) + mm / HV_WROWS + 16 : 1);   // (greedy chunks)
     hv.Xh = cv.take<double>(big ? mm + 2 : 1);
-    hv.Xhz = cv.take<double>(big ? mm + 2 : 1);
     hv.sH = cv.take<double>(HV_HMAX);
-    hv.zH = cv.take<uint32_t>(HV_HMAX / 32);
+    hv.zunits = cv.take<int>(ucap2);
     int* hv_bsum = cv.take<int>(big ? std::max(nn, mm + 1) / 1024 + 64 : 1);
     int* hv_misc = cv.take<int>(64);
     unsigned* hv_hist = cv.take<unsigned>(big ? 65536 : 1);
@@ -805,13 +805,15 @@ ml_status hv_build(ml_ctx* c) {
               const_cast<float*>(hv.sval), const_cast<uint16_t*>(hv.sidx));
     if (!sync()) return cuda_fail(c, "hv_build");
     cudaMemsetAsync(hv.Xh, 0, sizeof(double) * (size_t)m, c->st);
-    cudaMemsetAsync(hv.Xhz, 0, sizeof(double) * (size_t)m, c->st);
     cudaMemsetAsync(hv.sH, 0, sizeof(double) * HV_HMAX, c->st);
-    cudaMemsetAsync(hv.zH, 0, sizeof(uint32_t) * (HV_HMAX / 32), c->st);
     hv.nh = nh;
     hv.nts = nts;
     hv.nnzh = nnzh;
-    hv.mode = 2;      // (off by default until it beats the column units: ml_set_engine bit 4 / 5 select it)
+    // on by default (chosen per relaxation by the free set's share of H) when H holds >= HV_AUTO nonzeros: below
+    // that a warp gets too few chunks to amortise its ring, and the heavy instantiation's larger shared memory costs
+    // the H sigma gathers L1 (measured: cfg 5 solve 460 -> 422 ms; cfg 3-4 slower with it)
+    hv.mode = (long long)nnzh >= HV_AUTO ? 0 : 2;
+    c->hv_mode0 = hv.mode;
     hv.frac = 0.25;
     hv.on = 1;
     return cuda_fail(c, "hv_build");
@@ -992,6 +994,11 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
     if (b) ML_LAUNCH(c, k_check_finite, c->gM, b, (long long)X->m, c->ctl, 8);
     ML_LAUNCH(c, k_init_rows, c->gM, P, (int)X->m);
     if (c->big_inner) ML_LAUNCH(c, k_xstats, GRID_CAP, X->csc_val, X->nnz, X->csr_rowptr, (int)X->m, c->ctl);
+    if (c->big_inner && c->inner_fn_hv && has_csr && X->nnz >= HV_AUTO) {   // large X: the heavy path by default
+        c->hv_built = true;
+        const ml_status hs = hv_build(c);
+        if (hs != ML_OK) { *out = c; return hs; }
+    }
     if (c->mp_grid_all)   // the static merge-path plan over all columns (X is fixed for the context's life)
         ML_LAUNCH(c, k_mp_search, std::max(1, (c->mp_tiles_cap + ML_NT) / ML_NT), c->mp_all, c->mp_tiles_cap);
     // static heavy schedules: all columns (slot 0) and all rows (slot 3)
@@ -1355,7 +1362,6 @@ ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
     if (want && c->mp_grid_all == 0) return ML_E_INVAL;   // (small m: the shared-memory passes; no merge-path plan)
     c->mp = want;
     c->P.dyn = (flags & 8u) ? 1 : 0;   // bit 3: dynamic unit claims in the large-m inner solver whatever the unit count
-    // bit 4: the heavy-column path in every relaxation; bit 6: when A holds >= 1/4 of H's nonzeros; else never
     if ((flags & (16u | 64u)) && !c->hv_built) {   // the heavy path's copy is built on first request (X is fixed)
         c->hv_built = true;
         if (c->big_inner && c->inner_fn_hv && c->X.csr_rowptr) {
@@ -1364,7 +1370,8 @@ ml_status ml_set_engine(ml_ctx* c, uint32_t flags) {
         }
     }
     if ((flags & 16u) && !c->P.hv.on) return ML_E_INVAL;
-    c->P.hv.mode = (flags & 16u) ? 1 : (flags & 64u) ? 0 : 2;   // bit 6: by the free set's share of H
+    // bit 4: always; bit 6: by the free set's share of H; bit 5: never; none: the context's default (hv_build)
+    c->P.hv.mode = (flags & 16u) ? 1 : (flags & 64u) ? 0 : (flags & 32u) ? 2 : c->hv_mode0;
     return ML_OK;
 }
 
@@ -1422,3 +1429,35 @@ int64_t ml_trace(ml_ctx* c, void* rows_host, int64_t cap) {
 }
 
 }  // extern "C"
+
+#ifdef IR_HVDBG
+// (debug builds only) the heavy sweep alone on this context's S copy, in a kernel of its own: cycles vs k_inner's
+__global__ void __launch_bounds__(256, 1) k_hv_sweep_alone(HvPrm hv) {
+    double* s = reinterpret_cast<double*>(hv_dyn + HV_SH_OFF);
+    for (int i = threadIdx.x; i < HV_HMAX; i += blockDim.x) s[i] = 0.001 * (i & 255);
+    __syncthreads();
+    hv_sweep(hv);
+}
+extern "C" double ml_debug_hv_sweep(ml_ctx* c, int reps, int nv) {
+    if (!c || !c->P.hv.on) return -1.0;
+    const size_t smem = hv_smem_bytes();
+    cudaFuncSetAttribute(k_hv_sweep_alone, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(e0, c->st);
+        (void)nv;
+        k_hv_sweep_alone<<<c->inner_P, 256, smem, c->st>>>(c->P.hv);
+        cudaEventRecord(e1, c->st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return best;
+}
+#endif

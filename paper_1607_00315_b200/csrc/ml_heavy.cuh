@@ -12,7 +12,8 @@
 // own chunks through a private HV_WST-stage TMA ring (its lane 0 issues the bulk copies of the values, the ids and
 // the chunk's slice of row starts) and reduces a chunk with groups of L = 2^lg lanes per row (lg per chunk from its
 // row count: one round of 32 / L rows); no block barriers.  Each row is a fixed-order sum: bitwise reproducible.
-// The H sigma products of the heavy columns stay on the column units (L2 gathers of D o X sigma).
+// X_A z (the snap path's zeroing columns, z = s there: rare) and H sigma of the heavy columns stay on the column
+// units (fixed-point reductions, L2 gathers of D o X sigma).
 #pragma once
 #include "ml_common.cuh"
 
@@ -20,17 +21,17 @@ namespace ml {
 
 constexpr int HV_HMAX = 8192;              // heavy columns at most (s_H: 64 KB of shared memory)
 constexpr int HV_WCH = 768;                // entries per warp chunk at most
-constexpr int HV_WROWS = 8;                // rows per warp chunk at most (one round of groups of >= 4 lanes)
+constexpr int HV_WROWS = 32;               // rows per warp chunk at most (one round of groups of 32 / 2^lg lanes)
 constexpr int HV_WST = 2;                  // stages of a warp's ring
 constexpr int HV_MINLEN = 32;              // shortest heavy column
+constexpr long long HV_AUTO = 1LL << 26;   // the path is on by default when H holds this many nonzeros (ml.cu)
 constexpr int HV_W = 8;                    // warps per block (k_inner)
 // a stage: values (HV_WCH + 8 from a 16-byte boundary), ids, row starts (HV_WROWS + 1 from a 16-byte boundary)
 constexpr size_t HV_WSTAGE = (((size_t)(HV_WCH + 8) * 6 + (size_t)(HV_WROWS + 8) * 4) + 15) / 16 * 16;
 constexpr size_t HV_WRING = (size_t)HV_WST * HV_WSTAGE + 64;   // + the stages' mbarriers
 // dynamic shared memory of the sub-phase (it aliases the column rings of k_inner)
 constexpr size_t HV_SH_OFF = 0;                                            // s_H
-constexpr size_t HV_ZH_OFF = (size_t)8 * HV_HMAX;                          // zeroing bits of H
-constexpr size_t HV_SRING_OFF = HV_ZH_OFF + (size_t)4 * (HV_HMAX / 32);    // the warps' rings
+constexpr size_t HV_SRING_OFF = (size_t)8 * HV_HMAX;                       // the warps' rings
 static_assert(HV_SRING_OFF % 16 == 0 && HV_WSTAGE % 16 == 0 && HV_WRING % 16 == 0, "ring alignment");
 __host__ __device__ constexpr size_t hv_smem_bytes() { return HV_SRING_OFF + (size_t)HV_W * HV_WRING; }
 
@@ -50,8 +51,8 @@ struct HvPrm {
     const int* soff;        // [m + 1] row starts in the S copy
     const HvChunk* schunk;  // [nts]
     double* sH;             // [HV_HMAX] the S coefficient of each heavy column of A this iteration (0 elsewhere)
-    uint32_t* zH;           // [HV_HMAX / 32] its zeroing flags (the snap path's z = s on those columns)
-    double* Xh; double* Xhz;   // [m] X_H s_H, X_H z_H
+    double* Xh;             // [m] X_H s_H
+    int* zunits;            // [units] this iteration's units of the zeroing heavy columns (X_A z goes through them)
     int* phid;              // [n] heavy id of free-set position p this relaxation (-1: light)
 };
 
@@ -60,19 +61,15 @@ struct HvPrm {
 extern __shared__ __align__(16) unsigned char hv_dyn[];
 
 // Rows of a staged chunk by groups of L = 2^LG lanes: lane gl sums entries gl, gl + L, ... of its row, 8 at a time
-// (loads first, then the fused multiply-adds in order), then the group's fixed shuffle tree; Xh[row] (Xhz[row]).
-template <int NV, int LG>
-__device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, const int* so, const HvChunk& ch,
-                                        double* Xh, double* Xhz) {
+// (loads first, then the fused multiply-adds in order), then the group's fixed shuffle tree; Xh[row].
+template <int LG>
+__device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, const int* so, const HvChunk& ch, double* Xh) {
     constexpr int L = 1 << LG, NG = 32 >> LG;
     const int lane = threadIdx.x & 31, grp = lane >> LG, gl = lane & (L - 1);
     const int eb = ch.e0 & ~7, ob = ch.r0 & 3;
     const double* s = reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF);
-    const uint32_t* zb = reinterpret_cast<const uint32_t*>(hv_dyn + HV_ZH_OFF);
     for (int r = grp; r - grp < ch.nr; r += NG) {   // (every lane runs every round: the shuffles need all lanes)
-        double acc[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+        double acc = 0.0;
         int b = 0, e = 0;
         if (r < ch.nr) { b = so[ob + r] - eb; e = so[ob + r + 1] - eb; }
         for (int i = b + gl; i < e; i += 8 * L) {
@@ -86,28 +83,16 @@ __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, con
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (i + u * L < e) {
-                    const uint32_t h = ix[u] & (HV_HMAX - 1);
-                    const double sh = s[h];
-                    acc[0] = fma((double)x[u], sh, acc[0]);
-                    if constexpr (NV == 2) acc[1] = fma((double)x[u], ((zb[h >> 5] >> (h & 31)) & 1u) ? sh : 0.0, acc[1]);
-                }
+                if (i + u * L < e) acc = fma((double)x[u], s[ix[u] & (HV_HMAX - 1)], acc);
         }
 #pragma unroll
-        for (int d = L >> 1; d > 0; d >>= 1) {
-#pragma unroll
-            for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], d);
-        }
-        if (gl == 0 && r < ch.nr) {
-            Xh[ch.r0 + r] = acc[0];
-            if constexpr (NV == 2) Xhz[ch.r0 + r] = acc[1];
-        }
+        for (int d = L >> 1; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        if (gl == 0 && r < ch.nr) Xh[ch.r0 + r] = acc;
     }
 }
 
 // This warp's chunks (an equal share of all warps of the grid, in order) through its private ring.
 // (out of line: called once per S phase, so that its loop gets registers of its own instead of k_inner's spills)
-template <int NV>
 __device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = nullptr) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef IR_HVDBG
@@ -144,12 +129,12 @@ __device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = 
         const uint16_t* si = reinterpret_cast<const uint16_t*>(b + (size_t)(HV_WCH + 8) * 4);
         const int* so = reinterpret_cast<const int*>(b + (size_t)(HV_WCH + 8) * 6);
         switch (ch.lg) {
-            case 0: hv_rows<NV, 0>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
-            case 1: hv_rows<NV, 1>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
-            case 2: hv_rows<NV, 2>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
-            case 3: hv_rows<NV, 3>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
-            case 4: hv_rows<NV, 4>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
-            default: hv_rows<NV, 5>(sv, si, so, ch, hv.Xh, hv.Xhz); break;
+            case 0: hv_rows<0>(sv, si, so, ch, hv.Xh); break;
+            case 1: hv_rows<1>(sv, si, so, ch, hv.Xh); break;
+            case 2: hv_rows<2>(sv, si, so, ch, hv.Xh); break;
+            case 3: hv_rows<3>(sv, si, so, ch, hv.Xh); break;
+            case 4: hv_rows<4>(sv, si, so, ch, hv.Xh); break;
+            default: hv_rows<5>(sv, si, so, ch, hv.Xh); break;
         }
         __syncwarp();   // stage st consumed by every lane
         if (lane == 0 && c + HV_WST < c1) issue(c + HV_WST, st);

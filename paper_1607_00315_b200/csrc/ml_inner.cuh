@@ -401,7 +401,6 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 
     int next_pcd = 1, cg_restart = 1, acc_steps = 0, stop = 0, pcd = 1, zs = 0, ksnap = 0;   // R6: PCD first
     double fq = 1.0, fqi = 1.0;   // BIG: this iteration's fixed-point scale of X_A s (and its inverse)
-    bool hvz = false;             // BIG, heavy mode: some heavy column of A is a zeroing column this iteration
     double beta = 0.0, bk = 0.0, bq = 0.0, bcg = 0.0, rz = 0.0, rz_prev = 0.0, slope = 0.0, ss = 0.0, ps = 0.0;
     double sHs = 0.0, vq = 0.0;
     const double vmax_C = c->vmax;
@@ -440,7 +439,6 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         }
         if (hvb) {   // no heavy column of A has a coefficient yet (D writes those of A's)
             for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX; i += G * blockDim.x) P.hv.sH[i] = 0.0;
-            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HV_HMAX / 32; i += G * blockDim.x) P.hv.zH[i] = 0u;
         }
         {
             const double v[5] = {(double)nu_loc, (double)nz_loc, (double)nu_l, (double)nz_l, nzh};
@@ -540,7 +538,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             for (int h = 0; h < 2; ++h) { base[h] += wtot[h]; zbase[h] += zwtot[h]; }
             __syncthreads();
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) { P.unz[NU] = NZ; c->s_ctr = 0u; c->g_ctr = 0u; }
+        if (blockIdx.x == 0 && threadIdx.x == 0) { P.unz[NU] = NZ; c->s_ctr = 0u; c->g_ctr = 0u; c->zcnt = 0u; }
         grid.sync();
         nU = NU;
         nUS = NUL;
@@ -618,13 +616,15 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     v[10] = fmax(v[10], fabs(u));   // (max |coef| of the X_A u pass: its fixed-point scale)
                     v[11] = fmax(v[11], fabs(vv));
                 }
-                if (BIG && hvm) {   // a heavy column of A: its S coefficient (and zeroing flag) for the S copy
-                    const int h = P.hv.phid[p0 + k];
+                if (BIG && hvm) {   // a heavy column of A: its S coefficient for the S copy; a zeroing one's units for
+                    const int h = P.hv.phid[p0 + k];      // the z pass (X_A z through the units: z is rare)
                     if (h >= 0) {
                         P.hv.sH[h] = pcd ? X.s[k] : X.u[k];
-                        const uint32_t bit = 1u << (h & 31);
-                        if (pcd && X.u[k] != 0.0) atomicOr(P.hv.zH + (h >> 5), bit);
-                        else atomicAnd(P.hv.zH + (h >> 5), ~bit);
+                        if (pcd && X.u[k] != 0.0) {
+                            const int ua = P.ustart[p0 + k], ub = P.uend[p0 + k];
+                            const unsigned zb = atomicAdd(&c->zcnt, (unsigned)(ub - ua));
+                            for (int u = ua; u < ub; ++u) P.hv.zunits[zb + (unsigned)(u - ua)] = u;
+                        }
                     }
                 }
             }
@@ -661,22 +661,24 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         // ------------------------------------------------ S: X_A coef (and X_A z) over my columns
         if constexpr (BIG) {   // per-warp rings, fixed-point reductions into Xu / Xzu (kept zero between uses)
             const double* coef = pcd ? AS.s : AS.u;
-            if constexpr (HVP) if (hvm) {   // heavy columns first: s_H (and its zeroing bits) in shared memory, the S copy's row sums
+            if constexpr (HVP) if (hvm) {   // heavy columns first: s_H in shared memory, the S copy's row sums
                 double* sHs = reinterpret_cast<double*>(smraw + HV_SH_OFF);
-                uint32_t* zHs = reinterpret_cast<uint32_t*>(smraw + HV_ZH_OFF);
-                int zor = 0;
                 for (int i = threadIdx.x; i < P.hv.nh; i += blockDim.x) sHs[i] = ld_cg(P.hv.sH + i);
-                for (int i = threadIdx.x; i < (P.hv.nh + 31) / 32; i += blockDim.x) {
-                    const uint32_t z = ld_cg(P.hv.zH + i);
-                    zHs[i] = z;
-                    zor |= z != 0u;
-                }
-                hvz = __syncthreads_or(zor) != 0;
+                __syncthreads();
 #ifdef IR_HVDBG
                 const unsigned long long hv_t0 = gtimer();
 #endif
-                if (hvz) hv_sweep<2>(P.hv, c->tph + 2);
-                else hv_sweep<1>(P.hv, c->tph + 2);
+                hv_sweep(P.hv, c->tph + 2);
+                // X_A z of the zeroing heavy columns (the snap path's z = s there): their units, a warp each, with the
+                // same fixed-point reductions as the column stream (order-independent)
+                const unsigned nzu = ld_cg(&c->zcnt);
+                for (unsigned k = (unsigned)(blockIdx.x * IR_W + wid); k < nzu; k += (unsigned)(G * IR_W)) {
+                    const int u = ld_cg(P.hv.zunits + k);
+                    const int2 ex = ld_cg(P.uext + u);
+                    const double cf = ld_cg(coef + ld_cg(P.upos + u));
+                    for (int e = ex.x + lane; e < ex.y; e += 32)
+                        red_add_fixed(P.Xzu + __ldg(S.idx + e), (double)__ldg(S.val + e) * cf, fq);
+                }
                 __syncthreads();   // (the rings' shared memory is reused by the column stream below)
                 if (blockIdx.x == 0 && threadIdx.x == 0) nsc += hv_nz;
 #ifdef IR_HVDBG   // (block 0's heavy S time in slot 0, heavy G time in slot 1: the small-|A| D / S slots)
@@ -836,7 +838,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
         PH_MARK(1);
         if constexpr (BIG) {
             grid.sync();   // B1
-            if (blockIdx.x == 0 && threadIdx.x == 0) c->s_ctr = 0u;   // (every warp's S claims are done)
+            if (blockIdx.x == 0 && threadIdx.x == 0) { c->s_ctr = 0u; c->zcnt = 0u; }   // (S claims and z units done)
         }
         else {   // B1, split: the G rings (aliasing the consumed S ring) are set up and issued while it completes
             const unsigned bar_old = gbar_arrive(&c->gbar);
@@ -895,8 +897,7 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         const int k = k0 + u * blockDim.x;
                         const bool in = k < nr;
                         xu[u] = in ? ld_fixed(P.Xu + r0 + k, fqi) + (hvm ? ld_cg(P.hv.Xh + r0 + k) : 0.0) : 0.0;
-                        xzu[u] = (in && dual) ? ld_fixed(P.Xzu + r0 + k, fqi) + (hvz ? ld_cg(P.hv.Xhz + r0 + k) : 0.0)
-                                              : 0.0;
+                        xzu[u] = (in && dual) ? ld_fixed(P.Xzu + r0 + k, fqi) : 0.0;
                         xo[u] = (in && !pcd) ? xs_r[k] : 0.0;
                         dd[u] = in ? P.rD[r0 + k].y : 0.0;
                     }

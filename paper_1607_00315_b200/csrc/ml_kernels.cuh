@@ -47,6 +47,7 @@ struct Ctl {
     double xmax;                 // max |X_ij| (large m: the fixed-point scale of X_A s)
     int maxrow, pad5;            // longest row of X
     long long hv_relax;          // relaxations that ran the heavy-column path (diagnostics, ml_heavy_info)
+    unsigned zcnt, pad6;         // heavy path: units of the zeroing heavy columns listed this iteration
 };
 
 // heavy-segment schedule for one segment list

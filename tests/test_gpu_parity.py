@@ -632,7 +632,8 @@ def test_select_coarse_exact_full_size(cfg):
 def test_full_size_solve_vs_oracle_golden(cfg):
     """Full-size solve at BASELINE configs 4 and 5 against the oracle's own solution, committed under tests/golden/
     by tools/make_golden.py (which calls only oracle/): F within 1e-6 relative, both kappa <= 1e-6, supports equal
-    outside the band ||g_j| - lambda| < 1e-4 (BASELINE.json north_star), and w on the common support close."""
+    outside the band ||g_j| - lambda| < 1e-4 (BASELINE.json north_star), and w on the common support close.  cfg 5 runs
+    the default heavy-column path (its X_A s from the row-major copy), cfg 4 the column units only."""
     import json
     import os
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", f"cfg{cfg}_solution.npz"))
@@ -641,6 +642,8 @@ def test_full_size_solve_vs_oracle_golden(cfg):
     assert (meta["m"], meta["n"], meta["nnz"]) == (ds.m, ds.n, ds.nnz) and meta["lam"] == ds.lam
     ctx = ml.Context(ds)
     r = ctx.ml_solve()
+    info = ctx.ml_heavy_info()   # cfg 5 takes the heavy-column path by default (include/ml.h, ml_set_engine)
+    assert (info["built"] == 1 and info["relaxations"] > 0) if cfg == 5 else info["relaxations"] == 0, info
     assert r["status"] == 0 and r["kappa"] <= 1e-6 and meta["kappa"] <= 1e-6
     assert abs(r["F"] - meta["F"]) <= 1e-6 * abs(meta["F"]), (r["F"], meta["F"])
     w = ctx.ml_get_w().cpu().numpy()
