@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(256, 1) k_lib(HvPrm hv, const double* sH) {
     double* s = reinterpret_cast<double*>(hv_dyn);
     for (int i = threadIdx.x; i < HV_HMAX; i += blockDim.x) s[i] = sH[i];
     __syncthreads();
-    hv_sweep<1>(hv);
+    hv_sweep(hv);
 }
 
 template <int LG, bool GATHER, int WCH, int WST, int WROWS>
@@ -181,7 +181,7 @@ int main(int argc, char** argv) {
         cudaMalloc(&dhc, hc.size() * sizeof(HvChunk));
         cudaMemcpy(dhc, hc.data(), hc.size() * sizeof(HvChunk), cudaMemcpyHostToDevice);
         HvPrm hv{};
-        hv.nts = (int)hc.size(); hv.sval = dv; hv.sidx = dk; hv.soff = drp; hv.schunk = dhc; hv.Xh = dXh; hv.Xhz = dXh;
+        hv.nts = (int)hc.size(); hv.sval = dv; hv.sidx = dk; hv.soff = drp; hv.schunk = dhc; hv.Xh = dXh;
         const size_t smem = hv_smem_bytes();
         cudaFuncSetAttribute(k_lib, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaEvent_t e0, e1;
