@@ -335,12 +335,14 @@ def run_ours(args):
         pinned = [None if k in skip else torch.from_numpy(a).pin_memory() for k, a in enumerate(keep)]
         h2d = sum(t.numel() * t.element_size() for t in pinned if t is not None)
         d2h = 8 * ds.n
+        w_host = torch.empty(ds.n, dtype=torch.float64).pin_memory()   # the result's host buffer (pinned, like X's)
         e2e_steps = max(1, min(args.steps, 3))
         # one untimed end-to-end step first, as for the device metric's warm-up: the process's first context pays
         # the caching allocator's device allocations and the first device-to-host copy's setup (~0.4 s, once)
         c2 = ml.Context.from_host(ds, pinned, device=str(device))
         c2.ml_solve(opts)
-        c2.ml_get_w().cpu()
+        w_host.copy_(c2.ml_get_w(), non_blocking=True)
+        torch.cuda.synchronize(device)
         c2.close()
         del c2
         barrier(ws)
@@ -350,10 +352,11 @@ def run_ours(args):
         for _ in range(e2e_steps):
             c2 = ml.Context.from_host(ds, pinned, device=str(device))
             r2 = c2.ml_solve(opts)
-            w = c2.ml_get_w().cpu()
+            w_host.copy_(c2.ml_get_w(), non_blocking=True)   # D2H of the result into pinned host memory
+            torch.cuda.synchronize(device)
             nnz_e += r2["nnz_touched"]
             c2.close()
-            del c2, w
+            del c2
         torch.cuda.synchronize(device)
         te = (time.perf_counter() - t0) * 1e3
         te_max, = allreduce([te], "max", ws, device)
