@@ -948,8 +948,8 @@ static ml_status create_impl(const ml_data* X, const double* b, double lambda, v
         // heavy-column path (its shared memory would shrink L1 for the default one)
         const void* kfn = (const void*)k_inner<1024, IN_GST, true>;
         const size_t b = inner_big_smem_bytes<1024, IN_GST>();
-        const void* kfh = (const void*)k_inner<1024, IN_GST, true, true>;
-        const size_t bh = std::max(inner_big_smem_bytes<1024, IN_GST>(), hv_smem_bytes());
+        const void* kfh = (const void*)k_inner<IR_HSCH, IR_HST, true, true>;
+        const size_t bh = std::max(inner_big_smem_bytes<IR_HSCH, IR_HST>(), hv_smem_bytes());
         int bps = 0, bph = 0;
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) == cudaSuccess)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * IR_W, b);
@@ -1097,7 +1097,8 @@ static void api_gather(ml_ctx* c, const int32_t* C, int nC, double* g_C, double*
     Seg S = seg_cols(c, C);
     ML_LAUNCH(c, (k_heavy<OpGH, false>), c->gHeavy, S, units_claim(c, slot), OpGH{c->P.rD}, (const double*)nullptr,
               (double*)nullptr, (const int*)nullptr, (const int*)nullptr, acc_of(c, CLS_API));
-    const int grid = std::max(1, std::min(GRID_CAP, (nC + TILE - 1) / TILE));
+    // (thread-per-column tiles, Gc == 4: 32 registers, latency-bound serial column loops: 8 resident blocks per SM)
+    const int grid = std::max(1, std::min((c->Gc == 4 ? 2 : 1) * GRID_CAP, (nC + TILE - 1) / TILE));
     ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_out<GG, 0, OpGH>), grid, S, OpGH{c->P.rD}, (const int*)nullptr, nC,
                                    g_C, h_C, acc_of(c, CLS_API)));
 }

@@ -20,9 +20,15 @@
 namespace ml {
 
 constexpr int HV_HMAX = 8192;              // heavy columns at most (s_H: 64 KB of shared memory)
-constexpr int HV_WCH = 768;                // entries per warp chunk at most
+#ifndef HV_WCH_V
+#define HV_WCH_V 768
+#endif
+#ifndef HV_WST_V
+#define HV_WST_V 2
+#endif
+constexpr int HV_WCH = HV_WCH_V;           // entries per warp chunk at most (build knobs: -DHV_WCH_V, -DHV_WST_V)
 constexpr int HV_WROWS = 32;               // rows per warp chunk at most (one round of groups of 32 / 2^lg lanes)
-constexpr int HV_WST = 2;                  // stages of a warp's ring
+constexpr int HV_WST = HV_WST_V;           // stages of a warp's ring
 constexpr int HV_MINLEN = 32;              // shortest heavy column
 constexpr long long HV_AUTO = 1LL << 26;   // the path is on by default when H holds this many nonzeros (ml.cu)
 constexpr int HV_W = 8;                    // warps per block (k_inner)

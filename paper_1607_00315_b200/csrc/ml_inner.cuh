@@ -66,6 +66,13 @@ constexpr int IR_NLS = ML_MAXLS - 4;
 enum { IR_SO = 0, IR_SO2 = 10, IR_SU = 10 + 2 * IR_NLS, IR_SO3 = IR_SU + 5, IR_NSLOT = IR_SO3 + 6 };
 // IR_SU .. +4: unit counts, nnz; the same without the heavy columns; nnz of A's heavy columns (BIG); IR_SO3: trials 1/2, 1/4, 1/8 of a large-m outer line search (l1, loss) when
 // alpha = 1 failed
+// the heavy-path instantiation's column rings (elements per chunk, stages per warp): build knobs for measurement
+#ifndef IR_HSCH
+#define IR_HSCH 1024
+#endif
+#ifndef IR_HST
+#define IR_HST IN_GST
+#endif
 #ifndef IR_UNIT_V
 #define IR_UNIT_V 2048
 #endif

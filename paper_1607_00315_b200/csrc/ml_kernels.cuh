@@ -77,34 +77,57 @@ struct Seg {
 __device__ __forceinline__ int seg_idx(const Seg& S, long long k, int cb) { return S.idx ? __ldg(S.idx + k) : (int)(k - cb); }
 
 // ------------------------------------------------------------------ per-element operations
+// An operation is applied to a batch of elements in three phases, so that every gather of the batch is in flight
+// before the first fused multiply-add waits for one (a gather behind a data-dependent branch or behind the previous
+// element's multiply-add is one L2 round trip per element: measured 1.08 -> see profiles/r02_kernels.md):
+//   pre(c, ok)     first-level lookup of the element with index c (OpMargin: its support-bitmap word)
+//   fetch(c, q)    the gathered operand (predicated on q = pre's result)
+//   fma(a0, a1, x, q, v)   accumulate in element order (skipped when !q)
 struct OpMargin {     // z_i = sum_k X_ik w_k, gathers gated by the support bitmap
     const double* w; const uint32_t* bits;
+    typedef double Val;
     __device__ __forceinline__ void prepare() {}
-    __device__ __forceinline__ void add(double& a0, double&, int c, float v) const {
-        if ((__ldg(bits + (c >> 5)) >> (c & 31)) & 1u) a0 += (double)v * __ldg(w + c);
+    __device__ __forceinline__ bool pre(int c, bool ok) const {
+        const uint32_t wd = ok ? __ldg(bits + (c >> 5)) : 0u;
+        return (wd >> (c & 31)) & 1u;
+    }
+    __device__ __forceinline__ Val fetch(int c, bool q) const { return q ? __ldg(w + c) : 0.0; }
+    __device__ __forceinline__ void fma(double& a0, double&, float x, bool q, Val v) const {
+        if (q) a0 += (double)x * v;
     }
 };
 struct OpGH {         // g_j = sum_i X_ij r_i ; h_j = sum_i X_ij^2 D_i
     const double2* rD;
+    typedef double2 Val;
     __device__ __forceinline__ void prepare() {}
-    __device__ __forceinline__ void add(double& a0, double& a1, int r, float v) const {
-        double2 q = __ldg(rD + r);
-        double x = (double)v;
-        a0 += x * q.x;
-        a1 += (x * x) * q.y;
+    __device__ __forceinline__ bool pre(int, bool ok) const { return ok; }
+    __device__ __forceinline__ Val fetch(int r, bool q) const { return q ? __ldg(rD + r) : make_double2(0.0, 0.0); }
+    __device__ __forceinline__ void fma(double& a0, double& a1, float v, bool q, Val t) const {
+        if (q) {
+            double x = (double)v;
+            a0 += x * t.x;
+            a1 += (x * x) * t.y;
+        }
     }
 };
 struct OpDot {        // acc = sum_i X_ij v_i
     const double* v;
+    typedef double Val;
     __device__ __forceinline__ void prepare() {}
-    __device__ __forceinline__ void add(double& a0, double&, int r, float x) const { a0 += (double)x * __ldg(v + r); }
+    __device__ __forceinline__ bool pre(int, bool ok) const { return ok; }
+    __device__ __forceinline__ Val fetch(int r, bool q) const { return q ? __ldg(v + r) : 0.0; }
+    __device__ __forceinline__ void fma(double& a0, double&, float x, bool q, Val t) const {
+        if (q) a0 += (double)x * t;
+    }
 };
 // Reduce the elements [b, e) of one segment with G lanes (lane in [0, G)).  Each lane streams U 16-byte vectors of
-// indices and U of values per iteration (all loads issued before use), peeling the unaligned ends.
+// indices and U of values per iteration (all loads issued before use), peeling the unaligned ends; then, GB vectors
+// at a time: the first-level lookups of their 4 GB elements, their gathers, their multiply-adds in element order.
 // cb: the start of the segment's column / row (dense X: the index of element k is k - cb)
-template <int G, int U = 2, class Op>
+template <int G, int U = 2, int GB = 2, class Op>
 __device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int e, int lane, double& a0, double& a1,
                                           int cb) {
+    static_assert(U % GB == 0, "gather batches");
     for (int k = (b & ~3) + 4 * lane; k < e; k += 4 * U * G) {
         int4 iv[U];
         float4 vv[U];
@@ -130,17 +153,27 @@ __device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int
             } else { iv[u] = make_int4(0, 0, 0, 0); vv[u] = make_float4(0.f, 0.f, 0.f, 0.f); }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int ku = k + 4 * G * u;
-            if (ku >= b && ku + 3 < e) {
-                op.add(a0, a1, iv[u].x, vv[u].x); op.add(a0, a1, iv[u].y, vv[u].y);
-                op.add(a0, a1, iv[u].z, vv[u].z); op.add(a0, a1, iv[u].w, vv[u].w);
-            } else if (ku < e) {
-                if (ku >= b) op.add(a0, a1, iv[u].x, vv[u].x);
-                if (ku + 1 >= b && ku + 1 < e) op.add(a0, a1, iv[u].y, vv[u].y);
-                if (ku + 2 >= b && ku + 2 < e) op.add(a0, a1, iv[u].z, vv[u].z);
-                if (ku + 3 >= b && ku + 3 < e) op.add(a0, a1, iv[u].w, vv[u].w);
+        for (int u0 = 0; u0 < U; u0 += GB) {
+            int ci[4 * GB];
+            float xv[4 * GB];
+            bool q[4 * GB];
+            typename Op::Val gv[4 * GB];
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const int ku = k + 4 * G * (u0 + u);
+                ci[4 * u + 0] = iv[u0 + u].x; ci[4 * u + 1] = iv[u0 + u].y;
+                ci[4 * u + 2] = iv[u0 + u].z; ci[4 * u + 3] = iv[u0 + u].w;
+                xv[4 * u + 0] = vv[u0 + u].x; xv[4 * u + 1] = vv[u0 + u].y;
+                xv[4 * u + 2] = vv[u0 + u].z; xv[4 * u + 3] = vv[u0 + u].w;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) q[4 * u + t] = (ku + t >= b) && (ku + t < e);
             }
+#pragma unroll
+            for (int t = 0; t < 4 * GB; ++t) q[t] = op.pre(ci[t], q[t]);
+#pragma unroll
+            for (int t = 0; t < 4 * GB; ++t) gv[t] = op.fetch(ci[t], q[t]);
+#pragma unroll
+            for (int t = 0; t < 4 * GB; ++t) op.fma(a0, a1, xv[t], q[t], gv[t]);
         }
     }
 }
@@ -150,11 +183,59 @@ __device__ __forceinline__ void seg_accum(const Seg& S, const Op& op, int b, int
 // Heavy segments (> S.split) are not streamed here: their results come from S.hres, written by k_heavy.
 // TS (segments per tile, a multiple of ML_NT / G, at most TILE): smaller tiles spread a short segment list over more
 // blocks (the coarse free-set gathers of the large-m path)
+//
+// G == 4 with whole tiles (segments of a few nonzeros on average: the columns of cfg 5, 45 % of them empty, 1.25
+// nonzeros per column below the split): ONE THREAD PER SEGMENT, four elements per iteration (loads, lookups, gathers,
+// then the multiply-adds in element order).  The groups-of-4 engine spent ~800 warp instructions per 32 columns on
+// vector bookkeeping for ~40 nonzeros (measured: 12 G columns/s whatever the occupancy); adjacent threads' elements
+// are adjacent in memory, so the scalar loads of a warp share sectors.  (Measured with R segments per group at once
+// instead: slower, the registers cost a resident block.)
+// thread-per-segment tiles: a thread reads back only the res slot it wrote, so the callers' block barriers around
+// the tile are not needed (a tile then costs each warp its own longest segment, not the block's)
+template <int G, int TS = TILE> __host__ __device__ constexpr bool seg_tile_private() { return G == 4 && TS == TILE; }
+template <int G, int TS = TILE> __device__ __forceinline__ void seg_tile_sync() {
+    if constexpr (!seg_tile_private<G, TS>()) __syncthreads();
+}
 template <int G, class Op, int TS = TILE>
 __device__ __forceinline__ void seg_tile(const Seg& S, const Op& op, int nseg, int tile, double2* res, long long& streamed,
                                          long long& segs) {
     constexpr int NG = ML_NT / G;
     static_assert(TS % NG == 0 && TS <= TILE, "tile size");
+    if constexpr (seg_tile_private<G, TS>()) {
+        const int p = tile * TS + threadIdx.x;
+        int b = 0, e = 0;
+        bool heavy = false;
+        if (p < nseg) {
+            const int j = S.list ? __ldg(S.list + p) : p;
+            b = __ldg(S.ptr + j);
+            e = __ldg(S.ptr + j + 1);
+            segs += 1;
+            if (e - b > S.split) { heavy = true; e = b; }
+            else streamed += e - b;
+        }
+        double a0 = 0.0, a1 = 0.0;
+        const int cb = b;
+        for (int k = b; k < e; k += 4) {
+            int ci[4];
+            float xv[4];
+            bool q[4];
+            typename Op::Val gv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                q[t] = k + t < e;
+                ci[t] = q[t] ? seg_idx(S, k + t, cb) : 0;
+                xv[t] = q[t] ? __ldg(S.val + k + t) : 0.f;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) q[t] = op.pre(ci[t], q[t]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) gv[t] = op.fetch(ci[t], q[t]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) op.fma(a0, a1, xv[t], q[t], gv[t]);
+        }
+        if (p < nseg) res[threadIdx.x] = heavy ? ld_cg(S.hres + p) : make_double2(a0, a1);
+        return;
+    }
     __shared__ int sb[TILE], se[TILE];
     {
         const int p = tile * TS + threadIdx.x;
@@ -333,7 +414,7 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
     long long streamed = 0, segs = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         seg_tile<G>(S, op, P.m, tile, res, streamed, segs);
-        __syncthreads();
+        seg_tile_sync<G>();
         const int i = tile * TILE + threadIdx.x;
         if (i < P.m) {
             const double z = res[threadIdx.x].x;
@@ -342,7 +423,7 @@ __global__ void __launch_bounds__(ML_NT) k_margins(Prm P, Seg S, long long* acc)
             P.rD[i] = make_double2(st.r, st.D);
             lsum += st.ell;
         }
-        __syncthreads();
+        seg_tile_sync<G>();
     }
     acc_add(acc, streamed, segs);
     Red<1> r;
@@ -399,7 +480,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
                 } else {
                     seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
                 }
-                __syncthreads();
+                if (MPOUT) __syncthreads(); else seg_tile_sync<G, TS>();
                 const int p = tile * TS + threadIdx.x;
                 if (threadIdx.x < TS && p < nC) {
                     const int j = S.list ? S.list[p] : p;
@@ -413,7 +494,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
                     l1p += fabs(ww[t]);
                     flag[t] = (ww[t] != 0.0) || (fabs(gg[t]) > P.lam);
                 }
-                __syncthreads();
+                if (MPOUT) __syncthreads(); else seg_tile_sync<G, TS>();
             }
             const unsigned bal = __ballot_sync(0xffffffffu, flag[t]);
             if (lane == 0) s_wcnt[t][wid] = __popc(bal);
@@ -530,14 +611,14 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
     long long streamed = 0, segs = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         seg_tile<G>(S, op, nseg, tile, res, streamed, segs);
-        __syncthreads();
+        seg_tile_sync<G>();
         const int p = tile * TILE + threadIdx.x;
         if (p < nseg) {
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
             else out0[p] = q.x;
         }
-        __syncthreads();
+        seg_tile_sync<G>();
     }
     acc_add(nnz_acc, streamed, segs);
 }
