@@ -577,6 +577,16 @@ void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* lis
               (const double*)nullptr, (double*)nullptr, &c->ctl->skip, (const int*)nullptr, acc_of(c, cls));
     const int ts = finest ? TILE : 64;   // (k_gather_free's tile size)
     const int grid = std::max(1, std::min(GRID_CAP, (nC_host + ts - 1) / ts));
+    if (finest && c->Gc == 4 && !list) {
+        // Columns of a few nonzeros (cfg 5): the sums of all columns by the lean thread-per-column pass (32 registers,
+        // 8 resident blocks per SM, no block barriers), then the compaction from S.hres.  Fused, the compaction's
+        // barriers and look-back chain ran at 3 blocks per SM: 1.30 ms against 0.51 + 0.2 ms for the two passes.
+        const int g2 = std::max(1, std::min(2 * GRID_CAP, (nC_host + TILE - 1) / TILE));
+        ML_LAUNCH(c, (k_gather_out<4, 3, OpGH>), g2, S, OpGH{c->P.rD}, (const int*)nullptr, nC_host, (double*)nullptr,
+                  (double*)nullptr, acc_of(c, cls));
+        ML_LAUNCH(c, (k_gather_free<32, true, true>), grid, c->P, S, AS, (long long*)nullptr);
+        return;
+    }
     if (finest) { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, true>), grid, c->P, S, AS, acc_of(c, cls))); }
     else { ML_DISPATCH_G(c->Gc, ML_LAUNCH(c, (k_gather_free<GG, false>), grid, c->P, S, AS, acc_of(c, cls))); }
 }

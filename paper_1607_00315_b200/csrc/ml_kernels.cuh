@@ -469,32 +469,42 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
         int jj[SUP], flag[SUP];
         double gg[SUP], hh[SUP], ww[SUP];
         double v1p = 0.0, l1p = 0.0;
+        // the group's tiles: the sums (MPOUT: straight from S.hres, no shared memory, no barriers), then the bitmap
+        // words of all SUP columns of a thread, then their w, then the flags (each a batch of independent loads)
+        bool okc[SUP];
+        uint32_t wb[SUP];
 #pragma unroll
         for (int t = 0; t < SUP; ++t) {
             const int tile = sup * SUP + t;
+            const int p = tile * TS + threadIdx.x;
             jj[t] = 0; flag[t] = 0; gg[t] = 0.0; hh[t] = 0.0; ww[t] = 0.0;
-            if (tile < ntiles) {   // (uniform over the block)
-                if (MPOUT) {
-                    const int p = tile * TS + threadIdx.x;
-                    if (threadIdx.x < TS && p < nC) res[threadIdx.x] = S.hres[p];
-                } else {
-                    seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
-                }
-                if (MPOUT) __syncthreads(); else seg_tile_sync<G, TS>();
-                const int p = tile * TS + threadIdx.x;
-                if (threadIdx.x < TS && p < nC) {
-                    const int j = S.list ? S.list[p] : p;
-                    jj[t] = j;
-                    gg[t] = res[threadIdx.x].x;
-                    hh[t] = res[threadIdx.x].y;
-                    if ((P.wbits[j >> 5] >> (j & 31)) & 1u) ww[t] = P.w[j];
-                    const double v = (ww[t] != 0.0) ? gg[t] + P.lam * sgn(ww[t]) : soft(gg[t], P.lam);
-                    vmax_loc = fmax(vmax_loc, fabs(v));
-                    v1p += fabs(v);
-                    l1p += fabs(ww[t]);
-                    flag[t] = (ww[t] != 0.0) || (fabs(gg[t]) > P.lam);
-                }
-                if (MPOUT) __syncthreads(); else seg_tile_sync<G, TS>();
+            okc[t] = tile < ntiles && threadIdx.x < TS && p < nC;
+            if (MPOUT) {
+                if (okc[t]) { const double2 q = S.hres[p]; gg[t] = q.x; hh[t] = q.y; }
+            } else if (tile < ntiles) {   // (uniform over the block)
+                seg_tile<G, OpGH, TS>(S, op, nC, tile, res, streamed, segs);
+                seg_tile_sync<G, TS>();
+                if (okc[t]) { gg[t] = res[threadIdx.x].x; hh[t] = res[threadIdx.x].y; }
+                seg_tile_sync<G, TS>();
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < SUP; ++t) {
+            const int p = (sup * SUP + t) * TS + threadIdx.x;
+            if (okc[t]) jj[t] = S.list ? S.list[p] : p;
+            wb[t] = okc[t] ? P.wbits[jj[t] >> 5] : 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < SUP; ++t)
+            if (okc[t] && ((wb[t] >> (jj[t] & 31)) & 1u)) ww[t] = P.w[jj[t]];
+#pragma unroll
+        for (int t = 0; t < SUP; ++t) {
+            if (okc[t]) {
+                const double v = (ww[t] != 0.0) ? gg[t] + P.lam * sgn(ww[t]) : soft(gg[t], P.lam);
+                vmax_loc = fmax(vmax_loc, fabs(v));
+                v1p += fabs(v);
+                l1p += fabs(ww[t]);
+                flag[t] = (ww[t] != 0.0) || (fabs(gg[t]) > P.lam);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, flag[t]);
             if (lane == 0) s_wcnt[t][wid] = __popc(bal);
@@ -508,33 +518,48 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
         int total = 0;
         for (int t = 0; t < SUP; ++t)
             for (int k = 0; k < ML_NW; ++k) total += s_wcnt[t][k];
-        if (threadIdx.x == 0) {
-            if (FINEST) {
+        if (wid == 0) {
+            if (FINEST && lane == 0) {
                 double a = 0.0, b = 0.0;
                 for (int k = 0; k < ML_NW; ++k) { a += s_red[k]; b += s_red[ML_NW + k]; }
                 P.tilepart[sup] = make_double2(a, b);
             }
-            // publish and look back (epoch-tagged status words: epoch<<34 | flag<<32 | count)
+            // publish and look back (epoch-tagged status words: epoch<<34 | flag<<32 | count; flag 1: this group's
+            // count, flag 2: the inclusive prefix).  The look-back is warp-parallel: lane l reads predecessor
+            // base - l, the nearest inclusive prefix ends it (one L2 round trip per 32 predecessors; one thread
+            // walking them one by one made the prefix frontier the bottleneck of the pass: 0.74 ms of look-backs for
+            // the 19.5 k groups of cfg 5's finest compaction).
             const unsigned long long e34 = (unsigned long long)epoch << 34;
             int excl = 0;
-            if (sup == 0) {
+            if (lane == 0) {
                 __threadfence();
-                atomicExch(P.status + 0, e34 | (2ull << 32) | (unsigned)total);
-            } else {
-                __threadfence();
-                atomicExch(P.status + sup, e34 | (1ull << 32) | (unsigned)total);
-                int pred = sup - 1;
-                while (true) {
-                    unsigned long long st = *((volatile unsigned long long*)(P.status + pred));
-                    if ((st >> 34) != epoch || ((st >> 32) & 3ull) == 0) continue;
-                    excl += (int)(st & 0xffffffffull);
-                    if (((st >> 32) & 3ull) == 2) break;
-                    --pred;
-                }
-                __threadfence();
-                atomicExch(P.status + sup, e34 | (2ull << 32) | (unsigned)(excl + total));
+                atomicExch(P.status + sup, e34 | ((sup == 0 ? 2ull : 1ull) << 32) | (unsigned)total);
             }
-            s_excl = excl;
+            if (sup > 0) {
+                int wbase = sup - 1;
+                while (true) {
+                    const int pred = wbase - lane;
+                    unsigned long long st = 0ull;
+                    if (pred >= 0) {
+                        do { st = *((volatile unsigned long long*)(P.status + pred)); }
+                        while ((st >> 34) != epoch || ((st >> 32) & 3ull) == 0);
+                    }
+                    const bool incl = pred >= 0 && ((st >> 32) & 3ull) == 2;
+                    const unsigned mi = __ballot_sync(0xffffffffu, incl);
+                    const int first = mi ? __ffs(mi) - 1 : 32;   // the nearest predecessor with an inclusive prefix
+                    int v = (pred >= 0 && lane <= first) ? (int)(st & 0xffffffffull) : 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    excl += v;
+                    if (mi) break;   // (group 0 always publishes an inclusive prefix: the walk ends there at the latest)
+                    wbase -= 32;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(P.status + sup, e34 | (2ull << 32) | (unsigned)(excl + total));
+                }
+            }
+            if (lane == 0) s_excl = excl;
         }
         __syncthreads();
         int base = s_excl;
@@ -599,6 +624,8 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
 // ------------------------------------------------------------------ plain gathers (API outputs / Hessian-vector)
 // MODE 0: out0[p] = g, out1[p] = h (either may be null)      (ml_eval_f_grad, ml_diag_hess)
 // MODE 1: out0[p] = sum X_ij v_i (+ eps_h * s[p] if s)       (Hs = X_A^T (D o Xs) + eps s, ml_hessvec)
+// MODE 3: S.hres[p] = (g, h) for every position (the finest gather in two passes: k_gather_free<., ., true> then
+//         compacts the free set from S.hres)
 // MODE 2: PCD-CG epilogue: s_p = u_p + b s_prev_p, Hs_p = acc + eps s_p, first kink b_k = min_{x s < 0} -x/s,
 //         last block: the CG step decision (R6')
 template <int G, int MODE, class Op>
@@ -616,6 +643,7 @@ __global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* n
         if (p < nseg) {
             const double2 q = res[threadIdx.x];
             if (MODE == 0) { if (out0) out0[p] = q.x; if (out1) out1[p] = q.y; }
+            else if (MODE == 3) S.hres[p] = q;
             else out0[p] = q.x;
         }
         seg_tile_sync<G>();
