@@ -204,7 +204,7 @@ def roof_entry(name, prof, ds, peak, traffic=None):
     ach = b / (p["ms"] * 1e-3) / 1e9
     return {"achieved": round(ach, 1), "frac": round(ach / peak, 4), "passes": p["passes"],
             "bytes_per_pass": int(b / p["passes"]), "us_per_pass": round(1e3 * p["ms"] / p["passes"], 2),
-            "traffic": traffic}
+            "traffic": traffic, "gnnz_per_s": round(p["nnz"] / (p["ms"] * 1e-3) / 1e9, 1)}
 
 
 def hessvec_rate(ctx, ds, torch, device):
@@ -322,6 +322,21 @@ def run_ours(args):
             rooflines[name] = ent
     ctx.ml_profile(0)
     hv = hessvec_rate(ctx, ds, torch, device)
+    # The second roofline of the large-m column passes: each nonzero of a sparse column
+    # gathers one 32-byte L2 sector ((r, D), D o X sigma, or a bitmap word), and the chip serves a fixed number of
+    # random sectors per second whatever the occupancy (tools/ubench/l2gather.cu, measured; profiles/l2gather.json).
+    l2g = None
+    gpath = os.path.join(ROOT, "profiles", "l2gather.json")
+    if ds.m > 8192 and os.path.exists(gpath):
+        try:
+            gpk = json.load(open(gpath))
+            l2g = {"peak": round(gpk["gathers_per_s"] / 1e9, 1), "unit": "G gathers/s", "peak_kind": "measured (committed)",
+                   "as_hbm_frac_at_8B_per_nnz": round(8 * gpk["gathers_per_s"] / 1e9 / peak, 3),
+                   "classes": {n: {"gnnz_per_s": e["gnnz_per_s"], "frac": round(e["gnnz_per_s"] * 1e9 / gpk["gathers_per_s"], 3)}
+                               for n, e in rooflines.items()},
+                   "source": gpk["source"]}
+        except Exception:
+            l2g = None
 
     # end-to-end through the public API with host buffers
     e2e = None
@@ -386,7 +401,7 @@ def run_ours(args):
             "solve": {"ok": ok, "F": r0["F"], "kappa": r0["kappa"], "cycles": r0["cycles"],
                       "relaxations": r0["relaxations"], "nnz_w": r0["nnz_w"], "x_nnz_streamed": r0["nnz_touched"],
                       "x_passes": r0["x_passes"]},
-            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "rooflines": rooflines, "hessvec": hv,
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "rooflines": rooflines, "l2_gather_roofline": l2g, "hessvec": hv,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

@@ -34,7 +34,8 @@ constexpr long long HV_AUTO = 1LL << 26;   // the path is on by default when H h
 constexpr int HV_W = 8;                    // warps per block (k_inner)
 // a stage: values (HV_WCH + 8 from a 16-byte boundary), ids, row starts (HV_WROWS + 1 from a 16-byte boundary)
 constexpr size_t HV_WSTAGE = (((size_t)(HV_WCH + 8) * 6 + (size_t)(HV_WROWS + 8) * 4) + 15) / 16 * 16;
-constexpr size_t HV_WRING = (size_t)HV_WST * HV_WSTAGE + 64;   // + the stages' mbarriers
+constexpr size_t HV_WRING = (size_t)HV_WST * HV_WSTAGE + 64 + (size_t)32 * HV_WST;   // + the stages' mbarriers (64 B)
+                                                                                    // and chunk descriptors
 // dynamic shared memory of the sub-phase (it aliases the column rings of k_inner)
 constexpr size_t HV_SH_OFF = 0;                                            // s_H
 constexpr size_t HV_SRING_OFF = (size_t)8 * HV_HMAX;                       // the warps' rings
@@ -66,30 +67,47 @@ struct HvPrm {
 // rings are addressed through it, so that the out-of-line hv_sweep still emits shared loads.
 extern __shared__ __align__(16) unsigned char hv_dyn[];
 
-// Rows of a staged chunk by groups of L = 2^LG lanes: lane gl sums entries gl, gl + L, ... of its row, 8 at a time
-// (loads first, then the fused multiply-adds in order), then the group's fixed shuffle tree; Xh[row].
+// Rows of a staged chunk by groups of L = 2^LG lanes.  Lane gl takes the row's aligned 4-entry vectors gl, gl + L,
+// ... (one 16-byte load of values and one 8-byte load of ids per vector, the entries outside [b, e) of the first
+// and last vector masked), two vectors at a time: loads, then the s_H gathers, then the fused multiply-adds in
+// order; then the group's fixed shuffle tree; Xh[row].
+// (ncu, cfg 5: the sweep is bound by shared-memory wavefronts.  With one 4-byte and one 2-byte load per entry the 16
+// rows a warp reads together start at arbitrary offsets: 2.6 wavefronts per request of values and 2.7 of ids against
+// 1, 182 M of the 324 M wavefronts of a launch; vectors need a quarter of the requests.)
 template <int LG>
 __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, const int* so, const HvChunk& ch, double* Xh) {
     constexpr int L = 1 << LG, NG = 32 >> LG;
     const int lane = threadIdx.x & 31, grp = lane >> LG, gl = lane & (L - 1);
     const int eb = ch.e0 & ~7, ob = ch.r0 & 3;
     const double* s = reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF);
+    const float4* sv4 = reinterpret_cast<const float4*>(sv);
+    const uint2* si4 = reinterpret_cast<const uint2*>(si);
     for (int r = grp; r - grp < ch.nr; r += NG) {   // (every lane runs every round: the shuffles need all lanes)
         double acc = 0.0;
         int b = 0, e = 0;
         if (r < ch.nr) { b = so[ob + r] - eb; e = so[ob + r + 1] - eb; }
-        for (int i = b + gl; i < e; i += 8 * L) {
+        for (int v = (b >> 2) + gl; 4 * v < e; v += 2 * L) {
             float x[8];
             uint32_t ix[8];
+            bool ok[8];
+            double g[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const bool ok = i + u * L < e;
-                x[u] = ok ? sv[i + u * L] : 0.0f;
-                ix[u] = ok ? si[i + u * L] : 0u;
+            for (int u = 0; u < 2; ++u) {
+                const int vu = v + u * L;
+                const bool in = 4 * vu < e;
+                const float4 xv = in ? sv4[vu] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const uint2 iv = in ? si4[vu] : make_uint2(0u, 0u);
+                x[4 * u + 0] = xv.x; x[4 * u + 1] = xv.y; x[4 * u + 2] = xv.z; x[4 * u + 3] = xv.w;
+                ix[4 * u + 0] = iv.x & 0xffffu; ix[4 * u + 1] = iv.x >> 16;
+                ix[4 * u + 2] = iv.y & 0xffffu; ix[4 * u + 3] = iv.y >> 16;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) ok[4 * u + t] = in && 4 * vu + t >= b && 4 * vu + t < e;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (i + u * L < e) acc = fma((double)x[u], s[ix[u] & (HV_HMAX - 1)], acc);
+            for (int t = 0; t < 8; ++t) g[t] = ok[t] ? s[ix[t] & (HV_HMAX - 1)] : 0.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (ok[t]) acc = fma((double)x[t], g[t], acc);
         }
 #pragma unroll
         for (int d = L >> 1; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
@@ -108,12 +126,17 @@ __device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = 
     uint64_t* bar = reinterpret_cast<uint64_t*>(ring + (size_t)HV_WST * HV_WSTAGE);
     const long long gw = (long long)blockIdx.x * HV_W + w, NW = (long long)gridDim.x * HV_W;
     const int c0 = (int)(hv.nts * gw / NW), c1 = (int)(hv.nts * (gw + 1) / NW);
-    auto issue = [&](int c, int st) {
-        const HvChunk k = hv.schunk[c];
+    // A stage's chunk descriptor sits in shared memory next to the barriers: lane 0 writes it when it issues the
+    // stage's copies, every lane reads it when the stage is consumed.  The descriptor of the chunk issued at the end
+    // of an iteration is loaded at its start, so that no L2 round trip of a descriptor is left on the warp's critical
+    // path (two per 768-entry chunk before: ~1400 of ~1900 cycles per chunk).
+    HvChunk* dsc = reinterpret_cast<HvChunk*>(ring + (size_t)HV_WST * HV_WSTAGE + 64);
+    auto issue = [&](const HvChunk& k, int st) {
         const int a0 = k.e0 & ~7, a1 = (k.e1 + 7) & ~7;
         const int o0 = k.r0 & ~3, o1 = (k.r0 + k.nr + 1 + 3) & ~3;
         unsigned char* b = ring + (size_t)st * HV_WSTAGE;
         const uint32_t n = (uint32_t)(a1 - a0), no = (uint32_t)(o1 - o0);
+        dsc[st] = k;
         mbar_arrive_expect_tx(bar + st, 6u * n + 4u * no);
         bulk_g2s(b, hv.sval + a0, 4u * n, bar + st);
         bulk_g2s(b + (size_t)(HV_WCH + 8) * 4, hv.sidx + a0, 2u * n, bar + st);
@@ -122,14 +145,17 @@ __device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = 
     if (lane == 0) {
         for (int k = 0; k < HV_WST; ++k) mbar_init(bar + k, 1);
         fence_mbar_init();
-        for (int k = 0; k < HV_WST && c0 + k < c1; ++k) issue(c0 + k, k);
+        for (int k = 0; k < HV_WST && c0 + k < c1; ++k) issue(hv.schunk[c0 + k], k);
     }
     __syncwarp();
     uint32_t phase = 0u;
     for (int c = c0, st = 0; c < c1; ++c, st = (st + 1) % HV_WST) {
-        const HvChunk ch = hv.schunk[c];
+        const bool more = c + HV_WST < c1;
+        HvChunk nxt;
+        if (more) nxt = hv.schunk[c + HV_WST];   // (every lane, one address: a broadcast load, used at the end)
         mbar_wait(bar + st, (phase >> st) & 1u);
         phase ^= 1u << st;
+        const HvChunk ch = dsc[st];
         const unsigned char* b = ring + (size_t)st * HV_WSTAGE;
         const float* sv = reinterpret_cast<const float*>(b);
         const uint16_t* si = reinterpret_cast<const uint16_t*>(b + (size_t)(HV_WCH + 8) * 4);
@@ -142,8 +168,9 @@ __device__ __noinline__ void hv_sweep(const HvPrm hv, unsigned long long* dbg = 
             case 4: hv_rows<4>(sv, si, so, ch, hv.Xh); break;
             default: hv_rows<5>(sv, si, so, ch, hv.Xh); break;
         }
-        __syncwarp();   // stage st consumed by every lane
-        if (lane == 0 && c + HV_WST < c1) issue(c + HV_WST, st);
+        __syncwarp();   // stage st consumed by every lane (its descriptor too)
+        if (lane == 0 && more) issue(nxt, st);
+        __syncwarp();   // (the next descriptor of stage st is visible to every lane)
     }
     __syncwarp();
     if (lane == 0)
