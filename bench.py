@@ -201,10 +201,11 @@ def roof_entry(name, prof, ds, peak, traffic=None):
     if p["ms"] <= 0 or p["passes"] <= 0:
         return None
     b = class_bytes(name, prof, ds)
+    nnz = p["nnz"] if name != "inner_fused" else prof["scatter_XAs"]["nnz"] + prof["gather_Hs"]["nnz"]
     ach = b / (p["ms"] * 1e-3) / 1e9
     return {"achieved": round(ach, 1), "frac": round(ach / peak, 4), "passes": p["passes"],
             "bytes_per_pass": int(b / p["passes"]), "us_per_pass": round(1e3 * p["ms"] / p["passes"], 2),
-            "traffic": traffic, "gnnz_per_s": round(p["nnz"] / (p["ms"] * 1e-3) / 1e9, 1)}
+            "traffic": traffic, "gnnz_per_s": round(nnz / (p["ms"] * 1e-3) / 1e9, 1)}
 
 
 def hessvec_rate(ctx, ds, torch, device):

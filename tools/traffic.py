@@ -2,7 +2,7 @@
 dram__bytes_write.sum --csv) of one solve, in launch order: the classes of bench.py's rooflines.
 
   margins        k_heavy<OpMargin> + k_margins<G>            (one margins pass)
-  gather_fine    k_heavy<OpGH> + k_gather_free<G, 1>         (finest gather, A2/A3 over all columns)
+  gather_fine    k_heavy<OpGH> [+ k_gather_out<4, 3>] + k_gather_free<G, 1>   (finest gather, A2/A3 over all columns)
   gather_coarse  k_heavy<OpGH> + k_gather_free<G, 0>         (coarse gather over a level list)
   inner_fused    k_inner<...>                                (one relaxation of the persistent inner solver)
 
@@ -27,8 +27,8 @@ def classify(ls):
 
     for d in ls:
         k = d["kernel"]
-        if k.startswith("k_heavy<OpMargin") or k.startswith("k_heavy<OpGH"):
-            pending.append(d)
+        if k.startswith("k_heavy<OpMargin") or k.startswith("k_heavy<OpGH") or k.startswith("k_gather_out"):
+            pending.append(d)   # (k_gather_out<4, 3>: the column sums of the two-pass finest gather)
         elif k.startswith("k_margins"):
             add("margins", pending + [d]); pending = []
         elif k.startswith("k_gather_free") and k.replace(" ", "").split(",")[1].startswith("1"):
