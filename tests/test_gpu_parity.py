@@ -57,6 +57,32 @@ def _full(cfg):
     return _CACHE[key]
 
 
+def _coo_dataset(m, n, per_row, seed, lam_factor):
+    """A sparse design from coordinates (no dense m x n array): row i holds Poisson(per_row) distinct random columns
+    (some rows stay empty), N(0,1) values, uniform labels; lambda = lam_factor * lambda_max."""
+    rng = np.random.default_rng(seed)
+    cnt = rng.poisson(per_row, m)
+    rows = np.repeat(np.arange(m), cnt)
+    cols = rng.integers(0, n, rows.size)
+    key = np.unique(rows.astype(np.int64) * n + cols)          # sorted by (row, col), duplicates dropped
+    rows, cols = (key // n).astype(np.int64), (key % n).astype(np.int64)
+    vals = rng.standard_normal(rows.size).astype(np.float32)
+    vals[vals == 0] = 1.0
+    rowptr = np.zeros(m + 1, np.int64)
+    np.add.at(rowptr, rows + 1, 1)
+    corder = np.lexsort((rows, cols))
+    colptr = np.zeros(n + 1, np.int64)
+    np.add.at(colptr, cols + 1, 1)
+    y = np.where(rng.random(m) < 0.5, 1, -1).astype(np.int8)
+    g0 = np.zeros(n)
+    np.add.at(g0, cols, vals.astype(np.float64) * y[rows])
+    lam = lam_factor * 0.5 * np.max(np.abs(g0))
+    return mlgen.Dataset(m=m, n=n, csr_rowptr=np.cumsum(rowptr).astype(np.int32), csr_col=cols.astype(np.int32),
+                         csr_val=vals, csc_colptr=np.cumsum(colptr).astype(np.int32),
+                         csc_row=rows[corder].astype(np.int32), csc_val=vals[corder], y=y, lam=float(lam),
+                         name=f"coo{m}x{n}s{seed}")
+
+
 def dataset(name):
     if name in _CACHE:
         return _CACHE[name]
@@ -78,6 +104,11 @@ def dataset(name):
         ds = mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40)
     elif name == "onehot":
         ds = mlgen.onehot(3000, 3)[0]
+    elif name == "shortcols":   # large m, ~4 nonzeros per column (45 % of cfg 5's columns are this short): one thread
+        # per column in the gather tiles, the finest gather in two passes, a look-back over > 32 groups
+        ds = mlgen.make(5, m=12000, n=120000)   # (cfg 5's recipe: Zipf columns, mean length 10, many empty)
+    elif name == "shortrows":   # large m, 1-7 nonzeros per row (some rows empty): one thread per row in the margins tiles
+        ds = _coo_dataset(90000, 12000, 4, seed=12, lam_factor=0.05)
     elif name == "lasso2s":    # squared loss (Q29) on the small-m dense design
         ds = mlgen.lasso(mlgen.make(2, m=300, n=3000), 1, k=40, noise=0.5, lam_factor=0.1)
     elif name == "lasso4s":    # squared loss on the large-m (global m-vector) path
@@ -121,7 +152,7 @@ def random_w(n, kind, seed):
     return w
 
 
-PER_KERNEL = ["cfg1", "cfg2s", "cfg2m", "cfg3s", "cfg4s", "sparse_edges", "onehot", "m1", "n1"]
+PER_KERNEL = ["cfg1", "cfg2s", "cfg2m", "cfg3s", "cfg4s", "sparse_edges", "onehot", "m1", "n1", "shortcols", "shortrows"]
 
 
 @pytest.mark.parametrize("name", PER_KERNEL)
@@ -162,7 +193,7 @@ def _lists(ds, seed):
     return out
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg2m", "cfg3s", "sparse_edges"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg2m", "cfg3s", "sparse_edges", "shortcols", "shortrows"])
 def test_restricted_gather_hessvec(name):
     """A2 / A5 restricted to lists C: empty, single, heaviest column, 1 %, half."""
     ds = dataset(name)
@@ -263,7 +294,8 @@ def _support_check(ds, w_g, w_o, g_o):
                                        ("mid6k", {"continuation": 1}), ("onehot", {"continuation": 1}),
                                        ("lasso2s", {}), ("lasso4s", {}), ("lasso_mid6k", {}),
                                        ("lasso2s", {"continuation": 1}), ("lasso4s", {"multilevel": 0, "K_fine": 10}),
-                                       ("tail3", {"multilevel": 0}), ("tail2", {"continuation": 1})])
+                                       ("tail3", {"multilevel": 0}), ("tail2", {"continuation": 1}),
+                                       ("shortcols", {}), ("shortrows", {})])
 def test_solve_parity(name, opts):
     """A9: ml_solve vs the oracle's solve (Algorithm 1 P:155-173 per P:798), both to kappa <= 1e-6."""
     ds = dataset(name)
