@@ -71,6 +71,7 @@ struct ml_ctx {
     // small-m shared-memory scatter
     bool sm_scatter = false;
     int scat_W = 0, scat_P = 0, gMP = 1;
+    int gFine2 = 0;          // grid of the two-pass finest gather's column-sum pass (occupancy x SMs)
     size_t scat_bytes = 0;
     bool sm_gather = false;
     bool sm_inner = false;   // persistent cooperative inner solver (k_inner), m-vectors in shared memory
@@ -581,7 +582,15 @@ void launch_relax_start(ml_ctx* c, int first_of_level, int level, const int* lis
         // Columns of a few nonzeros (cfg 5): the sums of all columns by the lean thread-per-column pass (32 registers,
         // 8 resident blocks per SM, no block barriers), then the compaction from S.hres.  Fused, the compaction's
         // barriers and look-back chain ran at 3 blocks per SM: 1.30 ms against 0.51 + 0.2 ms for the two passes.
-        const int g2 = std::max(1, std::min(2 * GRID_CAP, (nC_host + TILE - 1) / TILE));
+        if (!c->gFine2) {   // whole waves: the tile loop is grid-strided (1184 blocks at 6 per SM left a third wave of a
+                            // third of the blocks running alone: ncu, 55 % of the warp slots active)
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather_out<4, 3, OpGH>, ML_NT, 0) != cudaSuccess || occ < 1)
+                occ = 4;
+            cudaGetLastError();
+            c->gFine2 = occ * c->sms;
+        }
+        const int g2 = std::max(1, std::min(c->gFine2, (nC_host + TILE - 1) / TILE));
         ML_LAUNCH(c, (k_gather_out<4, 3, OpGH>), g2, S, OpGH{c->P.rD}, (const int*)nullptr, nC_host, (double*)nullptr,
                   (double*)nullptr, acc_of(c, cls));
         ML_LAUNCH(c, (k_gather_free<32, true, true>), grid, c->P, S, AS, (long long*)nullptr);

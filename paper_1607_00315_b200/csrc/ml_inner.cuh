@@ -683,7 +683,17 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     const int u = ld_cg(P.hv.zunits + k);
                     const int2 ex = ld_cg(P.uext + u);
                     const double cf = ld_cg(coef + ld_cg(P.upos + u));
-                    for (int e = ex.x + lane; e < ex.y; e += 32)
+                    int e = ex.x + lane;
+                    for (; e + 96 < ex.y; e += 128) {   // four elements per lane in flight (ncu: 2 % of a snap-path
+                                                        // launch waited here on one dependent load at a time)
+                        int r[4];
+                        double xv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) { r[u] = __ldg(S.idx + e + 32 * u); xv[u] = (double)__ldg(S.val + e + 32 * u) * cf; }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) red_add_fixed(P.Xzu + r[u], xv[u], fq);
+                    }
+                    for (; e < ex.y; e += 32)
                         red_add_fixed(P.Xzu + __ldg(S.idx + e), (double)__ldg(S.val + e) * cf, fq);
                 }
                 __syncthreads();   // (the rings' shared memory is reused by the column stream below)
