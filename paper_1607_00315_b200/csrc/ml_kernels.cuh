@@ -629,7 +629,8 @@ __global__ void __launch_bounds__(ML_NT) k_gather_free(Prm P, Seg S, ASet AS, lo
 // MODE 2: PCD-CG epilogue: s_p = u_p + b s_prev_p, Hs_p = acc + eps s_p, first kink b_k = min_{x s < 0} -x/s,
 //         last block: the CG step decision (R6')
 template <int G, int MODE, class Op>
-__global__ void __launch_bounds__(ML_NT) k_gather_out(Seg S, Op op, const int* nseg_dev, int nseg_host, double* out0,
+// (thread-per-column tiles, G == 4, are latency-bound: at most 32 registers, 8 resident blocks per SM)
+__global__ void __launch_bounds__(ML_NT, (G == 4 ? 8 : 1)) k_gather_out(Seg S, Op op, const int* nseg_dev, int nseg_host, double* out0,
                                                       double* out1, long long* nnz_acc) {
     __shared__ double2 res[TILE];
     op.prepare();
