@@ -148,6 +148,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double* Xu = cv.take<double>(mm);
     double* Xz = cv.take<double>(mm);
     double* svz = cv.take<double>(mm);
+    double2* sv2 = cv.take<double2>(mm > SMALL_M ? mm : 1);
     double* Xzu = cv.take<double>(mm);
     double* part = cv.take<double>((size_t)2 * GRID_CAP * NV_MAX);
     double2* tilepart = cv.take<double2>(ntile_n + 1);
@@ -223,7 +224,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     for (int k = 0; k < 4; ++k) c->um[k] = um[k];
     Prm& P = c->P;
     P.w = w; P.wbits = wbits; P.z = z; P.rD = rD; P.Xd = Xd; P.Xs = Xs; P.sv = sv; P.Xu = Xu; P.parts = parts;
-    P.Xz = Xz; P.svz = svz; P.Xzu = Xzu;
+    P.Xz = Xz; P.svz = svz; P.Xzu = Xzu; P.sv2 = sv2;
     P.irpart = irpart;
     P.uext = uext; P.upos = upos; P.upart = upart; P.ustart = ustart; P.uend = uend; P.unz = unz;
     c->slist = slist;

@@ -926,10 +926,10 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                         P.Xu[r0 + k] = 0.0;
                         xs_r[k] = xs;
                         P.sv[r0 + k] = dd[u] * xs;
-                        if (dual) {
+                        if (dual) {   // (D o Xs, D o Xz) side by side: the snap path's G phase gathers both with one sector
                             P.Xzu[r0 + k] = 0.0;
                             xz_r[k] = xzu[u];
-                            P.svz[r0 + k] = dd[u] * xzu[u];
+                            P.sv2[r0 + k] = make_double2(dd[u] * xs, dd[u] * xzu[u]);
                         }
                         a_ss += dd[u] * xs * xs;
                         a_sz += dd[u] * xs * xzu[u];
@@ -1116,17 +1116,18 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     double a1 = 0.0, az1 = 0.0;
                     for (; k + 32 * (IR_GU / 2) - 32 < kend; k += 32 * (IR_GU / 2)) {
                         int q[IR_GU / 2];
-                        double sa[IR_GU / 2], sz[IR_GU / 2];
+                        double2 sq[IR_GU / 2];   // (D o Xs, D o Xz) of a row share a sector: one gather per nonzero, not
+                                                 // two (the chip serves a fixed number of random sectors per second)
 #pragma unroll
                         for (int u = 0; u < IR_GU / 2; ++u) q[u] = ci[k + 32 * u];
 #pragma unroll
-                        for (int u = 0; u < IR_GU / 2; ++u) { sa[u] = ld_cg(P.sv + q[u]); sz[u] = ld_cg(P.svz + q[u]); }
+                        for (int u = 0; u < IR_GU / 2; ++u) sq[u] = ld_cg(P.sv2 + q[u]);
 #pragma unroll
                         for (int u = 0; u < IR_GU / 2; u += 2) {
-                            a = fma((double)cv[k + 32 * u], sa[u], a);
-                            az = fma((double)cv[k + 32 * u], sz[u], az);
-                            a1 = fma((double)cv[k + 32 * u + 32], sa[u + 1], a1);
-                            az1 = fma((double)cv[k + 32 * u + 32], sz[u + 1], az1);
+                            a = fma((double)cv[k + 32 * u], sq[u].x, a);
+                            az = fma((double)cv[k + 32 * u], sq[u].y, az);
+                            a1 = fma((double)cv[k + 32 * u + 32], sq[u + 1].x, a1);
+                            az1 = fma((double)cv[k + 32 * u + 32], sq[u + 1].y, az1);
                         }
                     }
                     a += a1;
@@ -1134,8 +1135,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                     for (; k < kend; k += 32) {
                         const int r = ci[k];
                         const double xv = (double)cv[k];
-                        a = fma(xv, ld_cg(P.sv + r), a);
-                        az = fma(xv, ld_cg(P.svz + r), az);
+                        const double2 sq = ld_cg(P.sv2 + r);
+                        a = fma(xv, sq.x, a);
+                        az = fma(xv, sq.y, az);
                     }
                 } else {
                     double a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -1169,8 +1171,11 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 for (; k < dsc.ve; k += 32) {
                     const int r = seg_idx(S, k, dsc.cb);
                     const double xv = (double)__ldg(S.val + k);
-                    a = fma(xv, ld_cg(P.sv + r), a);
-                    if (zs) az = fma(xv, ld_cg(P.svz + r), az);
+                    if (zs) {
+                        const double2 sq = ld_cg(P.sv2 + r);
+                        a = fma(xv, sq.x, a);
+                        az = fma(xv, sq.y, az);
+                    } else a = fma(xv, ld_cg(P.sv + r), a);
                 }
                 if (dsc.last) {   // unit end: its partial (combined per column after the barrier)
                     const double t = warp_sum(a), tz = zs ? warp_sum(az) : 0.0;

@@ -388,6 +388,7 @@ struct Prm {
     double* w; uint32_t* wbits; double* z; double2* rD;
     double* Xd; double* Xs; double* sv; double* Xu;   // Xu: scatter target of the atomic path (kept zero between uses)
     double* Xz; double* svz; double* Xzu;             // snap path: X_A z, D o Xz; Xzu: atomic scatter target of z (kept zero)
+    double2* sv2;                                     // large m, snap path: (D o Xs, D o Xz) per row, one 16-byte gather per nonzero
     double* parts; int nparts;                        // small-m scatter: per-block partials (+ group partials)
     double* irpart;                                   // persistent inner solver: slot-major block partials
     int2* uext; int* upos; double2* upart; int* ustart; int* uend; long long* unz;   // its column units (m > SMALL_M)
