@@ -29,6 +29,9 @@ constexpr int IR_SCH = 2048;               // S phase: block-shared ring of IR_S
 #ifndef IR_GU
 #define IR_GU 8   // BIG G phase: L2 gathers in flight per lane (multiple of 4)
 #endif
+#ifndef IR_GUZ
+#define IR_GUZ IR_GU   // the same on the snap path (16-byte gathers of (D o Xs, D o Xz)); even (8: G 430 us, 4: 435)
+#endif
 #ifndef IR_RB
 #define IR_RB 4   // BIG R phase: rows in flight per thread
 #endif
@@ -708,15 +711,20 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             }
             __syncwarp();
             g_phase = 0u;   // fresh barriers
-            ColStream<GSCH, GST> cs;
+            ColStream<GSCH, GST, true> cs;
             cs.streamed = 0;
             cs.segs = 0;
+            // a unit's coefficient and zeroing flag come with its descriptor (loaded for a whole batch of units at once:
+            // two dependent L2 round trips per batch, not per chunk of a few hundred nonzeros); zero-coefficient units
+            // are not streamed at all
+            cs.upos = P.upos;
+            cs.zsrc = (pcd && P.pcd_snap) ? AS.u : nullptr;
             if (nUS >= IR_DYN * G * IR_W || P.dyn) {   // many units per warp: dynamic claims (no block waits on another
                                                         // at B1)
                 cs.claim = &c->s_ctr;
-                stream_begin(cs, S, nullptr, 0, nUS, gbase, P.uext, nUS);
+                stream_begin(cs, S, coef, 0, nUS, gbase, P.uext, nUS);
             } else {
-                stream_begin(cs, S, nullptr, us0, us1, gbase, P.uext + us0, us1 - us0);
+                stream_begin(cs, S, coef, us0, us1, gbase, P.uext + us0, us1 - us0);
             }
             int stg = 0;
             while (true) {
@@ -724,10 +732,9 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 if (dsc.cf == 0.0) break;
                 mbar_wait(cs.bar + stg, (g_phase >> stg) & 1u);
                 g_phase ^= 1u << stg;
-                const int pu = __ldg(P.upos + dsc.p);
-                const double cf = ld_cg(coef + pu);
+                const double cf = dsc.cf;
                 if (cf != 0.0) {
-                    const int zf = pcd && P.pcd_snap && ld_cg(AS.u + pu) != 0.0;   // z_p = s_p on a zeroing column
+                    const int zf = dsc.pad;   // z_p = s_p on a zeroing column (pcd && pcd_snap && u_p != 0)
                     const int* ci = S.idx ? cs.sidx + stg * GSCH - dsc.a : S.rowtab - dsc.cb;
                     const float* cv = cs.sval + stg * GSCH - dsc.a;
                     const int kend = min(dsc.ve, dsc.ce);
@@ -1114,16 +1121,16 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
                 // the L2 gathers of D o X sigma are latency-bound: IR_GU gathers in flight per lane
                 if (zs) {
                     double a1 = 0.0, az1 = 0.0;
-                    for (; k + 32 * (IR_GU / 2) - 32 < kend; k += 32 * (IR_GU / 2)) {
-                        int q[IR_GU / 2];
-                        double2 sq[IR_GU / 2];   // (D o Xs, D o Xz) of a row share a sector: one gather per nonzero, not
+                    for (; k + 32 * (IR_GUZ) - 32 < kend; k += 32 * (IR_GUZ)) {
+                        int q[IR_GUZ];
+                        double2 sq[IR_GUZ];   // (D o Xs, D o Xz) of a row share a sector: one gather per nonzero, not
                                                  // two (the chip serves a fixed number of random sectors per second)
 #pragma unroll
-                        for (int u = 0; u < IR_GU / 2; ++u) q[u] = ci[k + 32 * u];
+                        for (int u = 0; u < IR_GUZ; ++u) q[u] = ci[k + 32 * u];
 #pragma unroll
-                        for (int u = 0; u < IR_GU / 2; ++u) sq[u] = ld_cg(P.sv2 + q[u]);
+                        for (int u = 0; u < IR_GUZ; ++u) sq[u] = ld_cg(P.sv2 + q[u]);
 #pragma unroll
-                        for (int u = 0; u < IR_GU / 2; u += 2) {
+                        for (int u = 0; u < IR_GUZ; u += 2) {
                             a = fma((double)cv[k + 32 * u], sq[u].x, a);
                             az = fma((double)cv[k + 32 * u], sq[u].y, az);
                             a1 = fma((double)cv[k + 32 * u + 32], sq[u + 1].x, a1);

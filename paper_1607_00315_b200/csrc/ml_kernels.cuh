@@ -88,8 +88,12 @@ struct OpMargin {     // z_i = sum_k X_ik w_k, gathers gated by the support bitm
     typedef double Val;
     __device__ __forceinline__ void prepare() {}
     __device__ __forceinline__ bool pre(int c, bool ok) const {
+#ifdef ML_MARGIN_NOBITS   // (experiment: w gathered for every nonzero, no bitmap lookup)
+        return ok;
+#else
         const uint32_t wd = ok ? __ldg(bits + (c >> 5)) : 0u;
         return (wd >> (c & 31)) & 1u;
+#endif
     }
     __device__ __forceinline__ Val fetch(int c, bool q) const { return q ? __ldg(w + c) : 0.0; }
     __device__ __forceinline__ void fma(double& a0, double&, float x, bool q, Val v) const {
@@ -684,7 +688,9 @@ __global__ void __launch_bounds__(ML_NT) k_scatter(Seg S, const int* nseg_dev, i
 // copy start, valid [vb, ve), copied to ce; cb: the start of the chunk's column (dense X: its row indices)
 struct ChunkDesc { int a, vb, ve, ce; int p, last, cb, pad; double cf; };
 
-template <int SCH, int NSTG>
+// IND: the S phase of the large-m inner solver (coefficients by indirection, below); a plain stream does not carry
+// (or test) those members, so that the long-lived G stream of k_inner keeps its registers
+template <int SCH, int NSTG, bool IND = false>
 struct ColStream {
     // warp-uniform producer state
     int p0, p1, W, wid, lane, nnz4;
@@ -694,6 +700,11 @@ struct ColStream {
     long long streamed, segs;
     const Seg* S;
     const double* coef;
+    // coefficient by indirection (the large-m S phase: position p is a column unit, its coefficient coef[upos[p]] was
+    // written by other blocks of this launch: L2 loads); zsrc: a second per-unit vector whose nonzero sets ChunkDesc::pad
+    const int* upos = nullptr;
+    const double* zsrc = nullptr;
+    int mzf = 0;
     int* sidx; float* sval; uint64_t* bar; ChunkDesc* desc;
     const int2* ext; int ext_p0, ext_n;   // optional cached segment extents of positions [ext_p0, ext_p0 + ext_n)
     // dynamic schedule (claim != nullptr): the warp claims CLAIM_B positions of [p0, p1) at a time from a grid-wide
@@ -712,9 +723,13 @@ struct ColStream {
     }
     __device__ void load_batch() {
         const int p = claim ? (lane < cbn ? cb0 + lane : p1) : p0 + wid + W * (batch * 32 + lane);
-        mb = 0; me = 0; mcf = 0.0;
+        mb = 0; me = 0; mcf = 0.0; mzf = 0;
         if (p < p1) {
-            mcf = coef ? coef[p] : 1.0;
+            if constexpr (IND) {
+                const int pu = __ldg(upos + p);
+                mcf = ld_cg(coef + pu);
+                if (zsrc && mcf != 0.0) mzf = ld_cg(zsrc + pu) != 0.0;
+            } else mcf = coef ? coef[p] : 1.0;
             if (mcf != 0.0) {
                 if (ext && p - ext_p0 < ext_n) {
                     const int2 x = ext[p - ext_p0];
@@ -746,6 +761,7 @@ struct ColStream {
             }
             const int b = __shfl_sync(0xffffffffu, mb, kk), e = __shfl_sync(0xffffffffu, me, kk);
             const double cf = __shfl_sync(0xffffffffu, mcf, kk);
+            if constexpr (IND) d.pad = __shfl_sync(0xffffffffu, mzf, kk);
             const int start = b + noff;
             if (cf == 0.0 || start >= e) {
                 if (!coef && noff == 0 && cf != 0.0) {   // gather mode: an empty column still gets its (zero) output
@@ -983,8 +999,8 @@ __global__ void k_gather_smem(Seg S, const int* nseg_dev, int nseg_host, const d
     acc_add(acc, cs.streamed, cs.segs);
 }
 
-template <int SCH, int NSTG>
-__device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG>& cs, const Seg& S, const double* coef, int p0, int p1,
+template <int SCH, int NSTG, bool IND>
+__device__ __forceinline__ void stream_begin(ColStream<SCH, NSTG, IND>& cs, const Seg& S, const double* coef, int p0, int p1,
                                              unsigned char* base, const int2* ext = nullptr, int ext_n = 0) {
     cs.ext = ext;
     cs.ext_p0 = p0;
