@@ -192,7 +192,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     double2* mp_out = cv.take<double2>(big ? nn : 1);
     // heavy-column path of the large-m inner solver (ml_heavy.cuh): the S and G copies of H's nonzeros (at most all
     // of X's), its warp chunks, per-row products, the zeroing columns' unit list
-    const size_t hvn = big ? (size_t)nnz + 16 : 1;
+    const size_t hvn = big ? (size_t)nnz + 3 * mm + 16 : 1;   // (rows padded to whole 4-entry vectors)
     HvPrm hv{};
     hv.hid = cv.take<int>(big ? nn : 1);
     hv.phid = cv.take<int>(big ? nn : 1);
@@ -201,7 +201,7 @@ void carve_all(Carve& cv, ml_ctx* c, int64_t m, int64_t n, int64_t nnz) {
     hv.sval = cv.take<float>(hvn);
     hv.sidx = cv.take<uint16_t>(hvn);
     hv.soff = cv.take<int>(big ? mm + 8 : 1);
-    hv.schunk = cv.take<HvChunk>(big ? (size_t)nnz / (HV_WCH / 2) + mm / HV_WROWS + 16 : 1);   // (greedy chunks)
+    hv.schunk = cv.take<HvChunk>(big ? ((size_t)nnz + 3 * mm) / (HV_WCH / 2) + mm / HV_WROWS + 16 : 1);   // (greedy chunks)
     hv.Xh = cv.take<double>(big ? mm + 2 : 1);
     hv.sH = cv.take<double>(HV_HMAX);
     hv.zunits = cv.take<int>(ucap2);
@@ -818,6 +818,7 @@ ml_status hv_build(ml_ctx* c) {
         while (r < m && r - r0 < HV_WROWS && hr[r + 1] - hr[r0] <= HV_WCH) ++r;
         chs.push_back(HvChunk{hr[r0], hr[r], r0, r - r0, hv_lg(r - r0), 0, 0, 0});
     }
+    if (chs.size() > ((size_t)c->X.nnz + 3 * (size_t)m) / (HV_WCH / 2) + (size_t)m / HV_WROWS + 16) return ML_OK;   // (the workspace's chunk list)
     const int nts = (int)chs.size();
     cudaMemcpyAsync(const_cast<HvChunk*>(hv.schunk), chs.data(), sizeof(HvChunk) * chs.size(), cudaMemcpyHostToDevice,
                     c->st);

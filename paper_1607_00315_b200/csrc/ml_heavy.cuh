@@ -67,10 +67,10 @@ struct HvPrm {
 // rings are addressed through it, so that the out-of-line hv_sweep still emits shared loads.
 extern __shared__ __align__(16) unsigned char hv_dyn[];
 
-// Rows of a staged chunk by groups of L = 2^LG lanes.  Lane gl takes the row's aligned 4-entry vectors gl, gl + L,
-// ... (one 16-byte load of values and one 8-byte load of ids per vector, the entries outside [b, e) of the first
-// and last vector masked), two vectors at a time: loads, then the s_H gathers, then the fused multiply-adds in
-// order; then the group's fixed shuffle tree; Xh[row].
+// Rows of a staged chunk by groups of L = 2^LG lanes.  Lane gl takes the row's 4-entry vectors gl, gl + L, ... (one
+// 16-byte load of values and one 8-byte load of ids per vector; the copy pads every row to whole vectors with zero
+// entries, so no element is masked), two vectors at a time: loads, then the s_H gathers, then the fused multiply-adds
+// in order; then the group's fixed shuffle tree; Xh[row].
 // (ncu, cfg 5: the sweep is bound by shared-memory wavefronts.  With one 4-byte and one 2-byte load per entry the 16
 // rows a warp reads together start at arbitrary offsets: 2.6 wavefronts per request of values and 2.7 of ids against
 // 1, 182 M of the 324 M wavefronts of a launch; vectors need a quarter of the requests.)
@@ -84,30 +84,22 @@ __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, con
     const uint2* si4 = reinterpret_cast<const uint2*>(si);
     for (int r = grp; r - grp < ch.nr; r += NG) {   // (every lane runs every round: the shuffles need all lanes)
         double acc = 0.0;
-        int b = 0, e = 0;
-        if (r < ch.nr) { b = so[ob + r] - eb; e = so[ob + r + 1] - eb; }
-        for (int v = (b >> 2) + gl; 4 * v < e; v += 2 * L) {
-            float x[8];
-            uint32_t ix[8];
-            bool ok[8];
+        int b4 = 0, e4 = 0;   // the row's vectors [b4, e4): rows are padded to whole vectors (k_hv_rowcnt / k_hv_rowfill)
+        if (r < ch.nr) { b4 = (so[ob + r] - eb) >> 2; e4 = (so[ob + r + 1] - eb) >> 2; }
+        for (int v = b4 + gl; v < e4; v += 2 * L) {
+            const bool in1 = v + L < e4;
+            const float4 x0 = sv4[v];
+            const uint2 i0 = si4[v];
+            const float4 x1 = in1 ? sv4[v + L] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint2 i1 = in1 ? si4[v + L] : make_uint2(0u, 0u);
             double g[8];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int vu = v + u * L;
-                const bool in = 4 * vu < e;
-                const float4 xv = in ? sv4[vu] : make_float4(0.f, 0.f, 0.f, 0.f);
-                const uint2 iv = in ? si4[vu] : make_uint2(0u, 0u);
-                x[4 * u + 0] = xv.x; x[4 * u + 1] = xv.y; x[4 * u + 2] = xv.z; x[4 * u + 3] = xv.w;
-                ix[4 * u + 0] = iv.x & 0xffffu; ix[4 * u + 1] = iv.x >> 16;
-                ix[4 * u + 2] = iv.y & 0xffffu; ix[4 * u + 3] = iv.y >> 16;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) ok[4 * u + t] = in && 4 * vu + t >= b && 4 * vu + t < e;
-            }
-#pragma unroll
-            for (int t = 0; t < 8; ++t) g[t] = ok[t] ? s[ix[t] & (HV_HMAX - 1)] : 0.0;
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-                if (ok[t]) acc = fma((double)x[t], g[t], acc);
+            constexpr uint32_t M = HV_HMAX - 1;   // (ids are < HV_HMAX; the mask keeps a stale word inside s_H)
+            g[0] = s[i0.x & M]; g[1] = s[(i0.x >> 16) & M]; g[2] = s[i0.y & M]; g[3] = s[(i0.y >> 16) & M];
+            g[4] = s[i1.x & M]; g[5] = s[(i1.x >> 16) & M]; g[6] = s[i1.y & M]; g[7] = s[(i1.y >> 16) & M];
+            acc = fma((double)x0.x, g[0], acc); acc = fma((double)x0.y, g[1], acc);
+            acc = fma((double)x0.z, g[2], acc); acc = fma((double)x0.w, g[3], acc);
+            acc = fma((double)x1.x, g[4], acc); acc = fma((double)x1.y, g[5], acc);
+            acc = fma((double)x1.z, g[6], acc); acc = fma((double)x1.w, g[7], acc);
         }
 #pragma unroll
         for (int d = L >> 1; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
@@ -277,6 +269,7 @@ __global__ void k_hv_rowcnt(const int* rowptr, const int* col, int m, const int*
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         int c = 0;
         for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) c += __ldg(hid + col[k]) >= 0;
+        c = (c + 3) & ~3;   // rows are padded to whole 4-entry vectors (zero value, id 0): hv_rows needs no element masks
         cnt[i] = c;
         mx = max(mx, c);
     }
@@ -295,16 +288,22 @@ __host__ __device__ __forceinline__ int hv_lg(int rows) {   // groups of L = 32 
 __global__ void k_hv_rowfill(const int* rowptr, const int* col, const float* val, int m, const int* hid, const int* hrp,
                              float* sval, uint16_t* sidx) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        const int o = hrp[i], L = hrp[i + 1] - o;
+        const int o = hrp[i], L = hrp[i + 1] - o;   // (L: the padded length, a multiple of 4)
         if (L == 0) continue;
-        int q = (int)(((unsigned)i * 2654435761u) >> 8) % L;
+        int q = (int)(((unsigned)i * 2654435761u) >> 8) % L, placed = 0;
         for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
             const int h = __ldg(hid + col[k]);
             if (h >= 0) {
                 sval[o + q] = val[k];
                 sidx[o + q] = (uint16_t)h;
                 q = q + 1 == L ? 0 : q + 1;
+                ++placed;
             }
+        }
+        for (; placed < L; ++placed) {   // the padding: zero entries of heavy column 0
+            sval[o + q] = 0.0f;
+            sidx[o + q] = 0;
+            q = q + 1 == L ? 0 : q + 1;
         }
     }
 }

@@ -40,6 +40,42 @@ __global__ void __launch_bounds__(256) k_gather(const int* __restrict__ idx, lon
     if (acc == 12345.678) out[0] = acc;
 }
 
+// the same index stream, one 64-bit red.global.add per index (the X_A s reductions of the light columns)
+template <int U>
+__global__ void __launch_bounds__(256) k_red(const int* __restrict__ idx, long long n, unsigned long long* tab) {
+    const long long stride = (long long)gridDim.x * blockDim.x * 4 * (U / 4);
+    for (long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; k < n; k += stride) {
+        int q[U];
+#pragma unroll
+        for (int u = 0; u < U / 4; ++u) {
+            const long long ku = k + (long long)u * gridDim.x * blockDim.x * 4;
+            int4 v = ku + 3 < n ? *reinterpret_cast<const int4*>(idx + ku) : make_int4(0, 0, 0, 0);
+            q[4 * u] = v.x; q[4 * u + 1] = v.y; q[4 * u + 2] = v.z; q[4 * u + 3] = v.w;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            asm volatile("red.global.add.u64 [%0], %1;" ::"l"(tab + q[u]), "l"((unsigned long long)(q[u] + 1)) : "memory");
+    }
+}
+static void run_red(const char* name, const int* d_idx, long long n, void* tab, int blocks_per_sm, double clk_ghz) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = 148 * blocks_per_sm;
+    for (int w = 0; w < 2; ++w) k_red<8><<<grid, 256>>>(d_idx, n, (unsigned long long*)tab);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) k_red<8><<<grid, 256>>>(d_idx, n, (unsigned long long*)tab);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    const double gps = n / (ms * 1e-3);
+    printf("%-34s red.global.add.u64 blk/SM=%d : %7.3f ms  %7.1f G reds/s  %5.2f per SM clk\n", name, blocks_per_sm, ms, gps * 1e-9,
+           gps / (148 * clk_ghz * 1e9));
+}
+
 template <int EB, int U, bool CG>
 static void run(const char* name, const int* d_idx, long long n, const void* tab, double* out, int blocks_per_sm, double clk_ghz) {
     typedef typename Elt<EB>::T T;
@@ -105,6 +141,9 @@ int main() {
         run<16, 8, false>(name, d_idx, n, tab, out, 3, ghz);
         run<16, 16, false>(name, d_idx, n, tab, out, 3, ghz);
         run<16, 8, false>(name, d_idx, n, tab, out, 6, ghz);
+        run_red(name, d_idx, n, tab, 1, ghz);
+        run_red(name, d_idx, n, tab, 4, ghz);
+        run_red(name, d_idx, n, tab, 8, ghz);
     }
     return 0;
 }
