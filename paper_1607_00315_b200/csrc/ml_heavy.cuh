@@ -74,16 +74,20 @@ extern __shared__ __align__(16) unsigned char hv_dyn[];
 // (ncu, cfg 5: the sweep is bound by shared-memory wavefronts.  With one 4-byte and one 2-byte load per entry the 16
 // rows a warp reads together start at arbitrary offsets: 2.6 wavefronts per request of values and 2.7 of ids against
 // 1, 182 M of the 324 M wavefronts of a launch; vectors need a quarter of the requests.)
+static_assert(8 * HV_HMAX <= 65536, "8 * id must fit the copy's 16-bit ids");
+__device__ __forceinline__ double hv_sh(const unsigned char* sb, uint32_t off8) {
+    return *reinterpret_cast<const double*>(sb + (off8 & 0xfff8u));
+}
 template <int LG>
 __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, const int* so, const HvChunk& ch, double* Xh) {
     constexpr int L = 1 << LG, NG = 32 >> LG;
     const int lane = threadIdx.x & 31, grp = lane >> LG, gl = lane & (L - 1);
     const int eb = ch.e0 & ~7, ob = ch.r0 & 3;
-    const double* s = reinterpret_cast<const double*>(hv_dyn + HV_SH_OFF);
+    const unsigned char* sb = hv_dyn + HV_SH_OFF;
     const float4* sv4 = reinterpret_cast<const float4*>(sv);
     const uint2* si4 = reinterpret_cast<const uint2*>(si);
     for (int r = grp; r - grp < ch.nr; r += NG) {   // (every lane runs every round: the shuffles need all lanes)
-        double acc = 0.0;
+        double acc = 0.0, acc1 = 0.0;   // (one chain per vector of the pair)
         int b4 = 0, e4 = 0;   // the row's vectors [b4, e4): rows are padded to whole vectors (k_hv_rowcnt / k_hv_rowfill)
         if (r < ch.nr) { b4 = (so[ob + r] - eb) >> 2; e4 = (so[ob + r + 1] - eb) >> 2; }
         for (int v = b4 + gl; v < e4; v += 2 * L) {
@@ -92,15 +96,18 @@ __device__ __forceinline__ void hv_rows(const float* sv, const uint16_t* si, con
             const uint2 i0 = si4[v];
             const float4 x1 = in1 ? sv4[v + L] : make_float4(0.f, 0.f, 0.f, 0.f);
             const uint2 i1 = in1 ? si4[v + L] : make_uint2(0u, 0u);
+            // the copy stores 8 * id: a 16-bit half is the byte offset into s_H (any value stays inside its 64 KB)
             double g[8];
-            constexpr uint32_t M = HV_HMAX - 1;   // (ids are < HV_HMAX; the mask keeps a stale word inside s_H)
-            g[0] = s[i0.x & M]; g[1] = s[(i0.x >> 16) & M]; g[2] = s[i0.y & M]; g[3] = s[(i0.y >> 16) & M];
-            g[4] = s[i1.x & M]; g[5] = s[(i1.x >> 16) & M]; g[6] = s[i1.y & M]; g[7] = s[(i1.y >> 16) & M];
+            g[0] = hv_sh(sb, i0.x & 0xffffu); g[1] = hv_sh(sb, i0.x >> 16);
+            g[2] = hv_sh(sb, i0.y & 0xffffu); g[3] = hv_sh(sb, i0.y >> 16);
+            g[4] = hv_sh(sb, i1.x & 0xffffu); g[5] = hv_sh(sb, i1.x >> 16);
+            g[6] = hv_sh(sb, i1.y & 0xffffu); g[7] = hv_sh(sb, i1.y >> 16);
             acc = fma((double)x0.x, g[0], acc); acc = fma((double)x0.y, g[1], acc);
             acc = fma((double)x0.z, g[2], acc); acc = fma((double)x0.w, g[3], acc);
-            acc = fma((double)x1.x, g[4], acc); acc = fma((double)x1.y, g[5], acc);
-            acc = fma((double)x1.z, g[6], acc); acc = fma((double)x1.w, g[7], acc);
+            acc1 = fma((double)x1.x, g[4], acc1); acc1 = fma((double)x1.y, g[5], acc1);
+            acc1 = fma((double)x1.z, g[6], acc1); acc1 = fma((double)x1.w, g[7], acc1);
         }
+        acc += acc1;
 #pragma unroll
         for (int d = L >> 1; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
         if (gl == 0 && r < ch.nr) Xh[ch.r0 + r] = acc;
@@ -295,7 +302,7 @@ __global__ void k_hv_rowfill(const int* rowptr, const int* col, const float* val
             const int h = __ldg(hid + col[k]);
             if (h >= 0) {
                 sval[o + q] = val[k];
-                sidx[o + q] = (uint16_t)h;
+                sidx[o + q] = (uint16_t)(8 * h);   // (the byte offset of s_H[h])
                 q = q + 1 == L ? 0 : q + 1;
                 ++placed;
             }

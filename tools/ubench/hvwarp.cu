@@ -119,7 +119,8 @@ int main(int argc, char** argv) {
     std::mt19937 rng(1);
     std::vector<int> rp(m + 8, 0);
     std::poisson_distribution<int> pois(rowlen);
-    for (int i = 0; i < m; ++i) rp[i + 1] = rp[i] + std::min(pois(rng), 500);
+    // (row lengths in whole 4-entry vectors, as the library's padded copy)
+    for (int i = 0; i < m; ++i) rp[i + 1] = rp[i] + ((std::min(pois(rng), 500) + 3) & ~3);
     for (int i = m + 1; i < m + 8; ++i) rp[i] = rp[m];
     const long long E = rp[m];
     std::vector<float> v(E + 16, 1.0f);
@@ -170,7 +171,9 @@ int main(int argc, char** argv) {
     run<1, true, 1024, 2, 16>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
     nch = chunks(384, 8);
     run<2, true, 384, 4, 8>(dch, nch, dv, dk, drp, dsH, dXh, E, sms);
-    {   // the library's hv_sweep with its own chunking (HV_WCH, HV_WROWS, lg by rows)
+    {   // the library's hv_sweep with its own chunking (HV_WCH, HV_WROWS, lg by rows); its copy stores 8 * id
+        for (auto& x : k) x = (uint16_t)(8 * x);
+        cudaMemcpy(dk, k.data(), k.size() * 2, cudaMemcpyHostToDevice);
         std::vector<HvChunk> hc;
         for (int r = 0; r < m;) {
             const int r0 = r;
