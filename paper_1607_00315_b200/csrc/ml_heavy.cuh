@@ -27,7 +27,10 @@ constexpr int HV_HMAX = 8192;              // heavy columns at most (s_H: 64 KB 
 #define HV_WST_V 2
 #endif
 constexpr int HV_WCH = HV_WCH_V;           // entries per warp chunk at most (build knobs: -DHV_WCH_V, -DHV_WST_V)
-constexpr int HV_WROWS = 32;               // rows per warp chunk at most (one round of groups of 32 / 2^lg lanes)
+#ifndef HV_WROWS_V
+#define HV_WROWS_V 32
+#endif
+constexpr int HV_WROWS = HV_WROWS_V;       // rows per warp chunk at most (one round of groups of 32 / 2^lg lanes)
 constexpr int HV_WST = HV_WST_V;           // stages of a warp's ring
 constexpr int HV_MINLEN = 32;              // shortest heavy column
 constexpr long long HV_AUTO = 1LL << 26;   // the path is on by default when H holds this many nonzeros (ml.cu)
