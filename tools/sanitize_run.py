@@ -10,8 +10,10 @@ import mlgen  # noqa: E402
 import paper_1607_00315_b200 as ml  # noqa: E402
 
 
-def run(ds, opts=None):
+def run(ds, opts=None, engine=0):
     ctx = ml.Context(ds)
+    if engine:
+        ctx.ml_set_engine(engine)
     rng = np.random.default_rng(0)
     w = np.zeros(ds.n)
     idx = rng.choice(ds.n, max(1, ds.n // 10), replace=False)
@@ -38,5 +40,10 @@ if __name__ == "__main__":
     run(mlgen.random_sparse(777, 1301, 0.02, seed=5, empty_rows=9, empty_cols=40))
     run(mlgen.onehot(3000, 3)[0])
     run(mlgen.make(1), ml.default_opts(inner_cg=2))
+    # short columns on the large-m path (thread-per-column tiles, two-pass finest gather), then the heavy-column path
+    # forced on (padded row-major copy, vector loads)
+    run(mlgen.make(5, m=12000, n=120000))
+    run(mlgen.make(5, m=12000, n=120000), engine=1 << 4)
+    run(mlgen.make(4, m=20000, n=40000), engine=1 << 4)
     run(mlgen.make(2, m=300, n=3000), ml.default_opts(continuation=1))
     run(mlgen.make(3, m=20000, n=30000), ml.default_opts(continuation=1))
