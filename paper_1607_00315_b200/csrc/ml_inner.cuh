@@ -1481,12 +1481,39 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
             const int nz0 = (w0 != 0.0), nz1 = (w1 != 0.0);
             if (nz0 != nz1) { atomicXor(P.wbits + (j >> 5), 1u << (j & 31)); v[1] += nz1 - nz0; }
         }
-        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            const double z = P.z[i] + alpha * xd_r[i - r0];
-            P.z[i] = z;
-            const RowState st = row_state_i(P.y, P.b, i, z);
-            P.rD[i] = make_double2(st.r, st.D);
-            v[0] += st.ell;
+        if (BIG) {   // (thousands of rows per block: four rows' loads in flight per thread; same order of the sums)
+            for (int i0 = r0 + threadIdx.x; i0 < r1; i0 += 4 * blockDim.x) {
+                double zz[4], xd[4], yb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    const bool in = i < r1;
+                    zz[u] = in ? P.z[i] : 0.0;
+                    xd[u] = in ? xd_r[i - r0] : 0.0;
+                    yb[u] = in ? (P.b ? P.b[i] : (double)P.y[i]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < r1) {
+                        const double z = zz[u] + alpha * xd[u];
+                        P.z[i] = z;
+                        RowState st;
+                        if (P.b) { const double r = z - yb[u]; st = RowState{r, 1.0, 0.5 * r * r}; }
+                        else st = row_state(z, yb[u]);
+                        P.rD[i] = make_double2(st.r, st.D);
+                        v[0] += st.ell;
+                    }
+                }
+            }
+        } else {
+            for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                const double z = P.z[i] + alpha * xd_r[i - r0];
+                P.z[i] = z;
+                const RowState st = row_state_i(P.y, P.b, i, z);
+                P.rD[i] = make_double2(st.r, st.D);
+                v[0] += st.ell;
+            }
         }
         ir_block_partials<2>(v, 0u, 0u, sh_w, part, IR_SO);
     }
