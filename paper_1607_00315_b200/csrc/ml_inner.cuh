@@ -1415,10 +1415,35 @@ __global__ void __launch_bounds__(256, 1) k_inner(Prm P, ASet AS, Seg S, int K, 
 #pragma unroll
             for (int k = 0; k < NT1; ++k) v[2 + k] += fabs(w + at[k] * d) - aw;
         }
-        for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            const double zi = P.z[i], xd = xd_r[i - r0];
+        if (BIG) {   // (four rows' loads in flight per thread; the sums in the same order)
+            for (int i0 = r0 + threadIdx.x; i0 < r1; i0 += 4 * blockDim.x) {
+                double zz[4], xd[4], yb[4];
 #pragma unroll
-            for (int k = 0; k < NT1; ++k) v[6 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    const bool in = i < r1;
+                    zz[u] = in ? P.z[i] : 0.0;
+                    xd[u] = in ? xd_r[i - r0] : 0.0;
+                    yb[u] = in ? (P.b ? P.b[i] : (double)P.y[i]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (i0 + u * (int)blockDim.x < r1) {
+#pragma unroll
+                        for (int k = 0; k < NT1; ++k) {
+                            const double dz = at[k] * xd[u];
+                            if (P.b) { const double r = zz[u] - yb[u]; v[6 + k] += dz * (r + 0.5 * dz); }
+                            else v[6 + k] += dloss(yb[u] * zz[u], yb[u] * dz);
+                        }
+                    }
+                }
+            }
+        } else {
+            for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                const double zi = P.z[i], xd = xd_r[i - r0];
+#pragma unroll
+                for (int k = 0; k < NT1; ++k) v[6 + k] += dloss_i(P.y, P.b, i, zi, at[k] * xd);
+            }
         }
         ir_block_partials<10>(v, 1u << 1, 0u, sh_w, part, IR_SO);
     }
