@@ -5,8 +5,9 @@
 // hold 65 % of 2e8), and they are the columns of every free set.  Through the column units of k_inner their X_A s
 // products are 64-bit reductions into global memory, bound by the REDG issue rate of the load/store units (~1.3 LSU
 // cycles per lane, B300_MICROARCH.md: 0.8-0.9 nonzeros per SM clock).  Here the heavy set H (at most HV_HMAX
-// columns, the longest, chosen once at ml_create) gets a row-major copy of its nonzeros (fp32 value + 16-bit heavy
-// id, 6 bytes): the "S copy".  s_H (the inner direction on H, HV_HMAX doubles) is staged in shared memory, and each
+// columns, the longest, chosen once at ml_create) gets a row-major copy of its nonzeros (fp32 value + 16 bits holding
+// 8 x the heavy id, the byte offset of s_H[id]; 6 bytes; every row padded to a whole number of 4-entry vectors with
+// zero entries): the "S copy".  s_H (the inner direction on H, HV_HMAX doubles) is staged in shared memory, and each
 // row's sum over its heavy entries is formed in registers and written once (Xh): no atomics.
 // The copy is cut into warp chunks of whole rows (at most HV_WCH entries and HV_WROWS rows); every warp streams its
 // own chunks through a private HV_WST-stage TMA ring (its lane 0 issues the bulk copies of the values, the ids and
