@@ -298,23 +298,69 @@ __host__ __device__ __forceinline__ int hv_lg(int rows) {   // groups of L = 32 
 // together would hit the same shared-memory banks
 __global__ void k_hv_rowfill(const int* rowptr, const int* col, const float* val, int m, const int* hid, const int* hrp,
                              float* sval, uint16_t* sidx) {
+    // Placement inside a row (any order is valid: a row's sum is over all its entries).  hv_rows gathers s_H[id] for 16
+    // lanes per shared-memory phase: with the usual 16 rows per round (L = 2), lane gl of row r reads position
+    // p = 4 gl + t (+ 8 for the second vector of a pair, + 16 per iteration).  The gathers of a phase fall into 16
+    // distinct 8-byte banks when id mod 16 = rho(p, r) below, so each entry is placed at a position that wants its
+    // residue as long as the row has one (ncu: 2.3 wavefronts per gather request with hashed rotations); rows of more
+    // than HV_PLACE entries keep the rotation.
+    constexpr int HV_PLACE = 192;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         const int o = hrp[i], L = hrp[i + 1] - o;   // (L: the padded length, a multiple of 4)
         if (L == 0) continue;
-        int q = (int)(((unsigned)i * 2654435761u) >> 8) % L, placed = 0;
+        if (L > HV_PLACE) {
+            int q = (int)(((unsigned)i * 2654435761u) >> 8) % L, placed = 0;
+            for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+                const int h = __ldg(hid + col[k]);
+                if (h >= 0) {
+                    sval[o + q] = val[k];
+                    sidx[o + q] = (uint16_t)(8 * h);   // (the byte offset of s_H[h])
+                    q = q + 1 == L ? 0 : q + 1;
+                    ++placed;
+                }
+            }
+            for (; placed < L; ++placed) {   // the padding: zero entries of heavy column 0
+                sval[o + q] = 0.0f;
+                sidx[o + q] = 0;
+                q = q + 1 == L ? 0 : q + 1;
+            }
+            continue;
+        }
+        float ev[HV_PLACE];      // the row's heavy entries, then sorted by residue
+        uint16_t eh[HV_PLACE];
+        float bv[HV_PLACE];
+        uint16_t bh[HV_PLACE];
+        int cnt[17];
+        for (int r = 0; r < 17; ++r) cnt[r] = 0;
+        int c = 0;
         for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
             const int h = __ldg(hid + col[k]);
-            if (h >= 0) {
-                sval[o + q] = val[k];
-                sidx[o + q] = (uint16_t)(8 * h);   // (the byte offset of s_H[h])
-                q = q + 1 == L ? 0 : q + 1;
-                ++placed;
-            }
+            if (h >= 0) { ev[c] = val[k]; eh[c] = (uint16_t)h; cnt[(h & 15) + 1] += 1; ++c; }
         }
-        for (; placed < L; ++placed) {   // the padding: zero entries of heavy column 0
-            sval[o + q] = 0.0f;
-            sidx[o + q] = 0;
-            q = q + 1 == L ? 0 : q + 1;
+        for (int r = 0; r < 16; ++r) cnt[r + 1] += cnt[r];   // bucket starts
+        int fill[16], head[16];
+        for (int r = 0; r < 16; ++r) { fill[r] = cnt[r]; head[r] = cnt[r]; }
+        for (int e = 0; e < c; ++e) { const int r = eh[e] & 15; bv[fill[r]] = ev[e]; bh[fill[r]] = eh[e]; fill[r] += 1; }
+        // positions that find an entry of the residue they want
+        const int rr = i & 7;
+        for (int p2 = 0; p2 < L; ++p2) {
+            const int want = 8 * ((p2 >> 2) & 1) + ((rr + p2 + 4 * ((p2 >> 3) & 1)) & 7);
+            if (head[want] < cnt[want + 1]) {
+                sval[o + p2] = bv[head[want]];
+                sidx[o + p2] = (uint16_t)(8 * bh[head[want]]);
+                head[want] += 1;
+            } else sidx[o + p2] = 0xffffu;   // (free: filled below)
+        }
+        // the entries left over, in bucket order, into the free positions; then the padding (zero entries of column 0)
+        int r = 0;
+        for (int p2 = 0; p2 < L; ++p2) {
+            if (sidx[o + p2] != 0xffffu) continue;
+            while (r < 16 && head[r] >= cnt[r + 1]) ++r;
+            if (r < 16) {
+                sval[o + p2] = bv[head[r]];
+                sidx[o + p2] = (uint16_t)(8 * bh[head[r]]);
+                head[r] += 1;
+            } else { sval[o + p2] = 0.0f; sidx[o + p2] = 0; }
         }
     }
 }
